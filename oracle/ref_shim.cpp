@@ -14,6 +14,7 @@
 #include "flowroi/flow.hpp"
 #include "flowroi/registration.hpp"
 #include "flowroi/roi.hpp"
+#include "flowroi/rng.hpp"
 #include "flowroi/synthetic.hpp"
 
 #include "../include/froi/froi.h"
@@ -231,6 +232,13 @@ int ref_generate_synthetic(int n_cells, int n_frames, int w, int h, int depth, d
             }
     }
     SHIM_CATCH
+}
+
+// flowroi::Rng (rng.hpp:11-62) streams, to pin the Python fixture restatement.
+void ref_rng_stream(uint64_t seed, int n, uint64_t* u64_out, double* normal_out) {
+    Rng a(seed), b(seed);
+    for (int i = 0; i < n; ++i) u64_out[i] = a.next_u64();
+    for (int i = 0; i < n; ++i) normal_out[i] = b.normal(0.0, 1.0);
 }
 
 }  // extern "C"

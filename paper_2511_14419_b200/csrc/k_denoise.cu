@@ -1,0 +1,157 @@
+// k_denoise.cu — fused median + bilateral denoise (denoise.hpp:28-90), bit-exact.
+//
+// One CTA produces a 32x8 output tile of one frame slot.  The raw tile (halo = median radius +
+// bilateral radius, edge-replicated) and the median tile (halo = bilateral radius) live in
+// shared memory; the bilateral sums run in fp64 in the reference's dy-major / dx-minor order
+// with explicit round-to-nearest operations (no FMA), the range LUT and spatial weights are the
+// host-computed libm values, and rounding is std::lround (half away from zero).  The CTA also
+// reduces the integer sum of its denoised pixels for the registration mean
+// (registration.hpp:27-29), which is exact in integers.
+//
+// Roofline: HBM-bound at 2 B/px for u8 (read raw, write den) — SURVEY.md App. C row "D".
+#include "kernels.cuh"
+
+namespace froi {
+namespace {
+
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+
+__device__ __forceinline__ void cswap(int& a, int& b) {
+    const int t = min(a, b);
+    b = max(a, b);
+    a = t;
+}
+
+// Median of 9 by the classic 19-exchange selection network (exact for integers).
+__device__ __forceinline__ int median9(int p0, int p1, int p2, int p3, int p4, int p5, int p6,
+                                       int p7, int p8) {
+    cswap(p1, p2); cswap(p4, p5); cswap(p7, p8); cswap(p0, p1); cswap(p3, p4); cswap(p6, p7);
+    cswap(p1, p2); cswap(p4, p5); cswap(p7, p8); cswap(p0, p3); cswap(p5, p8); cswap(p4, p7);
+    cswap(p3, p6); cswap(p1, p4); cswap(p2, p5); cswap(p4, p7); cswap(p4, p2); cswap(p6, p4);
+    cswap(p4, p2);
+    return p4;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int enabled, int mr,
+                                                 int br, const void* const* frame_raw, T* den,
+                                                 unsigned long long* sums, const double* spatial_g,
+                                                 const double* lut_g) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int slot = blockIdx.z;
+    const T* src = (const T*)frame_raw[slot];
+    T* dst = den + (size_t)slot * W * H;
+    const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+    const int tid = threadIdx.y * TX + threadIdx.x;
+    const int R1 = mr + br;
+    const int rw = TX + 2 * R1, rh = TY + 2 * R1;
+    const int mw = TX + 2 * br, mh = TY + 2 * br;
+    const int side = 2 * br + 1;
+    double* spat_s = (double*)smem;                 // side*side
+    double* lut_s = spat_s + side * side;           // 256 (u8 only)
+    const bool lut_in_smem = sizeof(T) == 1;
+    int* raw_s = (int*)(lut_s + (lut_in_smem ? 256 : 0));
+    int* med_s = raw_s + rw * rh;
+
+    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+    int outv = 0;
+    if (!enabled) {
+        if (x < W && y < H) {
+            outv = src[(size_t)y * W + x];
+            dst[(size_t)y * W + x] = (T)outv;
+        }
+    } else {
+        for (int i = tid; i < side * side; i += NT) spat_s[i] = spatial_g[i];
+        if (lut_in_smem)
+            for (int i = tid; i < 256; i += NT) lut_s[i] = lut_g[i];
+        for (int i = tid; i < rw * rh; i += NT) {
+            const int ry = i / rw, rx = i - ry * rw;
+            const int gy = clampi(y0 - R1 + ry, 0, H - 1), gx = clampi(x0 - R1 + rx, 0, W - 1);
+            raw_s[i] = src[(size_t)gy * W + gx];
+        }
+        __syncthreads();
+        // median at clamped coordinates: med_s[X - (x0-br)] = median(clamp(X)) (denoise.hpp:32-43)
+        for (int i = tid; i < mw * mh; i += NT) {
+            const int my = i / mw, mx = i - my * mw;
+            const int cx = clampi(x0 - br + mx, 0, W - 1), cy = clampi(y0 - br + my, 0, H - 1);
+            const int rx = cx - (x0 - R1), ry = cy - (y0 - R1);
+            int m;
+            if (mr == 1) {
+                const int* r0 = raw_s + (ry - 1) * rw + rx;
+                const int* r1 = r0 + rw;
+                const int* r2 = r1 + rw;
+                m = median9(r0[-1], r0[0], r0[1], r1[-1], r1[0], r1[1], r2[-1], r2[0], r2[1]);
+            } else {
+                // order statistic n/2 by rank counting (exact, any radius)
+                const int n = (2 * mr + 1) * (2 * mr + 1), k = n / 2;
+                m = 0;
+                for (int a = 0; a < n; ++a) {
+                    const int va = raw_s[(ry + a / (2 * mr + 1) - mr) * rw + rx + a % (2 * mr + 1) - mr];
+                    int lt = 0, le = 0;
+                    for (int b = 0; b < n; ++b) {
+                        const int vb = raw_s[(ry + b / (2 * mr + 1) - mr) * rw + rx + b % (2 * mr + 1) - mr];
+                        lt += vb < va;
+                        le += vb <= va;
+                    }
+                    if (lt <= k && k < le) { m = va; break; }
+                }
+            }
+            med_s[i] = m;
+        }
+        __syncthreads();
+        if (x < W && y < H) {
+            // bilateral_filter (denoise.hpp:63-79)
+            const int c = med_s[(threadIdx.y + br) * mw + threadIdx.x + br];
+            double num = 0.0, dn = 0.0;
+            for (int dy = -br; dy <= br; ++dy) {
+                const int* row = med_s + (threadIdx.y + br + dy) * mw + threadIdx.x + br;
+                for (int dx = -br; dx <= br; ++dx) {
+                    const int v = row[dx];
+                    const int d = abs(v - c);
+                    const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
+                    const double wgt = dmul(spat_s[(dy + br) * side + dx + br], lw);
+                    num = dadd(num, dmul(wgt, (double)v));
+                    dn = dadd(dn, wgt);
+                }
+            }
+            double q = ddiv(num, dn);
+            q = (q < 0.0) ? 0.0 : q;
+            q = ((double)maxval < q) ? (double)maxval : q;
+            outv = (int)round(q);
+            dst[(size_t)y * W + x] = (T)outv;
+        }
+    }
+    // integer sum of the denoised tile for the registration mean
+    unsigned long long s = (unsigned long long)outv;
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+    if ((tid & 31) == 0 && s) atomicAdd(sums + slot, s);
+}
+
+}  // namespace
+
+void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw, void* d_den,
+                    unsigned long long* d_sums, const double* d_spatial, const double* d_lut,
+                    int n_slots, cudaStream_t s) {
+    if (n_slots <= 0) return;
+    const int mr = p.median_radius, br = p.bilateral_radius;
+    const int R1 = mr + br, side = 2 * br + 1;
+    const size_t smem = sizeof(double) * (side * side + (g.sample_bytes == 1 ? 256 : 0)) +
+                        sizeof(int) * ((TX + 2 * R1) * (TY + 2 * R1) + (TX + 2 * br) * (TY + 2 * br));
+    dim3 grid(cdiv(g.W, TX), cdiv(g.H, TY), n_slots), block(TX, TY);
+    if (g.sample_bytes == 1) {
+        if (smem > 48 * 1024)
+            FROI_CUDA(cudaFuncSetAttribute(k_denoise<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_denoise<uint8_t><<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br,
+                                                     d_frame_raw, (uint8_t*)d_den, d_sums,
+                                                     d_spatial, d_lut);
+    } else {
+        if (smem > 48 * 1024)
+            FROI_CUDA(cudaFuncSetAttribute(k_denoise<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_denoise<uint16_t><<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br,
+                                                      d_frame_raw, (uint16_t*)d_den, d_sums,
+                                                      d_spatial, d_lut);
+    }
+    FROI_LAUNCH_CHECK();
+}
+
+}  // namespace froi

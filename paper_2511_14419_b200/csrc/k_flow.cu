@@ -1,0 +1,563 @@
+// k_flow.cu — pyramid, polynomial expansion and the fused flow iteration
+// (flow.hpp:118-345), fp32 storage and arithmetic with fp64 coordinates / solve.
+//
+//   k_pyr_down   7-tap Gaussian (sigma 1, rows then columns, edge-replicated) fused with the
+//                bilinear resample to floor(w*scale) x floor(h*scale)            (flow.hpp:259-298)
+//   k_polyexp    5-tap separable Gaussian-weighted quadratic fit per pixel; writes the four
+//                planes the warp gathers together as one float4 {a11,a12,a22,bx} plus {by};
+//                the constant term c is only produced by the debug tap        (flow.hpp:118-153)
+//   k_flow_iter  one launch per (level, iteration), one CTA per 32x32 output tile of one pair:
+//                phase 1 builds the five normal-equation products G over the tile + 7 px halo
+//                (prior from the same level, or upsampled from the coarser level on the first
+//                iteration, then bilinear warp of the next frame's planes), phase 2/3 take the
+//                15x15 clipped box sums in shared memory, phase 4 solves the 2x2 system in fp64
+//                with the reference's singularity test                       (flow.hpp:204-255)
+//
+// Level-0 images are read straight from the denoised u8/u16 frames (normalised on the fly, with
+// the registration shift applied as a clamped gather, registration.hpp:100-107), so the fp32
+// level-0 image is never materialised.
+#include "kernels.cuh"
+
+namespace froi {
+namespace {
+
+// ------------------------------------------------------------------ sources
+template <typename T>
+struct FrameSrc {  // normalize_frame(apply_shift(den, s)) at level 0
+    const T* f;
+    int W, H, dx, dy;
+    double inv;  // 1.0 / maxval
+    __device__ __forceinline__ float at(int x, int y) const {
+        const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
+        const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
+        return (float)((double)f[(size_t)sy * W + sx] * inv);
+    }
+};
+
+struct ImageSrc {
+    const float* f;
+    int W, H;
+    __device__ __forceinline__ float at(int x, int y) const {
+        return f[(size_t)clampi(y, 0, H - 1) * W + clampi(x, 0, W - 1)];
+    }
+};
+
+// ------------------------------------------------------------------ polynomial expansion
+constexpr int PX = 32, PY = 16, PNT = 256;
+
+template <typename Src, bool kDebug>
+__device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r,
+                                             const DevParams& P, float4* outA, float* outB,
+                                             float* dbg_planes, float* smem) {
+    const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
+    const int sw = PX + 2 * r, sh = PY + 2 * r;
+    float* s_in = smem;               // sh * sw
+    float* s_r = s_in + sh * sw;      // 3 * sh * PX
+    const int tid = threadIdx.x;
+    // constant offset: the fit of A and b is invariant to it and it removes cancellation
+    const float c0 = src.at(x0, y0);
+    for (int i = tid; i < sh * sw; i += PNT) {
+        const int yy = i / sw, xx = i - yy * sw;
+        s_in[i] = src.at(x0 - r + xx, y0 - r + yy) - c0;
+    }
+    __syncthreads();
+    // correlate_rows with g0, g1, g2 (flow.hpp:55-70)
+    for (int i = tid; i < sh * PX; i += PNT) {
+        const int yy = i / PX, xx = i - yy * PX;
+        const float* row = s_in + yy * sw + xx;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        for (int t = 0; t <= 2 * r; ++t) {
+            const float v = row[t];
+            a0 += P.g0[t] * v;
+            a1 += P.g1[t] * v;
+            a2 += P.g2[t] * v;
+        }
+        s_r[i] = a0;
+        s_r[sh * PX + i] = a1;
+        s_r[2 * sh * PX + i] = a2;
+    }
+    __syncthreads();
+    // correlate_cols and the moment combination (flow.hpp:136-151)
+    for (int i = tid; i < PY * PX; i += PNT) {
+        const int yy = i / PX, xx = i - yy * PX;
+        const int x = x0 + xx, y = y0 + yy;
+        if (x >= w || y >= h) continue;
+        float s1 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
+        for (int t = 0; t <= 2 * r; ++t) {
+            const float r0 = s_r[(yy + t) * PX + xx];
+            const float r1 = s_r[sh * PX + (yy + t) * PX + xx];
+            const float r2 = s_r[2 * sh * PX + (yy + t) * PX + xx];
+            s1 += P.g0[t] * r0;
+            sx += P.g0[t] * r1;
+            sy += P.g1[t] * r0;
+            sxx += P.g0[t] * r2;
+            syy += P.g2[t] * r0;
+            sxy += P.g1[t] * r1;
+        }
+        const float inv_m20 = P.poly_moments[0], inv_m22 = P.poly_moments[1];
+        const float i00 = P.poly_moments[2], i01 = P.poly_moments[3];
+        const float i11 = P.poly_moments[4], i12 = P.poly_moments[5];
+        const float bx = sx * inv_m20, by = sy * inv_m20;
+        const float a12 = 0.5f * sxy * inv_m22;
+        const float a11 = i01 * s1 + i11 * sxx + i12 * syy;
+        const float a22 = i01 * s1 + i12 * sxx + i11 * syy;
+        const size_t o = (size_t)y * w + x;
+        if (kDebug) {
+            const size_t n = (size_t)w * h;
+            dbg_planes[o] = i00 * s1 + i01 * (sxx + syy) + c0;
+            dbg_planes[n + o] = bx;
+            dbg_planes[2 * n + o] = by;
+            dbg_planes[3 * n + o] = a11;
+            dbg_planes[4 * n + o] = a12;
+            dbg_planes[5 * n + o] = a22;
+        } else {
+            outA[o] = make_float4(a11, a12, a22, bx);
+            outB[o] = by;
+        }
+    }
+}
+
+// Frame slots: level-0 expansion from the denoised frame (unshifted).
+template <typename T>
+__global__ void __launch_bounds__(PNT) k_polyexp_frame(Geom g, DevParams P, const T* den,
+                                                       float4* exA, float* exB) {
+    extern __shared__ float smem_f[];
+    const int slot = blockIdx.z;
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, 1.0 / g.maxval};
+    polyexp_tile<FrameSrc<T>, false>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)slot * g.lsum,
+                                     exB + (size_t)slot * g.lsum, nullptr, smem_f);
+}
+
+// Pair slots: level-0 expansion of apply_shift(den[t], s) when s != 0.
+template <typename T>
+__global__ void __launch_bounds__(PNT) k_polyexp_shifted(Geom g, DevParams P, const T* den,
+                                                         const int* next, const PairInfo* info,
+                                                         float4* exA, float* exB) {
+    extern __shared__ float smem_f[];
+    const int p = blockIdx.z;
+    const PairInfo I = info[p];
+    if (!I.shifted) return;
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, 1.0 / g.maxval};
+    polyexp_tile<FrameSrc<T>, false>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)p * g.lsum,
+                                     exB + (size_t)p * g.lsum, nullptr, smem_f);
+}
+
+// Levels >= 1 from a float pyramid image (frame slots if info == nullptr, else pair slots).
+__global__ void __launch_bounds__(PNT) k_polyexp_level(Geom g, DevParams P, int l,
+                                                       const float* pyr, long long pyr_stride,
+                                                       const PairInfo* info, float4* exA,
+                                                       float* exB) {
+    extern __shared__ float smem_f[];
+    const int z = blockIdx.z;
+    if (info && !info[z].shifted) return;
+    const long long poff = g.loff[l] - g.loff[1];
+    ImageSrc src{pyr + (size_t)z * pyr_stride + poff, g.lw[l], g.lh[l]};
+    polyexp_tile<ImageSrc, false>(src, g.lw[l], g.lh[l], P.poly_radius, P,
+                                  exA + (size_t)z * g.lsum + g.loff[l],
+                                  exB + (size_t)z * g.lsum + g.loff[l], nullptr, smem_f);
+}
+
+__global__ void __launch_bounds__(PNT) k_polyexp_debug(Geom g, DevParams P, const float* img,
+                                                       float* planes) {
+    extern __shared__ float smem_f[];
+    ImageSrc src{img, g.W, g.H};
+    polyexp_tile<ImageSrc, true>(src, g.W, g.H, P.poly_radius, P, nullptr, nullptr, planes, smem_f);
+}
+
+// ------------------------------------------------------------------ pyramid
+constexpr int QX = 32, QY = 8, QNT = 256;
+
+__device__ __forceinline__ void bl_index(double s, int n, int& i0, int& i1, double& f) {
+    // bilinear() index rule (flow.hpp:157-168)
+    s = s < 0.0 ? 0.0 : (s > (double)(n - 1) ? (double)(n - 1) : s);
+    const int lim = n - 2 >= 0 ? n - 2 : 0;
+    i0 = min((int)s, lim);
+    i1 = min(i0 + 1, n - 1);
+    f = s - i0;
+}
+
+template <typename Src>
+__device__ __forceinline__ void pyr_tile(const Src& src, int w, int h, int tw, int th,
+                                         const float* kblur, float* out, float* smem, int rwmax,
+                                         int rhmax) {
+    const int ox0 = blockIdx.x * QX, oy0 = blockIdx.y * QY;
+    const double sx = (double)w / tw, sy = (double)h / th;
+    int xa, xb, ya, yb, t0, t1;
+    double f;
+    bl_index((ox0 + 0.5) * sx - 0.5, w, xa, t1, f);
+    bl_index((min(ox0 + QX - 1, tw - 1) + 0.5) * sx - 0.5, w, t0, xb, f);
+    bl_index((oy0 + 0.5) * sy - 0.5, h, ya, t1, f);
+    bl_index((min(oy0 + QY - 1, th - 1) + 0.5) * sy - 0.5, h, t0, yb, f);
+    const int RW = xb - xa + 1, RH = yb - ya + 1;
+    if (RW > rwmax || RH > rhmax) __trap();
+    const int iw = RW + 6, ih = RH + 6;
+    float* s_in = smem;             // ih * iw
+    float* s_rb = s_in + ih * iw;   // ih * RW
+    float* s_bl = s_rb + ih * RW;   // RH * RW
+    for (int i = threadIdx.x; i < ih * iw; i += QNT) {
+        const int yy = i / iw, xx = i - yy * iw;
+        s_in[i] = src.at(xa - 3 + xx, ya - 3 + yy);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < ih * RW; i += QNT) {
+        const int yy = i / RW, xx = i - yy * RW;
+        const float* row = s_in + yy * iw + xx;
+        float acc = 0.f;
+        for (int t = 0; t < 7; ++t) acc += kblur[t] * row[t];
+        s_rb[i] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < RH * RW; i += QNT) {
+        const int yy = i / RW, xx = i - yy * RW;
+        float acc = 0.f;
+        for (int t = 0; t < 7; ++t) acc += kblur[t] * s_rb[(yy + t) * RW + xx];
+        s_bl[i] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < QX * QY; i += QNT) {
+        const int yy = i / QX, xx = i - yy * QX;
+        const int x = ox0 + xx, y = oy0 + yy;
+        if (x >= tw || y >= th) continue;
+        int x0, x1, y0, y1;
+        double fx, fy;
+        bl_index((x + 0.5) * sx - 0.5, w, x0, x1, fx);
+        bl_index((y + 0.5) * sy - 0.5, h, y0, y1, fy);
+        const float* r0 = s_bl + (y0 - ya) * RW;
+        const float* r1 = s_bl + (y1 - ya) * RW;
+        const float ffx = (float)fx, ffy = (float)fy;
+        const float top = r0[x0 - xa] * (1.f - ffx) + r0[x1 - xa] * ffx;
+        const float bot = r1[x0 - xa] * (1.f - ffx) + r1[x1 - xa] * ffx;
+        out[(size_t)y * tw + x] = top * (1.f - ffy) + bot * ffy;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T* den, float* pyr,
+                                                    int rwmax, int rhmax) {
+    extern __shared__ float smem_f[];
+    const int slot = blockIdx.z;
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, 1.0 / g.maxval};
+    pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)slot * (g.lsum - g.loff[1]),
+             smem_f, rwmax, rhmax);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(QNT) k_pyr0_shifted(Geom g, DevParams P, const T* den,
+                                                      const int* next, const PairInfo* info,
+                                                      float* pyr, int rwmax, int rhmax) {
+    extern __shared__ float smem_f[];
+    const int p = blockIdx.z;
+    const PairInfo I = info[p];
+    if (!I.shifted) return;
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, 1.0 / g.maxval};
+    pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)p * (g.lsum - g.loff[1]),
+             smem_f, rwmax, rhmax);
+}
+
+__global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, float* pyr,
+                                                   const PairInfo* info, int rwmax, int rhmax) {
+    // level l -> l+1, l >= 1
+    extern __shared__ float smem_f[];
+    const int z = blockIdx.z;
+    if (info && !info[z].shifted) return;
+    float* base = pyr + (size_t)z * (g.lsum - g.loff[1]);
+    ImageSrc src{base + (g.loff[l] - g.loff[1]), g.lw[l], g.lh[l]};
+    pyr_tile(src, g.lw[l], g.lh[l], g.lw[l + 1], g.lh[l + 1], P.blur,
+             base + (g.loff[l + 1] - g.loff[1]), smem_f, rwmax, rhmax);
+}
+
+// ------------------------------------------------------------------ flow iteration
+constexpr int FX = 32, FY = 32, FNT = 256;
+
+struct IterArgs {
+    int l;        // level
+    int mode;     // 0 zero prior, 1 prior from flow_in (same level), 2 upsample flow_in (level l+1)
+    const float2* flow_in;
+    float2* flow_out;
+};
+
+__device__ __forceinline__ double bilinear_d(const float2* p, int comp, int w, int h, double x,
+                                             double y) {
+    int x0, x1, y0, y1;
+    double fx, fy;
+    bl_index(x, w, x0, x1, fx);
+    bl_index(y, h, y0, y1, fy);
+    const float2 a = p[(size_t)y0 * w + x0], b = p[(size_t)y0 * w + x1];
+    const float2 c = p[(size_t)y1 * w + x0], d = p[(size_t)y1 * w + x1];
+    const double va = comp ? a.y : a.x, vb = comp ? b.y : b.x;
+    const double vc = comp ? c.y : c.x, vd = comp ? d.y : d.x;
+    const double top = va * (1 - fx) + vb * fx;
+    const double bot = vc * (1 - fx) + vd * fx;
+    return top * (1 - fy) + bot * fy;
+}
+
+__device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, size_t pair_off,
+                                           int x, int y) {
+    if (a.mode == 0) return make_float2(0.f, 0.f);
+    const int w = g.lw[a.l];
+    if (a.mode == 1) return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * w + x];
+    // upscale the coarser estimate (flow.hpp:318-337)
+    const int cw = g.lw[a.l + 1], ch = g.lh[a.l + 1];
+    const double fx = (double)w / cw, fy = (double)g.lh[a.l] / ch;
+    const double sx = (x + 0.5) / fx - 0.5, sy = (y + 0.5) / fy - 0.5;
+    const float2* c = a.flow_in + pair_off + g.loff[a.l + 1];
+    return make_float2((float)(bilinear_d(c, 0, cw, ch, sx, sy) * fx),
+                       (float)(bilinear_d(c, 1, cw, ch, sx, sy) * fy));
+}
+
+__global__ void __launch_bounds__(FNT) k_flow_iter(Geom g, int R, IterArgs a,
+                                                   const float4* __restrict__ exA_f,
+                                                   const float* __restrict__ exB_f,
+                                                   const float4* __restrict__ exA_p,
+                                                   const float* __restrict__ exB_p,
+                                                   const int* __restrict__ prev,
+                                                   const int* __restrict__ next,
+                                                   const PairInfo* __restrict__ info) {
+    extern __shared__ float smem_f[];
+    const int p = blockIdx.z;
+    const int l = a.l;
+    const int w = g.lw[l], h = g.lh[l];
+    const int x0 = blockIdx.x * FX, y0 = blockIdx.y * FY;
+    const int HW = FX + 2 * R, HH = FY + 2 * R;
+    const size_t plane = (size_t)HW * HH;
+    float* G = smem_f;                 // 5 * HH * HW
+    float* V = G + 5 * plane;          // 5 * FY * HW
+    const size_t pair_off = (size_t)p * g.lsum;
+    const size_t lo = g.loff[l];
+    const float4* pA = exA_f + (size_t)prev[p] * g.lsum + lo;
+    const float* pB = exB_f + (size_t)prev[p] * g.lsum + lo;
+    const bool sh = info[p].shifted != 0;
+    const float4* nA = (sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo;
+    const float* nB = (sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo;
+
+    // phase 1: normal-equation products over tile + halo (flow.hpp:212-232)
+    for (int i = threadIdx.x; i < (int)plane; i += FNT) {
+        const int hy = i / HW, hx = i - hy * HW;
+        const int gx = x0 - R + hx, gy = y0 - R + hy;
+        float g11 = 0.f, g12 = 0.f, g22 = 0.f, h1 = 0.f, h2 = 0.f;
+        if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+            const float2 pr = prior_at(g, a, pair_off, gx, gy);
+            const float du = pr.x, dv = pr.y;
+            int xa, xb, ya, yb;
+            double fxd, fyd;
+            bl_index(gx + (double)du, w, xa, xb, fxd);
+            bl_index(gy + (double)dv, h, ya, yb, fyd);
+            const float fx = (float)fxd, fy = (float)fyd;
+            const float4 q00 = __ldg(nA + (size_t)ya * w + xa), q01 = __ldg(nA + (size_t)ya * w + xb);
+            const float4 q10 = __ldg(nA + (size_t)yb * w + xa), q11 = __ldg(nA + (size_t)yb * w + xb);
+            const float b00 = __ldg(nB + (size_t)ya * w + xa), b01 = __ldg(nB + (size_t)ya * w + xb);
+            const float b10 = __ldg(nB + (size_t)yb * w + xa), b11 = __ldg(nB + (size_t)yb * w + xb);
+            const float ofx = 1.f - fx, ofy = 1.f - fy;
+#define BL(c) ((q00.c * ofx + q01.c * fx) * ofy + (q10.c * ofx + q11.c * fx) * fy)
+            const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
+#undef BL
+            const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
+            const size_t o = (size_t)gy * w + gx;
+            const float4 pa = __ldg(pA + o);
+            const float pb = __ldg(pB + o);
+            const float a11 = 0.5f * (pa.x + na11);
+            const float a12 = 0.5f * (pa.y + na12);
+            const float a22 = 0.5f * (pa.z + na22);
+            const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
+            const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
+            g11 = a11 * a11 + a12 * a12;
+            g12 = (a11 + a22) * a12;
+            g22 = a12 * a12 + a22 * a22;
+            h1 = a11 * db1 + a12 * db2;
+            h2 = a12 * db1 + a22 * db2;
+        }
+        G[i] = g11;
+        G[plane + i] = g12;
+        G[2 * plane + i] = g22;
+        G[3 * plane + i] = h1;
+        G[4 * plane + i] = h2;
+    }
+    __syncthreads();
+    // phase 2: vertical window sums (out-of-image products are zero; divisor applied later)
+    for (int t = threadIdx.x; t < 5 * HW; t += FNT) {
+        const int c = t / HW, hx = t - c * HW;
+        const float* col = G + c * plane + hx;
+        float* vo = V + (size_t)c * FY * HW + hx;
+        float acc = 0.f;
+        for (int k = 0; k < 2 * R; ++k) acc += col[k * HW];
+        for (int ty = 0; ty < FY; ++ty) {
+            acc += col[(ty + 2 * R) * HW];
+            vo[ty * HW] = acc;
+            acc -= col[ty * HW];
+        }
+    }
+    __syncthreads();
+    // phase 3: horizontal window sums into G (reused as S[5][FY][FX])
+    for (int t = threadIdx.x; t < 5 * FY; t += FNT) {
+        const int c = t / FY, ty = t - c * FY;
+        const float* row = V + (size_t)c * FY * HW + ty * HW;
+        float* so = G + (size_t)c * FY * FX + ty * FX;
+        float acc = 0.f;
+        for (int k = 0; k < 2 * R; ++k) acc += row[k];
+        for (int tx = 0; tx < FX; ++tx) {
+            acc += row[tx + 2 * R];
+            so[tx] = acc;
+            acc -= row[tx];
+        }
+    }
+    __syncthreads();
+    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253)
+    float2* out = a.flow_out + pair_off + lo;
+    for (int i = threadIdx.x; i < FX * FY; i += FNT) {
+        const int ty = i / FX, tx = i - ty * FX;
+        const int x = x0 + tx, y = y0 + ty;
+        if (x >= w || y >= h) continue;
+        const int cx = min(w - 1, x + R) - max(0, x - R) + 1;
+        const int cy = min(h - 1, y + R) - max(0, y - R) + 1;
+        const double inv = 1.0 / (double)(cx * cy);
+        const double g11 = G[i] * inv, g12 = G[FX * FY + i] * inv, g22 = G[2 * FX * FY + i] * inv;
+        const double h1 = G[3 * FX * FY + i] * inv, h2 = G[4 * FX * FY + i] * inv;
+        const double det = g11 * g22 - g12 * g12;
+        const double frob2 = g11 * g11 + 2.0 * g12 * g12 + g22 * g22;
+        float2 r;
+        if (!(det > 1e-9 * frob2)) {
+            r = prior_at(g, a, pair_off, x, y);
+        } else {
+            r.x = (float)((g22 * h1 - g12 * h2) / det);
+            r.y = (float)((-g12 * h1 + g11 * h2) / det);
+        }
+        out[(size_t)y * w + x] = r;
+    }
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    if (bytes > 48 * 1024)
+        FROI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+}
+
+size_t polyexp_smem(int r) { return sizeof(float) * ((PY + 2 * r) * (PX + 2 * r) + 3 * (PY + 2 * r) * PX); }
+
+void pyr_bounds(const Geom& g, int l, int& rwmax, int& rhmax) {
+    const double sx = (double)g.lw[l] / g.lw[l + 1], sy = (double)g.lh[l] / g.lh[l + 1];
+    rwmax = (int)(QX * sx) + 4;
+    rhmax = (int)(QY * sy) + 4;
+}
+size_t pyr_smem(int rwmax, int rhmax) {
+    return sizeof(float) * ((rhmax + 6) * (rwmax + 6) + (rhmax + 6) * rwmax + rhmax * rwmax);
+}
+
+}  // namespace
+
+void launch_expand_frames(const Geom& g, const DevParams& P, const FlowBuffers& b, int n_slots,
+                          cudaStream_t s) {
+    if (n_slots <= 0) return;
+    const size_t pe = polyexp_smem(P.poly_radius);
+    // level 0 expansion straight from the denoised frame
+    {
+        dim3 grid(cdiv(g.W, PX), cdiv(g.H, PY), n_slots);
+        if (g.sample_bytes == 1) {
+            set_smem(k_polyexp_frame<uint8_t>, pe);
+            k_polyexp_frame<uint8_t><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, b.exA_f, b.exB_f);
+        } else {
+            set_smem(k_polyexp_frame<uint16_t>, pe);
+            k_polyexp_frame<uint16_t><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, b.exA_f, b.exB_f);
+        }
+        FROI_LAUNCH_CHECK();
+    }
+    for (int l = 0; l + 1 < g.L; ++l) {
+        int rwmax, rhmax;
+        pyr_bounds(g, l, rwmax, rhmax);
+        const size_t ps = pyr_smem(rwmax, rhmax);
+        dim3 grid(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_slots);
+        if (l == 0) {
+            if (g.sample_bytes == 1) {
+                set_smem(k_pyr0_frame<uint8_t>, ps);
+                k_pyr0_frame<uint8_t><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, b.pyr_f, rwmax, rhmax);
+            } else {
+                set_smem(k_pyr0_frame<uint16_t>, ps);
+                k_pyr0_frame<uint16_t><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, b.pyr_f, rwmax, rhmax);
+            }
+        } else {
+            set_smem(k_pyr_level, ps);
+            k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_f, nullptr, rwmax, rhmax);
+        }
+        FROI_LAUNCH_CHECK();
+        set_smem(k_polyexp_level, pe);
+        dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_slots);
+        k_polyexp_level<<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_f, g.lsum - g.loff[1], nullptr,
+                                            b.exA_f, b.exB_f);
+        FROI_LAUNCH_CHECK();
+    }
+}
+
+void launch_expand_shifted(const Geom& g, const DevParams& P, const FlowBuffers& b,
+                           const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
+    if (n_pairs <= 0) return;
+    const size_t pe = polyexp_smem(P.poly_radius);
+    {
+        dim3 grid(cdiv(g.W, PX), cdiv(g.H, PY), n_pairs);
+        if (g.sample_bytes == 1) {
+            set_smem(k_polyexp_shifted<uint8_t>, pe);
+            k_polyexp_shifted<uint8_t><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, d_next, d_info, b.exA_p, b.exB_p);
+        } else {
+            set_smem(k_polyexp_shifted<uint16_t>, pe);
+            k_polyexp_shifted<uint16_t><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, d_next, d_info, b.exA_p, b.exB_p);
+        }
+        FROI_LAUNCH_CHECK();
+    }
+    for (int l = 0; l + 1 < g.L; ++l) {
+        int rwmax, rhmax;
+        pyr_bounds(g, l, rwmax, rhmax);
+        const size_t ps = pyr_smem(rwmax, rhmax);
+        dim3 grid(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_pairs);
+        if (l == 0) {
+            if (g.sample_bytes == 1) {
+                set_smem(k_pyr0_shifted<uint8_t>, ps);
+                k_pyr0_shifted<uint8_t><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
+            } else {
+                set_smem(k_pyr0_shifted<uint16_t>, ps);
+                k_pyr0_shifted<uint16_t><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
+            }
+        } else {
+            set_smem(k_pyr_level, ps);
+            k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_p, d_info, rwmax, rhmax);
+        }
+        FROI_LAUNCH_CHECK();
+        set_smem(k_polyexp_level, pe);
+        dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_pairs);
+        k_polyexp_level<<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_p, g.lsum - g.loff[1], d_info,
+                                            b.exA_p, b.exB_p);
+        FROI_LAUNCH_CHECK();
+    }
+}
+
+int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const int* d_prev,
+                const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
+    if (n_pairs <= 0) return 0;
+    const int R = P.window_radius;
+    const size_t smem = sizeof(float) * (5 * (size_t)(FX + 2 * R) * (FY + 2 * R) + 5 * (size_t)FY * (FX + 2 * R));
+    set_smem(k_flow_iter, smem);
+    float2* buf[2] = {b.flow0, b.flow1};
+    int cur = 0;
+    for (int l = g.L - 1; l >= 0; --l) {
+        for (int it = 0; it < P.iterations; ++it) {
+            IterArgs a;
+            a.l = l;
+            a.mode = it > 0 ? 1 : (l == g.L - 1 ? 0 : 2);
+            a.flow_in = buf[cur];
+            a.flow_out = buf[1 - cur];
+            dim3 grid(cdiv(g.lw[l], FX), cdiv(g.lh[l], FY), n_pairs);
+            k_flow_iter<<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
+                                                d_prev, d_next, d_info);
+            FROI_LAUNCH_CHECK();
+            cur = 1 - cur;
+        }
+    }
+    return cur;
+}
+
+void launch_expand_image(const Geom& g, const DevParams& P, const float* d_img, float* d_planes,
+                         cudaStream_t s) {
+    const size_t pe = polyexp_smem(P.poly_radius);
+    set_smem(k_polyexp_debug, pe);
+    k_polyexp_debug<<<dim3(cdiv(g.W, PX), cdiv(g.H, PY), 1), PNT, pe, s>>>(g, P, d_img, d_planes);
+    FROI_LAUNCH_CHECK();
+}
+
+}  // namespace froi

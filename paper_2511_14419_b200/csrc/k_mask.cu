@@ -1,0 +1,924 @@
+// k_mask.cu — mask stage (roi.hpp:47-246, registration.hpp:111-121), bit-exact given the flow.
+//
+// Per pair, on the level-0 flow (registered coordinates) and the raw frame t:
+//   saliency   S = w*N(|flow|) + (1.0-w)*N(|grad I|) recomputed on the fly wherever needed:
+//              |flow| is glibc hypotf (float), |grad I| the restated glibc hypot of central
+//              differences of apply_shift(raw, s)/maxval, N the 1st/99th-percentile clamp.
+//   selection  exact order statistics by MSD radix select on the IEEE bit patterns (11-bit
+//              digits, integer histograms, no float atomics): the four percentiles in one set of
+//              passes, then the round(t*n)-th largest saliency; a pass also records min/max of the
+//              still-matching keys so tied groups finish early.
+//   threshold  S > boundary plus ties admitted in row-major order (per-chunk tie counts, an
+//              exclusive scan, then warp-ballot ranks), written as 32-bit packed words.
+//   cleanup    open(r_o) then close(r_c) on packed words in shared memory (square windows,
+//              shrinking at the borders), then 8-connected CCL: tile-local union-find in shared
+//              memory, boundary merge with atomicMin union-find in global memory, area sums at
+//              the roots, area filter (min_area).
+//   output     unshift (zero fill) fused with the area filter into PBM-layout bytes
+//              (MSB first, row stride ceil(W/8)), plus the pixel count and component count.
+#include "kernels.cuh"
+
+namespace froi {
+namespace {
+
+// ------------------------------------------------------------------ per-pixel sources
+template <typename T>
+struct PairPix {
+    const float2* flow;
+    const T* raw;
+    int W, H, dx, dy;
+    double inv_maxval;
+    int grad_src;
+
+    __device__ __forceinline__ double fmag(int x, int y) const {
+        const float2 f = flow[(size_t)y * W + x];
+        return (double)hypotf_glibc(f.x, f.y);
+    }
+    // normalize_frame(apply_shift(raw, s)) at clamped coordinates
+    __device__ __forceinline__ double img(int x, int y) const {
+        const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
+        const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
+        return dmul((double)raw[(size_t)sy * W + sx], inv_maxval);
+    }
+    // gradient_magnitude (roi.hpp:65-74)
+    __device__ __forceinline__ double grad(int x, int y) const {
+        double gx, gy;
+        if (grad_src == 0) {
+            gx = dmul(0.5, dsub(img(x + 1, y), img(x - 1, y)));
+            gy = dmul(0.5, dsub(img(x, y + 1), img(x, y - 1)));
+        } else {
+            gx = dmul(0.5, dsub(fmag(min(x + 1, W - 1), y), fmag(max(x - 1, 0), y)));
+            gy = dmul(0.5, dsub(fmag(x, min(y + 1, H - 1)), fmag(x, max(y - 1, 0))));
+        }
+        return hypot_glibc(gx, gy);
+    }
+};
+
+__device__ __forceinline__ double normalize(double v, double lo, double inv, int zero) {
+    if (zero) return 0.0;
+    const double t = dmul(dsub(v, lo), inv);
+    return t < 0.0 ? 0.0 : (1.0 < t ? 1.0 : t);
+}
+
+template <typename T>
+__device__ __forceinline__ double saliency_at(const PairPix<T>& px, const PairInfo& I, double w,
+                                              double w1, int x, int y) {
+    const double nf = normalize(px.fmag(x, y), I.fmag_lo, I.fmag_inv, I.fmag_zero);
+    const double ng = normalize(px.grad(x, y), I.grad_lo, I.grad_inv, I.grad_zero);
+    return dadd(dmul(w, nf), dmul(w1, ng));
+}
+
+template <typename T>
+__device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P,
+                                               const MaskBuffers& b, const PairInfo& I, int p) {
+    PairPix<T> px;
+    px.flow = b.flow + (size_t)p * b.flow_stride;
+    px.raw = (const T*)b.raw[p];
+    px.W = g.W;
+    px.H = g.H;
+    px.dx = I.dx;
+    px.dy = I.dy;
+    px.inv_maxval = 1.0 / (double)g.maxval;
+    px.grad_src = P.gradient_source;
+    return px;
+}
+
+// ------------------------------------------------------------------ radix select
+constexpr int SNT = 512;
+
+__device__ __forceinline__ void sel_digit(int bits_done, int& shift, int& width) {
+    width = min(kSelBits, 64 - bits_done);
+    shift = 64 - bits_done - width;
+}
+
+__device__ __forceinline__ bool sel_match(unsigned long long key, const SelState& s) {
+    return s.bits_done == 0 || (key >> (64 - s.bits_done)) == (s.prefix >> (64 - s.bits_done));
+}
+
+// PHASE 0: queries 0,1 on |flow|, 2,3 on |grad|.  PHASE 1: query 0 on S (or on b.map).
+template <typename T, int PHASE>
+__global__ void __launch_bounds__(SNT) k_sel_pass(Geom g, DevParams P, MaskBuffers b,
+                                                  const double* map) {
+    __shared__ unsigned int hist[kMaxQueries][kSelBins];
+    __shared__ SelState st[kMaxQueries];
+    __shared__ unsigned long long smn[kMaxQueries], smx[kMaxQueries];
+    __shared__ int any_active;
+    const int p = blockIdx.y;
+    const int nq = PHASE == 0 ? 4 : 1;
+    if (threadIdx.x < nq) {
+        st[threadIdx.x] = b.sel[p * kMaxQueries + threadIdx.x];
+        smn[threadIdx.x] = ~0ull;
+        smx[threadIdx.x] = 0ull;
+    }
+    if (threadIdx.x == 0) any_active = 0;
+    __syncthreads();
+    if (threadIdx.x == 0)
+        for (int q = 0; q < nq; ++q) any_active |= !st[q].done;
+    for (int i = threadIdx.x; i < nq * kSelBins; i += SNT) (&hist[0][0])[i] = 0;
+    __syncthreads();
+    if (!any_active) return;
+    const PairInfo I = b.info[p];
+    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
+    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    bool act[kMaxQueries];
+    int sh[kMaxQueries], wd[kMaxQueries];
+    unsigned long long lmn[kMaxQueries], lmx[kMaxQueries];
+    for (int q = 0; q < nq; ++q) {
+        act[q] = !st[q].done;
+        sel_digit(st[q].bits_done, sh[q], wd[q]);
+        lmn[q] = ~0ull;
+        lmx[q] = 0ull;
+    }
+    const bool need_f = PHASE == 0 && (act[0] || act[1]);
+    const bool need_g = PHASE == 0 && (act[2] || act[3]);
+    const long long n = (long long)g.W * g.H;
+    const long long per = cdiv<long long>(n, gridDim.x);
+    const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+    for (long long i = i0 + threadIdx.x; i < i1; i += SNT) {
+        const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
+        unsigned long long k0 = 0, k1 = 0;
+        if (PHASE == 0) {
+            if (need_f) k0 = dkey(px.fmag(x, y));
+            if (need_g) k1 = dkey(px.grad(x, y));
+        } else {
+            k0 = dkey(map ? map[i] : saliency_at(px, I, w, w1, x, y));
+        }
+#pragma unroll
+        for (int q = 0; q < nq; ++q) {
+            if (!act[q]) continue;
+            const unsigned long long key = (PHASE == 0 && q >= 2) ? k1 : k0;
+            if (!sel_match(key, st[q])) continue;
+            atomicAdd(&hist[q][(key >> sh[q]) & ((1u << wd[q]) - 1)], 1u);
+            lmn[q] = min(lmn[q], key);
+            lmx[q] = max(lmx[q], key);
+        }
+    }
+    for (int q = 0; q < nq; ++q) {
+        if (!act[q]) continue;
+        unsigned long long a = lmn[q], c = lmx[q];
+        for (int o = 16; o > 0; o >>= 1) {
+            a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
+            c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
+        }
+        if ((threadIdx.x & 31) == 0) {
+            atomicMin(&smn[q], a);
+            atomicMax(&smx[q], c);
+        }
+    }
+    __syncthreads();
+    for (int q = 0; q < nq; ++q) {
+        if (!act[q]) continue;
+        unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
+        for (int i = threadIdx.x; i < kSelBins; i += SNT)
+            if (hist[q][i]) atomicAdd(gh + i, hist[q][i]);
+        if (threadIdx.x == 0) {
+            atomicMin(&b.sel[p * kMaxQueries + q].mn, smn[q]);
+            atomicMax(&b.sel[p * kMaxQueries + q].mx, smx[q]);
+        }
+    }
+}
+
+// One CTA per (pair, query): locate the digit holding the rank, narrow the prefix.
+__global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
+    const int p = blockIdx.x / nq, q = blockIdx.x % nq;
+    SelState* sp = b.sel + p * kMaxQueries + q;
+    __shared__ SelState s;
+    __shared__ unsigned int part[256];
+    if (threadIdx.x == 0) s = *sp;
+    __syncthreads();
+    if (s.done) return;
+    unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
+    constexpr int PER = kSelBins / 256;
+    unsigned int loc[PER];
+    unsigned int tot = 0;
+    for (int j = 0; j < PER; ++j) {
+        loc[j] = gh[threadIdx.x * PER + j];
+        tot += loc[j];
+    }
+    part[threadIdx.x] = tot;
+    __syncthreads();
+    // inclusive scan of per-thread totals (Hillis-Steele)
+    for (int o = 1; o < 256; o <<= 1) {
+        const unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    const unsigned long long before = threadIdx.x ? part[threadIdx.x - 1] : 0ull;
+    const unsigned long long r = s.rank;
+    if (r >= before && r < (unsigned long long)part[threadIdx.x]) {
+        unsigned long long c = before;
+        for (int j = 0; j < PER; ++j) {
+            if (r < c + loc[j]) {
+                const int bin = threadIdx.x * PER + j;
+                int shift, width;
+                sel_digit(s.bits_done, shift, width);
+                SelState n = s;
+                n.prefix = s.prefix | ((unsigned long long)bin << shift);
+                n.rank = r - c;
+                n.count = loc[j];
+                n.bits_done = s.bits_done + width;
+                if (s.mn == s.mx) {  // every prefix match is the same value
+                    n.done = 1;
+                    n.result = s.mn;
+                } else if (n.bits_done >= 64) {
+                    n.done = 1;
+                    n.result = n.prefix;
+                }
+                n.mn = ~0ull;
+                n.mx = 0ull;
+                *sp = n;
+                break;
+            }
+            c += loc[j];
+        }
+    }
+    for (int j = 0; j < PER; ++j) gh[threadIdx.x * PER + j] = 0u;
+}
+
+__global__ void k_sel_init_a(Geom g, MaskBuffers b, unsigned long long ilo, unsigned long long ihi) {
+    const int p = blockIdx.x;
+    if (threadIdx.x < kMaxQueries) {
+        SelState s;
+        s.prefix = 0;
+        s.rank = (threadIdx.x & 1) ? ihi : ilo;
+        s.result = 0;
+        s.mn = ~0ull;
+        s.mx = 0;
+        s.count = 0;
+        s.bits_done = 0;
+        s.done = 0;
+        b.sel[p * kMaxQueries + threadIdx.x] = s;
+    }
+}
+
+// robust_normalize parameters (roi.hpp:47-63), then the threshold query (roi.hpp:114-120).
+__global__ void k_sel_init_b(MaskBuffers b, unsigned long long n, unsigned long long target,
+                             int from_stats) {
+    const int p = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    PairInfo& I = b.info[p];
+    if (from_stats) {
+        const SelState* s = b.sel + p * kMaxQueries;
+        I.fmag_lo = dfromkey(s[0].result);
+        I.fmag_hi = dfromkey(s[1].result);
+        I.grad_lo = dfromkey(s[2].result);
+        I.grad_hi = dfromkey(s[3].result);
+        const double df = dsub(I.fmag_hi, I.fmag_lo), dg = dsub(I.grad_hi, I.grad_lo);
+        I.fmag_zero = !(df > 1e-12);
+        I.grad_zero = !(dg > 1e-12);
+        I.fmag_inv = I.fmag_zero ? 0.0 : ddiv(1.0, df);
+        I.grad_inv = I.grad_zero ? 0.0 : ddiv(1.0, dg);
+    }
+    I.target = target;
+    SelState s;
+    s.prefix = 0;
+    s.rank = n - target;  // (target-1)-th largest == (n-target)-th smallest
+    s.result = 0;
+    s.mn = ~0ull;
+    s.mx = 0;
+    s.count = 0;
+    s.bits_done = 0;
+    s.done = target == 0;
+    b.sel[p * kMaxQueries] = s;
+    for (int q = 1; q < kMaxQueries; ++q) b.sel[p * kMaxQueries + q].done = 1;
+}
+
+// ------------------------------------------------------------------ threshold
+constexpr int TNT = 256;
+constexpr int TROWS = 4;  // rows per tie chunk
+
+__global__ void k_sel_finish_b(MaskBuffers b) {
+    const int p = blockIdx.x;
+    if (threadIdx.x != 0) return;
+    PairInfo& I = b.info[p];
+    const SelState s = b.sel[p * kMaxQueries];
+    if (I.target == 0) {
+        I.thr_mode = 1;
+        I.boundary = 0.0;
+        return;
+    }
+    I.boundary = dfromkey(s.result);
+    I.thr_mode = (I.boundary > 0.0) ? 0 : 2;
+}
+
+template <typename T>
+__device__ __forceinline__ double sal_or_map(const PairPix<T>& px, const PairInfo& I, double w,
+                                             double w1, const double* map, int x, int y, int W) {
+    return map ? map[(size_t)y * W + x] : saliency_at(px, I, w, w1, x, y);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(TNT) k_thr_count(Geom g, DevParams P, MaskBuffers b,
+                                                   const double* map) {
+    const int p = blockIdx.y, chunk = blockIdx.x;
+    const PairInfo I = b.info[p];
+    __shared__ unsigned long long sg, se;
+    if (threadIdx.x == 0) { sg = 0; se = 0; }
+    __syncthreads();
+    if (I.thr_mode != 0) return;
+    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
+    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
+    unsigned int cg = 0, ce = 0;
+    for (int y = y0; y < y1; ++y)
+        for (int x = threadIdx.x; x < g.W; x += TNT) {
+            const double s = sal_or_map(px, I, w, w1, map, x, y, g.W);
+            cg += s > I.boundary;
+            ce += s == I.boundary;
+        }
+    for (int o = 16; o > 0; o >>= 1) {
+        cg += __shfl_xor_sync(0xffffffffu, cg, o);
+        ce += __shfl_xor_sync(0xffffffffu, ce, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        atomicAdd(&sg, (unsigned long long)cg);
+        atomicAdd(&se, (unsigned long long)ce);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const int nch = gridDim.x;
+        b.tie_cnt[((size_t)p * nch + chunk) * 2 + 0] = sg;
+        b.tie_cnt[((size_t)p * nch + chunk) * 2 + 1] = se;
+    }
+}
+
+// Exclusive scan of the per-chunk tie counts; total count above the boundary.
+__global__ void __launch_bounds__(1024) k_thr_scan(MaskBuffers b, int nch) {
+    const int p = blockIdx.x;
+    PairInfo& I = b.info[p];
+    if (I.thr_mode != 0) return;
+    __shared__ unsigned long long sgt[1024], seq[1024];
+    unsigned long long* tc = b.tie_cnt + (size_t)p * nch * 2;
+    const int per = cdiv(nch, 1024);
+    unsigned long long g = 0, e = 0;
+    for (int j = 0; j < per; ++j) {
+        const int c = threadIdx.x * per + j;
+        if (c < nch) {
+            g += tc[c * 2];
+            e += tc[c * 2 + 1];
+        }
+    }
+    sgt[threadIdx.x] = g;
+    seq[threadIdx.x] = e;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {
+        const unsigned long long vg = threadIdx.x >= o ? sgt[threadIdx.x - o] : 0;
+        const unsigned long long ve = threadIdx.x >= o ? seq[threadIdx.x - o] : 0;
+        __syncthreads();
+        sgt[threadIdx.x] += vg;
+        seq[threadIdx.x] += ve;
+        __syncthreads();
+    }
+    unsigned long long run = threadIdx.x ? seq[threadIdx.x - 1] : 0;
+    for (int j = 0; j < per; ++j) {
+        const int c = threadIdx.x * per + j;
+        if (c < nch) {
+            const unsigned long long ce = tc[c * 2 + 1];
+            tc[c * 2 + 1] = run;  // exclusive prefix of ties before this chunk
+            run += ce;
+        }
+    }
+    if (threadIdx.x == 0) {
+        I.count_gt = sgt[1023];
+        I.need = I.target > I.count_gt ? I.target - I.count_gt : 0;
+    }
+}
+
+// Packed thresholded mask, bit x%32 of word (y, x/32); ties admitted in row-major order.
+template <typename T>
+__global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuffers b,
+                                                   const double* map) {
+    const int p = blockIdx.y, chunk = blockIdx.x;
+    const PairInfo I = b.info[p];
+    const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
+    uint32_t* out = b.bits_thr + (size_t)p * g.H * g.WW;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int NW = TNT / 32;
+    __shared__ unsigned int wcnt[NW];
+    __shared__ unsigned long long base;
+    if (I.thr_mode == 1) {
+        for (int i = threadIdx.x; i < (y1 - y0) * g.WW; i += TNT) out[(size_t)y0 * g.WW + i] = 0u;
+        return;
+    }
+    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
+    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    if (threadIdx.x == 0) base = I.thr_mode == 0 ? b.tie_cnt[((size_t)p * gridDim.x + chunk) * 2 + 1] : 0;
+    __syncthreads();
+    const int nwords = (y1 - y0) * g.WW;
+    for (int r0 = 0; r0 < nwords; r0 += NW) {
+        const int wi = r0 + warp;
+        bool gt = false, eq = false;
+        if (wi < nwords) {
+            const int y = y0 + wi / g.WW, x = (wi % g.WW) * 32 + lane;
+            if (x < g.W) {
+                const double s = sal_or_map(px, I, w, w1, map, x, y, g.W);
+                if (I.thr_mode == 0) {
+                    gt = s > I.boundary;
+                    eq = s == I.boundary;
+                } else {
+                    gt = s > 0.0;
+                }
+            }
+        }
+        const unsigned int eqm = __ballot_sync(0xffffffffu, eq);
+        const unsigned int gtm = __ballot_sync(0xffffffffu, gt);
+        if (lane == 0) wcnt[warp] = __popc(eqm);
+        __syncthreads();
+        unsigned long long before = base;
+        for (int k = 0; k < warp; ++k) before += wcnt[k];
+        const unsigned long long rank = before + __popc(eqm & ((1u << lane) - 1u));
+        const bool admit = eq && rank < I.need;
+        const unsigned int word = gtm | __ballot_sync(0xffffffffu, admit);
+        if (lane == 0 && wi < nwords) out[(size_t)y0 * g.WW + wi] = word;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int k = 0; k < NW; ++k) t += wcnt[k];
+            base += t;
+        }
+        __syncthreads();
+    }
+}
+
+// ------------------------------------------------------------------ morphology
+constexpr int MROWS = 32, MNT = 256;
+
+// One separable square op on rows [va, vb) of buffer `in` (rows ya.. in smem), result in `out`.
+__device__ void morph_op(const uint32_t* in, uint32_t* out, uint32_t* tmp, int nrows, int WW,
+                         int W, int H, int ya, int& va, int& vb, int r, bool erode) {
+    if (r <= 0) {
+        for (int i = threadIdx.x; i < nrows * WW; i += MNT) out[i] = in[i];
+        __syncthreads();
+        return;
+    }
+    const uint32_t fill = erode ? 0xffffffffu : 0u;
+    const int tail = W & 31;
+    const uint32_t tail_mask = tail ? ((1u << tail) - 1u) : 0xffffffffu;
+    // horizontal pass: outside-the-row pixels act as `fill` (shrinking windows)
+    for (int i = threadIdx.x; i < nrows * WW; i += MNT) {
+        const int row = i / WW, j = i - row * WW;
+        auto word = [&](int jj) -> uint32_t {
+            if (jj < 0 || jj >= WW) return fill;
+            uint32_t v = in[row * WW + jj];
+            if (jj == WW - 1) v = (v & tail_mask) | (fill & ~tail_mask);
+            return v;
+        };
+        const uint32_t c = word(j), lft = word(j - 1), rgt = word(j + 1);
+        uint32_t acc = c;
+        for (int k = 1; k <= r; ++k) {
+            // pixel x-k: shift left by k bringing bits from the left word; x+k likewise
+            const uint32_t sl = k < 32 ? ((c << k) | (lft >> (32 - k))) : lft;
+            const uint32_t sr = k < 32 ? ((c >> k) | (rgt << (32 - k))) : rgt;
+            acc = erode ? (acc & sl & sr) : (acc | sl | sr);
+        }
+        if (j == WW - 1) acc &= tail_mask;
+        tmp[i] = acc;
+    }
+    __syncthreads();
+    // vertical pass: rows outside the image are skipped (not filled)
+    const int nva = (va == 0) ? 0 : va + r, nvb = (vb == H) ? H : vb - r;
+    for (int i = threadIdx.x; i < nrows * WW; i += MNT) {
+        const int row = i / WW, j = i - row * WW;
+        const int y = ya + row;
+        if (y < nva || y >= nvb) continue;
+        uint32_t acc = erode ? 0xffffffffu : 0u;
+        const int lo = max(0, y - r), hi = min(H - 1, y + r);
+        for (int t = lo; t <= hi; ++t) {
+            const uint32_t v = tmp[(t - ya) * WW + j];
+            acc = erode ? (acc & v) : (acc | v);
+        }
+        out[i] = acc;
+    }
+    va = nva;
+    vb = nvb;
+    __syncthreads();
+}
+
+// morph_close(morph_open(m, ro), rc) (roi.hpp:179-180, 239) on a band of MROWS rows.
+__global__ void __launch_bounds__(MNT) k_morph(Geom g, MaskBuffers b, int ro, int rc) {
+    extern __shared__ uint32_t msm[];
+    const int p = blockIdx.y;
+    const int y0 = blockIdx.x * MROWS;
+    const int halo = 2 * ro + 2 * rc;
+    const int ya = max(0, y0 - halo), yb = min(g.H, y0 + MROWS + halo);
+    const int nrows = yb - ya;
+    uint32_t* A = msm;
+    uint32_t* B = A + nrows * g.WW;
+    uint32_t* Tm = B + nrows * g.WW;
+    const uint32_t* src = b.bits_thr + (size_t)p * g.H * g.WW;
+    for (int i = threadIdx.x; i < nrows * g.WW; i += MNT) A[i] = src[(size_t)ya * g.WW + i];
+    __syncthreads();
+    int va = ya, vb = yb;
+    morph_op(A, B, Tm, nrows, g.WW, g.W, g.H, ya, va, vb, ro, true);   // erode
+    morph_op(B, A, Tm, nrows, g.WW, g.W, g.H, ya, va, vb, ro, false);  // dilate
+    morph_op(A, B, Tm, nrows, g.WW, g.W, g.H, ya, va, vb, rc, false);  // dilate
+    morph_op(B, A, Tm, nrows, g.WW, g.W, g.H, ya, va, vb, rc, true);   // erode
+    uint32_t* dst = b.bits_clean + (size_t)p * g.H * g.WW;
+    const int ye = min(g.H, y0 + MROWS);
+    for (int i = threadIdx.x; i < (ye - y0) * g.WW; i += MNT)
+        dst[(size_t)y0 * g.WW + i] = A[(y0 - ya) * g.WW + i];
+}
+
+// ------------------------------------------------------------------ connected components
+constexpr int CT = 32;  // CCL tile edge
+
+__device__ __forceinline__ int lfind(const int* P, int x) {
+    while (P[x] != x) x = P[x];
+    return x;
+}
+__device__ __forceinline__ void lunite(int* P, int a, int b) {
+    bool done = false;
+    while (!done) {
+        a = lfind(P, a);
+        b = lfind(P, b);
+        if (a < b) {
+            const int old = atomicMin(&P[b], a);
+            done = old == b;
+            b = old;
+        } else if (b < a) {
+            const int old = atomicMin(&P[a], b);
+            done = old == a;
+            a = old;
+        } else {
+            done = true;
+        }
+    }
+}
+__device__ __forceinline__ int gfind(int* L, int x) {
+    while (true) {
+        const int p = __ldcg(L + x);
+        if (p == x) return x;
+        x = p;
+    }
+}
+__device__ __forceinline__ void gunite(int* L, int a, int b) {
+    bool done = false;
+    while (!done) {
+        a = gfind(L, a);
+        b = gfind(L, b);
+        if (a < b) {
+            const int old = atomicMin(&L[b], a);
+            done = old == b;
+            b = old;
+        } else if (b < a) {
+            const int old = atomicMin(&L[a], b);
+            done = old == a;
+            a = old;
+        } else {
+            done = true;
+        }
+    }
+}
+
+__device__ __forceinline__ bool bit_at(const uint32_t* m, int WW, int x, int y) {
+    return (m[(size_t)y * WW + (x >> 5)] >> (x & 31)) & 1u;
+}
+
+// Tile-local union-find (8-connected, label_components roi.hpp:184-234 semantics).
+__global__ void __launch_bounds__(CT* CT) k_ccl_local(Geom g, MaskBuffers b) {
+    __shared__ int P[CT * CT];
+    __shared__ unsigned int area[CT * CT];
+    const int p = blockIdx.z;
+    const int tx0 = blockIdx.x * CT, ty0 = blockIdx.y * CT;
+    const int x = tx0 + threadIdx.x, y = ty0 + threadIdx.y;
+    const int li = threadIdx.y * CT + threadIdx.x;
+    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
+    const bool in = x < g.W && y < g.H;
+    const bool set = in && bit_at(m, g.WW, x, y);
+    P[li] = set ? li : -1;
+    area[li] = 0;
+    __syncthreads();
+    if (set) {
+        if (threadIdx.x > 0 && P[li - 1] >= 0) lunite(P, li, li - 1);
+        if (threadIdx.y > 0) {
+            if (threadIdx.x > 0 && P[li - CT - 1] >= 0) lunite(P, li, li - CT - 1);
+            if (P[li - CT] >= 0) lunite(P, li, li - CT);
+            if (threadIdx.x < CT - 1 && P[li - CT + 1] >= 0) lunite(P, li, li - CT + 1);
+        }
+    }
+    __syncthreads();
+    int root = -1;
+    if (set) {
+        root = lfind(P, li);
+        atomicAdd(&area[root], 1u);
+    }
+    __syncthreads();
+    const size_t base = (size_t)p * g.W * g.H;
+    const bool is_root = set && root == li;
+    if (set) {
+        const int gr = (ty0 + root / CT) * g.W + tx0 + root % CT;
+        b.labels[base + (size_t)y * g.W + x] = gr;
+        if (is_root) {
+            b.area_local[base + (size_t)y * g.W + x] = area[li];
+            b.area_total[base + (size_t)y * g.W + x] = 0u;
+        }
+    }
+    const unsigned int rb = __ballot_sync(0xffffffffu, is_root);
+    if (threadIdx.x == 0 && y < g.H) b.bits_root[(size_t)p * g.H * g.WW + (size_t)y * g.WW + (tx0 >> 5)] = rb;
+}
+
+// Union across tile borders: each CTA handles the left column, top row and right column of
+// one tile and links every set pixel to its W, NW, N, NE neighbours in other tiles.
+__global__ void __launch_bounds__(3 * CT) k_ccl_merge(Geom g, MaskBuffers b) {
+    const int p = blockIdx.z;
+    const int tx0 = blockIdx.x * CT, ty0 = blockIdx.y * CT;
+    const int t = threadIdx.x;
+    int x, y;
+    if (t < CT) { x = tx0; y = ty0 + t; }
+    else if (t < 2 * CT) { x = tx0 + t - CT; y = ty0; }
+    else { x = tx0 + CT - 1; y = ty0 + t - 2 * CT; }
+    if (x >= g.W || y >= g.H) return;
+    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
+    if (!bit_at(m, g.WW, x, y)) return;
+    int* L = b.labels + (size_t)p * g.W * g.H;
+    const int me = y * g.W + x;
+    const int nx[4] = {x - 1, x - 1, x, x + 1};
+    const int ny[4] = {y, y - 1, y - 1, y - 1};
+    for (int k = 0; k < 4; ++k) {
+        if (nx[k] < 0 || nx[k] >= g.W || ny[k] < 0) continue;
+        if ((nx[k] / CT) == (x / CT) && (ny[k] / CT) == (y / CT)) continue;
+        if (!bit_at(m, g.WW, nx[k], ny[k])) continue;
+        gunite(L, me, ny[k] * g.W + nx[k]);
+    }
+}
+
+// Area of every component accumulated at its global root (a local root too).
+__global__ void __launch_bounds__(256) k_ccl_area(Geom g, MaskBuffers b) {
+    const int p = blockIdx.y;
+    const long long n = (long long)g.H * g.WW;
+    const uint32_t* rb = b.bits_root + (size_t)p * n;
+    int* L = b.labels + (size_t)p * g.W * g.H;
+    for (long long wi = blockIdx.x * 256LL + threadIdx.x; wi < n; wi += (long long)gridDim.x * 256) {
+        uint32_t bits = rb[wi];
+        const int y = (int)(wi / g.WW), xb = (int)(wi % g.WW) * 32;
+        while (bits) {
+            const int k = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int me = y * g.W + xb + k;
+            const int r = gfind(L, me);
+            atomicAdd(&b.area_total[(size_t)p * g.W * g.H + r], b.area_local[(size_t)p * g.W * g.H + me]);
+        }
+    }
+}
+
+// Path compression to the global root; counts components that survive min_area.
+__global__ void __launch_bounds__(256) k_ccl_compress(Geom g, DevParams P, MaskBuffers b) {
+    const int p = blockIdx.y;
+    const long long n = (long long)g.H * g.WW;
+    const uint32_t* m = b.bits_clean + (size_t)p * n;
+    const uint32_t* rb = b.bits_root + (size_t)p * n;
+    int* L = b.labels + (size_t)p * g.W * g.H;
+    unsigned int comps = 0;
+    for (long long wi = blockIdx.x * 256LL + threadIdx.x; wi < n; wi += (long long)gridDim.x * 256) {
+        uint32_t bits = m[wi];
+        const uint32_t roots = rb[wi];
+        const int y = (int)(wi / g.WW), xb = (int)(wi % g.WW) * 32;
+        while (bits) {
+            const int k = __ffs(bits) - 1;
+            bits &= bits - 1;
+            const int me = y * g.W + xb + k;
+            const int r = gfind(L, me);
+            if (((roots >> k) & 1u) && r == me &&
+                b.area_total[(size_t)p * g.W * g.H + me] >= (unsigned)P.min_area)
+                ++comps;
+            L[me] = r;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
+    if ((threadIdx.x & 31) == 0 && comps) atomicAdd(&b.info[p].components, comps);
+}
+
+// Area filter + unshift_mask + PBM packing + pixel count.  One thread per PBM byte.
+__global__ void __launch_bounds__(256) k_output(Geom g, DevParams P, MaskBuffers b, int use_ccl) {
+    const int p = blockIdx.y;
+    const PairInfo I = b.info[p];
+    const long long nbytes = (long long)g.H * g.SB;
+    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
+    const int* L = b.labels + (size_t)p * g.W * g.H;
+    const unsigned int* A = b.area_total + (size_t)p * g.W * g.H;
+    uint8_t* out = b.out_pbm + (size_t)b.out_index[p] * nbytes;
+    unsigned int cnt = 0;
+    for (long long bi = blockIdx.x * 256LL + threadIdx.x; bi < nbytes; bi += (long long)gridDim.x * 256) {
+        const int y = (int)(bi / g.SB), x0 = (int)(bi % g.SB) * 8;
+        unsigned int byte = 0;
+        const int sy = y - I.dy;
+        if (sy >= 0 && sy < g.H) {
+            for (int k = 0; k < 8; ++k) {
+                const int x = x0 + k, sx = x - I.dx;
+                if (x >= g.W || sx < 0 || sx >= g.W) continue;
+                if (!bit_at(m, g.WW, sx, sy)) continue;
+                if (use_ccl && A[L[sy * g.W + sx]] < (unsigned)P.min_area) continue;
+                byte |= 0x80u >> k;
+            }
+        }
+        out[bi] = (uint8_t)byte;
+        cnt += __popc(byte);
+    }
+    for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&b.info[p].mask_count, cnt);
+}
+
+__global__ void k_reset_counts(MaskBuffers b) {
+    b.info[blockIdx.x].mask_count = 0;
+    b.info[blockIdx.x].components = 0;
+}
+
+__global__ void k_unpack_masks(const uint8_t* pbm, uint8_t* bytes, int W, int H, int SB, int n) {
+    const long long per = (long long)W * H;
+    const long long total = per * n;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+        const long long k = i / per, r = i - k * per;
+        const int y = (int)(r / W), x = (int)(r - (long long)y * W);
+        bytes[i] = (pbm[k * H * SB + (long long)y * SB + (x >> 3)] >> (7 - (x & 7))) & 1u;
+    }
+}
+
+__global__ void k_pack_words(const uint8_t* bytes, uint32_t* words, int W, int H, int WW) {
+    const long long n = (long long)H * WW;
+    for (long long wi = blockIdx.x * 256LL + threadIdx.x; wi < n; wi += (long long)gridDim.x * 256) {
+        const int y = (int)(wi / WW), xb = (int)(wi % WW) * 32;
+        uint32_t v = 0;
+        for (int k = 0; k < 32; ++k) {
+            const int x = xb + k;
+            if (x < W && bytes[(size_t)y * W + x]) v |= 1u << k;
+        }
+        words[wi] = v;
+    }
+}
+
+__global__ void k_ensemble(const uint8_t* in, uint8_t* out, long long per, int n, int k) {
+    const long long total = per * n;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < total; i += (long long)gridDim.x * 256) {
+        const int t = (int)(i / per);
+        const long long o = i - (long long)t * per;
+        uint8_t v = 0;
+        const int lo = max(0, t - k), hi = min(n - 1, t + k);
+        for (int j = lo; j <= hi; ++j) v |= in[(long long)j * per + o];
+        out[i] = v;
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_saliency_map(Geom g, DevParams P, MaskBuffers b,
+                                                      double* out) {
+    const PairInfo I = b.info[0];
+    const PairPix<T> px = make_pix<T>(g, P, b, I, 0);
+    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    const long long n = (long long)g.W * g.H;
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
+        const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
+        out[i] = saliency_at(px, I, w, w1, x, y);
+    }
+}
+
+int grid_for(long long work, int per_block) {
+    long long b = cdiv<long long>(work, per_block);
+    if (b > 148 * 16) b = 148 * 16;
+    return (int)(b < 1 ? 1 : b);
+}
+
+template <typename T>
+void run_selects(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
+                 const double* map, bool phase_a, cudaStream_t s, uint64_t* launches) {
+    const long long n = (long long)g.W * g.H;
+    int bpp = (int)cdiv<long long>(148 * 4, n_pairs);
+    bpp = max(1, min(bpp, (int)cdiv<long long>(n, 4096)));
+    const int passes = cdiv(64, kSelBits);
+    if (phase_a) {
+        k_sel_init_a<<<n_pairs, 32, 0, s>>>(g, b, (unsigned long long)(0.01 * (double)(n - 1)),
+                                           (unsigned long long)(0.99 * (double)(n - 1)));
+        FROI_LAUNCH_CHECK();
+        ++*launches;
+        for (int it = 0; it < passes; ++it) {
+            k_sel_pass<T, 0><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, nullptr);
+            k_sel_scan<<<n_pairs * 4, 256, 0, s>>>(b, 4);
+            FROI_LAUNCH_CHECK();
+            *launches += 2;
+        }
+    }
+    const unsigned long long target = (unsigned long long)llround(P.roi_threshold * (double)n);
+    k_sel_init_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, target, phase_a ? 1 : 0);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
+    for (int it = 0; it < passes; ++it) {
+        k_sel_pass<T, 1><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, map);
+        k_sel_scan<<<n_pairs, 256, 0, s>>>(b, 1);
+        FROI_LAUNCH_CHECK();
+        *launches += 2;
+    }
+    k_sel_finish_b<<<n_pairs, 32, 0, s>>>(b);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
+}
+
+template <typename T>
+void run_threshold(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
+                   const double* map, cudaStream_t s, uint64_t* launches) {
+    const int nch = cdiv(g.H, TROWS);
+    k_thr_count<T><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    k_thr_scan<<<n_pairs, 1024, 0, s>>>(b, nch);
+    k_thr_write<T><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    FROI_LAUNCH_CHECK();
+    *launches += 3;
+}
+
+void run_cleanup_output(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
+                        int ro, int rc, int min_area, cudaStream_t s, uint64_t* launches) {
+    DevParams Q = P;
+    Q.min_area = min_area;
+    k_reset_counts<<<n_pairs, 1, 0, s>>>(b);
+    const int halo = 2 * ro + 2 * rc;
+    const size_t smem = sizeof(uint32_t) * 3 * (size_t)(MROWS + 2 * halo) * g.WW;
+    if (smem > 48 * 1024)
+        FROI_CUDA(cudaFuncSetAttribute(k_morph, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_morph<<<dim3(cdiv(g.H, MROWS), n_pairs), MNT, smem, s>>>(g, b, ro, rc);
+    FROI_LAUNCH_CHECK();
+    *launches += 2;
+    const bool use_ccl = min_area > 1;
+    if (use_ccl) {
+        dim3 tiles(cdiv(g.W, CT), cdiv(g.H, CT), n_pairs);
+        k_ccl_local<<<tiles, dim3(CT, CT), 0, s>>>(g, b);
+        k_ccl_merge<<<tiles, 3 * CT, 0, s>>>(g, b);
+        const int gw = grid_for((long long)g.H * g.WW, 256);
+        k_ccl_area<<<dim3(gw, n_pairs), 256, 0, s>>>(g, b);
+        k_ccl_compress<<<dim3(gw, n_pairs), 256, 0, s>>>(g, Q, b);
+        FROI_LAUNCH_CHECK();
+        *launches += 4;
+    }
+    k_output<<<dim3(grid_for((long long)g.H * g.SB, 256), n_pairs), 256, 0, s>>>(g, Q, b, use_ccl ? 1 : 0);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
+}
+
+}  // namespace
+
+void launch_mask_stage(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
+                       cudaStream_t s, uint64_t* launches) {
+    if (n_pairs <= 0) return;
+    if (g.sample_bytes == 1) {
+        run_selects<uint8_t>(g, P, b, n_pairs, nullptr, true, s, launches);
+        run_threshold<uint8_t>(g, P, b, n_pairs, nullptr, s, launches);
+    } else {
+        run_selects<uint16_t>(g, P, b, n_pairs, nullptr, true, s, launches);
+        run_threshold<uint16_t>(g, P, b, n_pairs, nullptr, s, launches);
+    }
+    run_cleanup_output(g, P, b, n_pairs, P.open_radius, P.close_radius, P.min_area, s, launches);
+}
+
+void launch_saliency_map(const Geom& g, const DevParams& P, const MaskBuffers& b, double* d_out,
+                         cudaStream_t s) {
+    uint64_t l = 0;
+    const int gr = grid_for((long long)g.W * g.H, 256);
+    if (g.sample_bytes == 1) {
+        run_selects<uint8_t>(g, P, b, 1, nullptr, true, s, &l);
+        k_saliency_map<uint8_t><<<gr, 256, 0, s>>>(g, P, b, d_out);
+    } else {
+        run_selects<uint16_t>(g, P, b, 1, nullptr, true, s, &l);
+        k_saliency_map<uint16_t><<<gr, 256, 0, s>>>(g, P, b, d_out);
+    }
+    FROI_LAUNCH_CHECK();
+}
+
+void launch_threshold_from_map(const Geom& g, const DevParams& P, const MaskBuffers& b,
+                               const double* d_map, double threshold, cudaStream_t s) {
+    uint64_t l = 0;
+    DevParams Q = P;
+    Q.roi_threshold = threshold;
+    if (g.sample_bytes == 1) {
+        run_selects<uint8_t>(g, Q, b, 1, d_map, false, s, &l);
+        run_threshold<uint8_t>(g, Q, b, 1, d_map, s, &l);
+    } else {
+        run_selects<uint16_t>(g, Q, b, 1, d_map, false, s, &l);
+        run_threshold<uint16_t>(g, Q, b, 1, d_map, s, &l);
+    }
+}
+
+void launch_cleanup_only(const Geom& g, const DevParams& P, const MaskBuffers& b,
+                         int open_radius, int close_radius, int min_area, cudaStream_t s) {
+    uint64_t l = 0;
+    run_cleanup_output(g, P, b, 1, open_radius, close_radius, min_area, s, &l);
+}
+
+void launch_unpack_pbm(const Geom& g, const uint8_t* d_pbm, uint8_t* d_bytes, int n_masks,
+                       cudaStream_t s) {
+    if (n_masks <= 0) return;
+    k_unpack_masks<<<grid_for((long long)g.W * g.H * n_masks, 256), 256, 0, s>>>(d_pbm, d_bytes, g.W,
+                                                                               g.H, g.SB, n_masks);
+    FROI_LAUNCH_CHECK();
+}
+
+void launch_pack_bytes_to_words(const Geom& g, const uint8_t* d_bytes, uint32_t* d_words,
+                                cudaStream_t s) {
+    k_pack_words<<<grid_for((long long)g.H * g.WW, 256), 256, 0, s>>>(d_bytes, d_words, g.W, g.H, g.WW);
+    FROI_LAUNCH_CHECK();
+}
+
+void launch_ensemble(const Geom& g, const uint8_t* d_in, uint8_t* d_out, int n, int k,
+                     cudaStream_t s) {
+    const long long per = (long long)g.H * g.SB;
+    k_ensemble<<<grid_for(per * n, 256), 256, 0, s>>>(d_in, d_out, per, n, k);
+    FROI_LAUNCH_CHECK();
+}
+
+}  // namespace froi

@@ -1,0 +1,161 @@
+// kernels.cuh — device data layout and kernel launchers of the RoI-extraction path.
+//
+// HBM layout (one context, W x H frames, sample type T = uint8 or uint16):
+//   frame slots  f in [0, Fcap): raw T[H*W] (ingest), den T[H*W], spec double2[ph*pw]
+//                (full complex spectrum of the windowed denoised frame), pyramid float
+//                images of levels >= 1, expansion planes per level: exA float4 {a11,a12,a22,bx}
+//                and exB float {by}, concatenated over levels (offset loff[l], lsum total px).
+//   pair slots   p in [0, Pcap): PairInfo, inverse-row columns double2[(2M+1)*ph], surface
+//                double[(2M+1)^2], shifted-next pyramid/expansions (only when the applied
+//                shift is non-zero), flow ping-pong float2[lsum] x 2, mask-stage scratch.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace froi {
+
+constexpr int kMaxLevels = 16;
+constexpr int kSelBits = 11;  // radix-select digit width
+constexpr int kSelBins = 1 << kSelBits;
+constexpr int kMaxQueries = 4;
+
+struct Geom {
+    int W, H, depth, maxval;
+    int sample_bytes;   // 1 or 2
+    int L;              // effective pyramid levels
+    int lw[kMaxLevels], lh[kMaxLevels];
+    long long loff[kMaxLevels];  // pixel offset of level l inside a per-frame pyramid buffer
+    long long lsum;              // total pixels over levels
+    int pw, ph, log2pw, log2ph;  // FFT grid (next_pow2)
+    int WW;                      // 32-bit words per packed mask row
+    int SB;                      // bytes per PBM row
+};
+
+struct PairInfo {
+    int est_dx, est_dy;
+    double confidence;
+    int dx, dy;  // applied (0,0 after the 1.5 fallback)
+    int shifted;
+    int pad0;
+    // mask stage
+    double fmag_lo, fmag_hi, grad_lo, grad_hi;
+    double fmag_inv, grad_inv;
+    int fmag_zero, grad_zero;  // robust_normalize degenerate -> all zeros
+    double boundary;
+    unsigned long long target;
+    unsigned long long count_gt;
+    unsigned long long need;
+    int thr_mode;  // 0 normal, 1 empty (target 0), 2 positive-only (boundary <= 0)
+    unsigned int mask_count;
+    unsigned int components;
+    unsigned int pad1;
+};
+
+struct SelState {
+    unsigned long long prefix;
+    unsigned long long rank;
+    unsigned long long result;
+    unsigned long long mn, mx;  // min / max key of prefix matches in the last pass
+    unsigned long long count;   // prefix matches after the last pass
+    int bits_done;
+    int done;
+};
+
+// Per-batch device tables.
+struct BatchTables {
+    const void** frame_raw;  // [Fcap] raw frame pointer of each frame slot
+    int* pair_prev;          // [Pcap] frame slot of frame t-1
+    int* pair_next;          // [Pcap] frame slot of frame t
+};
+
+// Device parameter block (constant per context).
+struct DevParams {
+    // denoise
+    int denoise_enabled, median_radius, bilateral_radius;
+    // flow
+    int window_radius, iterations, poly_radius;
+    float poly_moments[7];  // inv_m20, inv_m22, i00, i01, i11, i12, unused
+    float g0[16], g1[16], g2[16];  // polynomial-expansion kernels (radius <= 7)
+    float blur[7];                 // pyramid Gaussian (sigma 1, radius 3)
+    double pyr_scale;
+    // roi
+    double roi_threshold, flow_weight;
+    int min_area, open_radius, close_radius, gradient_source, max_shift;
+};
+
+// ---------------------------------------------------------------- launchers
+// k_denoise.cu
+void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw, void* d_den,
+                    unsigned long long* d_sums, const double* d_spatial, const double* d_lut,
+                    int n_slots, cudaStream_t s);
+
+// k_register.cu
+void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long long* d_sums,
+                        const double* d_wx, const double* d_wy, const double2* d_tw_row,
+                        const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s);
+void launch_register_pairs(const Geom& g, const DevParams& p, const double2* d_spec,
+                           const int* d_prev, const int* d_next, const double2* d_itw_row,
+                           const double2* d_itw_col, double2* d_cols, double* d_surf,
+                           PairInfo* d_info, int n_pairs, cudaStream_t s);
+
+// k_flow.cu
+struct FlowBuffers {
+    const void* den;     // frame-slot denoised frames (T)
+    float* pyr_f;        // frame-slot pyramid images, levels >= 1 ([slot][lsum - W*H])
+    float4* exA_f;       // frame-slot expansions [slot][lsum]
+    float* exB_f;
+    float* pyr_p;        // pair-slot shifted pyramids
+    float4* exA_p;       // pair-slot shifted expansions
+    float* exB_p;
+    float2* flow0;       // pair-slot flow ping-pong [pair][lsum]
+    float2* flow1;
+};
+void launch_expand_frames(const Geom& g, const DevParams& p, const FlowBuffers& b, int n_slots,
+                          cudaStream_t s);
+void launch_expand_shifted(const Geom& g, const DevParams& p, const FlowBuffers& b,
+                           const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s);
+// Runs all levels and iterations; returns which buffer holds the level-0 flow (0 or 1).
+int launch_flow(const Geom& g, const DevParams& p, const FlowBuffers& b, const int* d_prev,
+                const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s);
+// Debug tap: expansion (6 planes incl. c) of a float image of level-0 geometry.
+void launch_expand_image(const Geom& g, const DevParams& p, const float* d_img, float* d_planes,
+                         cudaStream_t s);
+
+// k_mask.cu
+struct MaskBuffers {
+    const float2* flow;           // [pair][lsum] level-0 flow at offset 0
+    long long flow_stride;        // elements between pairs
+    const void** raw;             // [pair] raw frame t pointer (T)
+    SelState* sel;                // [pair][kMaxQueries]
+    unsigned int* hist;           // [pair][kMaxQueries][kSelBins]
+    unsigned long long* tie_cnt;  // [pair][chunks][2]
+    uint32_t* bits_thr;           // [pair][H*WW] thresholded (registered)
+    uint32_t* bits_clean;         // [pair][H*WW] after open/close (registered)
+    uint32_t* bits_root;          // [pair][H*WW] local-root marks
+    int* labels;                  // [pair][H*W]
+    unsigned int* area_local;     // [pair][H*W]
+    unsigned int* area_total;     // [pair][H*W]
+    uint8_t* out_pbm;             // output PBM masks
+    const long long* out_index;   // [pair] mask index in out_pbm (frame index)
+    PairInfo* info;
+};
+void launch_mask_stage(const Geom& g, const DevParams& p, const MaskBuffers& b, int n_pairs,
+                       cudaStream_t s, uint64_t* launches);
+// Debug taps on the same kernels.
+void launch_saliency_map(const Geom& g, const DevParams& p, const MaskBuffers& b, double* d_out,
+                         cudaStream_t s);
+void launch_threshold_from_map(const Geom& g, const DevParams& p, const MaskBuffers& b,
+                               const double* d_map, double threshold, cudaStream_t s);
+void launch_cleanup_only(const Geom& g, const DevParams& p, const MaskBuffers& b,
+                         int open_radius, int close_radius, int min_area, cudaStream_t s);
+void launch_unpack_pbm(const Geom& g, const uint8_t* d_pbm, uint8_t* d_bytes, int n_masks,
+                       cudaStream_t s);
+void launch_pack_bytes_to_words(const Geom& g, const uint8_t* d_bytes, uint32_t* d_words,
+                                cudaStream_t s);
+void launch_ensemble(const Geom& g, const uint8_t* d_in, uint8_t* d_out, int n, int k,
+                     cudaStream_t s);
+
+}  // namespace froi

@@ -1,0 +1,1214 @@
+// runtime.cu — per-GPU context, batch scheduler and the C ABI (include/froi/froi.h).
+//
+// A context owns one CUDA stream and fixed device arenas sized for `Pcap` adjacent pairs per
+// batch (frame slots: raw, denoised, spectrum, pyramid + expansions; pair slots: registration
+// scratch, shifted expansions, flow ping-pong, mask-stage scratch).  extract_* calls split the
+// work into batches of pairs (pairs of one well are independent once their frames are denoised,
+// roi.hpp:325), launch every stage for the whole batch at once (grid.z = slot), and gather
+// packed masks + per-pair stats.  Host tables are double-buffered in pinned memory.
+//
+// Host-side constants that must match the reference bit for bit (bilateral LUT and spatial
+// weights, Hann windows, FFT twiddle recurrence) are computed here with the same libm calls and
+// expression order as the reference; this file is compiled with -ffp-contract=off.
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/froi/froi.h"
+#include "kernels.cuh"
+
+using namespace froi;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int status, const std::string& msg) {
+    g_last_error = msg;
+    return status;
+}
+
+#define ABI_TRY try {
+#define ABI_CATCH                                   \
+    }                                               \
+    catch (const froi::Error& e) {                  \
+        return fail(e.status, e.what());            \
+    }                                               \
+    catch (const std::bad_alloc&) {                 \
+        return fail(3, "host allocation failed");   \
+    }                                               \
+    catch (const std::exception& e) {               \
+        return fail(3, e.what());                   \
+    }                                               \
+    return 0;
+
+constexpr double kPi = 3.14159265358979323846;
+
+int next_pow2(int n) {
+    int p = 1;
+    while (p < n) p <<= 1;
+    return p;
+}
+int ilog2(int n) {
+    int l = 0;
+    while ((1 << l) < n) ++l;
+    return l;
+}
+
+std::string validate(const froi_params* p) {
+    if (!p) return "params must not be null";
+    // RoiParams::validate (roi.hpp:29-37)
+    if (!(p->roi_threshold > 0.0 && p->roi_threshold < 1.0)) return "roi: roi_threshold must be in (0,1)";
+    if (p->flow_weight < 0.0 || p->flow_weight > 1.0) return "roi: flow_weight must be in [0,1]";
+    if (p->adjacent_factor < 0) return "roi: adjacent_factor must be >= 0";
+    if (p->min_area < 0) return "roi: min_area must be >= 0";
+    if (p->open_radius < 0 || p->close_radius < 0) return "roi: radii must be >= 0";
+    // FlowParams::validate (flow.hpp:20-29)
+    if (p->pyramid_levels < 1) return "flow: pyramid_levels must be >= 1";
+    if (!(p->pyramid_scale > 0.0 && p->pyramid_scale < 1.0)) return "flow: pyramid_scale must be in (0,1)";
+    if (p->window_size < 3 || p->window_size % 2 == 0) return "flow: window_size must be odd and >= 3";
+    if (p->poly_n < 3 || p->poly_n % 2 == 0) return "flow: poly_n must be odd and >= 3";
+    if (p->iterations < 1) return "flow: iterations must be >= 1";
+    if (p->poly_sigma <= 0.0) return "flow: poly_sigma must be > 0";
+    // DenoiseParams::validate (denoise.hpp:18-23)
+    if (p->median_radius < 1 || p->bilateral_radius < 1) return "denoise: radii must be >= 1";
+    if (p->bilateral_sigma_spatial <= 0 || p->bilateral_sigma_range <= 0) return "denoise: sigmas must be > 0";
+    if (p->gradient_source != FROI_GRADIENT_IMAGE && p->gradient_source != FROI_GRADIENT_FLOW)
+        return "roi: unknown gradient_source";
+    // limits of this implementation's shared-memory tiles
+    if (p->poly_n > 15) return "flow: poly_n > 15 is not supported by the GPU kernels";
+    if (p->window_size > 61) return "flow: window_size > 61 is not supported by the GPU kernels";
+    if (p->median_radius > 3) return "denoise: median_radius > 3 is not supported by the GPU kernels";
+    if (p->bilateral_radius > 7) return "denoise: bilateral_radius > 7 is not supported by the GPU kernels";
+    if (p->open_radius > 31 || p->close_radius > 31) return "roi: radii > 31 are not supported by the GPU kernels";
+    return "";
+}
+
+Geom make_geom(const froi_params& p, int W, int H, int depth) {
+    Geom g{};
+    g.W = W;
+    g.H = H;
+    g.depth = depth;
+    g.maxval = (1 << depth) - 1;
+    g.sample_bytes = depth == 8 ? 1 : 2;
+    // build_pyramid (flow.hpp:289-298)
+    g.lw[0] = W;
+    g.lh[0] = H;
+    g.L = 1;
+    for (int l = 1; l < p.pyramid_levels && l < kMaxLevels; ++l) {
+        const int tw = int(g.lw[l - 1] * p.pyramid_scale), th = int(g.lh[l - 1] * p.pyramid_scale);
+        if (tw < 32 || th < 32) break;
+        g.lw[l] = tw;
+        g.lh[l] = th;
+        g.L = l + 1;
+    }
+    long long off = 0;
+    for (int l = 0; l < g.L; ++l) {
+        g.loff[l] = off;
+        off += (long long)g.lw[l] * g.lh[l];
+        off = (off + 3) & ~3LL;  // keep float4 rows of the next level 16-byte aligned
+    }
+    if (g.L == 1) g.loff[1] = off;
+    else for (int l = g.L; l < kMaxLevels; ++l) g.loff[l] = off;
+    g.lsum = off;
+    g.pw = next_pow2(W);
+    g.ph = next_pow2(H);
+    g.log2pw = ilog2(g.pw);
+    g.log2ph = ilog2(g.ph);
+    g.WW = (W + 31) / 32;
+    g.SB = (W + 7) / 8;
+    return g;
+}
+
+DevParams make_dev_params(const froi_params& p) {
+    DevParams d{};
+    d.denoise_enabled = p.denoise_enabled ? 1 : 0;
+    d.median_radius = p.median_radius;
+    d.bilateral_radius = p.bilateral_radius;
+    d.window_radius = (p.window_size - 1) / 2;
+    d.iterations = p.iterations;
+    d.poly_radius = (p.poly_n - 1) / 2;
+    // polynomial_expansion kernels and expansion_moments (flow.hpp:92-127), fp64 then float
+    const int r = d.poly_radius;
+    std::vector<double> g0(p.poly_n), g1(p.poly_n), g2(p.poly_n);
+    for (int t = -r; t <= r; ++t) {
+        const double w = std::exp(-double(t) * t / (2.0 * p.poly_sigma * p.poly_sigma));
+        g0[t + r] = w;
+        g1[t + r] = w * t;
+        g2[t + r] = w * t * t;
+    }
+    double s0 = 0, s2 = 0, s4 = 0;
+    for (int t = -r; t <= r; ++t) {
+        const double w = g0[t + r];
+        s0 += w;
+        s2 += w * t * t;
+        s4 += w * t * t * t * t;
+    }
+    const double m00 = s0 * s0, m20 = s2 * s0, m40 = s4 * s0, m22 = s2 * s2;
+    const double det = m00 * (m40 * m40 - m22 * m22) - m20 * (m20 * m40 - m22 * m20) +
+                       m20 * (m20 * m22 - m40 * m20);
+    d.poly_moments[0] = float(1.0 / m20);
+    d.poly_moments[1] = float(1.0 / m22);
+    d.poly_moments[2] = float((m40 * m40 - m22 * m22) / det);
+    d.poly_moments[3] = float((m20 * m22 - m20 * m40) / det);
+    d.poly_moments[4] = float((m00 * m40 - m20 * m20) / det);
+    d.poly_moments[5] = float((m20 * m20 - m00 * m22) / det);
+    for (int i = 0; i < p.poly_n; ++i) {
+        d.g0[i] = float(g0[i]);
+        d.g1[i] = float(g1[i]);
+        d.g2[i] = float(g2[i]);
+    }
+    // gaussian_blur3(., 1.0) (flow.hpp:259-272): radius max(1, ceil(2.5)) = 3
+    double k[7], sum = 0.0;
+    for (int t = -3; t <= 3; ++t) {
+        k[t + 3] = std::exp(-double(t) * t / (2.0 * 1.0 * 1.0));
+        sum += k[t + 3];
+    }
+    for (int i = 0; i < 7; ++i) d.blur[i] = float(k[i] / sum);
+    d.pyr_scale = p.pyramid_scale;
+    d.roi_threshold = p.roi_threshold;
+    d.flow_weight = p.flow_weight;
+    d.min_area = p.min_area;
+    d.open_radius = p.open_radius;
+    d.close_radius = p.close_radius;
+    d.gradient_source = p.gradient_source;
+    d.max_shift = p.max_shift;
+    return d;
+}
+
+// fft_inplace twiddle sequence (fft.hpp:27-37): stage len = 2h stores w_0..w_{h-1} at [h-1, 2h-2]
+std::vector<double2> twiddles(int n, bool inverse) {
+    std::vector<double2> tw(n > 1 ? n - 1 : 1);
+    for (int len = 2; len <= n; len <<= 1) {
+        const double ang = (inverse ? 2.0 : -2.0) * kPi / len;
+        const double wr = std::cos(ang), wi = std::sin(ang);
+        double cr = 1.0, ci = 0.0;
+        for (int k = 0; k < len / 2; ++k) {
+            tw[len / 2 - 1 + k] = make_double2(cr, ci);
+            const double nr = cr * wr - ci * wi;  // std::complex product without FMA
+            const double ni = cr * wi + ci * wr;
+            cr = nr;
+            ci = ni;
+        }
+    }
+    return tw;
+}
+
+template <typename T>
+T* dalloc(size_t count, size_t* total) {
+    void* p = nullptr;
+    const size_t bytes = count * sizeof(T);
+    FROI_CUDA(cudaMalloc(&p, bytes ? bytes : 16));
+    *total += bytes;
+    return (T*)p;
+}
+
+}  // namespace
+
+struct froi_ctx {
+    int device = 0;
+    froi_params params{};
+    Geom g{};
+    DevParams dp{};
+    cudaStream_t stream = nullptr;
+    int Pcap = 0, Fcap = 0;
+    size_t frame_bytes = 0;  // W*H*sample_bytes
+    size_t device_bytes = 0;
+    // constants
+    double *d_spatial = nullptr, *d_lut = nullptr, *d_wx = nullptr, *d_wy = nullptr;
+    double2 *d_tw_row = nullptr, *d_tw_col = nullptr, *d_itw_row = nullptr, *d_itw_col = nullptr;
+    // frame slots
+    uint8_t* d_raw = nullptr;
+    uint8_t* d_den = nullptr;
+    unsigned long long* d_sums = nullptr;
+    double2* d_spec = nullptr;
+    float* d_pyr_f = nullptr;
+    float4* d_exA_f = nullptr;
+    float* d_exB_f = nullptr;
+    // pair slots
+    PairInfo* d_info = nullptr;
+    double2* d_cols = nullptr;
+    double* d_surf = nullptr;
+    float* d_pyr_p = nullptr;
+    float4* d_exA_p = nullptr;
+    float* d_exB_p = nullptr;
+    float2* d_flow0 = nullptr;
+    float2* d_flow1 = nullptr;
+    SelState* d_sel = nullptr;
+    unsigned int* d_hist = nullptr;
+    unsigned long long* d_tie = nullptr;
+    uint32_t *d_bits_thr = nullptr, *d_bits_clean = nullptr, *d_bits_root = nullptr;
+    int* d_labels = nullptr;
+    unsigned int *d_area_local = nullptr, *d_area_total = nullptr;
+    uint8_t* d_out_batch = nullptr;  // [Pcap] PBM masks for taps
+    // tables (device + pinned host, double-buffered)
+    const void** d_frame_raw[2] = {nullptr, nullptr};
+    int* d_prev[2] = {nullptr, nullptr};
+    int* d_next[2] = {nullptr, nullptr};
+    const void** d_pair_raw[2] = {nullptr, nullptr};
+    long long* d_out_index[2] = {nullptr, nullptr};
+    void* h_tables[2] = {nullptr, nullptr};
+    size_t tables_bytes = 0;
+    cudaEvent_t tables_free[2] = {nullptr, nullptr};
+    int tb = 0;
+    PairInfo* h_info = nullptr;  // pinned [Pcap]
+    // sequence-level output buffer (PBM) for host outputs
+    uint8_t* d_seq_out = nullptr;
+    size_t seq_out_cap = 0;
+    uint8_t* d_seq_tmp = nullptr;
+    size_t seq_tmp_cap = 0;
+    // streaming state
+    int stream_wells = 0;
+    std::vector<long long> stream_next_t;  // next frame index per well
+    uint8_t* d_carry = nullptr;            // last raw frame per well
+    size_t carry_cap = 0;
+    // timing
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    froi_stage_times times{};
+    uint64_t launches = 0;
+
+    MaskBuffers mask_buffers(int tb_) const {
+        MaskBuffers b;
+        b.flow = nullptr;
+        b.flow_stride = g.lsum;
+        b.raw = d_pair_raw[tb_];
+        b.sel = d_sel;
+        b.hist = d_hist;
+        b.tie_cnt = d_tie;
+        b.bits_thr = d_bits_thr;
+        b.bits_clean = d_bits_clean;
+        b.bits_root = d_bits_root;
+        b.labels = d_labels;
+        b.area_local = d_area_local;
+        b.area_total = d_area_total;
+        b.out_pbm = d_out_batch;
+        b.out_index = d_out_index[tb_];
+        b.info = d_info;
+        return b;
+    }
+    FlowBuffers flow_buffers() const {
+        FlowBuffers b;
+        b.den = d_den;
+        b.pyr_f = d_pyr_f;
+        b.exA_f = d_exA_f;
+        b.exB_f = d_exB_f;
+        b.pyr_p = d_pyr_p;
+        b.exA_p = d_exA_p;
+        b.exB_p = d_exB_p;
+        b.flow0 = d_flow0;
+        b.flow1 = d_flow1;
+        return b;
+    }
+};
+
+namespace {
+
+void ctx_alloc(froi_ctx* c) {
+    const Geom& g = c->g;
+    const size_t px = (size_t)g.W * g.H;
+    const int P = c->Pcap, F = c->Fcap;
+    size_t& t = c->device_bytes;
+    c->frame_bytes = px * g.sample_bytes;
+    // constants
+    const froi_params& p = c->params;
+    {
+        const int br = p.bilateral_radius, side = 2 * br + 1;
+        std::vector<double> spatial((size_t)side * side);
+        for (int dy = -br; dy <= br; ++dy)
+            for (int dx = -br; dx <= br; ++dx)
+                spatial[(dy + br) * side + (dx + br)] =
+                    std::exp(-(dx * dx + dy * dy) / (2.0 * p.bilateral_sigma_spatial * p.bilateral_sigma_spatial));
+        std::vector<double> lut((size_t)g.maxval + 1);
+        for (int d = 0; d <= g.maxval; ++d) {
+            const double tt = double(d) / g.maxval;
+            lut[d] = std::exp(-tt * tt / (2.0 * p.bilateral_sigma_range * p.bilateral_sigma_range));
+        }
+        std::vector<double> wx(g.pw), wy(g.ph);
+        for (int x = 0; x < g.pw; ++x) wx[x] = 0.5 - 0.5 * std::cos(2.0 * kPi * x / g.pw);
+        for (int y = 0; y < g.ph; ++y) wy[y] = 0.5 - 0.5 * std::cos(2.0 * kPi * y / g.ph);
+        c->d_spatial = dalloc<double>(spatial.size(), &t);
+        c->d_lut = dalloc<double>(lut.size(), &t);
+        c->d_wx = dalloc<double>(wx.size(), &t);
+        c->d_wy = dalloc<double>(wy.size(), &t);
+        FROI_CUDA(cudaMemcpy(c->d_spatial, spatial.data(), spatial.size() * 8, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_lut, lut.data(), lut.size() * 8, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_wx, wx.data(), wx.size() * 8, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_wy, wy.data(), wy.size() * 8, cudaMemcpyHostToDevice));
+        const auto twr = twiddles(g.pw, false), twc = twiddles(g.ph, false);
+        const auto itwr = twiddles(g.pw, true), itwc = twiddles(g.ph, true);
+        c->d_tw_row = dalloc<double2>(twr.size(), &t);
+        c->d_tw_col = dalloc<double2>(twc.size(), &t);
+        c->d_itw_row = dalloc<double2>(itwr.size(), &t);
+        c->d_itw_col = dalloc<double2>(itwc.size(), &t);
+        FROI_CUDA(cudaMemcpy(c->d_tw_row, twr.data(), twr.size() * 16, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_tw_col, twc.data(), twc.size() * 16, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_itw_row, itwr.data(), itwr.size() * 16, cudaMemcpyHostToDevice));
+        FROI_CUDA(cudaMemcpy(c->d_itw_col, itwc.data(), itwc.size() * 16, cudaMemcpyHostToDevice));
+    }
+    const size_t pyr_px = (size_t)(g.lsum - g.loff[1]);
+    c->d_raw = dalloc<uint8_t>(c->frame_bytes * F, &t);
+    c->d_den = dalloc<uint8_t>(c->frame_bytes * F, &t);
+    c->d_sums = dalloc<unsigned long long>(F, &t);
+    c->d_spec = dalloc<double2>((size_t)g.pw * g.ph * F, &t);
+    c->d_pyr_f = dalloc<float>(pyr_px * F, &t);
+    c->d_exA_f = dalloc<float4>((size_t)g.lsum * F, &t);
+    c->d_exB_f = dalloc<float>((size_t)g.lsum * F, &t);
+    const int M = p.max_shift, nc = 2 * M + 1;
+    c->d_info = dalloc<PairInfo>(P, &t);
+    c->d_cols = dalloc<double2>((size_t)nc * g.ph * P, &t);
+    c->d_surf = dalloc<double>((size_t)nc * nc * P, &t);
+    c->d_pyr_p = dalloc<float>(pyr_px * P, &t);
+    c->d_exA_p = dalloc<float4>((size_t)g.lsum * P, &t);
+    c->d_exB_p = dalloc<float>((size_t)g.lsum * P, &t);
+    c->d_flow0 = dalloc<float2>((size_t)g.lsum * P, &t);
+    c->d_flow1 = dalloc<float2>((size_t)g.lsum * P, &t);
+    c->d_sel = dalloc<SelState>((size_t)kMaxQueries * P, &t);
+    c->d_hist = dalloc<unsigned int>((size_t)kMaxQueries * kSelBins * P, &t);
+    FROI_CUDA(cudaMemset(c->d_hist, 0, sizeof(unsigned int) * (size_t)kMaxQueries * kSelBins * P));
+    const int nch = (g.H + 3) / 4;
+    c->d_tie = dalloc<unsigned long long>((size_t)nch * 2 * P, &t);
+    const size_t words = (size_t)g.H * g.WW;
+    c->d_bits_thr = dalloc<uint32_t>(words * P, &t);
+    c->d_bits_clean = dalloc<uint32_t>(words * P, &t);
+    c->d_bits_root = dalloc<uint32_t>(words * P, &t);
+    c->d_labels = dalloc<int>(px * P, &t);
+    c->d_area_local = dalloc<unsigned int>(px * P, &t);
+    c->d_area_total = dalloc<unsigned int>(px * P, &t);
+    c->d_out_batch = dalloc<uint8_t>((size_t)g.H * g.SB * P, &t);
+    // tables
+    c->tables_bytes = sizeof(void*) * F + sizeof(int) * 2 * P + sizeof(void*) * P + sizeof(long long) * P;
+    for (int i = 0; i < 2; ++i) {
+        c->d_frame_raw[i] = (const void**)dalloc<void*>(F, &t);
+        c->d_prev[i] = dalloc<int>(P, &t);
+        c->d_next[i] = dalloc<int>(P, &t);
+        c->d_pair_raw[i] = (const void**)dalloc<void*>(P, &t);
+        c->d_out_index[i] = dalloc<long long>(P, &t);
+        FROI_CUDA(cudaMallocHost(&c->h_tables[i], c->tables_bytes));
+        FROI_CUDA(cudaEventCreateWithFlags(&c->tables_free[i], cudaEventDisableTiming));
+    }
+    FROI_CUDA(cudaMallocHost((void**)&c->h_info, sizeof(PairInfo) * P));
+    for (int i = 0; i < 4; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
+}
+
+void ctx_free(froi_ctx* c) {
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    void* ptrs[] = {c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
+                    c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
+                    c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
+                    c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_tie, c->d_bits_thr,
+                    c->d_bits_clean, c->d_bits_root, c->d_labels, c->d_area_local, c->d_area_total,
+                    c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry};
+    for (void* p : ptrs)
+        if (p) cudaFree(p);
+    for (int i = 0; i < 2; ++i) {
+        if (c->d_frame_raw[i]) cudaFree((void*)c->d_frame_raw[i]);
+        if (c->d_prev[i]) cudaFree(c->d_prev[i]);
+        if (c->d_next[i]) cudaFree(c->d_next[i]);
+        if (c->d_pair_raw[i]) cudaFree((void*)c->d_pair_raw[i]);
+        if (c->d_out_index[i]) cudaFree(c->d_out_index[i]);
+        if (c->h_tables[i]) cudaFreeHost(c->h_tables[i]);
+        if (c->tables_free[i]) cudaEventDestroy(c->tables_free[i]);
+    }
+    if (c->h_info) cudaFreeHost(c->h_info);
+    for (auto& e : c->ev)
+        if (e) cudaEventDestroy(e);
+    if (c->stream) cudaStreamDestroy(c->stream);
+}
+
+void ensure_seq_out(froi_ctx* c, size_t bytes) {
+    if (c->seq_out_cap >= bytes) return;
+    if (c->d_seq_out) FROI_CUDA(cudaFree(c->d_seq_out));
+    c->d_seq_out = nullptr;
+    FROI_CUDA(cudaMalloc(&c->d_seq_out, bytes));
+    c->seq_out_cap = bytes;
+}
+void ensure_seq_tmp(froi_ctx* c, size_t bytes) {
+    if (c->seq_tmp_cap >= bytes) return;
+    if (c->d_seq_tmp) FROI_CUDA(cudaFree(c->d_seq_tmp));
+    c->d_seq_tmp = nullptr;
+    FROI_CUDA(cudaMalloc(&c->d_seq_tmp, bytes));
+    c->seq_tmp_cap = bytes;
+}
+
+// One adjacent pair (frame a -> frame b) of some well.
+struct PairJob {
+    const void* raw_prev;  // device pointers to the raw frames
+    const void* raw_next;
+    long long out_index;   // mask index in the output PBM buffer
+    long long stats_index; // index into the caller's stats array (or -1)
+};
+
+// Runs one batch of pairs.  frames given on device; output PBM masks written at out_index of
+// out_pbm (device).  h_stats_pairs receives the PairInfo of each pair (host, after sync).
+void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t j1, uint8_t* out_pbm,
+               std::vector<PairInfo>& infos) {
+    const Geom& g = c->g;
+    const int n_pairs = int(j1 - j0);
+    cudaStream_t s = c->stream;
+    const int tb = c->tb;
+    c->tb ^= 1;
+    FROI_CUDA(cudaEventSynchronize(c->tables_free[tb]));
+    // frame slots: unique raw pointers in order
+    uint8_t* h = (uint8_t*)c->h_tables[tb];
+    const void** h_frame_raw = (const void**)h;
+    int* h_prev = (int*)(h + sizeof(void*) * c->Fcap);
+    int* h_next = h_prev + c->Pcap;
+    const void** h_pair_raw = (const void**)(h_next + c->Pcap);
+    long long* h_out = (long long*)(h_pair_raw + c->Pcap);
+    int nf = 0;
+    const void* last = nullptr;
+    for (size_t j = j0; j < j1; ++j) {
+        const PairJob& J = jobs[j];
+        int sp, sn;
+        if (nf > 0 && last == J.raw_prev) sp = nf - 1;
+        else {
+            h_frame_raw[nf] = J.raw_prev;
+            sp = nf++;
+        }
+        h_frame_raw[nf] = J.raw_next;
+        sn = nf++;
+        last = J.raw_next;
+        const int p = int(j - j0);
+        h_prev[p] = sp;
+        h_next[p] = sn;
+        h_pair_raw[p] = J.raw_next;
+        h_out[p] = J.out_index;
+    }
+    FROI_CUDA(cudaMemcpyAsync(c->d_frame_raw[tb], h_frame_raw, sizeof(void*) * nf, cudaMemcpyHostToDevice, s));
+    FROI_CUDA(cudaMemcpyAsync(c->d_prev[tb], h_prev, sizeof(int) * n_pairs, cudaMemcpyHostToDevice, s));
+    FROI_CUDA(cudaMemcpyAsync(c->d_next[tb], h_next, sizeof(int) * n_pairs, cudaMemcpyHostToDevice, s));
+    FROI_CUDA(cudaMemcpyAsync(c->d_pair_raw[tb], h_pair_raw, sizeof(void*) * n_pairs, cudaMemcpyHostToDevice, s));
+    FROI_CUDA(cudaMemcpyAsync(c->d_out_index[tb], h_out, sizeof(long long) * n_pairs, cudaMemcpyHostToDevice, s));
+    FROI_CUDA(cudaEventRecord(c->tables_free[tb], s));
+
+    FROI_CUDA(cudaEventRecord(c->ev[0], s));
+    FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
+    launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->d_spatial, c->d_lut, nf, s);
+    FROI_CUDA(cudaEventRecord(c->ev[1], s));
+    launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
+    FlowBuffers fb = c->flow_buffers();
+    launch_expand_frames(g, c->dp, fb, nf, s);
+    launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
+                          c->d_cols, c->d_surf, c->d_info, n_pairs, s);
+    launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+    const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
+    FROI_CUDA(cudaEventRecord(c->ev[2], s));
+    MaskBuffers mb = c->mask_buffers(tb);
+    mb.flow = cur ? c->d_flow1 : c->d_flow0;
+    mb.out_pbm = out_pbm;
+    launch_mask_stage(g, c->dp, mb, n_pairs, s, &c->launches);
+    FROI_CUDA(cudaEventRecord(c->ev[3], s));
+    FROI_CUDA(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(PairInfo) * n_pairs, cudaMemcpyDeviceToHost, s));
+    FROI_CUDA(cudaStreamSynchronize(s));
+    float ms[3];
+    FROI_CUDA(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
+    FROI_CUDA(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
+    FROI_CUDA(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
+    c->times.denoise_ns += (uint64_t)(ms[0] * 1e6);
+    c->times.flow_ns += (uint64_t)(ms[1] * 1e6);
+    c->times.roi_ns += (uint64_t)(ms[2] * 1e6);
+    // launches: denoise 1, fft 2, expand (1 + 2(L-1)) x2, register 3, flow L*iters (+ mask stage)
+    c->launches += 1 + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations;
+    for (int p = 0; p < n_pairs; ++p) infos.push_back(c->h_info[p]);
+}
+
+void fill_stats(const Geom& g, const PairInfo& I, froi_frame_stats* st) {
+    st->dx = I.dx;
+    st->dy = I.dy;
+    st->confidence = I.confidence;
+    st->mask_count = I.mask_count;
+    st->raw_fraction = double(I.mask_count) / double((long long)g.W * g.H);
+    st->components = I.components;
+}
+
+// Ingest host frames (any sample width) into a device buffer of the context's sample type.
+void upload_frames(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, long long n,
+                   uint8_t* dst) {
+    const Geom& g = c->g;
+    const size_t px = (size_t)g.W * g.H;
+    if (sample_bytes == g.sample_bytes && stride == c->frame_bytes) {
+        FROI_CUDA(cudaMemcpyAsync(dst, frames, c->frame_bytes * n, cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
+    if (sample_bytes == g.sample_bytes) {
+        FROI_CUDA(cudaMemcpy2DAsync(dst, c->frame_bytes, frames, stride, c->frame_bytes, n,
+                                    cudaMemcpyHostToDevice, c->stream));
+        return;
+    }
+    // sample-width conversion on the host (API convenience path, not the throughput path)
+    std::vector<uint8_t> tmp(c->frame_bytes);
+    for (long long f = 0; f < n; ++f) {
+        const uint8_t* src = (const uint8_t*)frames + stride * f;
+        if (sample_bytes == 2 && g.sample_bytes == 1) {
+            const uint16_t* s16 = (const uint16_t*)src;
+            for (size_t i = 0; i < px; ++i) {
+                if (s16[i] > 255) throw Error(2, "frame sample exceeds the 8-bit depth");
+                tmp[i] = (uint8_t)s16[i];
+            }
+        } else {
+            uint16_t* d16 = (uint16_t*)tmp.data();
+            for (size_t i = 0; i < px; ++i) d16[i] = src[i];
+        }
+        FROI_CUDA(cudaMemcpy(dst + c->frame_bytes * f, tmp.data(), c->frame_bytes, cudaMemcpyHostToDevice));
+    }
+}
+
+void check_frames_range(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, long long n) {
+    // Frame invariant (core.hpp:24-25): every sample < 2^depth.
+    if (sample_bytes != 2 || c->g.depth == 16) return;
+    const size_t px = (size_t)c->g.W * c->g.H;
+    for (long long f = 0; f < n; ++f) {
+        const uint16_t* s16 = (const uint16_t*)((const uint8_t*)frames + stride * f);
+        for (size_t i = 0; i < px; ++i)
+            if (s16[i] > 255) throw Error(2, "frame sample exceeds the 8-bit depth");
+    }
+}
+
+// Whole wells: frames on device (well-major, contiguous in ctx sample type).
+void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int n_wells, int n_frames,
+                       uint8_t* d_out, std::vector<PairInfo>& infos) {
+    const Geom& g = c->g;
+    std::vector<PairJob> jobs;
+    jobs.reserve((size_t)n_wells * (n_frames - 1));
+    for (int w = 0; w < n_wells; ++w)
+        for (int t = 1; t < n_frames; ++t) {
+            PairJob J;
+            J.raw_prev = d_frames + stride * ((size_t)w * n_frames + t - 1);
+            J.raw_next = d_frames + stride * ((size_t)w * n_frames + t);
+            J.out_index = (long long)w * n_frames + t;
+            J.stats_index = J.out_index;
+            jobs.push_back(J);
+        }
+    c->times = froi_stage_times{};
+    c->launches = 0;
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap) {
+        const size_t j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
+        run_batch(c, jobs, j0, j1, d_out, infos);
+    }
+    // frame 0 borrows frame 1's mask (roi.hpp:348)
+    const size_t mb = (size_t)g.H * g.SB;
+    for (int w = 0; w < n_wells; ++w)
+        FROI_CUDA(cudaMemcpyAsync(d_out + mb * ((size_t)w * n_frames), d_out + mb * ((size_t)w * n_frames + 1),
+                                  mb, cudaMemcpyDeviceToDevice, c->stream));
+    // temporal ensemble on the pre-ensemble masks (roi.hpp:356-362)
+    if (c->params.adjacent_factor > 0) {
+        ensure_seq_tmp(c, mb * n_frames);
+        for (int w = 0; w < n_wells; ++w) {
+            uint8_t* base = d_out + mb * ((size_t)w * n_frames);
+            launch_ensemble(g, base, c->d_seq_tmp, n_frames, c->params.adjacent_factor, c->stream);
+            FROI_CUDA(cudaMemcpyAsync(base, c->d_seq_tmp, mb * n_frames, cudaMemcpyDeviceToDevice, c->stream));
+            ++c->launches;
+        }
+    }
+}
+
+void stats_for_wells(froi_ctx* c, const std::vector<PairInfo>& infos, int n_wells, int n_frames,
+                     froi_frame_stats* stats) {
+    if (!stats) return;
+    size_t k = 0;
+    for (int w = 0; w < n_wells; ++w) {
+        froi_frame_stats* s = stats + (size_t)w * n_frames;
+        for (int t = 1; t < n_frames; ++t) fill_stats(c->g, infos[k++], &s[t]);
+        s[0] = s[1];
+        s[0].dx = 0;
+        s[0].dy = 0;
+        s[0].confidence = 1.0;
+    }
+}
+
+void deliver_masks(froi_ctx* c, const uint8_t* d_pbm, long long n_masks, int layout, uint8_t* host_out) {
+    const Geom& g = c->g;
+    const size_t mb = (size_t)g.H * g.SB;
+    if (layout == FROI_MASK_PBM) {
+        FROI_CUDA(cudaMemcpyAsync(host_out, d_pbm, mb * n_masks, cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+        return;
+    }
+    const size_t px = (size_t)g.W * g.H;
+    const long long chunk = std::max<long long>(1, (long long)(256u << 20) / (long long)px);
+    ensure_seq_tmp(c, px * std::min<long long>(chunk, n_masks));
+    for (long long m0 = 0; m0 < n_masks; m0 += chunk) {
+        const long long nm = std::min(chunk, n_masks - m0);
+        launch_unpack_pbm(g, d_pbm + mb * m0, c->d_seq_tmp, (int)nm, c->stream);
+        FROI_CUDA(cudaMemcpyAsync(host_out + px * m0, c->d_seq_tmp, px * nm, cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    }
+}
+
+int check_layout(int layout) {
+    return layout == FROI_MASK_BYTES || layout == FROI_MASK_PBM;
+}
+
+}  // namespace
+
+// =============================================================================== C ABI
+extern "C" {
+
+const char* froi_version(void) { return "froi-b200 0.1 (sm_100a)"; }
+
+const char* froi_last_error(void) { return g_last_error.c_str(); }
+
+void froi_params_default(froi_params* p) {
+    if (!p) return;
+    p->denoise_enabled = 1;
+    p->median_radius = 1;
+    p->bilateral_sigma_spatial = 2.0;
+    p->bilateral_sigma_range = 0.04;
+    p->bilateral_radius = 2;
+    p->pyramid_levels = 3;
+    p->pyramid_scale = 0.5;
+    p->window_size = 15;
+    p->iterations = 3;
+    p->poly_n = 5;
+    p->poly_sigma = 1.1;
+    p->roi_threshold = 0.2;
+    p->flow_weight = 0.7;
+    p->adjacent_factor = 0;
+    p->min_area = 20;
+    p->open_radius = 1;
+    p->close_radius = 1;
+    p->gradient_source = FROI_GRADIENT_IMAGE;
+    p->max_shift = 16;
+}
+
+int froi_params_validate(const froi_params* p) {
+    const std::string m = validate(p);
+    if (!m.empty()) return fail(1, m);
+    return 0;
+}
+
+int froi_pyramid_levels(const froi_params* p, int width, int height, int* levels_out, int* widths,
+                        int* heights) {
+    const std::string m = validate(p);
+    if (!m.empty()) return fail(1, m);
+    if (width <= 0 || height <= 0) return fail(2, "frame dimensions must be positive");
+    const Geom g = make_geom(*p, width, height, 8);
+    if (levels_out) *levels_out = g.L;
+    for (int l = 0; l < g.L; ++l) {
+        if (widths) widths[l] = g.lw[l];
+        if (heights) heights[l] = g.lh[l];
+    }
+    return 0;
+}
+
+int froi_device_count(int* count) {
+    int n = 0;
+    const cudaError_t e = cudaGetDeviceCount(&n);
+    if (count) *count = e == cudaSuccess ? n : 0;
+    if (e != cudaSuccess) return fail(3, std::string("cudaGetDeviceCount: ") + cudaGetErrorString(e));
+    return 0;
+}
+
+int froi_ctx_create(int device, const froi_params* p, int width, int height, int depth, int max_pairs,
+                    froi_ctx** out) {
+    if (!out) return fail(1, "out must not be null");
+    *out = nullptr;
+    const std::string m = validate(p);
+    if (!m.empty()) return fail(1, m);
+    if (width <= 0 || height <= 0) return fail(2, "frame dimensions must be positive");
+    if (depth != 8 && depth != 16) return fail(2, "unsupported bit depth " + std::to_string(depth));
+    if (p->max_shift < 1 || p->max_shift >= std::min(width, height) / 4)
+        return fail(1, "estimate_shift: max_shift must be in [1, min(w,h)/4)");
+    if (next_pow2(width) > 8192 || next_pow2(height) > 8192)
+        return fail(1, "frames wider or taller than 8192 px are not supported by the GPU FFT");
+    froi_ctx* c = new froi_ctx();
+    ABI_TRY
+    c->device = device;
+    c->params = *p;
+    c->g = make_geom(*p, width, height, depth);
+    c->dp = make_dev_params(*p);
+    FROI_CUDA(cudaSetDevice(device));
+    FROI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (max_pairs <= 0) {
+        const double mpx = double(width) * height / (1024.0 * 1024.0);
+        max_pairs = std::max(2, std::min(64, int(32.0 / std::max(mpx, 0.25))));
+    }
+    c->Pcap = max_pairs;
+    c->Fcap = 2 * max_pairs;
+    ctx_alloc(c);
+    *out = c;
+    return 0;
+    }
+    catch (const froi::Error& e) {
+        ctx_free(c);
+        delete c;
+        return fail(e.status, e.what());
+    }
+    catch (const std::exception& e) {
+        ctx_free(c);
+        delete c;
+        return fail(3, e.what());
+    }
+}
+
+void froi_ctx_destroy(froi_ctx* ctx) {
+    if (!ctx) return;
+    ctx_free(ctx);
+    delete ctx;
+}
+
+int froi_ctx_get_params(const froi_ctx* ctx, froi_params* out) {
+    if (!ctx || !out) return fail(1, "null argument");
+    *out = ctx->params;
+    return 0;
+}
+
+int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p) {
+    if (!ctx) return fail(1, "null context");
+    const std::string m = validate(p);
+    if (!m.empty()) return fail(1, m);
+    const froi_params& o = ctx->params;
+    if (p->pyramid_levels != o.pyramid_levels || p->pyramid_scale != o.pyramid_scale ||
+        p->max_shift != o.max_shift || p->bilateral_radius != o.bilateral_radius ||
+        p->bilateral_sigma_spatial != o.bilateral_sigma_spatial ||
+        p->bilateral_sigma_range != o.bilateral_sigma_range)
+        return fail(1, "set_params cannot change pyramid geometry, max_shift or bilateral tables; "
+                       "create a new context");
+    ctx->params = *p;
+    ctx->dp = make_dev_params(*p);
+    return 0;
+}
+
+int froi_ctx_stage_times(const froi_ctx* ctx, froi_stage_times* out) {
+    if (!ctx || !out) return fail(1, "null argument");
+    *out = ctx->times;
+    return 0;
+}
+
+int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out) {
+    if (!ctx || !out) return fail(1, "null argument");
+    *out = ctx->launches;
+    return 0;
+}
+
+int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, int n_wells,
+                       int n_frames, int layout, uint8_t* masks_out, froi_frame_stats* stats_out) {
+    if (!c || !frames || !masks_out) return fail(1, "null argument");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(1, "sample_bytes must be 1 or 2");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (n_wells < 1) return fail(2, "need at least one well");
+    if (n_frames < 2) return fail(2, "extract_roi: sequence needs at least 2 frames");
+    if (stride < (size_t)c->g.W * c->g.H * sample_bytes) return fail(1, "frame stride too small");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    check_frames_range(c, frames, sample_bytes, stride, (long long)n_wells * n_frames);
+    const long long nm = (long long)n_wells * n_frames;
+    const size_t mb = (size_t)c->g.H * c->g.SB;
+    // ingest: all frames resident on the device (30 GB for BASELINE config 3 fits in HBM)
+    uint8_t* d_frames = nullptr;
+    FROI_CUDA(cudaMalloc(&d_frames, c->frame_bytes * nm));
+    struct Guard {
+        uint8_t* p;
+        ~Guard() { if (p) cudaFree(p); }
+    } guard{d_frames};
+    upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
+    ensure_seq_out(c, mb * nm);
+    std::vector<PairInfo> infos;
+    extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos);
+    deliver_masks(c, c->d_seq_out, nm, layout, masks_out);
+    stats_for_wells(c, infos, n_wells, n_frames, stats_out);
+    ABI_CATCH
+}
+
+int froi_extract_roi(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, int n_frames,
+                     int layout, uint8_t* masks_out, froi_frame_stats* stats_out) {
+    return froi_extract_wells(c, frames, sample_bytes, stride, 1, n_frames, layout, masks_out, stats_out);
+}
+
+int froi_extract_wells_device(froi_ctx* c, const void* d_frames, int sample_bytes, size_t stride,
+                              int n_wells, int n_frames, uint8_t* d_masks_pbm,
+                              froi_frame_stats* stats_out) {
+    if (!c || !d_frames || !d_masks_pbm) return fail(1, "null argument");
+    if (sample_bytes != c->g.sample_bytes) return fail(1, "device frames must use the context sample width");
+    if (n_wells < 1) return fail(2, "need at least one well");
+    if (n_frames < 2) return fail(2, "extract_roi: sequence needs at least 2 frames");
+    if (stride < c->frame_bytes) return fail(1, "frame stride too small");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    std::vector<PairInfo> infos;
+    extract_wells_dev(c, (const uint8_t*)d_frames, stride, n_wells, n_frames, d_masks_pbm, infos);
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    stats_for_wells(c, infos, n_wells, n_frames, stats_out);
+    ABI_CATCH
+}
+
+int froi_stream_reset(froi_ctx* c, int n_wells) {
+    if (!c) return fail(1, "null context");
+    if (n_wells < 1) return fail(2, "need at least one well");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    c->stream_wells = n_wells;
+    c->stream_next_t.assign(n_wells, 0);
+    const size_t need = c->frame_bytes * n_wells;
+    if (c->carry_cap < need) {
+        if (c->d_carry) FROI_CUDA(cudaFree(c->d_carry));
+        c->d_carry = nullptr;
+        FROI_CUDA(cudaMalloc(&c->d_carry, need));
+        c->carry_cap = need;
+    }
+    ABI_CATCH
+}
+
+int froi_stream_push(froi_ctx* c, const void* frames, int frames_on_device, int sample_bytes,
+                     size_t stride, int chunk, int layout, uint8_t* masks_out, int masks_on_device,
+                     froi_frame_stats* stats_out) {
+    if (!c || !frames || !masks_out) return fail(1, "null argument");
+    if (c->stream_wells < 1) return fail(1, "froi_stream_reset first");
+    if (c->params.adjacent_factor != 0) return fail(1, "streaming requires adjacent_factor == 0");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (masks_on_device && layout != FROI_MASK_PBM) return fail(1, "device masks are PBM only");
+    if (chunk < 1) return fail(2, "chunk must be >= 1");
+    const bool first = c->stream_next_t[0] == 0;
+    if (first && chunk < 2) return fail(2, "the first push of a sequence needs at least 2 frames");
+    if (frames_on_device && sample_bytes != c->g.sample_bytes)
+        return fail(1, "device frames must use the context sample width");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const Geom& g = c->g;
+    const int nw = c->stream_wells;
+    const long long nm = (long long)nw * chunk;
+    const size_t mb = (size_t)g.H * g.SB;
+    // device view of the pushed frames
+    uint8_t* d_frames;
+    size_t dstride;
+    if (frames_on_device) {
+        d_frames = (uint8_t*)frames;
+        dstride = stride;
+    } else {
+        ensure_seq_tmp(c, c->frame_bytes * nm);
+        d_frames = c->d_seq_tmp;
+        dstride = c->frame_bytes;
+        upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
+    }
+    uint8_t* d_out = masks_on_device ? masks_out : nullptr;
+    if (!d_out) {
+        ensure_seq_out(c, mb * nm);
+        d_out = c->d_seq_out;
+    }
+    std::vector<PairJob> jobs;
+    for (int w = 0; w < nw; ++w) {
+        for (int k = 0; k < chunk; ++k) {
+            if (first && k == 0) continue;
+            PairJob J;
+            J.raw_prev = k == 0 ? (const void*)(c->d_carry + c->frame_bytes * w)
+                                : (const void*)(d_frames + dstride * ((size_t)w * chunk + k - 1));
+            J.raw_next = d_frames + dstride * ((size_t)w * chunk + k);
+            J.out_index = (long long)w * chunk + k;
+            J.stats_index = J.out_index;
+            jobs.push_back(J);
+        }
+    }
+    c->times = froi_stage_times{};
+    c->launches = 0;
+    std::vector<PairInfo> infos;
+    for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap)
+        run_batch(c, jobs, j0, std::min(jobs.size(), j0 + (size_t)c->Pcap), d_out, infos);
+    if (first)
+        for (int w = 0; w < nw; ++w)
+            FROI_CUDA(cudaMemcpyAsync(d_out + mb * ((size_t)w * chunk), d_out + mb * ((size_t)w * chunk + 1), mb,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+    // carry the last frame of every well
+    for (int w = 0; w < nw; ++w)
+        FROI_CUDA(cudaMemcpyAsync(c->d_carry + c->frame_bytes * w, d_frames + dstride * ((size_t)w * chunk + chunk - 1),
+                                  c->frame_bytes, cudaMemcpyDeviceToDevice, c->stream));
+    if (!masks_on_device) deliver_masks(c, d_out, nm, layout, masks_out);
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    if (stats_out) {
+        size_t k = 0;
+        for (int w = 0; w < nw; ++w)
+            for (int t = first ? 1 : 0; t < chunk; ++t) fill_stats(g, infos[k++], &stats_out[(size_t)w * chunk + t]);
+        if (first)
+            for (int w = 0; w < nw; ++w) {
+                froi_frame_stats& s0 = stats_out[(size_t)w * chunk];
+                s0 = stats_out[(size_t)w * chunk + 1];
+                s0.dx = 0;
+                s0.dy = 0;
+                s0.confidence = 1.0;
+            }
+    }
+    for (int w = 0; w < nw; ++w) c->stream_next_t[w] += chunk;
+    ABI_CATCH
+}
+
+// ------------------------------------------------------------------ sub-operator taps
+namespace {
+
+// Puts 1..2 host uint16 frames into raw slots 0..n-1 (converted to the context sample type).
+void taps_upload(froi_ctx* c, const uint16_t* const* frames, int n) {
+    for (int i = 0; i < n; ++i) upload_frames(c, frames[i], 2, (size_t)c->g.W * c->g.H * 2, 1, c->d_raw + c->frame_bytes * i);
+    const void* ptrs[2] = {c->d_raw, c->d_raw + c->frame_bytes};
+    FROI_CUDA(cudaMemcpyAsync(c->d_frame_raw[0], ptrs, sizeof(void*) * 2, cudaMemcpyHostToDevice, c->stream));
+    const int prev = 0, next = 1;
+    FROI_CUDA(cudaMemcpyAsync(c->d_prev[0], &prev, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(c->d_next[0], &next, sizeof(int), cudaMemcpyHostToDevice, c->stream));
+    const long long zero = 0;
+    FROI_CUDA(cudaMemcpyAsync(c->d_out_index[0], &zero, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void taps_copy_den(froi_ctx* c, int n) {  // den := raw, sums (denoise disabled)
+    DevParams d = c->dp;
+    d.denoise_enabled = 0;
+    FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * n, c->stream));
+    launch_denoise(c->g, d, c->d_frame_raw[0], c->d_den, c->d_sums, c->d_spatial, c->d_lut, n, c->stream);
+}
+
+void taps_set_info(froi_ctx* c, int dx, int dy) {
+    PairInfo I{};
+    I.dx = dx;
+    I.dy = dy;
+    I.shifted = 0;  // taps never use the shifted-expansion buffers
+    I.confidence = 1.0;
+    FROI_CUDA(cudaMemcpyAsync(c->d_info, &I, sizeof(I), cudaMemcpyHostToDevice, c->stream));
+}
+
+void words_to_bytes(const Geom& g, const std::vector<uint32_t>& words, uint8_t* out) {
+    for (int y = 0; y < g.H; ++y)
+        for (int x = 0; x < g.W; ++x) out[(size_t)y * g.W + x] = (words[(size_t)y * g.WW + (x >> 5)] >> (x & 31)) & 1u;
+}
+
+void pbm_to_bytes(const Geom& g, const std::vector<uint8_t>& pbm, uint8_t* out) {
+    for (int y = 0; y < g.H; ++y)
+        for (int x = 0; x < g.W; ++x) out[(size_t)y * g.W + x] = (pbm[(size_t)y * g.SB + (x >> 3)] >> (7 - (x & 7))) & 1u;
+}
+
+void upload_mask_words(froi_ctx* c, const uint8_t* mask) {
+    const size_t px = (size_t)c->g.W * c->g.H;
+    ensure_seq_tmp(c, px);
+    FROI_CUDA(cudaMemcpyAsync(c->d_seq_tmp, mask, px, cudaMemcpyHostToDevice, c->stream));
+    launch_pack_bytes_to_words(c->g, c->d_seq_tmp, c->d_bits_thr, c->stream);
+}
+
+void upload_flow(froi_ctx* c, const float* u, const float* v) {
+    const size_t px = (size_t)c->g.W * c->g.H;
+    std::vector<float2> f(px);
+    for (size_t i = 0; i < px; ++i) f[i] = make_float2(u[i], v[i]);
+    FROI_CUDA(cudaMemcpy(c->d_flow0, f.data(), sizeof(float2) * px, cudaMemcpyHostToDevice));
+}
+
+}  // namespace
+
+int froi_denoise(froi_ctx* c, const uint16_t* in, uint16_t* out) {
+    if (!c || !in || !out) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const uint16_t* fr[1] = {in};
+    taps_upload(c, fr, 1);
+    FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long), c->stream));
+    launch_denoise(c->g, c->dp, c->d_frame_raw[0], c->d_den, c->d_sums, c->d_spatial, c->d_lut, 1, c->stream);
+    const size_t px = (size_t)c->g.W * c->g.H;
+    std::vector<uint8_t> h(c->frame_bytes);
+    FROI_CUDA(cudaMemcpyAsync(h.data(), c->d_den, c->frame_bytes, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < px; ++i) out[i] = c->g.sample_bytes == 1 ? h[i] : ((const uint16_t*)h.data())[i];
+    ABI_CATCH
+}
+
+int froi_estimate_shift(froi_ctx* c, const uint16_t* reference, const uint16_t* moving, int max_shift,
+                        froi_shift* out) {
+    if (!c || !reference || !moving || !out) return fail(1, "null argument");
+    if (max_shift < 1 || max_shift >= std::min(c->g.W, c->g.H) / 4)
+        return fail(1, "estimate_shift: max_shift must be in [1, min(w,h)/4)");
+    if (max_shift > c->params.max_shift) return fail(1, "max_shift exceeds the context's max_shift");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const uint16_t* fr[2] = {reference, moving};
+    taps_upload(c, fr, 2);
+    taps_copy_den(c, 2);
+    launch_fft_forward(c->g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, 2, c->stream);
+    DevParams d = c->dp;
+    d.max_shift = max_shift;
+    launch_register_pairs(c->g, d, c->d_spec, c->d_prev[0], c->d_next[0], c->d_itw_row, c->d_itw_col, c->d_cols,
+                          c->d_surf, c->d_info, 1, c->stream);
+    PairInfo I;
+    FROI_CUDA(cudaMemcpyAsync(&I, c->d_info, sizeof(I), cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    out->dx = I.est_dx;
+    out->dy = I.est_dy;
+    out->confidence = I.confidence;
+    ABI_CATCH
+}
+
+int froi_compute_flow(froi_ctx* c, const uint16_t* prev, const uint16_t* next, float* u, float* v) {
+    if (!c || !prev || !next || !u || !v) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const uint16_t* fr[2] = {prev, next};
+    taps_upload(c, fr, 2);
+    taps_copy_den(c, 2);
+    FlowBuffers fb = c->flow_buffers();
+    launch_expand_frames(c->g, c->dp, fb, 2, c->stream);
+    taps_set_info(c, 0, 0);
+    const int cur = launch_flow(c->g, c->dp, fb, c->d_prev[0], c->d_next[0], c->d_info, 1, c->stream);
+    const size_t px = (size_t)c->g.W * c->g.H;
+    std::vector<float2> f(px);
+    FROI_CUDA(cudaMemcpyAsync(f.data(), cur ? c->d_flow1 : c->d_flow0, sizeof(float2) * px, cudaMemcpyDeviceToHost,
+                              c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    for (size_t i = 0; i < px; ++i) {
+        u[i] = f[i].x;
+        v[i] = f[i].y;
+    }
+    ABI_CATCH
+}
+
+int froi_polynomial_expansion(froi_ctx* c, const float* image, float* planes) {
+    if (!c || !image || !planes) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)c->g.W * c->g.H;
+    float* d_img = nullptr;
+    FROI_CUDA(cudaMalloc(&d_img, sizeof(float) * 7 * px));
+    struct Guard {
+        float* p;
+        ~Guard() { cudaFree(p); }
+    } guard{d_img};
+    float* d_planes = d_img + px;
+    FROI_CUDA(cudaMemcpyAsync(d_img, image, sizeof(float) * px, cudaMemcpyHostToDevice, c->stream));
+    launch_expand_image(c->g, c->dp, d_img, d_planes, c->stream);
+    FROI_CUDA(cudaMemcpyAsync(planes, d_planes, sizeof(float) * 6 * px, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    ABI_CATCH
+}
+
+int froi_saliency(froi_ctx* c, const float* u, const float* v, const uint16_t* frame, double* out) {
+    if (!c || !u || !v || !frame || !out) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const uint16_t* fr[1] = {frame};
+    taps_upload(c, fr, 1);
+    const void* rp = c->d_raw;
+    FROI_CUDA(cudaMemcpyAsync(c->d_pair_raw[0], &rp, sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    upload_flow(c, u, v);
+    taps_set_info(c, 0, 0);
+    const size_t px = (size_t)c->g.W * c->g.H;
+    double* d_out = (double*)c->d_flow1;
+    MaskBuffers mb = c->mask_buffers(0);
+    mb.flow = c->d_flow0;
+    launch_saliency_map(c->g, c->dp, mb, d_out, c->stream);
+    FROI_CUDA(cudaMemcpyAsync(out, d_out, sizeof(double) * px, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    ABI_CATCH
+}
+
+int froi_threshold_mask(froi_ctx* c, const double* map, double roi_threshold, uint8_t* mask) {
+    if (!c || !map || !mask) return fail(1, "null argument");
+    if (!(roi_threshold > 0.0 && roi_threshold < 1.0))
+        return fail(1, "threshold_mask: roi_threshold must be in (0,1)");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)c->g.W * c->g.H;
+    double* d_map = (double*)c->d_flow1;
+    FROI_CUDA(cudaMemcpyAsync(d_map, map, sizeof(double) * px, cudaMemcpyHostToDevice, c->stream));
+    taps_set_info(c, 0, 0);
+    MaskBuffers mb = c->mask_buffers(0);
+    mb.flow = c->d_flow0;
+    launch_threshold_from_map(c->g, c->dp, mb, d_map, roi_threshold, c->stream);
+    std::vector<uint32_t> words((size_t)c->g.H * c->g.WW);
+    FROI_CUDA(cudaMemcpyAsync(words.data(), c->d_bits_thr, words.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    words_to_bytes(c->g, words, mask);
+    ABI_CATCH
+}
+
+int froi_morph_cleanup(froi_ctx* c, uint8_t* mask, int open_radius, int close_radius, int min_area) {
+    if (!c || !mask) return fail(1, "null argument");
+    if (open_radius < 0 || close_radius < 0 || open_radius > 31 || close_radius > 31)
+        return fail(1, "roi: radii must be in [0, 31]");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    upload_mask_words(c, mask);
+    taps_set_info(c, 0, 0);
+    const long long zero = 0;
+    FROI_CUDA(cudaMemcpyAsync(c->d_out_index[0], &zero, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    MaskBuffers mb = c->mask_buffers(0);
+    mb.flow = c->d_flow0;
+    launch_cleanup_only(c->g, c->dp, mb, open_radius, close_radius, min_area, c->stream);
+    std::vector<uint8_t> pbm((size_t)c->g.H * c->g.SB);
+    FROI_CUDA(cudaMemcpyAsync(pbm.data(), c->d_out_batch, pbm.size(), cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    pbm_to_bytes(c->g, pbm, mask);
+    ABI_CATCH
+}
+
+int froi_component_areas(froi_ctx* c, const uint8_t* mask, uint32_t* areas_out, size_t cap,
+                         size_t* n_components) {
+    if (!c || !mask || !n_components) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    upload_mask_words(c, mask);
+    taps_set_info(c, 0, 0);
+    const long long zero = 0;
+    FROI_CUDA(cudaMemcpyAsync(c->d_out_index[0], &zero, sizeof(long long), cudaMemcpyHostToDevice, c->stream));
+    MaskBuffers mb = c->mask_buffers(0);
+    mb.flow = c->d_flow0;
+    launch_cleanup_only(c->g, c->dp, mb, 0, 0, 2, c->stream);  // no morphology, CCL forced
+    const Geom& g = c->g;
+    const size_t px = (size_t)g.W * g.H;
+    std::vector<uint32_t> roots((size_t)g.H * g.WW);
+    std::vector<int> labels(px);
+    std::vector<uint32_t> area(px);
+    FROI_CUDA(cudaMemcpyAsync(roots.data(), c->d_bits_root, roots.size() * 4, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(labels.data(), c->d_labels, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(area.data(), c->d_area_total, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    size_t n = 0;
+    for (int y = 0; y < g.H; ++y)
+        for (int x = 0; x < g.W; ++x) {
+            const size_t i = (size_t)y * g.W + x;
+            if (!((roots[(size_t)y * g.WW + (x >> 5)] >> (x & 31)) & 1u)) continue;
+            if (labels[i] != (int)i) continue;  // local root that is not the global root
+            if (areas_out && n < cap) areas_out[n] = area[i];
+            ++n;
+        }
+    *n_components = n;
+    ABI_CATCH
+}
+
+int froi_mask_from_flow(froi_ctx* c, const float* u, const float* v, const uint16_t* raw_frame, int dx,
+                        int dy, uint8_t* mask, froi_frame_stats* stats) {
+    if (!c || !u || !v || !raw_frame || !mask) return fail(1, "null argument");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const uint16_t* fr[1] = {raw_frame};
+    taps_upload(c, fr, 1);
+    const void* rp = c->d_raw;
+    FROI_CUDA(cudaMemcpyAsync(c->d_pair_raw[0], &rp, sizeof(void*), cudaMemcpyHostToDevice, c->stream));
+    upload_flow(c, u, v);
+    taps_set_info(c, dx, dy);
+    MaskBuffers mb = c->mask_buffers(0);
+    mb.flow = c->d_flow0;
+    uint64_t l = 0;
+    launch_mask_stage(c->g, c->dp, mb, 1, c->stream, &l);
+    std::vector<uint8_t> pbm((size_t)c->g.H * c->g.SB);
+    PairInfo I;
+    FROI_CUDA(cudaMemcpyAsync(pbm.data(), c->d_out_batch, pbm.size(), cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(&I, c->d_info, sizeof(I), cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    pbm_to_bytes(c->g, pbm, mask);
+    if (stats) fill_stats(c->g, I, stats);
+    ABI_CATCH
+}
+
+int froi_temporal_ensemble(froi_ctx* c, const uint8_t* masks, int n, int k, uint8_t* out) {
+    if (!c || !masks || !out) return fail(1, "null argument");
+    if (n < 1) return fail(2, "temporal_ensemble: need at least one mask");
+    if (k < 0) return fail(1, "roi: adjacent_factor must be >= 0");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)c->g.W * c->g.H;
+    ensure_seq_tmp(c, 2 * px * n);
+    FROI_CUDA(cudaMemcpyAsync(c->d_seq_tmp, masks, px * n, cudaMemcpyHostToDevice, c->stream));
+    Geom g1 = c->g;  // byte-per-pixel layout: treat each row as W "bytes"
+    g1.SB = g1.W;
+    launch_ensemble(g1, c->d_seq_tmp, c->d_seq_tmp + px * n, n, k, c->stream);
+    FROI_CUDA(cudaMemcpyAsync(out, c->d_seq_tmp + px * n, px * n, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    ABI_CATCH
+}
+
+}  // extern "C"

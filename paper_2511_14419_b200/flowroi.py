@@ -1,0 +1,428 @@
+"""Host-side mirror of the reference's stage API (``namespace flowroi``), backed by the GPU.
+
+Same names, argument meaning and error behaviour as the reference's inline C++ API, over numpy
+arrays instead of ``Frame`` / ``RoiMask`` structs:
+
+=========================================  ===============================================
+reference (/root/reference/proj/include/)  here
+=========================================  ===============================================
+``extract_roi`` roi.hpp:309-364            ``extract_roi(seq, params, workers, info, timers)``
+``compute_flow`` flow.hpp:304-345          ``compute_flow(prev, next, params, depth)``
+``denoise`` denoise.hpp:84-90              ``denoise(frame, params, depth)``
+``estimate_shift`` registration.hpp:46-97  ``estimate_shift(reference, moving, max_shift, depth)``
+``polynomial_expansion`` flow.hpp:118-153  ``polynomial_expansion(img, poly_n, poly_sigma)``
+``saliency`` roi.hpp:81-103                ``saliency(u, v, frame, flow_weight, source, depth)``
+``threshold_mask`` roi.hpp:109-138         ``threshold_mask(map, roi_threshold)``
+``morph_cleanup`` roi.hpp:237-246          ``morph_cleanup(mask, open_r, close_r, min_area)``
+``label_components`` roi.hpp:184-234       ``component_areas(mask)`` (areas only)
+``temporal_ensemble`` roi.hpp:249-261      ``temporal_ensemble(masks, t, k)``
+=========================================  ===============================================
+
+A frame is a 2-D uint8/uint16 array; ``depth`` (8 or 16) is ``Frame::depth`` and defaults to 8
+for uint8 arrays and 16 otherwise.  Masks are uint8 0/1 arrays (``RoiMask`` layout).  Every
+call computes on the GPU through libfroi.so; errors raise UsageError / DataError exactly where the
+reference throws usage_error / data_error.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native
+from .params import (CFrameStats, CParams, CShift, CStageTimes, DataError, ExtractInfo,
+                     ExtractParams, FlowParams, Shift, StageTimes, UsageError)
+
+__all__ = [
+    "Sequence", "extract_roi", "extract_wells", "compute_flow", "denoise", "estimate_shift",
+    "polynomial_expansion", "saliency", "threshold_mask", "morph_cleanup", "component_areas",
+    "temporal_ensemble", "mask_from_flow", "Context", "device_count",
+]
+
+
+@dataclass
+class Sequence:
+    """``flowroi::Sequence`` (core.hpp:61-75): frames [n, h, w] sharing one geometry."""
+    frames: np.ndarray
+    depth: int = 8
+    frame_interval_s: float = 8.0
+
+    def __len__(self) -> int:
+        return int(self.frames.shape[0])
+
+
+def device_count() -> int:
+    n = ctypes.c_int(0)
+    _native.lib.froi_device_count(ctypes.byref(n))
+    return n.value
+
+
+def _default_depth(a: np.ndarray) -> int:
+    return 8 if a.dtype == np.uint8 else 16
+
+
+def _frames_array(frames: np.ndarray, depth: int) -> np.ndarray:
+    a = np.asarray(frames)
+    if a.dtype not in (np.uint8, np.uint16):
+        if np.issubdtype(a.dtype, np.integer):
+            a = a.astype(np.uint16)
+        else:
+            raise DataError("frames must be uint8 or uint16 samples")
+    if depth == 8 and a.dtype == np.uint16:
+        if a.size and int(a.max()) > 255:
+            raise DataError("frame sample exceeds the 8-bit depth")
+        a = a.astype(np.uint8)
+    return np.ascontiguousarray(a)
+
+
+class Context:
+    """A per-GPU context (froi_ctx): device arenas for one frame geometry and parameter set."""
+
+    def __init__(self, width: int, height: int, depth: int = 8,
+                 params: ExtractParams | None = None, device: int = 0, max_pairs: int = 0):
+        self.params = (params or ExtractParams()).copy()
+        self.width, self.height, self.depth, self.device = width, height, depth, device
+        self._cp = self.params.to_c()
+        self._h = ctypes.c_void_p()
+        _native.check(_native.lib.froi_ctx_create(device, ctypes.byref(self._cp), width, height,
+                                                  depth, max_pairs, ctypes.byref(self._h)),
+                      "froi_ctx_create")
+        self.lock = threading.Lock()
+
+    def close(self) -> None:
+        if self._h:
+            _native.lib.froi_ctx_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - interpreter shutdown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self) -> ctypes.c_void_p:
+        return self._h
+
+    def stage_times(self) -> StageTimes:
+        t = CStageTimes()
+        _native.check(_native.lib.froi_ctx_stage_times(self._h, ctypes.byref(t)))
+        return StageTimes(t.denoise_ns, t.flow_ns, t.roi_ns, t.encode_ns)
+
+    def launch_count(self) -> int:
+        n = ctypes.c_uint64(0)
+        _native.check(_native.lib.froi_ctx_launch_count(self._h, ctypes.byref(n)))
+        return n.value
+
+    def extract_wells(self, frames: np.ndarray, layout: str = "bytes"):
+        """frames [wells, n, h, w] -> (masks, stats).  masks: [wells, n, h, w] bytes, or
+        [wells, n, h, ceil(w/8)] PBM rows when layout == "pbm"."""
+        a = _frames_array(frames, self.depth)
+        if a.ndim == 3:
+            a = a[None]
+        nw, n, h, w = a.shape
+        if (h, w) != (self.height, self.width):
+            raise DataError("extract_roi: frame dimensions do not match the context")
+        pbm = layout == "pbm"
+        out = np.empty((nw, n, h, (w + 7) // 8 if pbm else w), np.uint8)
+        stats = (CFrameStats * (nw * n))()
+        with self.lock:
+            _native.check(_native.lib.froi_extract_wells(
+                self._h, a.ctypes.data, a.itemsize, h * w * a.itemsize, nw, n, 1 if pbm else 0,
+                out.ctypes.data, stats), "extract_roi")
+        return out, stats
+
+
+_ctx_cache: dict = {}
+_ctx_lock = threading.Lock()
+
+
+def _context(width: int, height: int, depth: int, params: ExtractParams, device: int = 0) -> Context:
+    cp = params.to_c()
+    key = (device, width, height, depth, bytes(cp))
+    with _ctx_lock:
+        ctx = _ctx_cache.get(key)
+        if ctx is None:
+            if len(_ctx_cache) >= 8:
+                _ctx_cache.pop(next(iter(_ctx_cache))).close()
+            ctx = Context(width, height, depth, params, device)
+            _ctx_cache[key] = ctx
+        return ctx
+
+
+def _split_shifts(stats, n: int) -> list:
+    return [Shift(stats[i].dx, stats[i].dy, stats[i].confidence) for i in range(n)]
+
+
+def extract_roi(seq, params: ExtractParams | None = None, workers: int = 1,
+                info: ExtractInfo | None = None, timers: StageTimes | None = None,
+                depth: int | None = None) -> np.ndarray:
+    """``flowroi::extract_roi`` (roi.hpp:309-364) on the GPU.  Returns masks [n, h, w] (uint8 0/1).
+
+    ``workers`` keeps the reference signature; the output never depends on it
+    (parallel.hpp:17-19).  A single sequence runs on one GPU."""
+    params = params or ExtractParams()
+    params.roi.validate()
+    params.flow.validate()
+    if isinstance(seq, Sequence):
+        frames, depth = seq.frames, seq.depth
+    else:
+        frames = np.asarray(seq)
+        depth = depth or _default_depth(frames)
+    if frames.ndim != 3:
+        raise DataError("extract_roi: expected frames [n, h, w]")
+    n, h, w = frames.shape
+    if n < 2:
+        raise DataError("extract_roi: sequence needs at least 2 frames")
+    params.denoise.validate()
+    ctx = _context(w, h, depth, params)
+    masks, stats = ctx.extract_wells(frames[None])
+    if info is not None:
+        info.shifts = _split_shifts(stats, n)
+        info.raw_fractions = [stats[i].raw_fraction for i in range(n)]
+        info.mask_counts = [stats[i].mask_count for i in range(n)]
+        info.components = [stats[i].components for i in range(n)]
+    if timers is not None:
+        t = ctx.stage_times()
+        timers.denoise_ns += t.denoise_ns
+        timers.flow_ns += t.flow_ns
+        timers.roi_ns += t.roi_ns
+    return masks[0]
+
+
+def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth: int | None = None,
+                  devices: list[int] | None = None, layout: str = "bytes"):
+    """Independent wells [wells, n, h, w], sharded well-wise over ``devices`` (one host thread
+    per GPU, no collective).  Returns (masks, list of per-well ExtractInfo)."""
+    params = params or ExtractParams()
+    params.validate()
+    frames = np.asarray(frames)
+    depth = depth or _default_depth(frames)
+    nw, n, h, w = frames.shape
+    devices = devices or [0]
+    results: dict = {}
+    errors: list = []
+
+    def work(dev: int, wells: list[int]):
+        try:
+            ctx = _context(w, h, depth, params, dev)
+            m, st = ctx.extract_wells(frames[wells], layout)
+            results[dev] = (wells, m, st)
+        except Exception as e:  # first error re-raised like parallel_for (parallel.hpp:31-48)
+            errors.append(e)
+
+    shards = {d: [i for i in range(nw) if i % len(devices) == k] for k, d in enumerate(devices)}
+    threads = [threading.Thread(target=work, args=(d, ws)) for d, ws in shards.items() if ws]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    if errors:
+        raise errors[0]
+    out = np.empty((nw, n, h, (w + 7) // 8 if layout == "pbm" else w), np.uint8)
+    infos = [None] * nw
+    for wells, m, st in results.values():
+        for k, wi in enumerate(wells):
+            out[wi] = m[k]
+            s = st[k * n:(k + 1) * n]
+            infos[wi] = ExtractInfo(shifts=[Shift(x.dx, x.dy, x.confidence) for x in s],
+                                    raw_fractions=[x.raw_fraction for x in s],
+                                    mask_counts=[x.mask_count for x in s],
+                                    components=[x.components for x in s])
+    return out, infos
+
+
+def _u16(a: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(np.asarray(a), dtype=np.uint16)
+
+
+def denoise(frame: np.ndarray, params: ExtractParams | None = None, depth: int | None = None) -> np.ndarray:
+    """``flowroi::denoise`` (denoise.hpp:84-90)."""
+    params = params or ExtractParams()
+    params.denoise.validate()
+    f = np.asarray(frame)
+    depth = depth or _default_depth(f)
+    h, w = f.shape
+    ctx = _context(w, h, depth, params)
+    a = _u16(f)
+    out = np.empty_like(a)
+    with ctx.lock:
+        _native.check(_native.lib.froi_denoise(ctx.handle, a.ctypes.data, out.ctypes.data), "denoise")
+    return out.astype(f.dtype) if f.dtype == np.uint8 else out
+
+
+def estimate_shift(reference: np.ndarray, moving: np.ndarray, max_shift: int = 16,
+                   depth: int | None = None) -> Shift:
+    """``flowroi::estimate_shift`` (registration.hpp:46-97)."""
+    a, b = np.asarray(reference), np.asarray(moving)
+    if a.shape != b.shape:
+        raise DataError("estimate_shift: frames must share dimensions and depth")
+    h, w = a.shape
+    if max_shift < 1 or max_shift >= min(w, h) // 4:
+        raise UsageError("estimate_shift: max_shift must be in [1, min(w,h)/4)")
+    depth = depth or _default_depth(a)
+    p = ExtractParams()
+    p.max_shift = max_shift
+    ctx = _context(w, h, depth, p)
+    s = CShift()
+    with ctx.lock:
+        _native.check(_native.lib.froi_estimate_shift(ctx.handle, _u16(a).ctypes.data,
+                                                      _u16(b).ctypes.data, max_shift,
+                                                      ctypes.byref(s)), "estimate_shift")
+    return Shift(s.dx, s.dy, s.confidence)
+
+
+def compute_flow(prev: np.ndarray, nxt: np.ndarray, params: FlowParams | ExtractParams | None = None,
+                 depth: int | None = None):
+    """``flowroi::compute_flow`` (flow.hpp:304-345): returns (u, v) float32 [h, w]."""
+    ep = ExtractParams()
+    if isinstance(params, ExtractParams):
+        ep = params.copy()
+    elif isinstance(params, FlowParams):
+        ep.flow = params
+    ep.flow.validate()
+    a, b = np.asarray(prev), np.asarray(nxt)
+    if a.shape != b.shape:
+        raise DataError("compute_flow: frames must share dimensions")
+    h, w = a.shape
+    depth = depth or _default_depth(a)
+    ep.max_shift = max(1, min(ep.max_shift, min(w, h) // 4 - 1))
+    ctx = _context(w, h, depth, ep)
+    u = np.empty((h, w), np.float32)
+    v = np.empty((h, w), np.float32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_compute_flow(ctx.handle, _u16(a).ctypes.data,
+                                                    _u16(b).ctypes.data, u.ctypes.data,
+                                                    v.ctypes.data), "compute_flow")
+    return u, v
+
+
+def polynomial_expansion(img: np.ndarray, poly_n: int = 5, poly_sigma: float = 1.1) -> np.ndarray:
+    """``flowroi::polynomial_expansion`` (flow.hpp:118-153) in fp32: planes [6, h, w] in the
+    order c, bx, by, a11, a12, a22."""
+    im = np.ascontiguousarray(img, dtype=np.float32)
+    h, w = im.shape
+    ep = ExtractParams()
+    ep.flow.poly_n = poly_n
+    ep.flow.poly_sigma = poly_sigma
+    ep.flow.validate()
+    ep.max_shift = max(1, min(ep.max_shift, min(w, h) // 4 - 1))
+    ctx = _context(w, h, 8, ep)
+    planes = np.empty((6, h, w), np.float32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_polynomial_expansion(ctx.handle, im.ctypes.data,
+                                                            planes.ctypes.data), "polynomial_expansion")
+    return planes
+
+
+def _small_ctx(w: int, h: int, depth: int, ep: ExtractParams) -> Context:
+    ep.max_shift = max(1, min(ep.max_shift, min(w, h) // 4 - 1))
+    return _context(w, h, depth, ep)
+
+
+def saliency(u: np.ndarray, v: np.ndarray, frame: np.ndarray, flow_weight: float = 0.7,
+             gradient_source: int = 0, depth: int | None = None) -> np.ndarray:
+    """``flowroi::saliency`` (roi.hpp:81-103): float64 map."""
+    f = np.asarray(frame)
+    h, w = f.shape
+    if np.shape(u) != (h, w) or np.shape(v) != (h, w):
+        raise DataError("saliency: flow/frame dimension mismatch")
+    depth = depth or _default_depth(f)
+    ep = ExtractParams()
+    ep.roi.flow_weight = flow_weight
+    ep.roi.gradient_source = gradient_source
+    ep.roi.validate()
+    ctx = _small_ctx(w, h, depth, ep)
+    out = np.empty((h, w), np.float64)
+    uu = np.ascontiguousarray(u, dtype=np.float32)
+    vv = np.ascontiguousarray(v, dtype=np.float32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_saliency(ctx.handle, uu.ctypes.data, vv.ctypes.data,
+                                                _u16(f).ctypes.data, out.ctypes.data), "saliency")
+    return out
+
+
+def threshold_mask(sal: np.ndarray, roi_threshold: float) -> np.ndarray:
+    """``flowroi::threshold_mask`` (roi.hpp:109-138)."""
+    if not (0.0 < roi_threshold < 1.0):
+        raise UsageError("threshold_mask: roi_threshold must be in (0,1)")
+    m = np.ascontiguousarray(sal, dtype=np.float64)
+    h, w = m.shape
+    ctx = _small_ctx(w, h, 8, ExtractParams())
+    out = np.empty((h, w), np.uint8)
+    with ctx.lock:
+        _native.check(_native.lib.froi_threshold_mask(ctx.handle, m.ctypes.data, roi_threshold,
+                                                      out.ctypes.data), "threshold_mask")
+    return out
+
+
+def morph_cleanup(mask: np.ndarray, open_radius: int = 1, close_radius: int = 1,
+                  min_area: int = 20) -> np.ndarray:
+    """``flowroi::morph_cleanup`` (roi.hpp:237-246)."""
+    m = np.array(mask, dtype=np.uint8, copy=True, order="C")
+    h, w = m.shape
+    ctx = _small_ctx(w, h, 8, ExtractParams())
+    with ctx.lock:
+        _native.check(_native.lib.froi_morph_cleanup(ctx.handle, m.ctypes.data, open_radius,
+                                                     close_radius, min_area), "morph_cleanup")
+    return m
+
+
+def morph_open(mask: np.ndarray, radius: int) -> np.ndarray:
+    """``flowroi::morph_open`` (roi.hpp:179)."""
+    return morph_cleanup(mask, radius, 0, 0)
+
+
+def morph_close(mask: np.ndarray, radius: int) -> np.ndarray:
+    """``flowroi::morph_close`` (roi.hpp:180)."""
+    return morph_cleanup(mask, 0, radius, 0)
+
+
+def component_areas(mask: np.ndarray) -> np.ndarray:
+    """Areas of the 8-connected components (``label_components``, roi.hpp:184-234), sorted."""
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    h, w = m.shape
+    ctx = _small_ctx(w, h, 8, ExtractParams())
+    n = ctypes.c_size_t(0)
+    areas = np.zeros(w * h, np.uint32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_component_areas(ctx.handle, m.ctypes.data, areas.ctypes.data,
+                                                       areas.size, ctypes.byref(n)), "component_areas")
+    return np.sort(areas[:n.value].astype(np.int64))
+
+
+def temporal_ensemble(masks: np.ndarray, t: int, k: int) -> np.ndarray:
+    """``flowroi::temporal_ensemble`` (roi.hpp:249-261): union of masks [t-k, t+k]."""
+    m = np.ascontiguousarray(masks, dtype=np.uint8)
+    n, h, w = m.shape
+    if t < 0 or t >= n:
+        raise DataError("temporal_ensemble: index out of range")
+    ctx = _small_ctx(w, h, 8, ExtractParams())
+    out = np.empty_like(m)
+    with ctx.lock:
+        _native.check(_native.lib.froi_temporal_ensemble(ctx.handle, m.ctypes.data, n, k,
+                                                         out.ctypes.data), "temporal_ensemble")
+    return out[t]
+
+
+def mask_from_flow(u: np.ndarray, v: np.ndarray, raw: np.ndarray, dx: int = 0, dy: int = 0,
+                   params: ExtractParams | None = None, depth: int | None = None):
+    """Mask stage of one pair (roi.hpp:340-345) from a given flow: returns (mask, stats)."""
+    params = params or ExtractParams()
+    f = np.asarray(raw)
+    h, w = f.shape
+    depth = depth or _default_depth(f)
+    ep = params.copy()
+    ctx = _small_ctx(w, h, depth, ep)
+    mask = np.empty((h, w), np.uint8)
+    st = CFrameStats()
+    uu = np.ascontiguousarray(u, dtype=np.float32)
+    vv = np.ascontiguousarray(v, dtype=np.float32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_mask_from_flow(ctx.handle, uu.ctypes.data, vv.ctypes.data,
+                                                      _u16(f).ctypes.data, dx, dy, mask.ctypes.data,
+                                                      ctypes.byref(st)), "mask_from_flow")
+    return mask, dict(mask_count=st.mask_count, components=st.components,
+                      raw_fraction=st.raw_fraction)
