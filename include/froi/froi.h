@@ -100,6 +100,22 @@ typedef struct froi_stage_times {
     uint64_t encode_ns; /* never touched here: encoding stays on the CPU */
 } froi_stage_times;
 
+/* Device time per kernel group, accumulated over the batches of the last extract call
+ * (CUDA events on the context stream), plus the work counts needed for roofline figures. */
+typedef struct froi_kernel_times {
+    uint64_t denoise_ns;        /* k_denoise */
+    uint64_t fft_forward_ns;    /* k_fft_rows_fwd + k_fft_cols */
+    uint64_t expand_ns;         /* pyramid + polynomial expansion of the frame slots */
+    uint64_t register_ns;       /* cross-power, inverse FFT, argmax */
+    uint64_t expand_shifted_ns; /* pyramid + expansion of registered next frames (s != 0) */
+    uint64_t flow_iter_ns;      /* all k_flow_iter launches */
+    uint64_t mask_ns;           /* saliency selection, threshold, morphology, CCL, output */
+    uint64_t pairs;             /* adjacent pairs processed */
+    uint64_t frames;            /* frame slots processed (denoise / FFT / expansion) */
+    uint64_t flow_iter_launches;
+    uint64_t batches;
+} froi_kernel_times;
+
 typedef struct froi_ctx froi_ctx;
 
 /* ---- library / host-only entries (no GPU needed) ---- */
@@ -128,6 +144,10 @@ int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p);
 int froi_ctx_stage_times(const froi_ctx* ctx, froi_stage_times* out);
 /* Number of kernels launched by the last extract call. */
 int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out);
+/* Per-kernel-group device times of the last extract call. */
+int froi_ctx_kernel_times(const froi_ctx* ctx, froi_kernel_times* out);
+/* The context's CUDA stream (cudaStream_t), for callers that time or order work around it. */
+int froi_ctx_stream(const froi_ctx* ctx, void** stream_out);
 
 /* ---- stage entry: extract_roi (roi.hpp:309-364) ----
  * Host frames: n_frames frames of width*height samples; frame f starts at
@@ -193,6 +213,10 @@ int froi_component_areas(froi_ctx* ctx, const uint8_t* mask, uint32_t* areas_out
  * stage in isolation from the flow's floating-point tolerance. */
 int froi_mask_from_flow(froi_ctx* ctx, const float* u, const float* v, const uint16_t* raw_frame,
                         int dx, int dy, uint8_t* mask, froi_frame_stats* stats);
+/* Parity tap: mask-stage order statistics of pair slot `pair` from the last call, as doubles
+ * {fmag_lo, fmag_hi, grad_lo, grad_hi, boundary, count_greater, need, target, thr_mode}
+ * (robust_normalize roi.hpp:47-63 and threshold_mask roi.hpp:109-138). n = entries wanted. */
+int froi_debug_pair_stats(froi_ctx* ctx, int pair, double* out, int n);
 /* temporal_ensemble (roi.hpp:249-261) over n W*H masks for every t; out: n masks. */
 int froi_temporal_ensemble(froi_ctx* ctx, const uint8_t* masks, int n, int k, uint8_t* out);
 

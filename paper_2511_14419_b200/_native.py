@@ -10,7 +10,8 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .params import CFrameStats, CParams, CShift, CStageTimes, DataError, InternalError, UsageError
+from .params import (CFrameStats, CKernelTimes, CParams, CShift, CStageTimes, DataError,
+                     InternalError, UsageError)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfroi.so")
 
@@ -32,6 +33,8 @@ SIGNATURES = {
     "froi_ctx_set_params": (_I, [_P, ctypes.POINTER(CParams)]),
     "froi_ctx_stage_times": (_I, [_P, ctypes.POINTER(CStageTimes)]),
     "froi_ctx_launch_count": (_I, [_P, ctypes.POINTER(ctypes.c_uint64)]),
+    "froi_ctx_kernel_times": (_I, [_P, ctypes.POINTER(CKernelTimes)]),
+    "froi_ctx_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "froi_extract_roi": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),
     "froi_extract_wells": (_I, [_P, _P, _I, _SZ, _I, _I, _I, _P, _P]),
     "froi_extract_wells_device": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),
@@ -46,6 +49,7 @@ SIGNATURES = {
     "froi_morph_cleanup": (_I, [_P, _P, _I, _I, _I]),
     "froi_component_areas": (_I, [_P, _P, _P, _SZ, ctypes.POINTER(_SZ)]),
     "froi_mask_from_flow": (_I, [_P, _P, _P, _P, _I, _I, _P, ctypes.POINTER(CFrameStats)]),
+    "froi_debug_pair_stats": (_I, [_P, _I, _P, _I]),
     "froi_temporal_ensemble": (_I, [_P, _P, _I, _I, _P]),
 }
 

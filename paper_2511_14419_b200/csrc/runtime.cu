@@ -266,8 +266,14 @@ struct froi_ctx {
     uint8_t* d_carry = nullptr;            // last raw frame per well
     size_t carry_cap = 0;
     // timing
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     froi_stage_times times{};
+    froi_kernel_times ktimes{};
+    // ingest arena (grow-only) + copy stream for H2D / compute overlap
+    uint8_t* d_arena = nullptr;
+    size_t arena_cap = 0;
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> well_ready;
     uint64_t launches = 0;
 
     MaskBuffers mask_buffers(int tb_) const {
@@ -390,7 +396,8 @@ void ctx_alloc(froi_ctx* c) {
         FROI_CUDA(cudaEventCreateWithFlags(&c->tables_free[i], cudaEventDisableTiming));
     }
     FROI_CUDA(cudaMallocHost((void**)&c->h_info, sizeof(PairInfo) * P));
-    for (int i = 0; i < 4; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
+    for (int i = 0; i < 8; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
+    FROI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
 }
 
 void ctx_free(froi_ctx* c) {
@@ -401,7 +408,7 @@ void ctx_free(froi_ctx* c) {
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_tie, c->d_bits_thr,
                     c->d_bits_clean, c->d_bits_root, c->d_labels, c->d_area_local, c->d_area_total,
-                    c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry};
+                    c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry, c->d_arena};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -416,6 +423,8 @@ void ctx_free(froi_ctx* c) {
     if (c->h_info) cudaFreeHost(c->h_info);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto e : c->well_ready) cudaEventDestroy(e);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -440,6 +449,7 @@ struct PairJob {
     const void* raw_next;
     long long out_index;   // mask index in the output PBM buffer
     long long stats_index; // index into the caller's stats array (or -1)
+    cudaEvent_t ready = nullptr;  // ingest of this pair's frames complete (copy stream)
 };
 
 // Runs one batch of pairs.  frames given on device; output PBM masks written at out_index of
@@ -485,32 +495,54 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
     FROI_CUDA(cudaMemcpyAsync(c->d_out_index[tb], h_out, sizeof(long long) * n_pairs, cudaMemcpyHostToDevice, s));
     FROI_CUDA(cudaEventRecord(c->tables_free[tb], s));
 
-    FROI_CUDA(cudaEventRecord(c->ev[0], s));
+    cudaEvent_t waited = nullptr;
+    for (size_t j = j0; j < j1; ++j)
+        if (jobs[j].ready && jobs[j].ready != waited) {
+            FROI_CUDA(cudaStreamWaitEvent(s, jobs[j].ready, 0));
+            waited = jobs[j].ready;
+        }
+    cudaEvent_t* ev = c->ev;
+    FROI_CUDA(cudaEventRecord(ev[0], s));
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
     launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->d_spatial, c->d_lut, nf, s);
-    FROI_CUDA(cudaEventRecord(c->ev[1], s));
+    FROI_CUDA(cudaEventRecord(ev[1], s));
     launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
+    FROI_CUDA(cudaEventRecord(ev[2], s));
     FlowBuffers fb = c->flow_buffers();
     launch_expand_frames(g, c->dp, fb, nf, s);
+    FROI_CUDA(cudaEventRecord(ev[3], s));
     launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
                           c->d_cols, c->d_surf, c->d_info, n_pairs, s);
+    FROI_CUDA(cudaEventRecord(ev[4], s));
     launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+    FROI_CUDA(cudaEventRecord(ev[5], s));
     const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
-    FROI_CUDA(cudaEventRecord(c->ev[2], s));
+    FROI_CUDA(cudaEventRecord(ev[6], s));
     MaskBuffers mb = c->mask_buffers(tb);
     mb.flow = cur ? c->d_flow1 : c->d_flow0;
     mb.out_pbm = out_pbm;
     launch_mask_stage(g, c->dp, mb, n_pairs, s, &c->launches);
-    FROI_CUDA(cudaEventRecord(c->ev[3], s));
+    FROI_CUDA(cudaEventRecord(ev[7], s));
     FROI_CUDA(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(PairInfo) * n_pairs, cudaMemcpyDeviceToHost, s));
     FROI_CUDA(cudaStreamSynchronize(s));
-    float ms[3];
-    FROI_CUDA(cudaEventElapsedTime(&ms[0], c->ev[0], c->ev[1]));
-    FROI_CUDA(cudaEventElapsedTime(&ms[1], c->ev[1], c->ev[2]));
-    FROI_CUDA(cudaEventElapsedTime(&ms[2], c->ev[2], c->ev[3]));
-    c->times.denoise_ns += (uint64_t)(ms[0] * 1e6);
-    c->times.flow_ns += (uint64_t)(ms[1] * 1e6);
-    c->times.roi_ns += (uint64_t)(ms[2] * 1e6);
+    float ms[7];
+    for (int i = 0; i < 7; ++i) FROI_CUDA(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+    auto ns = [](float m) { return (uint64_t)((double)m * 1e6); };
+    c->times.denoise_ns += ns(ms[0]);
+    c->times.flow_ns += ns(ms[1] + ms[2] + ms[3] + ms[4] + ms[5]);
+    c->times.roi_ns += ns(ms[6]);
+    froi_kernel_times& K = c->ktimes;
+    K.denoise_ns += ns(ms[0]);
+    K.fft_forward_ns += ns(ms[1]);
+    K.expand_ns += ns(ms[2]);
+    K.register_ns += ns(ms[3]);
+    K.expand_shifted_ns += ns(ms[4]);
+    K.flow_iter_ns += ns(ms[5]);
+    K.mask_ns += ns(ms[6]);
+    K.pairs += n_pairs;
+    K.frames += nf;
+    K.flow_iter_launches += (uint64_t)g.L * c->dp.iterations;
+    K.batches += 1;
     // launches: denoise 1, fft 2, expand (1 + 2(L-1)) x2, register 3, flow L*iters (+ mask stage)
     c->launches += 1 + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations;
     for (int p = 0; p < n_pairs; ++p) infos.push_back(c->h_info[p]);
@@ -570,7 +602,8 @@ void check_frames_range(froi_ctx* c, const void* frames, int sample_bytes, size_
 
 // Whole wells: frames on device (well-major, contiguous in ctx sample type).
 void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int n_wells, int n_frames,
-                       uint8_t* d_out, std::vector<PairInfo>& infos) {
+                       uint8_t* d_out, std::vector<PairInfo>& infos, const cudaEvent_t* ready = nullptr) {
+    // ready (nullable): per (well, frame) event after which the frame is resident
     const Geom& g = c->g;
     std::vector<PairJob> jobs;
     jobs.reserve((size_t)n_wells * (n_frames - 1));
@@ -581,9 +614,11 @@ void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int 
             J.raw_next = d_frames + stride * ((size_t)w * n_frames + t);
             J.out_index = (long long)w * n_frames + t;
             J.stats_index = J.out_index;
+            J.ready = ready ? ready[(size_t)w * n_frames + t] : nullptr;  // chunk holding frame t
             jobs.push_back(J);
         }
     c->times = froi_stage_times{};
+    c->ktimes = froi_kernel_times{};
     c->launches = 0;
     for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap) {
         const size_t j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
@@ -779,6 +814,18 @@ int froi_ctx_stage_times(const froi_ctx* ctx, froi_stage_times* out) {
     return 0;
 }
 
+int froi_ctx_kernel_times(const froi_ctx* ctx, froi_kernel_times* out) {
+    if (!ctx || !out) return fail(1, "null argument");
+    *out = ctx->ktimes;
+    return 0;
+}
+
+int froi_ctx_stream(const froi_ctx* ctx, void** stream_out) {
+    if (!ctx || !stream_out) return fail(1, "null argument");
+    *stream_out = (void*)ctx->stream;
+    return 0;
+}
+
 int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out) {
     if (!ctx || !out) return fail(1, "null argument");
     *out = ctx->launches;
@@ -798,17 +845,50 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
     check_frames_range(c, frames, sample_bytes, stride, (long long)n_wells * n_frames);
     const long long nm = (long long)n_wells * n_frames;
     const size_t mb = (size_t)c->g.H * c->g.SB;
-    // ingest: all frames resident on the device (30 GB for BASELINE config 3 fits in HBM)
-    uint8_t* d_frames = nullptr;
-    FROI_CUDA(cudaMalloc(&d_frames, c->frame_bytes * nm));
-    struct Guard {
-        uint8_t* p;
-        ~Guard() { if (p) cudaFree(p); }
-    } guard{d_frames};
-    upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
+    // ingest: frames resident on the device (BASELINE config 3 is 30 GB, well inside HBM); wells are
+    // copied on a separate stream and each well's pairs wait only for its own frames
+    const size_t need = c->frame_bytes * nm;
+    if (c->arena_cap < need) {
+        if (c->d_arena) FROI_CUDA(cudaFree(c->d_arena));
+        c->d_arena = nullptr;
+        c->arena_cap = 0;
+        FROI_CUDA(cudaMalloc(&c->d_arena, need));
+        c->arena_cap = need;
+    }
+    uint8_t* d_frames = c->d_arena;
+    // copy granularity: chunks of Pcap frames, each with an event the consuming batch waits on
+    const int fchunk = std::max(1, c->Pcap);
+    const int chunks_per_well = (n_frames + fchunk - 1) / fchunk;
+    const size_t n_events = (size_t)n_wells * chunks_per_well;
+    while (c->well_ready.size() < n_events) {
+        cudaEvent_t e;
+        FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->well_ready.push_back(e);
+    }
+    const bool direct = sample_bytes == c->g.sample_bytes && stride == c->frame_bytes;
+    std::vector<cudaEvent_t> ready;
+    if (direct) {
+        // the previous call's kernels may still read the arena: order the copies after them
+        FROI_CUDA(cudaEventRecord(c->ev[7], c->stream));
+        FROI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[7], 0));
+        ready.resize((size_t)n_wells * n_frames);
+        for (int w = 0; w < n_wells; ++w)
+            for (int k = 0; k < chunks_per_well; ++k) {
+                const int f0 = k * fchunk, f1 = std::min(n_frames, f0 + fchunk);
+                const size_t off = c->frame_bytes * ((size_t)n_frames * w + f0);
+                FROI_CUDA(cudaMemcpyAsync(d_frames + off, (const uint8_t*)frames + off,
+                                          c->frame_bytes * (f1 - f0), cudaMemcpyHostToDevice, c->copy_stream));
+                cudaEvent_t e = c->well_ready[(size_t)w * chunks_per_well + k];
+                FROI_CUDA(cudaEventRecord(e, c->copy_stream));
+                for (int f = f0; f < f1; ++f) ready[(size_t)w * n_frames + f] = e;
+            }
+    } else {
+        upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
+    }
     ensure_seq_out(c, mb * nm);
     std::vector<PairInfo> infos;
-    extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos);
+    extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos,
+                      direct ? ready.data() : nullptr);
     deliver_masks(c, c->d_seq_out, nm, layout, masks_out);
     stats_for_wells(c, infos, n_wells, n_frames, stats_out);
     ABI_CATCH
@@ -903,6 +983,7 @@ int froi_stream_push(froi_ctx* c, const void* frames, int frames_on_device, int 
         }
     }
     c->times = froi_stage_times{};
+    c->ktimes = froi_kernel_times{};
     c->launches = 0;
     std::vector<PairInfo> infos;
     for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap)
@@ -1191,6 +1272,19 @@ int froi_mask_from_flow(froi_ctx* c, const float* u, const float* v, const uint1
     FROI_CUDA(cudaStreamSynchronize(c->stream));
     pbm_to_bytes(c->g, pbm, mask);
     if (stats) fill_stats(c->g, I, stats);
+    ABI_CATCH
+}
+
+int froi_debug_pair_stats(froi_ctx* c, int pair, double* out, int n) {
+    if (!c || !out) return fail(1, "null argument");
+    if (pair < 0 || pair >= c->Pcap) return fail(1, "pair slot out of range");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    PairInfo I;
+    FROI_CUDA(cudaMemcpy(&I, c->d_info + pair, sizeof(I), cudaMemcpyDeviceToHost));
+    const double v[9] = {I.fmag_lo, I.fmag_hi, I.grad_lo, I.grad_hi, I.boundary, (double)I.count_gt,
+                         (double)I.need, (double)I.target, (double)I.thr_mode};
+    for (int i = 0; i < n && i < 9; ++i) out[i] = v[i];
     ABI_CATCH
 }
 

@@ -19,7 +19,8 @@ reference (/root/reference/proj/include/)  here
 =========================================  ===============================================
 
 A frame is a 2-D uint8/uint16 array; ``depth`` (8 or 16) is ``Frame::depth`` and defaults to 8
-for uint8 arrays and 16 otherwise.  Masks are uint8 0/1 arrays (``RoiMask`` layout).  Every
+like ``Frame`` (core.hpp:29) whatever the array dtype; a sample above the depth's maxval raises
+DataError instead of being reinterpreted.  Masks are uint8 0/1 arrays (``RoiMask`` layout).  Every
 call computes on the GPU through libfroi.so; errors raise UsageError / DataError exactly where the
 reference throws usage_error / data_error.
 """
@@ -60,7 +61,8 @@ def device_count() -> int:
 
 
 def _default_depth(a: np.ndarray) -> int:
-    return 8 if a.dtype == np.uint8 else 16
+    """Frame::depth defaults to 8 (core.hpp:29); 16-bit data must say depth=16."""
+    return 8
 
 
 def _frames_array(frames: np.ndarray, depth: int) -> np.ndarray:
@@ -110,6 +112,34 @@ class Context:
         t = CStageTimes()
         _native.check(_native.lib.froi_ctx_stage_times(self._h, ctypes.byref(t)))
         return StageTimes(t.denoise_ns, t.flow_ns, t.roi_ns, t.encode_ns)
+
+    def kernel_times(self) -> dict:
+        from .params import CKernelTimes
+        t = CKernelTimes()
+        _native.check(_native.lib.froi_ctx_kernel_times(self._h, ctypes.byref(t)))
+        return t.as_dict()
+
+    def stream(self) -> int:
+        s = ctypes.c_void_p()
+        _native.check(_native.lib.froi_ctx_stream(self._h, ctypes.byref(s)))
+        return s.value or 0
+
+    def extract_wells_device(self, d_frames: int, n_wells: int, n_frames: int, d_masks_pbm: int,
+                             stats=None) -> None:
+        """Device-resident variant (froi_extract_wells_device): pointers are device addresses."""
+        with self.lock:
+            _native.check(_native.lib.froi_extract_wells_device(
+                self._h, ctypes.c_void_p(d_frames), 1 if self.depth == 8 else 2,
+                self.width * self.height * (1 if self.depth == 8 else 2), n_wells, n_frames,
+                ctypes.c_void_p(d_masks_pbm), stats), "extract_wells_device")
+
+    def extract_wells_into(self, frames: np.ndarray, out: np.ndarray, stats=None, pbm: bool = True) -> None:
+        """Host frames [wells, n, h, w] -> preallocated host masks (PBM rows by default)."""
+        nw, n, h, w = frames.shape
+        with self.lock:
+            _native.check(_native.lib.froi_extract_wells(
+                self._h, frames.ctypes.data, frames.itemsize, h * w * frames.itemsize, nw, n,
+                1 if pbm else 0, out.ctypes.data, stats), "extract_roi")
 
     def launch_count(self) -> int:
         n = ctypes.c_uint64(0)
@@ -245,7 +275,7 @@ def denoise(frame: np.ndarray, params: ExtractParams | None = None, depth: int |
     f = np.asarray(frame)
     depth = depth or _default_depth(f)
     h, w = f.shape
-    ctx = _context(w, h, depth, params)
+    ctx = _small_ctx(w, h, depth, params.copy())
     a = _u16(f)
     out = np.empty_like(a)
     with ctx.lock:
@@ -267,10 +297,10 @@ def estimate_shift(reference: np.ndarray, moving: np.ndarray, max_shift: int = 1
     p.max_shift = max_shift
     ctx = _context(w, h, depth, p)
     s = CShift()
+    a16, b16 = _u16(a), _u16(b)
     with ctx.lock:
-        _native.check(_native.lib.froi_estimate_shift(ctx.handle, _u16(a).ctypes.data,
-                                                      _u16(b).ctypes.data, max_shift,
-                                                      ctypes.byref(s)), "estimate_shift")
+        _native.check(_native.lib.froi_estimate_shift(ctx.handle, a16.ctypes.data, b16.ctypes.data,
+                                                      max_shift, ctypes.byref(s)), "estimate_shift")
     return Shift(s.dx, s.dy, s.confidence)
 
 
@@ -292,10 +322,10 @@ def compute_flow(prev: np.ndarray, nxt: np.ndarray, params: FlowParams | Extract
     ctx = _context(w, h, depth, ep)
     u = np.empty((h, w), np.float32)
     v = np.empty((h, w), np.float32)
+    a16, b16 = _u16(a), _u16(b)
     with ctx.lock:
-        _native.check(_native.lib.froi_compute_flow(ctx.handle, _u16(a).ctypes.data,
-                                                    _u16(b).ctypes.data, u.ctypes.data,
-                                                    v.ctypes.data), "compute_flow")
+        _native.check(_native.lib.froi_compute_flow(ctx.handle, a16.ctypes.data, b16.ctypes.data,
+                                                    u.ctypes.data, v.ctypes.data), "compute_flow")
     return u, v
 
 
@@ -338,9 +368,10 @@ def saliency(u: np.ndarray, v: np.ndarray, frame: np.ndarray, flow_weight: float
     out = np.empty((h, w), np.float64)
     uu = np.ascontiguousarray(u, dtype=np.float32)
     vv = np.ascontiguousarray(v, dtype=np.float32)
+    f16 = _u16(f)
     with ctx.lock:
         _native.check(_native.lib.froi_saliency(ctx.handle, uu.ctypes.data, vv.ctypes.data,
-                                                _u16(f).ctypes.data, out.ctypes.data), "saliency")
+                                                f16.ctypes.data, out.ctypes.data), "saliency")
     return out
 
 
@@ -420,9 +451,10 @@ def mask_from_flow(u: np.ndarray, v: np.ndarray, raw: np.ndarray, dx: int = 0, d
     st = CFrameStats()
     uu = np.ascontiguousarray(u, dtype=np.float32)
     vv = np.ascontiguousarray(v, dtype=np.float32)
+    f16 = _u16(f)
     with ctx.lock:
         _native.check(_native.lib.froi_mask_from_flow(ctx.handle, uu.ctypes.data, vv.ctypes.data,
-                                                      _u16(f).ctypes.data, dx, dy, mask.ctypes.data,
+                                                      f16.ctypes.data, dx, dy, mask.ctypes.data,
                                                       ctypes.byref(st)), "mask_from_flow")
     return mask, dict(mask_count=st.mask_count, components=st.components,
                       raw_fraction=st.raw_fraction)

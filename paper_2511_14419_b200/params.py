@@ -22,7 +22,7 @@ from dataclasses import dataclass, field
 __all__ = [
     "UsageError", "DataError", "InternalError", "DenoiseParams", "FlowParams", "RoiParams",
     "ExtractParams", "Shift", "ExtractInfo", "StageTimes", "CParams", "CShift", "CFrameStats",
-    "CStageTimes", "GRADIENT_IMAGE", "GRADIENT_FLOW", "SHIFT_CONFIDENCE_THRESHOLD",
+    "CStageTimes", "CKernelTimes", "GRADIENT_IMAGE", "GRADIENT_FLOW", "SHIFT_CONFIDENCE_THRESHOLD",
     "DEFAULT_MAX_SHIFT",
 ]
 
@@ -147,6 +147,16 @@ class CFrameStats(ctypes.Structure):
 class CStageTimes(ctypes.Structure):
     _fields_ = [("denoise_ns", ctypes.c_uint64), ("flow_ns", ctypes.c_uint64),
                 ("roi_ns", ctypes.c_uint64), ("encode_ns", ctypes.c_uint64)]
+
+
+class CKernelTimes(ctypes.Structure):
+    """``froi_kernel_times`` (include/froi/froi.h)."""
+    _fields_ = [(n, ctypes.c_uint64) for n in (
+        "denoise_ns", "fft_forward_ns", "expand_ns", "register_ns", "expand_shifted_ns",
+        "flow_iter_ns", "mask_ns", "pairs", "frames", "flow_iter_launches", "batches")]
+
+    def as_dict(self) -> dict:
+        return {n: int(getattr(self, n)) for n, _ in self._fields_}
 
 
 @dataclass
