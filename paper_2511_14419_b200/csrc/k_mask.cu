@@ -61,14 +61,6 @@ __device__ __forceinline__ double normalize(double v, double lo, double inv, int
 }
 
 template <typename T>
-__device__ __forceinline__ double saliency_at(const PairPix<T>& px, const PairInfo& I, double w,
-                                              double w1, int x, int y) {
-    const double nf = normalize(px.fmag(x, y), I.fmag_lo, I.fmag_inv, I.fmag_zero);
-    const double ng = normalize(px.grad(x, y), I.grad_lo, I.grad_inv, I.grad_zero);
-    return dadd(dmul(w, nf), dmul(w1, ng));
-}
-
-template <typename T>
 __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P,
                                                const MaskBuffers& b, const PairInfo& I, int p) {
     PairPix<T> px;
@@ -84,6 +76,11 @@ __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P
 }
 
 // ------------------------------------------------------------------ radix select
+// Exact k-th order statistics over 64-bit keys (IEEE bit patterns of non-negative doubles).
+// Each query walks MSD digits of 11 bits with integer histograms; a pass also records min/max of
+// the keys still matching the prefix (all equal -> done), and once the selected bin holds at most
+// kSelCap keys the next pass collects them and k_sel_scan sorts them in shared memory.  The first
+// pass of phase A is fused into the producer that materialises |flow| and |grad I|.
 constexpr int SNT = 512;
 
 __device__ __forceinline__ void sel_digit(int bits_done, int& shift, int& width) {
@@ -95,79 +92,149 @@ __device__ __forceinline__ bool sel_match(unsigned long long key, const SelState
     return s.bits_done == 0 || (key >> (64 - s.bits_done)) == (s.prefix >> (64 - s.bits_done));
 }
 
-// PHASE 0: queries 0,1 on |flow|, 2,3 on |grad|.  PHASE 1: query 0 on S (or on b.map).
-template <typename T, int PHASE>
-__global__ void __launch_bounds__(SNT) k_sel_pass(Geom g, DevParams P, MaskBuffers b,
-                                                  const double* map) {
-    __shared__ unsigned int hist[kMaxQueries][kSelBins];
-    __shared__ SelState st[kMaxQueries];
-    __shared__ unsigned long long smn[kMaxQueries], smx[kMaxQueries];
+// Key sources.  Phase A: |flow| for queries 0,1 and |grad I| for 2,3 (producer or buffers).
+// Phase B: saliency for query 0, computed from the buffers, or read from a given map (tap).
+template <typename T>
+struct SrcProduce {
+    PairPix<T> px;
+    float* fm;
+    double* gr;
+    static constexpr int NQ = 4;
+    __device__ __forceinline__ void keys(long long i, int x, int y, const bool* act,
+                                         unsigned long long* k) const {
+        const float f = hypotf_glibc(px.flow[i].x, px.flow[i].y);
+        const double gg = px.grad(x, y);
+        fm[i] = f;
+        gr[i] = gg;
+        k[0] = k[1] = dkey((double)f);
+        k[2] = k[3] = dkey(gg);
+    }
+};
+
+struct SrcBufA {
+    const float* fm;
+    const double* gr;
+    static constexpr int NQ = 4;
+    __device__ __forceinline__ void keys(long long i, int, int, const bool* act,
+                                         unsigned long long* k) const {
+        if (act[0] || act[1]) k[0] = k[1] = dkey((double)fm[i]);
+        if (act[2] || act[3]) k[2] = k[3] = dkey(gr[i]);
+    }
+};
+
+__device__ __forceinline__ double sal_from(const PairInfo& I, double w, double w1, float f, double gg) {
+    const double nf = normalize((double)f, I.fmag_lo, I.fmag_inv, I.fmag_zero);
+    const double ng = normalize(gg, I.grad_lo, I.grad_inv, I.grad_zero);
+    return dadd(dmul(w, nf), dmul(w1, ng));
+}
+
+struct SrcSal {
+    const float* fm;
+    const double* gr;
+    PairInfo I;
+    double w, w1;
+    static constexpr int NQ = 1;
+    __device__ __forceinline__ double value(long long i) const { return sal_from(I, w, w1, fm[i], gr[i]); }
+    __device__ __forceinline__ void keys(long long i, int, int, const bool*, unsigned long long* k) const {
+        k[0] = dkey(value(i));
+    }
+};
+
+struct SrcMap {
+    const double* map;
+    static constexpr int NQ = 1;
+    __device__ __forceinline__ double value(long long i) const { return map[i]; }
+    __device__ __forceinline__ void keys(long long i, int, int, const bool*, unsigned long long* k) const {
+        k[0] = dkey(map[i]);
+    }
+};
+
+// One pass of every active query of one pair over a contiguous pixel range.
+template <class Src>
+__device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src, bool produce) {
+    constexpr int NQ = Src::NQ;
+    __shared__ unsigned int hist[NQ][kSelBins];
+    __shared__ SelState st[NQ];
+    __shared__ unsigned long long smn[NQ], smx[NQ];
     __shared__ int any_active;
-    const int p = blockIdx.y;
-    const int nq = PHASE == 0 ? 4 : 1;
-    if (threadIdx.x < nq) {
+    if (threadIdx.x < NQ) {
         st[threadIdx.x] = b.sel[p * kMaxQueries + threadIdx.x];
         smn[threadIdx.x] = ~0ull;
         smx[threadIdx.x] = 0ull;
     }
-    if (threadIdx.x == 0) any_active = 0;
+    for (int i = threadIdx.x; i < NQ * kSelBins; i += SNT) (&hist[0][0])[i] = 0;
     __syncthreads();
-    if (threadIdx.x == 0)
-        for (int q = 0; q < nq; ++q) any_active |= !st[q].done;
-    for (int i = threadIdx.x; i < nq * kSelBins; i += SNT) (&hist[0][0])[i] = 0;
+    if (threadIdx.x == 0) {
+        int a = 0;
+        for (int q = 0; q < NQ; ++q) a |= st[q].mode != SEL_DONE;
+        any_active = a;
+    }
     __syncthreads();
-    if (!any_active) return;
-    const PairInfo I = b.info[p];
-    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
-    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
-    bool act[kMaxQueries];
-    int sh[kMaxQueries], wd[kMaxQueries];
-    unsigned long long lmn[kMaxQueries], lmx[kMaxQueries];
-    for (int q = 0; q < nq; ++q) {
-        act[q] = !st[q].done;
+    if (!any_active && !produce) return;
+    bool act[NQ], col[NQ];
+    int sh[NQ], wd[NQ];
+    unsigned long long lmn[NQ], lmx[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        act[q] = st[q].mode != SEL_DONE;
+        col[q] = st[q].mode == SEL_COLLECT;
         sel_digit(st[q].bits_done, sh[q], wd[q]);
         lmn[q] = ~0ull;
         lmx[q] = 0ull;
     }
-    const bool need_f = PHASE == 0 && (act[0] || act[1]);
-    const bool need_g = PHASE == 0 && (act[2] || act[3]);
     const long long n = (long long)g.W * g.H;
     const long long per = cdiv<long long>(n, gridDim.x);
     const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
-    for (long long i = i0 + threadIdx.x; i < i1; i += SNT) {
-        const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
-        unsigned long long k0 = 0, k1 = 0;
-        if (PHASE == 0) {
-            if (need_f) k0 = dkey(px.fmag(x, y));
-            if (need_g) k1 = dkey(px.grad(x, y));
-        } else {
-            k0 = dkey(map ? map[i] : saliency_at(px, I, w, w1, x, y));
+    const int lane = threadIdx.x & 31;
+    for (long long base = i0; base < i1; base += SNT) {
+        const long long i = base + threadIdx.x;
+        const bool valid = i < i1;
+        unsigned long long k[NQ];
+        if (valid) {
+            const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
+            src.keys(i, x, y, act, k);
         }
 #pragma unroll
-        for (int q = 0; q < nq; ++q) {
+        for (int q = 0; q < NQ; ++q) {
             if (!act[q]) continue;
-            const unsigned long long key = (PHASE == 0 && q >= 2) ? k1 : k0;
-            if (!sel_match(key, st[q])) continue;
-            atomicAdd(&hist[q][(key >> sh[q]) & ((1u << wd[q]) - 1)], 1u);
-            lmn[q] = min(lmn[q], key);
-            lmx[q] = max(lmx[q], key);
+            const bool m = valid && sel_match(k[q], st[q]);
+            if (col[q]) {
+                // warp-aggregated append of the remaining candidates
+                const unsigned int bal = __ballot_sync(0xffffffffu, m);
+                if (bal) {
+                    unsigned int basei = 0;
+                    const int leader = __ffs(bal) - 1;
+                    if (lane == leader) basei = atomicAdd(b.cand_count + p * kMaxQueries + q, __popc(bal));
+                    basei = __shfl_sync(0xffffffffu, basei, leader);
+                    if (m) {
+                        const unsigned int idx = basei + __popc(bal & ((1u << lane) - 1u));
+                        if (idx < (unsigned)kSelCap)
+                            b.cand[((size_t)p * kMaxQueries + q) * kSelCap + idx] = k[q];
+                    }
+                }
+            } else if (m) {
+                atomicAdd(&hist[q][(k[q] >> sh[q]) & ((1u << wd[q]) - 1u)], 1u);
+                lmn[q] = min(lmn[q], k[q]);
+                lmx[q] = max(lmx[q], k[q]);
+            }
         }
     }
-    for (int q = 0; q < nq; ++q) {
-        if (!act[q]) continue;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        if (!act[q] || col[q]) continue;
         unsigned long long a = lmn[q], c = lmx[q];
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
             c = max(c, __shfl_xor_sync(0xffffffffu, c, o));
         }
-        if ((threadIdx.x & 31) == 0) {
+        if (lane == 0) {
             atomicMin(&smn[q], a);
             atomicMax(&smx[q], c);
         }
     }
     __syncthreads();
-    for (int q = 0; q < nq; ++q) {
-        if (!act[q]) continue;
+    for (int q = 0; q < NQ; ++q) {
+        if (!act[q] || col[q]) continue;
         unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
         for (int i = threadIdx.x; i < kSelBins; i += SNT)
             if (hist[q][i]) atomicAdd(gh + i, hist[q][i]);
@@ -178,15 +245,96 @@ __global__ void __launch_bounds__(SNT) k_sel_pass(Geom g, DevParams P, MaskBuffe
     }
 }
 
-// One CTA per (pair, query): locate the digit holding the rank, narrow the prefix.
+// Phase-A producer: |flow| (glibc hypotf) and |grad I| materialised + the first radix pass.
+template <typename T>
+__global__ void __launch_bounds__(SNT) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
+    const int p = blockIdx.y;
+    const PairInfo I = b.info[p];
+    SrcProduce<T> src;
+    src.px = make_pix<T>(g, P, b, I, p);
+    src.fm = b.fm + (size_t)p * g.W * g.H;
+    src.gr = b.gr + (size_t)p * g.W * g.H;
+    sel_pass_body(g, b, p, src, true);
+}
+
+__global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
+    const int p = blockIdx.y;
+    SrcBufA src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H};
+    sel_pass_body(g, b, p, src, false);
+}
+
+__global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map) {
+    const int p = blockIdx.y;
+    if (map) {
+        SrcMap src{map};
+        sel_pass_body(g, b, p, src, false);
+    } else {
+        SrcSal src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H, b.info[p],
+                   P.flow_weight, 1.0 - P.flow_weight};
+        sel_pass_body(g, b, p, src, false);
+    }
+}
+
+// One CTA per (pair, query): narrow the prefix after a histogram pass, or sort the collected
+// candidates after a collect pass.
 __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
+    extern __shared__ unsigned long long cs[];  // kSelCap candidates
     const int p = blockIdx.x / nq, q = blockIdx.x % nq;
     SelState* sp = b.sel + p * kMaxQueries + q;
     __shared__ SelState s;
     __shared__ unsigned int part[256];
+    __shared__ unsigned long long lo_pos, hi_pos;
     if (threadIdx.x == 0) s = *sp;
     __syncthreads();
-    if (s.done) return;
+    if (s.mode == SEL_DONE) return;
+    if (s.mode == SEL_COLLECT) {
+        unsigned int* cc = b.cand_count + p * kMaxQueries + q;
+        const unsigned int n = min((unsigned int)kSelCap, *cc);
+        int np2 = 1;
+        while (np2 < (int)n) np2 <<= 1;
+        const unsigned long long* src = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
+        for (int i = threadIdx.x; i < np2; i += 256) cs[i] = i < (int)n ? src[i] : ~0ull;
+        __syncthreads();
+        for (int k = 2; k <= np2; k <<= 1)
+            for (int j = k >> 1; j > 0; j >>= 1) {
+                for (int i = threadIdx.x; i < np2; i += 256) {
+                    const int ixj = i ^ j;
+                    if (ixj > i) {
+                        const bool up = (i & k) == 0;
+                        const unsigned long long a = cs[i], c = cs[ixj];
+                        if ((a > c) == up) {
+                            cs[i] = c;
+                            cs[ixj] = a;
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+        if (threadIdx.x == 0) {
+            const unsigned long long r = cs[s.rank];
+            unsigned long long lo = 0, hi = n;  // lower_bound
+            while (lo < hi) {
+                const unsigned long long mid = (lo + hi) / 2;
+                if (cs[mid] < r) lo = mid + 1; else hi = mid;
+            }
+            lo_pos = lo;
+            hi = n;
+            unsigned long long lo2 = lo;
+            while (lo2 < hi) {
+                const unsigned long long mid = (lo2 + hi) / 2;
+                if (cs[mid] <= r) lo2 = mid + 1; else hi = mid;
+            }
+            hi_pos = lo2;
+            SelState ns = s;
+            ns.result = r;
+            ns.count_lt = (s.k0 - s.rank) + lo_pos;
+            ns.count_eq = hi_pos - lo_pos;
+            ns.mode = SEL_DONE;
+            *sp = ns;
+            *cc = 0;
+        }
+        return;
+    }
     unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
     constexpr int PER = kSelBins / 256;
     unsigned int loc[PER];
@@ -197,7 +345,6 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
     }
     part[threadIdx.x] = tot;
     __syncthreads();
-    // inclusive scan of per-thread totals (Hillis-Steele)
     for (int o = 1; o < 256; o <<= 1) {
         const unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
         __syncthreads();
@@ -214,16 +361,24 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
                 int shift, width;
                 sel_digit(s.bits_done, shift, width);
                 SelState n = s;
-                n.prefix = s.prefix | ((unsigned long long)bin << shift);
-                n.rank = r - c;
-                n.count = loc[j];
-                n.bits_done = s.bits_done + width;
-                if (s.mn == s.mx) {  // every prefix match is the same value
-                    n.done = 1;
+                if (s.mn == s.mx) {  // every key of the prefix group equals the answer
+                    n.mode = SEL_DONE;
                     n.result = s.mn;
-                } else if (n.bits_done >= 64) {
-                    n.done = 1;
-                    n.result = n.prefix;
+                    n.count_lt = s.k0 - s.rank;
+                    n.count_eq = s.count;
+                } else {
+                    n.prefix = s.prefix | ((unsigned long long)bin << shift);
+                    n.rank = r - c;
+                    n.count = loc[j];
+                    n.bits_done = s.bits_done + width;
+                    if (n.bits_done >= 64) {
+                        n.mode = SEL_DONE;
+                        n.result = n.prefix;
+                        n.count_lt = s.k0 - n.rank;
+                        n.count_eq = n.count;
+                    } else if (n.count <= (unsigned long long)kSelCap) {
+                        n.mode = SEL_COLLECT;
+                    }
                 }
                 n.mn = ~0ull;
                 n.mx = 0ull;
@@ -236,20 +391,27 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
     for (int j = 0; j < PER; ++j) gh[threadIdx.x * PER + j] = 0u;
 }
 
-__global__ void k_sel_init_a(Geom g, MaskBuffers b, unsigned long long ilo, unsigned long long ihi) {
+__device__ __forceinline__ SelState sel_init(unsigned long long k0, unsigned long long n, bool done) {
+    SelState s;
+    s.prefix = 0;
+    s.rank = k0;
+    s.k0 = k0;
+    s.result = 0;
+    s.mn = ~0ull;
+    s.mx = 0;
+    s.count = n;
+    s.count_lt = 0;
+    s.count_eq = 0;
+    s.bits_done = 0;
+    s.mode = done ? SEL_DONE : SEL_HIST;
+    return s;
+}
+
+__global__ void k_sel_init_a(MaskBuffers b, unsigned long long n, unsigned long long ilo,
+                             unsigned long long ihi) {
     const int p = blockIdx.x;
-    if (threadIdx.x < kMaxQueries) {
-        SelState s;
-        s.prefix = 0;
-        s.rank = (threadIdx.x & 1) ? ihi : ilo;
-        s.result = 0;
-        s.mn = ~0ull;
-        s.mx = 0;
-        s.count = 0;
-        s.bits_done = 0;
-        s.done = 0;
-        b.sel[p * kMaxQueries + threadIdx.x] = s;
-    }
+    if (threadIdx.x < kMaxQueries)
+        b.sel[p * kMaxQueries + threadIdx.x] = sel_init((threadIdx.x & 1) ? ihi : ilo, n, false);
 }
 
 // robust_normalize parameters (roi.hpp:47-63), then the threshold query (roi.hpp:114-120).
@@ -271,24 +433,17 @@ __global__ void k_sel_init_b(MaskBuffers b, unsigned long long n, unsigned long 
         I.grad_inv = I.grad_zero ? 0.0 : ddiv(1.0, dg);
     }
     I.target = target;
-    SelState s;
-    s.prefix = 0;
-    s.rank = n - target;  // (target-1)-th largest == (n-target)-th smallest
-    s.result = 0;
-    s.mn = ~0ull;
-    s.mx = 0;
-    s.count = 0;
-    s.bits_done = 0;
-    s.done = target == 0;
-    b.sel[p * kMaxQueries] = s;
-    for (int q = 1; q < kMaxQueries; ++q) b.sel[p * kMaxQueries + q].done = 1;
+    // (target-1)-th largest == (n-target)-th smallest
+    b.sel[p * kMaxQueries] = sel_init(target ? n - target : 0, n, target == 0);
+    for (int q = 1; q < kMaxQueries; ++q) b.sel[p * kMaxQueries + q].mode = SEL_DONE;
 }
 
 // ------------------------------------------------------------------ threshold
 constexpr int TNT = 256;
 constexpr int TROWS = 4;  // rows per tie chunk
 
-__global__ void k_sel_finish_b(MaskBuffers b) {
+// threshold_mask decision (roi.hpp:114-137) from the exact counts of the selection.
+__global__ void k_sel_finish_b(MaskBuffers b, unsigned long long n) {
     const int p = blockIdx.x;
     if (threadIdx.x != 0) return;
     PairInfo& I = b.info[p];
@@ -299,74 +454,70 @@ __global__ void k_sel_finish_b(MaskBuffers b) {
         return;
     }
     I.boundary = dfromkey(s.result);
-    I.thr_mode = (I.boundary > 0.0) ? 0 : 2;
+    if (!(I.boundary > 0.0)) {
+        I.thr_mode = 2;
+        return;
+    }
+    I.count_eq = s.count_eq;
+    I.count_gt = n - s.count_lt - s.count_eq;
+    I.need = I.target - I.count_gt;
+    I.thr_mode = I.need >= I.count_eq ? 0 : 3;
 }
 
-template <typename T>
-__device__ __forceinline__ double sal_or_map(const PairPix<T>& px, const PairInfo& I, double w,
-                                             double w1, const double* map, int x, int y, int W) {
-    return map ? map[(size_t)y * W + x] : saliency_at(px, I, w, w1, x, y);
+template <class Src>
+__device__ __forceinline__ Src make_thr_src(const Geom& g, const DevParams& P, const MaskBuffers& b,
+                                            int p, const double* map);
+template <>
+__device__ __forceinline__ SrcSal make_thr_src<SrcSal>(const Geom& g, const DevParams& P,
+                                                       const MaskBuffers& b, int p, const double*) {
+    return SrcSal{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H, b.info[p],
+                  P.flow_weight, 1.0 - P.flow_weight};
+}
+template <>
+__device__ __forceinline__ SrcMap make_thr_src<SrcMap>(const Geom&, const DevParams&,
+                                                       const MaskBuffers&, int, const double* map) {
+    return SrcMap{map};
 }
 
-template <typename T>
+// Per-chunk tie counts, only for pairs that admit part of a tie group (thr_mode 3).
+template <class Src>
 __global__ void __launch_bounds__(TNT) k_thr_count(Geom g, DevParams P, MaskBuffers b,
                                                    const double* map) {
     const int p = blockIdx.y, chunk = blockIdx.x;
-    const PairInfo I = b.info[p];
-    __shared__ unsigned long long sg, se;
-    if (threadIdx.x == 0) { sg = 0; se = 0; }
+    const PairInfo& I = b.info[p];
+    if (I.thr_mode != 3) return;
+    __shared__ unsigned long long se;
+    if (threadIdx.x == 0) se = 0;
     __syncthreads();
-    if (I.thr_mode != 0) return;
-    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
-    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    const Src src = make_thr_src<Src>(g, P, b, p, map);
+    const double bd = I.boundary;
     const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
-    unsigned int cg = 0, ce = 0;
-    for (int y = y0; y < y1; ++y)
-        for (int x = threadIdx.x; x < g.W; x += TNT) {
-            const double s = sal_or_map(px, I, w, w1, map, x, y, g.W);
-            cg += s > I.boundary;
-            ce += s == I.boundary;
-        }
-    for (int o = 16; o > 0; o >>= 1) {
-        cg += __shfl_xor_sync(0xffffffffu, cg, o);
-        ce += __shfl_xor_sync(0xffffffffu, ce, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicAdd(&sg, (unsigned long long)cg);
-        atomicAdd(&se, (unsigned long long)ce);
-    }
+    unsigned int ce = 0;
+    for (long long i = (long long)y0 * g.W + threadIdx.x; i < (long long)y1 * g.W; i += TNT)
+        ce += src.value(i) == bd;
+    for (int o = 16; o > 0; o >>= 1) ce += __shfl_xor_sync(0xffffffffu, ce, o);
+    if ((threadIdx.x & 31) == 0 && ce) atomicAdd(&se, (unsigned long long)ce);
     __syncthreads();
-    if (threadIdx.x == 0) {
-        const int nch = gridDim.x;
-        b.tie_cnt[((size_t)p * nch + chunk) * 2 + 0] = sg;
-        b.tie_cnt[((size_t)p * nch + chunk) * 2 + 1] = se;
-    }
+    if (threadIdx.x == 0) b.tie_cnt[(size_t)p * gridDim.x + chunk] = se;
 }
 
-// Exclusive scan of the per-chunk tie counts; total count above the boundary.
+// Exclusive scan of the per-chunk tie counts (thr_mode 3 only).
 __global__ void __launch_bounds__(1024) k_thr_scan(MaskBuffers b, int nch) {
     const int p = blockIdx.x;
-    PairInfo& I = b.info[p];
-    if (I.thr_mode != 0) return;
-    __shared__ unsigned long long sgt[1024], seq[1024];
-    unsigned long long* tc = b.tie_cnt + (size_t)p * nch * 2;
+    if (b.info[p].thr_mode != 3) return;
+    __shared__ unsigned long long seq[1024];
+    unsigned long long* tc = b.tie_cnt + (size_t)p * nch;
     const int per = cdiv(nch, 1024);
-    unsigned long long g = 0, e = 0;
+    unsigned long long e = 0;
     for (int j = 0; j < per; ++j) {
         const int c = threadIdx.x * per + j;
-        if (c < nch) {
-            g += tc[c * 2];
-            e += tc[c * 2 + 1];
-        }
+        if (c < nch) e += tc[c];
     }
-    sgt[threadIdx.x] = g;
     seq[threadIdx.x] = e;
     __syncthreads();
     for (int o = 1; o < 1024; o <<= 1) {
-        const unsigned long long vg = threadIdx.x >= o ? sgt[threadIdx.x - o] : 0;
         const unsigned long long ve = threadIdx.x >= o ? seq[threadIdx.x - o] : 0;
         __syncthreads();
-        sgt[threadIdx.x] += vg;
         seq[threadIdx.x] += ve;
         __syncthreads();
     }
@@ -374,19 +525,15 @@ __global__ void __launch_bounds__(1024) k_thr_scan(MaskBuffers b, int nch) {
     for (int j = 0; j < per; ++j) {
         const int c = threadIdx.x * per + j;
         if (c < nch) {
-            const unsigned long long ce = tc[c * 2 + 1];
-            tc[c * 2 + 1] = run;  // exclusive prefix of ties before this chunk
+            const unsigned long long ce = tc[c];
+            tc[c] = run;
             run += ce;
         }
-    }
-    if (threadIdx.x == 0) {
-        I.count_gt = sgt[1023];
-        I.need = I.target > I.count_gt ? I.target - I.count_gt : 0;
     }
 }
 
 // Packed thresholded mask, bit x%32 of word (y, x/32); ties admitted in row-major order.
-template <typename T>
+template <class Src>
 __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuffers b,
                                                    const double* map) {
     const int p = blockIdx.y, chunk = blockIdx.x;
@@ -397,28 +544,37 @@ __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuff
     constexpr int NW = TNT / 32;
     __shared__ unsigned int wcnt[NW];
     __shared__ unsigned long long base;
+    const int nwords = (y1 - y0) * g.WW;
     if (I.thr_mode == 1) {
-        for (int i = threadIdx.x; i < (y1 - y0) * g.WW; i += TNT) out[(size_t)y0 * g.WW + i] = 0u;
+        for (int i = threadIdx.x; i < nwords; i += TNT) out[(size_t)y0 * g.WW + i] = 0u;
         return;
     }
-    const PairPix<T> px = make_pix<T>(g, P, b, I, p);
-    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
-    if (threadIdx.x == 0) base = I.thr_mode == 0 ? b.tie_cnt[((size_t)p * gridDim.x + chunk) * 2 + 1] : 0;
+    const Src src = make_thr_src<Src>(g, P, b, p, map);
+    if (I.thr_mode != 3) {
+        // no partial tie group: S >= b (mode 0) or S > 0 (mode 2), one word per warp
+        for (int wi = warp; wi < nwords; wi += NW) {
+            const int y = y0 + wi / g.WW, x = (wi % g.WW) * 32 + lane;
+            bool on = false;
+            if (x < g.W) {
+                const double s = src.value((long long)y * g.W + x);
+                on = I.thr_mode == 0 ? (s >= I.boundary) : (s > 0.0);
+            }
+            const unsigned int word = __ballot_sync(0xffffffffu, on);
+            if (lane == 0) out[(size_t)y0 * g.WW + wi] = word;
+        }
+        return;
+    }
+    if (threadIdx.x == 0) base = b.tie_cnt[(size_t)p * gridDim.x + chunk];
     __syncthreads();
-    const int nwords = (y1 - y0) * g.WW;
     for (int r0 = 0; r0 < nwords; r0 += NW) {
         const int wi = r0 + warp;
         bool gt = false, eq = false;
         if (wi < nwords) {
             const int y = y0 + wi / g.WW, x = (wi % g.WW) * 32 + lane;
             if (x < g.W) {
-                const double s = sal_or_map(px, I, w, w1, map, x, y, g.W);
-                if (I.thr_mode == 0) {
-                    gt = s > I.boundary;
-                    eq = s == I.boundary;
-                } else {
-                    gt = s > 0.0;
-                }
+                const double s = src.value((long long)y * g.W + x);
+                gt = s > I.boundary;
+                eq = s == I.boundary;
             }
         }
         const unsigned int eqm = __ballot_sync(0xffffffffu, eq);
@@ -759,17 +915,12 @@ __global__ void k_ensemble(const uint8_t* in, uint8_t* out, long long per, int n
     }
 }
 
-template <typename T>
 __global__ void __launch_bounds__(256) k_saliency_map(Geom g, DevParams P, MaskBuffers b,
                                                       double* out) {
-    const PairInfo I = b.info[0];
-    const PairPix<T> px = make_pix<T>(g, P, b, I, 0);
-    const double w = P.flow_weight, w1 = 1.0 - P.flow_weight;
+    const SrcSal src = make_thr_src<SrcSal>(g, P, b, 0, nullptr);
     const long long n = (long long)g.W * g.H;
-    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256) {
-        const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
-        out[i] = saliency_at(px, I, w, w1, x, y);
-    }
+    for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
+        out[i] = src.value(i);
 }
 
 int grid_for(long long work, int per_block) {
@@ -778,47 +929,73 @@ int grid_for(long long work, int per_block) {
     return (int)(b < 1 ? 1 : b);
 }
 
-template <typename T>
-void run_selects(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
-                 const double* map, bool phase_a, cudaStream_t s, uint64_t* launches) {
+constexpr int kSelPasses = 6;  // worst case: 64 key bits / 11, collect + sort, ties early
+
+size_t scan_smem() { return sizeof(unsigned long long) * kSelCap; }
+
+void set_scan_smem() {
+    static bool done = false;
+    if (!done) {
+        FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+        done = true;
+    }
+}
+
+int blocks_per_pair(const Geom& g, int n_pairs) {
     const long long n = (long long)g.W * g.H;
     int bpp = (int)cdiv<long long>(148 * 4, n_pairs);
-    bpp = max(1, min(bpp, (int)cdiv<long long>(n, 4096)));
-    const int passes = cdiv(64, kSelBits);
-    if (phase_a) {
-        k_sel_init_a<<<n_pairs, 32, 0, s>>>(g, b, (unsigned long long)(0.01 * (double)(n - 1)),
-                                           (unsigned long long)(0.99 * (double)(n - 1)));
-        FROI_LAUNCH_CHECK();
-        ++*launches;
-        for (int it = 0; it < passes; ++it) {
-            k_sel_pass<T, 0><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, nullptr);
-            k_sel_scan<<<n_pairs * 4, 256, 0, s>>>(b, 4);
-            FROI_LAUNCH_CHECK();
-            *launches += 2;
-        }
-    }
-    const unsigned long long target = (unsigned long long)llround(P.roi_threshold * (double)n);
-    k_sel_init_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, target, phase_a ? 1 : 0);
+    return max(1, min(bpp, (int)cdiv<long long>(n, 8192)));
+}
+
+// Phase A: the four robust_normalize percentiles.
+template <typename T>
+void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs, cudaStream_t s,
+               uint64_t* launches) {
+    const long long n = (long long)g.W * g.H;
+    const int bpp = blocks_per_pair(g, n_pairs);
+    set_scan_smem();
+    k_sel_init_a<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, (unsigned long long)(0.01 * (double)(n - 1)),
+                                       (unsigned long long)(0.99 * (double)(n - 1)));
+    k_mag_grad<T><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b);
+    k_sel_scan<<<n_pairs * 4, 256, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
-    ++*launches;
-    for (int it = 0; it < passes; ++it) {
-        k_sel_pass<T, 1><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, map);
-        k_sel_scan<<<n_pairs, 256, 0, s>>>(b, 1);
+    *launches += 3;
+    for (int it = 0; it < kSelPasses; ++it) {
+        k_sel_pass_a<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, b);
+        k_sel_scan<<<n_pairs * 4, 256, scan_smem(), s>>>(b, 4);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }
-    k_sel_finish_b<<<n_pairs, 32, 0, s>>>(b);
+}
+
+// Phase B: the round(t*n)-th largest saliency (or map value) and the tie decision.
+void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
+                  const double* map, bool from_stats, cudaStream_t s, uint64_t* launches) {
+    const long long n = (long long)g.W * g.H;
+    const int bpp = blocks_per_pair(g, n_pairs);
+    set_scan_smem();
+    const unsigned long long target = (unsigned long long)llround(P.roi_threshold * (double)n);
+    k_sel_init_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, target, from_stats ? 1 : 0);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
+    for (int it = 0; it < kSelPasses + 1; ++it) {
+        k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, map);
+        k_sel_scan<<<n_pairs, 256, scan_smem(), s>>>(b, 1);
+        FROI_LAUNCH_CHECK();
+        *launches += 2;
+    }
+    k_sel_finish_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n);
     FROI_LAUNCH_CHECK();
     ++*launches;
 }
 
-template <typename T>
+template <class Src>
 void run_threshold(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
                    const double* map, cudaStream_t s, uint64_t* launches) {
     const int nch = cdiv(g.H, TROWS);
-    k_thr_count<T><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    k_thr_count<Src><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
     k_thr_scan<<<n_pairs, 1024, 0, s>>>(b, nch);
-    k_thr_write<T><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    k_thr_write<Src><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
     FROI_LAUNCH_CHECK();
     *launches += 3;
 }
@@ -856,27 +1033,20 @@ void run_cleanup_output(const Geom& g, const DevParams& P, const MaskBuffers& b,
 void launch_mask_stage(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
                        cudaStream_t s, uint64_t* launches) {
     if (n_pairs <= 0) return;
-    if (g.sample_bytes == 1) {
-        run_selects<uint8_t>(g, P, b, n_pairs, nullptr, true, s, launches);
-        run_threshold<uint8_t>(g, P, b, n_pairs, nullptr, s, launches);
-    } else {
-        run_selects<uint16_t>(g, P, b, n_pairs, nullptr, true, s, launches);
-        run_threshold<uint16_t>(g, P, b, n_pairs, nullptr, s, launches);
-    }
+    if (g.sample_bytes == 1) run_stats<uint8_t>(g, P, b, n_pairs, s, launches);
+    else run_stats<uint16_t>(g, P, b, n_pairs, s, launches);
+    run_boundary(g, P, b, n_pairs, nullptr, true, s, launches);
+    run_threshold<SrcSal>(g, P, b, n_pairs, nullptr, s, launches);
     run_cleanup_output(g, P, b, n_pairs, P.open_radius, P.close_radius, P.min_area, s, launches);
 }
 
 void launch_saliency_map(const Geom& g, const DevParams& P, const MaskBuffers& b, double* d_out,
                          cudaStream_t s) {
     uint64_t l = 0;
-    const int gr = grid_for((long long)g.W * g.H, 256);
-    if (g.sample_bytes == 1) {
-        run_selects<uint8_t>(g, P, b, 1, nullptr, true, s, &l);
-        k_saliency_map<uint8_t><<<gr, 256, 0, s>>>(g, P, b, d_out);
-    } else {
-        run_selects<uint16_t>(g, P, b, 1, nullptr, true, s, &l);
-        k_saliency_map<uint16_t><<<gr, 256, 0, s>>>(g, P, b, d_out);
-    }
+    if (g.sample_bytes == 1) run_stats<uint8_t>(g, P, b, 1, s, &l);
+    else run_stats<uint16_t>(g, P, b, 1, s, &l);
+    run_boundary(g, P, b, 1, nullptr, true, s, &l);
+    k_saliency_map<<<grid_for((long long)g.W * g.H, 256), 256, 0, s>>>(g, P, b, d_out);
     FROI_LAUNCH_CHECK();
 }
 
@@ -885,13 +1055,8 @@ void launch_threshold_from_map(const Geom& g, const DevParams& P, const MaskBuff
     uint64_t l = 0;
     DevParams Q = P;
     Q.roi_threshold = threshold;
-    if (g.sample_bytes == 1) {
-        run_selects<uint8_t>(g, Q, b, 1, d_map, false, s, &l);
-        run_threshold<uint8_t>(g, Q, b, 1, d_map, s, &l);
-    } else {
-        run_selects<uint16_t>(g, Q, b, 1, d_map, false, s, &l);
-        run_threshold<uint16_t>(g, Q, b, 1, d_map, s, &l);
-    }
+    run_boundary(g, Q, b, 1, d_map, false, s, &l);
+    run_threshold<SrcMap>(g, Q, b, 1, d_map, s, &l);
 }
 
 void launch_cleanup_only(const Geom& g, const DevParams& P, const MaskBuffers& b,

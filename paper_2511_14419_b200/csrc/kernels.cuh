@@ -21,6 +21,8 @@ constexpr int kMaxLevels = 16;
 constexpr int kSelBits = 11;  // radix-select digit width
 constexpr int kSelBins = 1 << kSelBits;
 constexpr int kMaxQueries = 4;
+constexpr int kSelCap = 8192;  // candidates sorted in shared memory once a radix bin is this small
+enum SelMode { SEL_HIST = 0, SEL_COLLECT = 1, SEL_DONE = 2 };
 
 struct Geom {
     int W, H, depth, maxval;
@@ -45,10 +47,11 @@ struct PairInfo {
     double fmag_inv, grad_inv;
     int fmag_zero, grad_zero;  // robust_normalize degenerate -> all zeros
     double boundary;
+    unsigned long long count_eq;
     unsigned long long target;
     unsigned long long count_gt;
     unsigned long long need;
-    int thr_mode;  // 0 normal, 1 empty (target 0), 2 positive-only (boundary <= 0)
+    int thr_mode;  // 0 all ties admitted (S >= b), 1 empty, 2 positive-only, 3 partial ties
     unsigned int mask_count;
     unsigned int components;
     unsigned int pad1;
@@ -56,12 +59,15 @@ struct PairInfo {
 
 struct SelState {
     unsigned long long prefix;
-    unsigned long long rank;
+    unsigned long long rank;     // rank within the current prefix group
+    unsigned long long k0;       // requested rank (0-based, ascending)
     unsigned long long result;
-    unsigned long long mn, mx;  // min / max key of prefix matches in the last pass
-    unsigned long long count;   // prefix matches after the last pass
+    unsigned long long mn, mx;   // min / max key of prefix matches in the last pass
+    unsigned long long count;    // elements matching the prefix
+    unsigned long long count_lt; // on completion: elements below the result
+    unsigned long long count_eq; // on completion: elements equal to the result
     int bits_done;
-    int done;
+    int mode;                    // SelMode
 };
 
 // Per-batch device tables.
@@ -131,6 +137,10 @@ struct MaskBuffers {
     const void** raw;             // [pair] raw frame t pointer (T)
     SelState* sel;                // [pair][kMaxQueries]
     unsigned int* hist;           // [pair][kMaxQueries][kSelBins]
+    unsigned long long* cand;     // [pair][kMaxQueries][kSelCap]
+    unsigned int* cand_count;     // [pair][kMaxQueries]
+    float* fm;                    // [pair][H*W] |flow| (FlowField::mag)
+    double* gr;                   // [pair][H*W] |grad I|
     unsigned long long* tie_cnt;  // [pair][chunks][2]
     uint32_t* bits_thr;           // [pair][H*WW] thresholded (registered)
     uint32_t* bits_clean;         // [pair][H*WW] after open/close (registered)

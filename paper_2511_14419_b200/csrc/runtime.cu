@@ -239,6 +239,10 @@ struct froi_ctx {
     float2* d_flow1 = nullptr;
     SelState* d_sel = nullptr;
     unsigned int* d_hist = nullptr;
+    unsigned long long* d_cand = nullptr;
+    unsigned int* d_cand_count = nullptr;
+    float* d_fm = nullptr;
+    double* d_gr = nullptr;
     unsigned long long* d_tie = nullptr;
     uint32_t *d_bits_thr = nullptr, *d_bits_clean = nullptr, *d_bits_root = nullptr;
     int* d_labels = nullptr;
@@ -283,6 +287,10 @@ struct froi_ctx {
         b.raw = d_pair_raw[tb_];
         b.sel = d_sel;
         b.hist = d_hist;
+        b.cand = d_cand;
+        b.cand_count = d_cand_count;
+        b.fm = d_fm;
+        b.gr = d_gr;
         b.tie_cnt = d_tie;
         b.bits_thr = d_bits_thr;
         b.bits_clean = d_bits_clean;
@@ -374,6 +382,11 @@ void ctx_alloc(froi_ctx* c) {
     c->d_sel = dalloc<SelState>((size_t)kMaxQueries * P, &t);
     c->d_hist = dalloc<unsigned int>((size_t)kMaxQueries * kSelBins * P, &t);
     FROI_CUDA(cudaMemset(c->d_hist, 0, sizeof(unsigned int) * (size_t)kMaxQueries * kSelBins * P));
+    c->d_cand = dalloc<unsigned long long>((size_t)kMaxQueries * kSelCap * P, &t);
+    c->d_cand_count = dalloc<unsigned int>((size_t)kMaxQueries * P, &t);
+    FROI_CUDA(cudaMemset(c->d_cand_count, 0, sizeof(unsigned int) * (size_t)kMaxQueries * P));
+    c->d_fm = dalloc<float>(px * P, &t);
+    c->d_gr = dalloc<double>(px * P, &t);
     const int nch = (g.H + 3) / 4;
     c->d_tie = dalloc<unsigned long long>((size_t)nch * 2 * P, &t);
     const size_t words = (size_t)g.H * g.WW;
@@ -406,7 +419,7 @@ void ctx_free(froi_ctx* c) {
     void* ptrs[] = {c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
-                    c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_tie, c->d_bits_thr,
+                    c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
                     c->d_bits_clean, c->d_bits_root, c->d_labels, c->d_area_local, c->d_area_total,
                     c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry, c->d_arena};
     for (void* p : ptrs)
