@@ -1,5 +1,5 @@
 // k_flow.cu — pyramid, polynomial expansion and the fused flow iteration
-// (flow.hpp:118-345), fp32 storage and arithmetic with fp64 coordinates / solve.
+// (flow.hpp:118-345): fp32 storage and arithmetic, exact fp32 warp coordinates, fp64 solve.
 //
 //   k_pyr_down   7-tap Gaussian (sigma 1, rows then columns, edge-replicated) fused with the
 //                bilinear resample to floor(w*scale) x floor(h*scale)            (flow.hpp:259-298)
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, f
 }
 
 // ------------------------------------------------------------------ flow iteration
-constexpr int FX = 32, FY = 32, FNT = 256;
+constexpr int FX = 32, FY = 32, FNT = 256, SEG = 8;
 
 struct IterArgs {
     int l;        // level
@@ -276,19 +276,35 @@ struct IterArgs {
     float2* flow_out;
 };
 
-__device__ __forceinline__ double bilinear_d(const float2* p, int comp, int w, int h, double x,
-                                             double y) {
-    int x0, x1, y0, y1;
-    double fx, fy;
-    bl_index(x, w, x0, x1, fx);
-    bl_index(y, h, y0, y1, fy);
-    const float2 a = p[(size_t)y0 * w + x0], b = p[(size_t)y0 * w + x1];
-    const float2 c = p[(size_t)y1 * w + x0], d = p[(size_t)y1 * w + x1];
-    const double va = comp ? a.y : a.x, vb = comp ? b.y : b.x;
-    const double vc = comp ? c.y : c.x, vd = comp ? d.y : d.x;
-    const double top = va * (1 - fx) + vb * fx;
-    const double bot = vc * (1 - fx) + vd * fx;
-    return top * (1 - fy) + bot * fy;
+// bilinear() index rule (flow.hpp:157-168) for the coordinate i + d, computed exactly in fp32:
+// the integer part goes to the index, d - floor(d) is exact, so (x0, fx) equal the reference's.
+__device__ __forceinline__ void bl_split(int i, float d, int n, int& i0, float& f) {
+    const float fl = floorf(d);
+    i0 = i + (int)fl;
+    f = d - fl;
+    if (i0 < 0) {
+        i0 = 0;
+        f = 0.f;
+    } else if (i0 >= n - 1) {
+        i0 = n - 2;
+        f = 1.f;
+    }
+}
+
+// Coarse-to-fine upsampling of the prior (flow.hpp:318-337), fp32.
+__device__ __forceinline__ float2 upsample_at(const float2* c, int cw, int ch, float fx, float fy,
+                                              int x, int y) {
+    const float sx = (x + 0.5f) / fx - 0.5f, sy = (y + 0.5f) / fy - 0.5f;
+    int x0, y0;
+    float ax, ay;
+    const float flx = floorf(sx), fly = floorf(sy);
+    bl_split((int)flx, sx - flx, cw, x0, ax);
+    bl_split((int)fly, sy - fly, ch, y0, ay);
+    const float2 a = c[(size_t)y0 * cw + x0], b = c[(size_t)y0 * cw + x0 + 1];
+    const float2 d = c[(size_t)(y0 + 1) * cw + x0], e = c[(size_t)(y0 + 1) * cw + x0 + 1];
+    const float u = ((a.x * (1.f - ax) + b.x * ax) * (1.f - ay) + (d.x * (1.f - ax) + e.x * ax) * ay) * fx;
+    const float v = ((a.y * (1.f - ax) + b.y * ax) * (1.f - ay) + (d.y * (1.f - ax) + e.y * ax) * ay) * fy;
+    return make_float2(u, v);
 }
 
 __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, size_t pair_off,
@@ -296,32 +312,28 @@ __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, siz
     if (a.mode == 0) return make_float2(0.f, 0.f);
     const int w = g.lw[a.l];
     if (a.mode == 1) return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * w + x];
-    // upscale the coarser estimate (flow.hpp:318-337)
     const int cw = g.lw[a.l + 1], ch = g.lh[a.l + 1];
-    const double fx = (double)w / cw, fy = (double)g.lh[a.l] / ch;
-    const double sx = (x + 0.5) / fx - 0.5, sy = (y + 0.5) / fy - 0.5;
-    const float2* c = a.flow_in + pair_off + g.loff[a.l + 1];
-    return make_float2((float)(bilinear_d(c, 0, cw, ch, sx, sy) * fx),
-                       (float)(bilinear_d(c, 1, cw, ch, sx, sy) * fy));
+    return upsample_at(a.flow_in + pair_off + g.loff[a.l + 1], cw, ch, (float)((double)w / cw),
+                       (float)((double)g.lh[a.l] / ch), x, y);
 }
 
-__global__ void __launch_bounds__(FNT) k_flow_iter(Geom g, int R, IterArgs a,
-                                                   const float4* __restrict__ exA_f,
-                                                   const float* __restrict__ exB_f,
-                                                   const float4* __restrict__ exA_p,
-                                                   const float* __restrict__ exB_p,
-                                                   const int* __restrict__ prev,
-                                                   const int* __restrict__ next,
-                                                   const PairInfo* __restrict__ info) {
+template <int MAXV>
+__global__ void __launch_bounds__(FNT, 4) k_flow_iter(Geom g, int R, IterArgs a,
+                                                      const float4* __restrict__ exA_f,
+                                                      const float* __restrict__ exB_f,
+                                                      const float4* __restrict__ exA_p,
+                                                      const float* __restrict__ exB_p,
+                                                      const int* __restrict__ prev,
+                                                      const int* __restrict__ next,
+                                                      const PairInfo* __restrict__ info) {
     extern __shared__ float smem_f[];
     const int p = blockIdx.z;
     const int l = a.l;
     const int w = g.lw[l], h = g.lh[l];
     const int x0 = blockIdx.x * FX, y0 = blockIdx.y * FY;
     const int HW = FX + 2 * R, HH = FY + 2 * R;
-    const size_t plane = (size_t)HW * HH;
-    float* G = smem_f;                 // 5 * HH * HW
-    float* V = G + 5 * plane;          // 5 * FY * HW
+    const int plane = HW * HH;
+    float* G = smem_f;  // 5 planes [HH][HW]; reused in place for the box sums
     const size_t pair_off = (size_t)p * g.lsum;
     const size_t lo = g.loff[l];
     const float4* pA = exA_f + (size_t)prev[p] * g.lsum + lo;
@@ -329,79 +341,127 @@ __global__ void __launch_bounds__(FNT) k_flow_iter(Geom g, int R, IterArgs a,
     const bool sh = info[p].shifted != 0;
     const float4* nA = (sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo;
     const float* nB = (sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // phase 1: normal-equation products over tile + halo (flow.hpp:212-232)
-    for (int i = threadIdx.x; i < (int)plane; i += FNT) {
-        const int hy = i / HW, hx = i - hy * HW;
-        const int gx = x0 - R + hx, gy = y0 - R + hy;
-        float g11 = 0.f, g12 = 0.f, g22 = 0.f, h1 = 0.f, h2 = 0.f;
-        if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-            const float2 pr = prior_at(g, a, pair_off, gx, gy);
-            const float du = pr.x, dv = pr.y;
-            int xa, xb, ya, yb;
-            double fxd, fyd;
-            bl_index(gx + (double)du, w, xa, xb, fxd);
-            bl_index(gy + (double)dv, h, ya, yb, fyd);
-            const float fx = (float)fxd, fy = (float)fyd;
-            const float4 q00 = __ldg(nA + (size_t)ya * w + xa), q01 = __ldg(nA + (size_t)ya * w + xb);
-            const float4 q10 = __ldg(nA + (size_t)yb * w + xa), q11 = __ldg(nA + (size_t)yb * w + xb);
-            const float b00 = __ldg(nB + (size_t)ya * w + xa), b01 = __ldg(nB + (size_t)ya * w + xb);
-            const float b10 = __ldg(nB + (size_t)yb * w + xa), b11 = __ldg(nB + (size_t)yb * w + xb);
-            const float ofx = 1.f - fx, ofy = 1.f - fy;
+    // phase 1: normal-equation products over tile + halo (flow.hpp:212-232); one warp per row
+    for (int hy = warp; hy < HH; hy += FNT / 32) {
+        const int gy = y0 - R + hy;
+        for (int hx = lane; hx < HW; hx += 32) {
+            const int gx = x0 - R + hx;
+            float g11 = 0.f, g12 = 0.f, g22 = 0.f, h1 = 0.f, h2 = 0.f;
+            if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+                const float2 pr = prior_at(g, a, pair_off, gx, gy);
+                const float du = pr.x, dv = pr.y;
+                int xa, ya;
+                float fx, fy;
+                bl_split(gx, du, w, xa, fx);
+                bl_split(gy, dv, h, ya, fy);
+                const float4* r0 = nA + (size_t)ya * w + xa;
+                const float* b0 = nB + (size_t)ya * w + xa;
+                const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r0 + w), q11 = __ldg(r0 + w + 1);
+                const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b0 + w), b11 = __ldg(b0 + w + 1);
+                const float ofx = 1.f - fx, ofy = 1.f - fy;
 #define BL(c) ((q00.c * ofx + q01.c * fx) * ofy + (q10.c * ofx + q11.c * fx) * fy)
-            const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
+                const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
 #undef BL
-            const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
-            const size_t o = (size_t)gy * w + gx;
-            const float4 pa = __ldg(pA + o);
-            const float pb = __ldg(pB + o);
-            const float a11 = 0.5f * (pa.x + na11);
-            const float a12 = 0.5f * (pa.y + na12);
-            const float a22 = 0.5f * (pa.z + na22);
-            const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
-            const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
-            g11 = a11 * a11 + a12 * a12;
-            g12 = (a11 + a22) * a12;
-            g22 = a12 * a12 + a22 * a22;
-            h1 = a11 * db1 + a12 * db2;
-            h2 = a12 * db1 + a22 * db2;
-        }
-        G[i] = g11;
-        G[plane + i] = g12;
-        G[2 * plane + i] = g22;
-        G[3 * plane + i] = h1;
-        G[4 * plane + i] = h2;
-    }
-    __syncthreads();
-    // phase 2: vertical window sums (out-of-image products are zero; divisor applied later)
-    for (int t = threadIdx.x; t < 5 * HW; t += FNT) {
-        const int c = t / HW, hx = t - c * HW;
-        const float* col = G + c * plane + hx;
-        float* vo = V + (size_t)c * FY * HW + hx;
-        float acc = 0.f;
-        for (int k = 0; k < 2 * R; ++k) acc += col[k * HW];
-        for (int ty = 0; ty < FY; ++ty) {
-            acc += col[(ty + 2 * R) * HW];
-            vo[ty * HW] = acc;
-            acc -= col[ty * HW];
+                const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
+                const size_t o = (size_t)gy * w + gx;
+                const float4 pa = __ldg(pA + o);
+                const float pb = __ldg(pB + o);
+                const float a11 = 0.5f * (pa.x + na11);
+                const float a12 = 0.5f * (pa.y + na12);
+                const float a22 = 0.5f * (pa.z + na22);
+                const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
+                const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
+                g11 = a11 * a11 + a12 * a12;
+                g12 = (a11 + a22) * a12;
+                g22 = a12 * a12 + a22 * a22;
+                h1 = a11 * db1 + a12 * db2;
+                h2 = a12 * db1 + a22 * db2;
+            }
+            const int i = hy * HW + hx;
+            G[i] = g11;
+            G[plane + i] = g12;
+            G[2 * plane + i] = g22;
+            G[3 * plane + i] = h1;
+            G[4 * plane + i] = h2;
         }
     }
     __syncthreads();
-    // phase 3: horizontal window sums into G (reused as S[5][FY][FX])
-    for (int t = threadIdx.x; t < 5 * FY; t += FNT) {
-        const int c = t / FY, ty = t - c * FY;
-        const float* row = V + (size_t)c * FY * HW + ty * HW;
-        float* so = G + (size_t)c * FY * FX + ty * FX;
-        float acc = 0.f;
-        for (int k = 0; k < 2 * R; ++k) acc += row[k];
-        for (int tx = 0; tx < FX; ++tx) {
-            acc += row[tx + 2 * R];
-            so[tx] = acc;
-            acc -= row[tx];
+    // phase 2: vertical 15-row sums, SEG outputs per task, results kept in registers and written
+    // back in place (rows 0..FY-1) after every task has read its inputs
+    // tasks per thread: 5 * HW * FY/SEG <= FNT * MAXV (MAXV 4 covers R <= 7, 8 covers R <= 30)
+    float vr[MAXV][SEG];
+    const int nv = 5 * HW * (FY / SEG);
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+        const int t = threadIdx.x + k * FNT;
+        if (t < nv) {
+            const int c = t / (HW * (FY / SEG));
+            const int rem = t - c * HW * (FY / SEG);
+            const int sg = rem / HW, hx = rem - sg * HW;
+            const float* col = G + c * plane + (sg * SEG) * HW + hx;
+            float acc = 0.f;
+            for (int j = 0; j <= 2 * R; ++j) acc += col[j * HW];
+            vr[k][0] = acc;
+#pragma unroll
+            for (int j = 1; j < SEG; ++j) {
+                acc += col[(j + 2 * R) * HW] - col[(j - 1) * HW];
+                vr[k][j] = acc;
+            }
         }
     }
     __syncthreads();
-    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253)
+#pragma unroll
+    for (int k = 0; k < MAXV; ++k) {
+        const int t = threadIdx.x + k * FNT;
+        if (t < nv) {
+            const int c = t / (HW * (FY / SEG));
+            const int rem = t - c * HW * (FY / SEG);
+            const int sg = rem / HW, hx = rem - sg * HW;
+            float* col = G + c * plane + (sg * SEG) * HW + hx;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) col[j * HW] = vr[k][j];
+        }
+    }
+    __syncthreads();
+    // phase 3: horizontal 15-column sums of the vertical sums, written back in place
+    constexpr int MAXH = 3;
+    float hr[MAXH][SEG];
+    const int nh = 5 * FY * (FX / SEG);
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) {
+        const int t = threadIdx.x + k * FNT;
+        if (t < nh) {
+            const int c = t / (FY * (FX / SEG));
+            const int rem = t - c * FY * (FX / SEG);
+            const int ty = rem / (FX / SEG), sg = rem - ty * (FX / SEG);
+            const float* row = G + c * plane + ty * HW + sg * SEG;
+            float acc = 0.f;
+            for (int j = 0; j <= 2 * R; ++j) acc += row[j];
+            hr[k][0] = acc;
+#pragma unroll
+            for (int j = 1; j < SEG; ++j) {
+                acc += row[j + 2 * R] - row[j - 1];
+                hr[k][j] = acc;
+            }
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) {
+        const int t = threadIdx.x + k * FNT;
+        if (t < nh) {
+            const int c = t / (FY * (FX / SEG));
+            const int rem = t - c * FY * (FX / SEG);
+            const int ty = rem / (FX / SEG), sg = rem - ty * (FX / SEG);
+            float* row = G + c * plane + ty * HW + sg * SEG;
+#pragma unroll
+            for (int j = 0; j < SEG; ++j) row[j] = hr[k][j];
+        }
+    }
+    __syncthreads();
+    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253), fp64
     float2* out = a.flow_out + pair_off + lo;
     for (int i = threadIdx.x; i < FX * FY; i += FNT) {
         const int ty = i / FX, tx = i - ty * FX;
@@ -410,16 +470,18 @@ __global__ void __launch_bounds__(FNT) k_flow_iter(Geom g, int R, IterArgs a,
         const int cx = min(w - 1, x + R) - max(0, x - R) + 1;
         const int cy = min(h - 1, y + R) - max(0, y - R) + 1;
         const double inv = 1.0 / (double)(cx * cy);
-        const double g11 = G[i] * inv, g12 = G[FX * FY + i] * inv, g22 = G[2 * FX * FY + i] * inv;
-        const double h1 = G[3 * FX * FY + i] * inv, h2 = G[4 * FX * FY + i] * inv;
+        const int si = ty * HW + tx;
+        const double g11 = G[si] * inv, g12 = G[plane + si] * inv, g22 = G[2 * plane + si] * inv;
+        const double h1 = G[3 * plane + si] * inv, h2 = G[4 * plane + si] * inv;
         const double det = g11 * g22 - g12 * g12;
         const double frob2 = g11 * g11 + 2.0 * g12 * g12 + g22 * g22;
         float2 r;
         if (!(det > 1e-9 * frob2)) {
             r = prior_at(g, a, pair_off, x, y);
         } else {
-            r.x = (float)((g22 * h1 - g12 * h2) / det);
-            r.y = (float)((-g12 * h1 + g11 * h2) / det);
+            const double rd = 1.0 / det;
+            r.x = (float)((g22 * h1 - g12 * h2) * rd);
+            r.y = (float)((-g12 * h1 + g11 * h2) * rd);
         }
         out[(size_t)y * w + x] = r;
     }
@@ -531,8 +593,10 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
                 const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
     if (n_pairs <= 0) return 0;
     const int R = P.window_radius;
-    const size_t smem = sizeof(float) * (5 * (size_t)(FX + 2 * R) * (FY + 2 * R) + 5 * (size_t)FY * (FX + 2 * R));
-    set_smem(k_flow_iter, smem);
+    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R) * (FY + 2 * R);
+    const bool small = R <= 7;
+    if (small) set_smem(k_flow_iter<4>, smem);
+    else set_smem(k_flow_iter<8>, smem);
     float2* buf[2] = {b.flow0, b.flow1};
     int cur = 0;
     for (int l = g.L - 1; l >= 0; --l) {
@@ -543,8 +607,12 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
             a.flow_in = buf[cur];
             a.flow_out = buf[1 - cur];
             dim3 grid(cdiv(g.lw[l], FX), cdiv(g.lh[l], FY), n_pairs);
-            k_flow_iter<<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
-                                                d_prev, d_next, d_info);
+            if (small)
+                k_flow_iter<4><<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
+                                                       d_prev, d_next, d_info);
+            else
+                k_flow_iter<8><<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
+                                                       d_prev, d_next, d_info);
             FROI_LAUNCH_CHECK();
             cur = 1 - cur;
         }
