@@ -1,6 +1,6 @@
 // k_denoise.cu — fused median + bilateral denoise (denoise.hpp:28-90), bit-exact.
 //
-// One CTA produces a 32x8 output tile of one frame slot.  The raw tile (halo = median radius +
+// One CTA produces a 32x16 output tile of one frame slot.  The raw tile (halo = median radius +
 // bilateral radius, edge-replicated) and the median tile (halo = bilateral radius) live in
 // shared memory; the bilateral sums run in fp64 in the reference's dy-major / dx-minor order
 // with explicit round-to-nearest operations (no FMA), the range LUT and spatial weights are the
@@ -14,7 +14,7 @@
 namespace froi {
 namespace {
 
-constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int TX = 32, TY = 16, NT = 256;  // 2 output rows per thread
 
 __device__ __forceinline__ void cswap(int& a, int& b) {
     const int t = min(a, b);
@@ -50,15 +50,19 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
     double* spat_s = (double*)smem;                 // side*side
     double* lut_s = spat_s + side * side;           // 256 (u8 only)
     const bool lut_in_smem = sizeof(T) == 1;
-    int* raw_s = (int*)(lut_s + (lut_in_smem ? 256 : 0));
+    double* medd_s = lut_s + (lut_in_smem ? 256 : 0);  // median tile as double (converted once)
+    int* raw_s = (int*)(medd_s + mw * mh);
     int* med_s = raw_s + rw * rh;
 
-    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-    int outv = 0;
+    unsigned long long sum = 0;
     if (!enabled) {
-        if (x < W && y < H) {
-            outv = src[(size_t)y * W + x];
-            dst[(size_t)y * W + x] = (T)outv;
+        for (int r = 0; r < TY; r += NT / TX) {
+            const int x = x0 + threadIdx.x, y = y0 + threadIdx.y + r;
+            if (x < W && y < H) {
+                const int v = src[(size_t)y * W + x];
+                dst[(size_t)y * W + x] = (T)v;
+                sum += (unsigned long long)v;
+            }
         }
     } else {
         for (int i = tid; i < side * side; i += NT) spat_s[i] = spatial_g[i];
@@ -97,34 +101,40 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
                 }
             }
             med_s[i] = m;
+            medd_s[i] = (double)m;
         }
         __syncthreads();
-        if (x < W && y < H) {
-            // bilateral_filter (denoise.hpp:63-79)
-            const int c = med_s[(threadIdx.y + br) * mw + threadIdx.x + br];
-            double num = 0.0, dn = 0.0;
-            for (int dy = -br; dy <= br; ++dy) {
-                const int* row = med_s + (threadIdx.y + br + dy) * mw + threadIdx.x + br;
-                for (int dx = -br; dx <= br; ++dx) {
-                    const int v = row[dx];
-                    const int d = abs(v - c);
-                    const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
-                    const double wgt = dmul(spat_s[(dy + br) * side + dx + br], lw);
-                    num = dadd(num, dmul(wgt, (double)v));
-                    dn = dadd(dn, wgt);
+        for (int r = 0; r < TY; r += NT / TX) {
+            const int ty = threadIdx.y + r;
+            const int x = x0 + threadIdx.x, y = y0 + ty;
+            if (x < W && y < H) {
+                // bilateral_filter (denoise.hpp:63-79): fp64, dy-major / dx-minor, no FMA
+                const int c = med_s[(ty + br) * mw + threadIdx.x + br];
+                double num = 0.0, dn = 0.0;
+                for (int dy = -br; dy <= br; ++dy) {
+                    const int* row = med_s + (ty + br + dy) * mw + threadIdx.x + br;
+                    const double* rowd = medd_s + (ty + br + dy) * mw + threadIdx.x + br;
+                    const double* sp = spat_s + (dy + br) * side + br;
+                    for (int dx = -br; dx <= br; ++dx) {
+                        const int d = abs(row[dx] - c);
+                        const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
+                        const double wgt = dmul(sp[dx], lw);
+                        num = dadd(num, dmul(wgt, rowd[dx]));
+                        dn = dadd(dn, wgt);
+                    }
                 }
+                double q = ddiv(num, dn);
+                q = (q < 0.0) ? 0.0 : q;
+                q = ((double)maxval < q) ? (double)maxval : q;
+                const int outv = (int)round(q);
+                dst[(size_t)y * W + x] = (T)outv;
+                sum += (unsigned long long)outv;
             }
-            double q = ddiv(num, dn);
-            q = (q < 0.0) ? 0.0 : q;
-            q = ((double)maxval < q) ? (double)maxval : q;
-            outv = (int)round(q);
-            dst[(size_t)y * W + x] = (T)outv;
         }
     }
     // integer sum of the denoised tile for the registration mean
-    unsigned long long s = (unsigned long long)outv;
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if ((tid & 31) == 0 && s) atomicAdd(sums + slot, s);
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+    if ((tid & 31) == 0 && sum) atomicAdd(sums + slot, sum);
 }
 
 }  // namespace
@@ -135,9 +145,10 @@ void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw,
     if (n_slots <= 0) return;
     const int mr = p.median_radius, br = p.bilateral_radius;
     const int R1 = mr + br, side = 2 * br + 1;
-    const size_t smem = sizeof(double) * (side * side + (g.sample_bytes == 1 ? 256 : 0)) +
+    const size_t smem = sizeof(double) * (side * side + (g.sample_bytes == 1 ? 256 : 0) +
+                                          (TX + 2 * br) * (TY + 2 * br)) +
                         sizeof(int) * ((TX + 2 * R1) * (TY + 2 * R1) + (TX + 2 * br) * (TY + 2 * br));
-    dim3 grid(cdiv(g.W, TX), cdiv(g.H, TY), n_slots), block(TX, TY);
+    dim3 grid(cdiv(g.W, TX), cdiv(g.H, TY), n_slots), block(TX, NT / TX);
     if (g.sample_bytes == 1) {
         if (smem > 48 * 1024)
             FROI_CUDA(cudaFuncSetAttribute(k_denoise<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

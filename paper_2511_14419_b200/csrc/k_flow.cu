@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, f
 }
 
 // ------------------------------------------------------------------ flow iteration
-constexpr int FX = 32, FY = 32, FNT = 256, SEG = 8;
+constexpr int FX = 64, FY = 32, FNT = 512;
 
 struct IterArgs {
     int l;        // level
@@ -317,8 +317,9 @@ __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, siz
                        (float)((double)g.lh[a.l] / ch), x, y);
 }
 
-template <int MAXV>
-__global__ void __launch_bounds__(FNT, 4) k_flow_iter(Geom g, int R, IterArgs a,
+// One CTA per FX x FY output tile of one pair (FNT threads, 2 CTAs per SM).
+template <int R>
+__global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const float4* __restrict__ exA_f,
                                                       const float* __restrict__ exB_f,
                                                       const float4* __restrict__ exA_p,
@@ -327,12 +328,11 @@ __global__ void __launch_bounds__(FNT, 4) k_flow_iter(Geom g, int R, IterArgs a,
                                                       const int* __restrict__ next,
                                                       const PairInfo* __restrict__ info) {
     extern __shared__ float smem_f[];
+    constexpr int HW = FX + 2 * R, HH = FY + 2 * R, PL = HW * HH;
     const int p = blockIdx.z;
     const int l = a.l;
     const int w = g.lw[l], h = g.lh[l];
     const int x0 = blockIdx.x * FX, y0 = blockIdx.y * FY;
-    const int HW = FX + 2 * R, HH = FY + 2 * R;
-    const int plane = HW * HH;
     float* G = smem_f;  // 5 planes [HH][HW]; reused in place for the box sums
     const size_t pair_off = (size_t)p * g.lsum;
     const size_t lo = g.loff[l];
@@ -381,87 +381,69 @@ __global__ void __launch_bounds__(FNT, 4) k_flow_iter(Geom g, int R, IterArgs a,
             }
             const int i = hy * HW + hx;
             G[i] = g11;
-            G[plane + i] = g12;
-            G[2 * plane + i] = g22;
-            G[3 * plane + i] = h1;
-            G[4 * plane + i] = h2;
+            G[PL + i] = g12;
+            G[2 * PL + i] = g22;
+            G[3 * PL + i] = h1;
+            G[4 * PL + i] = h2;
         }
     }
     __syncthreads();
-    // phase 2: vertical 15-row sums, SEG outputs per task, results kept in registers and written
-    // back in place (rows 0..FY-1) after every task has read its inputs
-    // tasks per thread: 5 * HW * FY/SEG <= FNT * MAXV (MAXV 4 covers R <= 7, 8 covers R <= 30)
-    float vr[MAXV][SEG];
-    const int nv = 5 * HW * (FY / SEG);
+    // phase 2: vertical (2R+1)-row running sums down each of the 5*HW columns (FY outputs each),
+    // held in registers and written back in place after every column has been read
+    float acc_r[FY];
+    const int vt = threadIdx.x;
+    const bool vact = vt < 5 * HW;
+    if (vact) {
+        const int c = vt / HW, hx = vt - c * HW;
+        const float* col = G + c * PL + hx;
+        float acc = 0.f;
 #pragma unroll
-    for (int k = 0; k < MAXV; ++k) {
-        const int t = threadIdx.x + k * FNT;
-        if (t < nv) {
-            const int c = t / (HW * (FY / SEG));
-            const int rem = t - c * HW * (FY / SEG);
-            const int sg = rem / HW, hx = rem - sg * HW;
-            const float* col = G + c * plane + (sg * SEG) * HW + hx;
-            float acc = 0.f;
-            for (int j = 0; j <= 2 * R; ++j) acc += col[j * HW];
-            vr[k][0] = acc;
+        for (int j = 0; j <= 2 * R; ++j) acc += col[j * HW];
+        acc_r[0] = acc;
 #pragma unroll
-            for (int j = 1; j < SEG; ++j) {
-                acc += col[(j + 2 * R) * HW] - col[(j - 1) * HW];
-                vr[k][j] = acc;
-            }
+        for (int j = 1; j < FY; ++j) {
+            acc += col[(j + 2 * R) * HW] - col[(j - 1) * HW];
+            acc_r[j] = acc;
         }
     }
     __syncthreads();
+    if (vact) {
+        const int c = vt / HW, hx = vt - c * HW;
+        float* col = G + c * PL + hx;
 #pragma unroll
-    for (int k = 0; k < MAXV; ++k) {
-        const int t = threadIdx.x + k * FNT;
-        if (t < nv) {
-            const int c = t / (HW * (FY / SEG));
-            const int rem = t - c * HW * (FY / SEG);
-            const int sg = rem / HW, hx = rem - sg * HW;
-            float* col = G + c * plane + (sg * SEG) * HW + hx;
+        for (int j = 0; j < FY; ++j) col[j * HW] = acc_r[j];
+    }
+    __syncthreads();
+    // phase 3: horizontal running sums along each of the 5*FY rows, in 32-wide segments
+    constexpr int NSEG = FX / 32;
+    const bool hact = threadIdx.x < 5 * FY * NSEG;
+    if (hact) {
+        const int c = threadIdx.x / (FY * NSEG);
+        const int rem = threadIdx.x - c * FY * NSEG;
+        const int ty = rem / NSEG, sg = rem - ty * NSEG;
+        const float* row = G + c * PL + ty * HW + sg * 32;
+        float acc = 0.f;
 #pragma unroll
-            for (int j = 0; j < SEG; ++j) col[j * HW] = vr[k][j];
+        for (int j = 0; j <= 2 * R; ++j) acc += row[j];
+        acc_r[0] = acc;
+#pragma unroll
+        for (int j = 1; j < 32; ++j) {
+            acc += row[j + 2 * R] - row[j - 1];
+            acc_r[j] = acc;
         }
     }
     __syncthreads();
-    // phase 3: horizontal 15-column sums of the vertical sums, written back in place
-    constexpr int MAXH = 3;
-    float hr[MAXH][SEG];
-    const int nh = 5 * FY * (FX / SEG);
+    if (hact) {
+        const int c = threadIdx.x / (FY * NSEG);
+        const int rem = threadIdx.x - c * FY * NSEG;
+        const int ty = rem / NSEG, sg = rem - ty * NSEG;
+        float* row = G + c * PL + ty * HW + sg * 32;
 #pragma unroll
-    for (int k = 0; k < MAXH; ++k) {
-        const int t = threadIdx.x + k * FNT;
-        if (t < nh) {
-            const int c = t / (FY * (FX / SEG));
-            const int rem = t - c * FY * (FX / SEG);
-            const int ty = rem / (FX / SEG), sg = rem - ty * (FX / SEG);
-            const float* row = G + c * plane + ty * HW + sg * SEG;
-            float acc = 0.f;
-            for (int j = 0; j <= 2 * R; ++j) acc += row[j];
-            hr[k][0] = acc;
-#pragma unroll
-            for (int j = 1; j < SEG; ++j) {
-                acc += row[j + 2 * R] - row[j - 1];
-                hr[k][j] = acc;
-            }
-        }
+        for (int j = 0; j < 32; ++j) row[j] = acc_r[j];
     }
     __syncthreads();
-#pragma unroll
-    for (int k = 0; k < MAXH; ++k) {
-        const int t = threadIdx.x + k * FNT;
-        if (t < nh) {
-            const int c = t / (FY * (FX / SEG));
-            const int rem = t - c * FY * (FX / SEG);
-            const int ty = rem / (FX / SEG), sg = rem - ty * (FX / SEG);
-            float* row = G + c * plane + ty * HW + sg * SEG;
-#pragma unroll
-            for (int j = 0; j < SEG; ++j) row[j] = hr[k][j];
-        }
-    }
-    __syncthreads();
-    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253), fp64
+    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
+    // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
     float2* out = a.flow_out + pair_off + lo;
     for (int i = threadIdx.x; i < FX * FY; i += FNT) {
         const int ty = i / FX, tx = i - ty * FX;
@@ -469,22 +451,37 @@ __global__ void __launch_bounds__(FNT, 4) k_flow_iter(Geom g, int R, IterArgs a,
         if (x >= w || y >= h) continue;
         const int cx = min(w - 1, x + R) - max(0, x - R) + 1;
         const int cy = min(h - 1, y + R) - max(0, y - R) + 1;
-        const double inv = 1.0 / (double)(cx * cy);
+        const float inv = 1.f / (float)(cx * cy);
         const int si = ty * HW + tx;
-        const double g11 = G[si] * inv, g12 = G[plane + si] * inv, g22 = G[2 * plane + si] * inv;
-        const double h1 = G[3 * plane + si] * inv, h2 = G[4 * plane + si] * inv;
-        const double det = g11 * g22 - g12 * g12;
-        const double frob2 = g11 * g11 + 2.0 * g12 * g12 + g22 * g22;
+        const float g11 = G[si] * inv, g12 = G[PL + si] * inv, g22 = G[2 * PL + si] * inv;
+        const float h1 = G[3 * PL + si] * inv, h2 = G[4 * PL + si] * inv;
+        const float q = g12 * g12;
+        const float qe = fmaf(g12, g12, -q);
+        const float det = fmaf(g11, g22, -q) - qe;
+        const float frob2 = fmaf(g11, g11, fmaf(2.f * g12, g12, g22 * g22));
         float2 r;
-        if (!(det > 1e-9 * frob2)) {
+        if (!(det > 1e-9f * frob2)) {
             r = prior_at(g, a, pair_off, x, y);
         } else {
-            const double rd = 1.0 / det;
-            r.x = (float)((g22 * h1 - g12 * h2) * rd);
-            r.y = (float)((-g12 * h1 + g11 * h2) * rd);
+            r.x = (g22 * h1 - g12 * h2) / det;
+            r.y = (g11 * h2 - g12 * h1) / det;
         }
         out[(size_t)y * w + x] = r;
     }
+}
+
+template <int R>
+void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
+                 const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R) * (FY + 2 * R);
+    static bool attr = false;
+    if (!attr) {
+        FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY), n_pairs);
+    k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info);
+    FROI_LAUNCH_CHECK();
 }
 
 template <typename K>
@@ -593,10 +590,6 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
                 const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
     if (n_pairs <= 0) return 0;
     const int R = P.window_radius;
-    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R) * (FY + 2 * R);
-    const bool small = R <= 7;
-    if (small) set_smem(k_flow_iter<4>, smem);
-    else set_smem(k_flow_iter<8>, smem);
     float2* buf[2] = {b.flow0, b.flow1};
     int cur = 0;
     for (int l = g.L - 1; l >= 0; --l) {
@@ -606,14 +599,16 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
             a.mode = it > 0 ? 1 : (l == g.L - 1 ? 0 : 2);
             a.flow_in = buf[cur];
             a.flow_out = buf[1 - cur];
-            dim3 grid(cdiv(g.lw[l], FX), cdiv(g.lh[l], FY), n_pairs);
-            if (small)
-                k_flow_iter<4><<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
-                                                       d_prev, d_next, d_info);
-            else
-                k_flow_iter<8><<<grid, FNT, smem, s>>>(g, R, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p,
-                                                       d_prev, d_next, d_info);
-            FROI_LAUNCH_CHECK();
+            switch (R) {  // window_size 3..15 (the reference default is 15)
+                case 1: launch_iter<1>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 2: launch_iter<2>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 3: launch_iter<3>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 4: launch_iter<4>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 5: launch_iter<5>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 6: launch_iter<6>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                case 7: launch_iter<7>(g, a, b, d_prev, d_next, d_info, n_pairs, s); break;
+                default: throw Error(1, "flow: window_size > 15 is not supported by the GPU flow kernel");
+            }
             cur = 1 - cur;
         }
     }

@@ -26,28 +26,57 @@ __device__ __forceinline__ int brev(int x, int log2n) {
     return log2n == 0 ? 0 : (int)(__brev((unsigned)x) >> (32 - log2n));
 }
 
+// (v * w) as GCC expands std::complex<double> multiplication, then u +- v (fft.hpp:32-35).
+__device__ __forceinline__ void bfly(double2& u, double2& v, const double2 w) {
+    const double vr = dsub(dmul(v.x, w.x), dmul(v.y, w.y));
+    const double vi = dadd(dmul(v.x, w.y), dmul(v.y, w.x));
+    const double2 nu = make_double2(dadd(u.x, vr), dadd(u.y, vi));
+    v = make_double2(dsub(u.x, vr), dsub(u.y, vi));
+    u = nu;
+}
+
 // In-place radix-2 stages over `ncol` interleaved transforms of length n (element i of
 // transform c at a[i*ncol + c]); input already bit-reversed.  tw: stage with half-length h
-// uses tw[h-1 .. 2h-2] (the reference's w sequence for len = 2h).
+// uses tw[h-1 .. 2h-2] (the reference's w sequence for len = 2h).  Two consecutive stages are
+// fused per pass on groups {i, i+h, i+2h, i+3h} held in registers: the butterflies and their
+// operands are exactly the reference's, only the number of shared-memory round trips halves.
 __device__ __forceinline__ void fft_stages(double2* a, int n, int log2n, int ncol,
                                            const double2* tw) {
-    const int nb = (n >> 1) * ncol;
-    for (int s = 0; s < log2n; ++s) {
+    int s = 0;
+    for (; s + 1 < log2n; s += 2) {
         const int h = 1 << s;
+        const int ng = (n >> 2) * ncol;
+        for (int j = threadIdx.x; j < ng; j += blockDim.x) {
+            const int c = j % ncol;
+            const int b = j / ncol;
+            const int k = b & (h - 1);
+            const int i = ((b >> s) << (s + 2)) + k;
+            double2* p0 = a + i * ncol + c;
+            double2 e0 = p0[0], e1 = p0[h * ncol], e2 = p0[2 * h * ncol], e3 = p0[3 * h * ncol];
+            const double2 w1 = tw[h - 1 + k];
+            bfly(e0, e1, w1);
+            bfly(e2, e3, w1);
+            bfly(e0, e2, tw[2 * h - 1 + k]);
+            bfly(e1, e3, tw[2 * h - 1 + k + h]);
+            p0[0] = e0;
+            p0[h * ncol] = e1;
+            p0[2 * h * ncol] = e2;
+            p0[3 * h * ncol] = e3;
+        }
+        __syncthreads();
+    }
+    if (s < log2n) {  // odd log2n: one trailing radix-2 stage
+        const int h = 1 << s;
+        const int nb = (n >> 1) * ncol;
         for (int j = threadIdx.x; j < nb; j += blockDim.x) {
             const int c = j % ncol;
             const int b = j / ncol;
             const int k = b & (h - 1);
             const int i1 = ((b >> s) << (s + 1)) + k;
-            const int i2 = i1 + h;
-            const double2 w = tw[h - 1 + k];
-            const double2 u = a[i1 * ncol + c];
-            const double2 v = a[i2 * ncol + c];
-            // (v * w) as GCC expands std::complex<double> multiplication
-            const double vr = dsub(dmul(v.x, w.x), dmul(v.y, w.y));
-            const double vi = dadd(dmul(v.x, w.y), dmul(v.y, w.x));
-            a[i1 * ncol + c] = make_double2(dadd(u.x, vr), dadd(u.y, vi));
-            a[i2 * ncol + c] = make_double2(dsub(u.x, vr), dsub(u.y, vi));
+            double2 u = a[i1 * ncol + c], v = a[(i1 + h) * ncol + c];
+            bfly(u, v, tw[h - 1 + k]);
+            a[i1 * ncol + c] = u;
+            a[(i1 + h) * ncol + c] = v;
         }
         __syncthreads();
     }
@@ -236,7 +265,7 @@ void set_smem(K kernel, size_t bytes) {
 }
 
 int column_block(const Geom& g) {
-    int cb = 8192 / g.ph;
+    int cb = 4096 / g.ph;  // 64 KB of column data per CTA
     if (cb < 1) cb = 1;
     if (cb > g.pw) cb = g.pw;
     return cb;

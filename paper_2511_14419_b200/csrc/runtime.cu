@@ -80,7 +80,7 @@ std::string validate(const froi_params* p) {
         return "roi: unknown gradient_source";
     // limits of this implementation's shared-memory tiles
     if (p->poly_n > 15) return "flow: poly_n > 15 is not supported by the GPU kernels";
-    if (p->window_size > 61) return "flow: window_size > 61 is not supported by the GPU kernels";
+    if (p->window_size > 15) return "flow: window_size > 15 is not supported by the GPU kernels";
     if (p->median_radius > 3) return "denoise: median_radius > 3 is not supported by the GPU kernels";
     if (p->bilateral_radius > 7) return "denoise: bilateral_radius > 7 is not supported by the GPU kernels";
     if (p->open_radius > 31 || p->close_radius > 31) return "roi: radii > 31 are not supported by the GPU kernels";
