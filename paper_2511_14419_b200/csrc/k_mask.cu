@@ -29,6 +29,7 @@ struct PairPix {
     int W, H, dx, dy;
     double inv_maxval;
     int grad_src;
+    const double* lut;  // shared-memory v/maxval table for 8-bit frames (nullptr: convert)
 
     __device__ __forceinline__ double fmag(int x, int y) const {
         const float2 f = flow[(size_t)y * W + x];
@@ -38,7 +39,8 @@ struct PairPix {
     __device__ __forceinline__ double img(int x, int y) const {
         const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
         const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
-        return dmul((double)raw[(size_t)sy * W + sx], inv_maxval);
+        const int v = raw[(size_t)sy * W + sx];
+        return lut ? lut[v] : dmul((double)v, inv_maxval);
     }
     // gradient_magnitude (roi.hpp:65-74)
     __device__ __forceinline__ double grad(int x, int y) const {
@@ -72,6 +74,7 @@ __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P
     px.dy = I.dy;
     px.inv_maxval = 1.0 / (double)g.maxval;
     px.grad_src = P.gradient_source;
+    px.lut = nullptr;
     return px;
 }
 
@@ -162,7 +165,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
         smn[threadIdx.x] = ~0ull;
         smx[threadIdx.x] = 0ull;
     }
-    for (int i = threadIdx.x; i < NQ * kSelBins; i += SNT) (&hist[0][0])[i] = 0;
+    for (int i = threadIdx.x; i < NQ * kSelBins; i += blockDim.x) (&hist[0][0])[i] = 0;
     __syncthreads();
     if (threadIdx.x == 0) {
         int a = 0;
@@ -186,7 +189,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     const long long per = cdiv<long long>(n, gridDim.x);
     const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
     const int lane = threadIdx.x & 31;
-    for (long long base = i0; base < i1; base += SNT) {
+    for (long long base = i0; base < i1; base += blockDim.x) {
         const long long i = base + threadIdx.x;
         const bool valid = i < i1;
         unsigned long long k[NQ];
@@ -212,10 +215,23 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                             b.cand[((size_t)p * kMaxQueries + q) * kSelCap + idx] = k[q];
                     }
                 }
-            } else if (m) {
-                atomicAdd(&hist[q][(k[q] >> sh[q]) & ((1u << wd[q]) - 1u)], 1u);
-                lmn[q] = min(lmn[q], k[q]);
-                lmx[q] = max(lmx[q], k[q]);
+            } else {
+                // histogram update; a warp whose matching keys share one bin adds once
+                const unsigned int bin = (unsigned int)((k[q] >> sh[q]) & ((1u << wd[q]) - 1u));
+                const unsigned int bal = __ballot_sync(0xffffffffu, m);
+                if (bal) {
+                    const int leader = __ffs(bal) - 1;
+                    const unsigned int b0 = __shfl_sync(0xffffffffu, bin, leader);
+                    if (__all_sync(0xffffffffu, !m || bin == b0)) {
+                        if (lane == leader) atomicAdd(&hist[q][b0], (unsigned int)__popc(bal));
+                    } else if (m) {
+                        atomicAdd(&hist[q][bin], 1u);
+                    }
+                }
+                if (m) {
+                    lmn[q] = min(lmn[q], k[q]);
+                    lmx[q] = max(lmx[q], k[q]);
+                }
             }
         }
     }
@@ -236,7 +252,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     for (int q = 0; q < NQ; ++q) {
         if (!act[q] || col[q]) continue;
         unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
-        for (int i = threadIdx.x; i < kSelBins; i += SNT)
+        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
             if (hist[q][i]) atomicAdd(gh + i, hist[q][i]);
         if (threadIdx.x == 0) {
             atomicMin(&b.sel[p * kMaxQueries + q].mn, smn[q]);
@@ -246,12 +262,19 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
 }
 
 // Phase-A producer: |flow| (glibc hypotf) and |grad I| materialised + the first radix pass.
+constexpr int PNT_MG = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(SNT) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
+__global__ void __launch_bounds__(PNT_MG) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
+    __shared__ double lut[256];
     const int p = blockIdx.y;
     const PairInfo I = b.info[p];
     SrcProduce<T> src;
     src.px = make_pix<T>(g, P, b, I, p);
+    if (sizeof(T) == 1) {
+        for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dmul((double)v, src.px.inv_maxval);
+        src.px.lut = lut;  // filled before the first barrier inside sel_pass_body
+    }
     src.fm = b.fm + (size_t)p * g.W * g.H;
     src.gr = b.gr + (size_t)p * g.W * g.H;
     sel_pass_body(g, b, p, src, true);
@@ -677,17 +700,25 @@ __global__ void __launch_bounds__(MNT) k_morph(Geom g, MaskBuffers b, int ro, in
 }
 
 // ------------------------------------------------------------------ connected components
-constexpr int CT = 32;  // CCL tile edge
+// 8-connected labelling on runs of set pixels (label_components roi.hpp:184-234 defines only
+// the partition and the areas, which is all the area filter uses).  A run [x0, x1] of row y
+// touches a run [c, d] of row y-1 iff c <= x1+1 and d >= x0-1.  Runs are extracted from the
+// packed words with bit tricks (one warp per row), unions are lock-free atomicMin union-find on
+// run ids, areas are summed at the roots, and surviving runs are painted into a keep mask.
+constexpr int RNT = 256;  // 8 warps = 8 rows per CTA
 
-__device__ __forceinline__ int lfind(const int* P, int x) {
-    while (P[x] != x) x = P[x];
-    return x;
+__device__ __forceinline__ int rfind(int* P, int x) {
+    while (true) {
+        const int p = __ldcg(P + x);
+        if (p == x) return x;
+        x = p;
+    }
 }
-__device__ __forceinline__ void lunite(int* P, int a, int b) {
+__device__ __forceinline__ void runite(int* P, int a, int b) {
     bool done = false;
     while (!done) {
-        a = lfind(P, a);
-        b = lfind(P, b);
+        a = rfind(P, a);
+        b = rfind(P, b);
         if (a < b) {
             const int old = atomicMin(&P[b], a);
             done = old == b;
@@ -701,158 +732,136 @@ __device__ __forceinline__ void lunite(int* P, int a, int b) {
         }
     }
 }
-__device__ __forceinline__ int gfind(int* L, int x) {
-    while (true) {
-        const int p = __ldcg(L + x);
-        if (p == x) return x;
-        x = p;
+
+__device__ __forceinline__ unsigned int warp_excl_scan(unsigned int v, unsigned int& total) {
+    const int lane = threadIdx.x & 31;
+    unsigned int x = v;
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    total = __shfl_sync(0xffffffffu, x, 31);
+    return x - v;
+}
+
+__global__ void __launch_bounds__(RNT) k_ccl_runs(Geom g, MaskBuffers b) {
+    const int p = blockIdx.y, lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (RNT / 32) + (threadIdx.x >> 5);
+    if (y >= g.H) return;
+    const uint32_t* m = b.bits_clean + ((size_t)p * g.H + y) * g.WW;
+    uint32_t* keep = b.bits_keep + ((size_t)p * g.H + y) * g.WW;
+    const size_t rbase = ((size_t)p * g.H + y) * g.RMAX;
+    uint16_t* x0 = b.run_x0 + rbase;
+    uint16_t* x1 = b.run_x1 + rbase;
+    int* par = b.run_par + (size_t)p * g.H * g.RMAX;
+    unsigned int* area = b.run_area + (size_t)p * g.H * g.RMAX;
+    unsigned int off_s = 0, off_e = 0;
+    uint32_t carry = 0;  // last word of the previous 32-word chunk
+    for (int w0 = 0; w0 < g.WW; w0 += 32) {
+        const int j = w0 + lane;
+        const uint32_t cur = j < g.WW ? m[j] : 0u;
+        if (j < g.WW) keep[j] = 0u;
+        uint32_t prv = __shfl_up_sync(0xffffffffu, cur, 1);
+        if (lane == 0) prv = carry;
+        uint32_t nxt = __shfl_down_sync(0xffffffffu, cur, 1);
+        if (lane == 31) nxt = (j + 1 < g.WW) ? m[j + 1] : 0u;
+        const uint32_t starts = cur & ~((cur << 1) | (prv >> 31));
+        const uint32_t ends = cur & ~((cur >> 1) | (nxt << 31));
+        unsigned int ts, te;
+        unsigned int ks = off_s + warp_excl_scan(__popc(starts), ts);
+        unsigned int ke = off_e + warp_excl_scan(__popc(ends), te);
+        for (uint32_t bits = starts; bits; bits &= bits - 1) x0[ks++] = (uint16_t)(j * 32 + __ffs(bits) - 1);
+        for (uint32_t bits = ends; bits; bits &= bits - 1) x1[ke++] = (uint16_t)(j * 32 + __ffs(bits) - 1);
+        off_s += ts;
+        off_e += te;
+        carry = __shfl_sync(0xffffffffu, cur, 31);
+    }
+    if (lane == 0) b.run_n[(size_t)p * g.H + y] = (int)off_s;
+    for (unsigned int k = lane; k < off_s; k += 32) {
+        const int id = y * g.RMAX + (int)k;
+        par[id] = id;
+        area[id] = 0u;
     }
 }
-__device__ __forceinline__ void gunite(int* L, int a, int b) {
-    bool done = false;
-    while (!done) {
-        a = gfind(L, a);
-        b = gfind(L, b);
-        if (a < b) {
-            const int old = atomicMin(&L[b], a);
-            done = old == b;
-            b = old;
-        } else if (b < a) {
-            const int old = atomicMin(&L[a], b);
-            done = old == a;
-            a = old;
-        } else {
-            done = true;
+
+__global__ void __launch_bounds__(RNT) k_ccl_union(Geom g, MaskBuffers b) {
+    const int p = blockIdx.y, lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (RNT / 32) + (threadIdx.x >> 5);
+    if (y < 1 || y >= g.H) return;
+    const int* rn = b.run_n + (size_t)p * g.H;
+    const int n = rn[y], np = rn[y - 1];
+    if (n == 0 || np == 0) return;
+    const size_t base = (size_t)p * g.H * g.RMAX;
+    const uint16_t* x0 = b.run_x0 + base + (size_t)y * g.RMAX;
+    const uint16_t* x1 = b.run_x1 + base + (size_t)y * g.RMAX;
+    const uint16_t* px0 = b.run_x0 + base + (size_t)(y - 1) * g.RMAX;
+    const uint16_t* px1 = b.run_x1 + base + (size_t)(y - 1) * g.RMAX;
+    int* par = b.run_par + base;
+    for (int k = lane; k < n; k += 32) {
+        const int a = x0[k], e = x1[k];
+        int lo = 0, hi = np;  // first run of row y-1 with x1 >= a-1
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if ((int)px1[mid] < a - 1) lo = mid + 1; else hi = mid;
+        }
+        for (int j = lo; j < np && (int)px0[j] <= e + 1; ++j)
+            runite(par, y * g.RMAX + k, (y - 1) * g.RMAX + j);
+    }
+}
+
+__global__ void __launch_bounds__(RNT) k_ccl_area(Geom g, MaskBuffers b) {
+    const int p = blockIdx.y, lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (RNT / 32) + (threadIdx.x >> 5);
+    if (y >= g.H) return;
+    const int n = b.run_n[(size_t)p * g.H + y];
+    const size_t base = (size_t)p * g.H * g.RMAX;
+    int* par = b.run_par + base;
+    for (int k = lane; k < n; k += 32) {
+        const int id = y * g.RMAX + k;
+        const int len = (int)b.run_x1[base + id] - (int)b.run_x0[base + id] + 1;
+        atomicAdd(&b.run_area[base + rfind(par, id)], (unsigned int)len);
+    }
+}
+
+// Paints the runs of components with area >= min_area into the keep mask; counts components.
+__global__ void __launch_bounds__(RNT) k_ccl_keep(Geom g, DevParams P, MaskBuffers b) {
+    const int p = blockIdx.y, lane = threadIdx.x & 31;
+    const int y = blockIdx.x * (RNT / 32) + (threadIdx.x >> 5);
+    unsigned int comps = 0;
+    if (y < g.H) {
+        const int n = b.run_n[(size_t)p * g.H + y];
+        const size_t base = (size_t)p * g.H * g.RMAX;
+        int* par = b.run_par + base;
+        uint32_t* keep = b.bits_keep + ((size_t)p * g.H + y) * g.WW;
+        for (int k = lane; k < n; k += 32) {
+            const int id = y * g.RMAX + k;
+            const int r = rfind(par, id);
+            const bool ok = b.run_area[base + r] >= (unsigned int)P.min_area;
+            comps += (ok && r == id);
+            if (!ok) continue;
+            const int a = b.run_x0[base + id], e = b.run_x1[base + id];
+            for (int wd = a >> 5; wd <= (e >> 5); ++wd) {
+                const int lo = max(a, wd * 32) - wd * 32, hi = min(e, wd * 32 + 31) - wd * 32;
+                const uint32_t msk = (hi == 31 ? 0xffffffffu : ((1u << (hi + 1)) - 1u)) & ~((1u << lo) - 1u);
+                atomicOr(keep + wd, msk);
+            }
         }
     }
+    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
+    if (lane == 0 && comps) atomicAdd(&b.info[p].components, comps);
 }
 
 __device__ __forceinline__ bool bit_at(const uint32_t* m, int WW, int x, int y) {
     return (m[(size_t)y * WW + (x >> 5)] >> (x & 31)) & 1u;
 }
 
-// Tile-local union-find (8-connected, label_components roi.hpp:184-234 semantics).
-__global__ void __launch_bounds__(CT* CT) k_ccl_local(Geom g, MaskBuffers b) {
-    __shared__ int P[CT * CT];
-    __shared__ unsigned int area[CT * CT];
-    const int p = blockIdx.z;
-    const int tx0 = blockIdx.x * CT, ty0 = blockIdx.y * CT;
-    const int x = tx0 + threadIdx.x, y = ty0 + threadIdx.y;
-    const int li = threadIdx.y * CT + threadIdx.x;
-    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
-    const bool in = x < g.W && y < g.H;
-    const bool set = in && bit_at(m, g.WW, x, y);
-    P[li] = set ? li : -1;
-    area[li] = 0;
-    __syncthreads();
-    if (set) {
-        if (threadIdx.x > 0 && P[li - 1] >= 0) lunite(P, li, li - 1);
-        if (threadIdx.y > 0) {
-            if (threadIdx.x > 0 && P[li - CT - 1] >= 0) lunite(P, li, li - CT - 1);
-            if (P[li - CT] >= 0) lunite(P, li, li - CT);
-            if (threadIdx.x < CT - 1 && P[li - CT + 1] >= 0) lunite(P, li, li - CT + 1);
-        }
-    }
-    __syncthreads();
-    int root = -1;
-    if (set) {
-        root = lfind(P, li);
-        atomicAdd(&area[root], 1u);
-    }
-    __syncthreads();
-    const size_t base = (size_t)p * g.W * g.H;
-    const bool is_root = set && root == li;
-    if (set) {
-        const int gr = (ty0 + root / CT) * g.W + tx0 + root % CT;
-        b.labels[base + (size_t)y * g.W + x] = gr;
-        if (is_root) {
-            b.area_local[base + (size_t)y * g.W + x] = area[li];
-            b.area_total[base + (size_t)y * g.W + x] = 0u;
-        }
-    }
-    const unsigned int rb = __ballot_sync(0xffffffffu, is_root);
-    if (threadIdx.x == 0 && y < g.H) b.bits_root[(size_t)p * g.H * g.WW + (size_t)y * g.WW + (tx0 >> 5)] = rb;
-}
-
-// Union across tile borders: each CTA handles the left column, top row and right column of
-// one tile and links every set pixel to its W, NW, N, NE neighbours in other tiles.
-__global__ void __launch_bounds__(3 * CT) k_ccl_merge(Geom g, MaskBuffers b) {
-    const int p = blockIdx.z;
-    const int tx0 = blockIdx.x * CT, ty0 = blockIdx.y * CT;
-    const int t = threadIdx.x;
-    int x, y;
-    if (t < CT) { x = tx0; y = ty0 + t; }
-    else if (t < 2 * CT) { x = tx0 + t - CT; y = ty0; }
-    else { x = tx0 + CT - 1; y = ty0 + t - 2 * CT; }
-    if (x >= g.W || y >= g.H) return;
-    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
-    if (!bit_at(m, g.WW, x, y)) return;
-    int* L = b.labels + (size_t)p * g.W * g.H;
-    const int me = y * g.W + x;
-    const int nx[4] = {x - 1, x - 1, x, x + 1};
-    const int ny[4] = {y, y - 1, y - 1, y - 1};
-    for (int k = 0; k < 4; ++k) {
-        if (nx[k] < 0 || nx[k] >= g.W || ny[k] < 0) continue;
-        if ((nx[k] / CT) == (x / CT) && (ny[k] / CT) == (y / CT)) continue;
-        if (!bit_at(m, g.WW, nx[k], ny[k])) continue;
-        gunite(L, me, ny[k] * g.W + nx[k]);
-    }
-}
-
-// Area of every component accumulated at its global root (a local root too).
-__global__ void __launch_bounds__(256) k_ccl_area(Geom g, MaskBuffers b) {
-    const int p = blockIdx.y;
-    const long long n = (long long)g.H * g.WW;
-    const uint32_t* rb = b.bits_root + (size_t)p * n;
-    int* L = b.labels + (size_t)p * g.W * g.H;
-    for (long long wi = blockIdx.x * 256LL + threadIdx.x; wi < n; wi += (long long)gridDim.x * 256) {
-        uint32_t bits = rb[wi];
-        const int y = (int)(wi / g.WW), xb = (int)(wi % g.WW) * 32;
-        while (bits) {
-            const int k = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int me = y * g.W + xb + k;
-            const int r = gfind(L, me);
-            atomicAdd(&b.area_total[(size_t)p * g.W * g.H + r], b.area_local[(size_t)p * g.W * g.H + me]);
-        }
-    }
-}
-
-// Path compression to the global root; counts components that survive min_area.
-__global__ void __launch_bounds__(256) k_ccl_compress(Geom g, DevParams P, MaskBuffers b) {
-    const int p = blockIdx.y;
-    const long long n = (long long)g.H * g.WW;
-    const uint32_t* m = b.bits_clean + (size_t)p * n;
-    const uint32_t* rb = b.bits_root + (size_t)p * n;
-    int* L = b.labels + (size_t)p * g.W * g.H;
-    unsigned int comps = 0;
-    for (long long wi = blockIdx.x * 256LL + threadIdx.x; wi < n; wi += (long long)gridDim.x * 256) {
-        uint32_t bits = m[wi];
-        const uint32_t roots = rb[wi];
-        const int y = (int)(wi / g.WW), xb = (int)(wi % g.WW) * 32;
-        while (bits) {
-            const int k = __ffs(bits) - 1;
-            bits &= bits - 1;
-            const int me = y * g.W + xb + k;
-            const int r = gfind(L, me);
-            if (((roots >> k) & 1u) && r == me &&
-                b.area_total[(size_t)p * g.W * g.H + me] >= (unsigned)P.min_area)
-                ++comps;
-            L[me] = r;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) comps += __shfl_xor_sync(0xffffffffu, comps, o);
-    if ((threadIdx.x & 31) == 0 && comps) atomicAdd(&b.info[p].components, comps);
-}
-
-// Area filter + unshift_mask + PBM packing + pixel count.  One thread per PBM byte.
+// Area filter result (keep mask or the cleaned mask) + unshift_mask + PBM packing + pixel count.
+// One thread per PBM byte.
 __global__ void __launch_bounds__(256) k_output(Geom g, DevParams P, MaskBuffers b, int use_ccl) {
     const int p = blockIdx.y;
     const PairInfo I = b.info[p];
     const long long nbytes = (long long)g.H * g.SB;
-    const uint32_t* m = b.bits_clean + (size_t)p * g.H * g.WW;
-    const int* L = b.labels + (size_t)p * g.W * g.H;
-    const unsigned int* A = b.area_total + (size_t)p * g.W * g.H;
+    const uint32_t* m = (use_ccl ? b.bits_keep : b.bits_clean) + (size_t)p * g.H * g.WW;
     uint8_t* out = b.out_pbm + (size_t)b.out_index[p] * nbytes;
     unsigned int cnt = 0;
     for (long long bi = blockIdx.x * 256LL + threadIdx.x; bi < nbytes; bi += (long long)gridDim.x * 256) {
@@ -863,9 +872,7 @@ __global__ void __launch_bounds__(256) k_output(Geom g, DevParams P, MaskBuffers
             for (int k = 0; k < 8; ++k) {
                 const int x = x0 + k, sx = x - I.dx;
                 if (x >= g.W || sx < 0 || sx >= g.W) continue;
-                if (!bit_at(m, g.WW, sx, sy)) continue;
-                if (use_ccl && A[L[sy * g.W + sx]] < (unsigned)P.min_area) continue;
-                byte |= 0x80u >> k;
+                if (bit_at(m, g.WW, sx, sy)) byte |= 0x80u >> k;
             }
         }
         out[bi] = (uint8_t)byte;
@@ -956,7 +963,7 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
     set_scan_smem();
     k_sel_init_a<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, (unsigned long long)(0.01 * (double)(n - 1)),
                                        (unsigned long long)(0.99 * (double)(n - 1)));
-    k_mag_grad<T><<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b);
+    k_mag_grad<T><<<dim3(2 * bpp, n_pairs), PNT_MG, 0, s>>>(g, P, b);
     k_sel_scan<<<n_pairs * 4, 256, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
     *launches += 3;
@@ -1014,12 +1021,11 @@ void run_cleanup_output(const Geom& g, const DevParams& P, const MaskBuffers& b,
     *launches += 2;
     const bool use_ccl = min_area > 1;
     if (use_ccl) {
-        dim3 tiles(cdiv(g.W, CT), cdiv(g.H, CT), n_pairs);
-        k_ccl_local<<<tiles, dim3(CT, CT), 0, s>>>(g, b);
-        k_ccl_merge<<<tiles, 3 * CT, 0, s>>>(g, b);
-        const int gw = grid_for((long long)g.H * g.WW, 256);
-        k_ccl_area<<<dim3(gw, n_pairs), 256, 0, s>>>(g, b);
-        k_ccl_compress<<<dim3(gw, n_pairs), 256, 0, s>>>(g, Q, b);
+        dim3 rows(cdiv(g.H, RNT / 32), n_pairs);
+        k_ccl_runs<<<rows, RNT, 0, s>>>(g, b);
+        k_ccl_union<<<rows, RNT, 0, s>>>(g, b);
+        k_ccl_area<<<rows, RNT, 0, s>>>(g, b);
+        k_ccl_keep<<<rows, RNT, 0, s>>>(g, Q, b);
         FROI_LAUNCH_CHECK();
         *launches += 4;
     }

@@ -34,6 +34,7 @@ struct Geom {
     int pw, ph, log2pw, log2ph;  // FFT grid (next_pow2)
     int WW;                      // 32-bit words per packed mask row
     int SB;                      // bytes per PBM row
+    int RMAX;                    // max runs of set pixels per row, (W+1)/2
 };
 
 struct PairInfo {
@@ -144,10 +145,12 @@ struct MaskBuffers {
     unsigned long long* tie_cnt;  // [pair][chunks][2]
     uint32_t* bits_thr;           // [pair][H*WW] thresholded (registered)
     uint32_t* bits_clean;         // [pair][H*WW] after open/close (registered)
-    uint32_t* bits_root;          // [pair][H*WW] local-root marks
-    int* labels;                  // [pair][H*W]
-    unsigned int* area_local;     // [pair][H*W]
-    unsigned int* area_total;     // [pair][H*W]
+    uint32_t* bits_keep;          // [pair][H*WW] pixels of components with area >= min_area
+    uint16_t* run_x0;             // [pair][H][RMAX] first x of each run of set pixels
+    uint16_t* run_x1;             // [pair][H][RMAX] last x
+    int* run_n;                   // [pair][H] runs per row
+    int* run_par;                 // [pair][H*RMAX] union-find parent (run ids y*RMAX + k)
+    unsigned int* run_area;       // [pair][H*RMAX] component area at the root run
     uint8_t* out_pbm;             // output PBM masks
     const long long* out_index;   // [pair] mask index in out_pbm (frame index)
     PairInfo* info;

@@ -120,6 +120,7 @@ Geom make_geom(const froi_params& p, int W, int H, int depth) {
     g.log2ph = ilog2(g.ph);
     g.WW = (W + 31) / 32;
     g.SB = (W + 7) / 8;
+    g.RMAX = (W + 1) / 2;
     return g;
 }
 
@@ -244,9 +245,10 @@ struct froi_ctx {
     float* d_fm = nullptr;
     double* d_gr = nullptr;
     unsigned long long* d_tie = nullptr;
-    uint32_t *d_bits_thr = nullptr, *d_bits_clean = nullptr, *d_bits_root = nullptr;
-    int* d_labels = nullptr;
-    unsigned int *d_area_local = nullptr, *d_area_total = nullptr;
+    uint32_t *d_bits_thr = nullptr, *d_bits_clean = nullptr, *d_bits_keep = nullptr;
+    uint16_t *d_run_x0 = nullptr, *d_run_x1 = nullptr;
+    int *d_run_n = nullptr, *d_run_par = nullptr;
+    unsigned int* d_run_area = nullptr;
     uint8_t* d_out_batch = nullptr;  // [Pcap] PBM masks for taps
     // tables (device + pinned host, double-buffered)
     const void** d_frame_raw[2] = {nullptr, nullptr};
@@ -294,10 +296,12 @@ struct froi_ctx {
         b.tie_cnt = d_tie;
         b.bits_thr = d_bits_thr;
         b.bits_clean = d_bits_clean;
-        b.bits_root = d_bits_root;
-        b.labels = d_labels;
-        b.area_local = d_area_local;
-        b.area_total = d_area_total;
+        b.bits_keep = d_bits_keep;
+        b.run_x0 = d_run_x0;
+        b.run_x1 = d_run_x1;
+        b.run_n = d_run_n;
+        b.run_par = d_run_par;
+        b.run_area = d_run_area;
         b.out_pbm = d_out_batch;
         b.out_index = d_out_index[tb_];
         b.info = d_info;
@@ -392,10 +396,13 @@ void ctx_alloc(froi_ctx* c) {
     const size_t words = (size_t)g.H * g.WW;
     c->d_bits_thr = dalloc<uint32_t>(words * P, &t);
     c->d_bits_clean = dalloc<uint32_t>(words * P, &t);
-    c->d_bits_root = dalloc<uint32_t>(words * P, &t);
-    c->d_labels = dalloc<int>(px * P, &t);
-    c->d_area_local = dalloc<unsigned int>(px * P, &t);
-    c->d_area_total = dalloc<unsigned int>(px * P, &t);
+    c->d_bits_keep = dalloc<uint32_t>(words * P, &t);
+    const size_t runs = (size_t)g.H * g.RMAX * P;
+    c->d_run_x0 = dalloc<uint16_t>(runs, &t);
+    c->d_run_x1 = dalloc<uint16_t>(runs, &t);
+    c->d_run_n = dalloc<int>((size_t)g.H * P, &t);
+    c->d_run_par = dalloc<int>(runs, &t);
+    c->d_run_area = dalloc<unsigned int>(runs, &t);
     c->d_out_batch = dalloc<uint8_t>((size_t)g.H * g.SB * P, &t);
     // tables
     c->tables_bytes = sizeof(void*) * F + sizeof(int) * 2 * P + sizeof(void*) * P + sizeof(long long) * P;
@@ -420,7 +427,7 @@ void ctx_free(froi_ctx* c) {
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
-                    c->d_bits_clean, c->d_bits_root, c->d_labels, c->d_area_local, c->d_area_total,
+                    c->d_bits_clean, c->d_bits_keep, c->d_run_x0, c->d_run_x1, c->d_run_n, c->d_run_par, c->d_run_area,
                     c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry, c->d_arena};
     for (void* p : ptrs)
         if (p) cudaFree(p);
@@ -1242,21 +1249,19 @@ int froi_component_areas(froi_ctx* c, const uint8_t* mask, uint32_t* areas_out, 
     mb.flow = c->d_flow0;
     launch_cleanup_only(c->g, c->dp, mb, 0, 0, 2, c->stream);  // no morphology, CCL forced
     const Geom& g = c->g;
-    const size_t px = (size_t)g.W * g.H;
-    std::vector<uint32_t> roots((size_t)g.H * g.WW);
-    std::vector<int> labels(px);
-    std::vector<uint32_t> area(px);
-    FROI_CUDA(cudaMemcpyAsync(roots.data(), c->d_bits_root, roots.size() * 4, cudaMemcpyDeviceToHost, c->stream));
-    FROI_CUDA(cudaMemcpyAsync(labels.data(), c->d_labels, px * 4, cudaMemcpyDeviceToHost, c->stream));
-    FROI_CUDA(cudaMemcpyAsync(area.data(), c->d_area_total, px * 4, cudaMemcpyDeviceToHost, c->stream));
+    const size_t runs = (size_t)g.H * g.RMAX;
+    std::vector<int> rn(g.H), par(runs);
+    std::vector<unsigned int> area(runs);
+    FROI_CUDA(cudaMemcpyAsync(rn.data(), c->d_run_n, sizeof(int) * g.H, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(par.data(), c->d_run_par, sizeof(int) * runs, cudaMemcpyDeviceToHost, c->stream));
+    FROI_CUDA(cudaMemcpyAsync(area.data(), c->d_run_area, sizeof(unsigned int) * runs, cudaMemcpyDeviceToHost, c->stream));
     FROI_CUDA(cudaStreamSynchronize(c->stream));
     size_t n = 0;
     for (int y = 0; y < g.H; ++y)
-        for (int x = 0; x < g.W; ++x) {
-            const size_t i = (size_t)y * g.W + x;
-            if (!((roots[(size_t)y * g.WW + (x >> 5)] >> (x & 31)) & 1u)) continue;
-            if (labels[i] != (int)i) continue;  // local root that is not the global root
-            if (areas_out && n < cap) areas_out[n] = area[i];
+        for (int k = 0; k < rn[y]; ++k) {
+            const int id = y * g.RMAX + k;
+            if (par[id] != id) continue;  // not a component root
+            if (areas_out && n < cap) areas_out[n] = area[id];
             ++n;
         }
     *n_components = n;
