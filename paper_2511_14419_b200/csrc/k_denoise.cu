@@ -32,11 +32,18 @@ __device__ __forceinline__ int median9(int p0, int p1, int p2, int p3, int p4, i
     return p4;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int enabled, int mr,
-                                                 int br, const void* const* frame_raw, T* den,
-                                                 unsigned long long* sums, const double* spatial_g,
+struct Spatial {
+    double w[225];  // (2*7+1)^2 spatial weights, host-computed libm values
+};
+
+// MR/BR > 0: compile-time radii (the default 1/2 path); 0: runtime radii.
+template <typename T, int MR, int BR>
+__global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int enabled, int mr_rt,
+                                                 int br_rt, const void* const* frame_raw, T* den,
+                                                 unsigned long long* sums, const __grid_constant__ Spatial sp_w,
                                                  const double* lut_g) {
+    const int mr = MR > 0 ? MR : mr_rt;
+    const int br = BR > 0 ? BR : br_rt;
     extern __shared__ __align__(16) unsigned char smem[];
     const int slot = blockIdx.z;
     const T* src = (const T*)frame_raw[slot];
@@ -65,7 +72,7 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
             }
         }
     } else {
-        for (int i = tid; i < side * side; i += NT) spat_s[i] = spatial_g[i];
+        for (int i = tid; i < side * side; i += NT) spat_s[i] = sp_w.w[i];
         if (lut_in_smem)
             for (int i = tid; i < 256; i += NT) lut_s[i] = lut_g[i];
         for (int i = tid; i < rw * rh; i += NT) {
@@ -111,16 +118,32 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
                 // bilateral_filter (denoise.hpp:63-79): fp64, dy-major / dx-minor, no FMA
                 const int c = med_s[(ty + br) * mw + threadIdx.x + br];
                 double num = 0.0, dn = 0.0;
-                for (int dy = -br; dy <= br; ++dy) {
-                    const int* row = med_s + (ty + br + dy) * mw + threadIdx.x + br;
-                    const double* rowd = medd_s + (ty + br + dy) * mw + threadIdx.x + br;
-                    const double* sp = spat_s + (dy + br) * side + br;
-                    for (int dx = -br; dx <= br; ++dx) {
-                        const int d = abs(row[dx] - c);
-                        const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
-                        const double wgt = dmul(sp[dx], lw);
-                        num = dadd(num, dmul(wgt, rowd[dx]));
-                        dn = dadd(dn, wgt);
+                if (BR > 0) {
+#pragma unroll
+                    for (int dy = -BR; dy <= BR; ++dy) {
+                        const int* row = med_s + (ty + BR + dy) * mw + threadIdx.x + BR;
+                        const double* rowd = medd_s + (ty + BR + dy) * mw + threadIdx.x + BR;
+#pragma unroll
+                        for (int dx = -BR; dx <= BR; ++dx) {
+                            const int d = abs(row[dx] - c);
+                            const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
+                            const double wgt = dmul(sp_w.w[(dy + BR) * (2 * BR + 1) + dx + BR], lw);
+                            num = dadd(num, dmul(wgt, rowd[dx]));
+                            dn = dadd(dn, wgt);
+                        }
+                    }
+                } else {
+                    for (int dy = -br; dy <= br; ++dy) {
+                        const int* row = med_s + (ty + br + dy) * mw + threadIdx.x + br;
+                        const double* rowd = medd_s + (ty + br + dy) * mw + threadIdx.x + br;
+                        const double* sp = spat_s + (dy + br) * side + br;
+                        for (int dx = -br; dx <= br; ++dx) {
+                            const int d = abs(row[dx] - c);
+                            const double lw = lut_in_smem ? lut_s[d] : __ldg(lut_g + d);
+                            const double wgt = dmul(sp[dx], lw);
+                            num = dadd(num, dmul(wgt, rowd[dx]));
+                            dn = dadd(dn, wgt);
+                        }
                     }
                 }
                 double q = ddiv(num, dn);
@@ -140,7 +163,7 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
 }  // namespace
 
 void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw, void* d_den,
-                    unsigned long long* d_sums, const double* d_spatial, const double* d_lut,
+                    unsigned long long* d_sums, const double* h_spatial, const double* d_lut,
                     int n_slots, cudaStream_t s) {
     if (n_slots <= 0) return;
     const int mr = p.median_radius, br = p.bilateral_radius;
@@ -149,18 +172,21 @@ void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw,
                                           (TX + 2 * br) * (TY + 2 * br)) +
                         sizeof(int) * ((TX + 2 * R1) * (TY + 2 * R1) + (TX + 2 * br) * (TY + 2 * br));
     dim3 grid(cdiv(g.W, TX), cdiv(g.H, TY), n_slots), block(TX, NT / TX);
+    Spatial sp{};
+    for (int i = 0; i < side * side; ++i) sp.w[i] = h_spatial[i];
+    const bool fast = mr == 1 && br == 2;
     if (g.sample_bytes == 1) {
+        auto k = fast ? k_denoise<uint8_t, 1, 2> : k_denoise<uint8_t, 0, 0>;
         if (smem > 48 * 1024)
-            FROI_CUDA(cudaFuncSetAttribute(k_denoise<uint8_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_denoise<uint8_t><<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br,
-                                                     d_frame_raw, (uint8_t*)d_den, d_sums,
-                                                     d_spatial, d_lut);
+            FROI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k<<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br, d_frame_raw,
+                                    (uint8_t*)d_den, d_sums, sp, d_lut);
     } else {
+        auto k = fast ? k_denoise<uint16_t, 1, 2> : k_denoise<uint16_t, 0, 0>;
         if (smem > 48 * 1024)
-            FROI_CUDA(cudaFuncSetAttribute(k_denoise<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        k_denoise<uint16_t><<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br,
-                                                      d_frame_raw, (uint16_t*)d_den, d_sums,
-                                                      d_spatial, d_lut);
+            FROI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k<<<grid, block, smem, s>>>(g.W, g.H, g.maxval, p.denoise_enabled, mr, br, d_frame_raw,
+                                    (uint16_t*)d_den, d_sums, sp, d_lut);
     }
     FROI_LAUNCH_CHECK();
 }

@@ -1,5 +1,6 @@
 // k_flow.cu — pyramid, polynomial expansion and the fused flow iteration
-// (flow.hpp:118-345): fp32 storage and arithmetic, exact fp32 warp coordinates, fp64 solve.
+// (flow.hpp:118-345): fp32 storage and arithmetic, exact fp32 warp coordinates, compensated
+// fp32 determinant in the 2x2 solve.
 //
 //   k_pyr_down   7-tap Gaussian (sigma 1, rows then columns, edge-replicated) fused with the
 //                bilinear resample to floor(w*scale) x floor(h*scale)            (flow.hpp:259-298)
@@ -271,16 +272,28 @@ constexpr int FX = 64, FY = 32, FNT = 512;
 
 struct IterArgs {
     int l;        // level
-    int mode;     // 0 zero prior, 1 prior from flow_in (same level), 2 upsample flow_in (level l+1)
+    int mode;     // 0 zero prior (coarsest level, first iteration), 1 prior = flow_in (same level)
     const float2* flow_in;
     float2* flow_out;
 };
 
+// floor(d) as (float, int) without the XU pipe: adding and removing 1.5*2^23 rounds to the
+// nearest integer (exact for |d| < 2^22), a compare turns it into floor.
+__device__ __forceinline__ float floor_split(float d, int& i) {
+    const float M = 12582912.0f;
+    d = fminf(fmaxf(d, -4194304.0f), 4194304.0f);
+    float r = __fsub_rn(__fadd_rn(d, M), M);
+    r = r > d ? r - 1.0f : r;
+    i = __float_as_int(__fadd_rn(r, M)) - 0x4B400000;
+    return r;
+}
+
 // bilinear() index rule (flow.hpp:157-168) for the coordinate i + d, computed exactly in fp32:
 // the integer part goes to the index, d - floor(d) is exact, so (x0, fx) equal the reference's.
 __device__ __forceinline__ void bl_split(int i, float d, int n, int& i0, float& f) {
-    const float fl = floorf(d);
-    i0 = i + (int)fl;
+    int fi;
+    const float fl = floor_split(d, fi);
+    i0 = i + fi;
     f = d - fl;
     if (i0 < 0) {
         i0 = 0;
@@ -291,30 +304,70 @@ __device__ __forceinline__ void bl_split(int i, float d, int n, int& i0, float& 
     }
 }
 
-// Coarse-to-fine upsampling of the prior (flow.hpp:318-337), fp32.
-__device__ __forceinline__ float2 upsample_at(const float2* c, int cw, int ch, float fx, float fy,
-                                              int x, int y) {
-    const float sx = (x + 0.5f) / fx - 0.5f, sy = (y + 0.5f) / fy - 0.5f;
+// Coarse-to-fine upsampling of the prior (flow.hpp:318-337), fp32: one thread per fine pixel,
+// run once per level before its first iteration.  rfx = 1/fx (exact for the default 0.5 scale).
+__global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* __restrict__ coarse,
+                                                  float2* __restrict__ fine, float fx, float fy,
+                                                  float rfx, float rfy) {
+    const int p = blockIdx.z;
+    const int w = g.lw[l], h = g.lh[l], cw = g.lw[l + 1], ch = g.lh[l + 1];
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (x >= w || y >= h) return;
+    const float2* c = coarse + (size_t)p * g.lsum + g.loff[l + 1];
+    const float sx = (x + 0.5f) * rfx - 0.5f, sy = (y + 0.5f) * rfy - 0.5f;
     int x0, y0;
     float ax, ay;
-    const float flx = floorf(sx), fly = floorf(sy);
-    bl_split((int)flx, sx - flx, cw, x0, ax);
-    bl_split((int)fly, sy - fly, ch, y0, ay);
+    bl_split(0, sx, cw, x0, ax);
+    bl_split(0, sy, ch, y0, ay);
     const float2 a = c[(size_t)y0 * cw + x0], b = c[(size_t)y0 * cw + x0 + 1];
     const float2 d = c[(size_t)(y0 + 1) * cw + x0], e = c[(size_t)(y0 + 1) * cw + x0 + 1];
     const float u = ((a.x * (1.f - ax) + b.x * ax) * (1.f - ay) + (d.x * (1.f - ax) + e.x * ax) * ay) * fx;
     const float v = ((a.y * (1.f - ax) + b.y * ax) * (1.f - ay) + (d.y * (1.f - ax) + e.y * ax) * ay) * fy;
-    return make_float2(u, v);
+    fine[(size_t)p * g.lsum + g.loff[l] + (size_t)y * w + x] = make_float2(u, v);
 }
 
 __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, size_t pair_off,
                                            int x, int y) {
     if (a.mode == 0) return make_float2(0.f, 0.f);
-    const int w = g.lw[a.l];
-    if (a.mode == 1) return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * w + x];
-    const int cw = g.lw[a.l + 1], ch = g.lh[a.l + 1];
-    return upsample_at(a.flow_in + pair_off + g.loff[a.l + 1], cw, ch, (float)((double)w / cw),
-                       (float)((double)g.lh[a.l] / ch), x, y);
+    return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * g.lw[a.l] + x];
+}
+
+// Normal-equation products G of one pixel (flow.hpp:212-232).
+struct GTerms {
+    float g11, g12, g22, h1, h2;
+};
+
+__device__ __forceinline__ GTerms g_terms(const float4* __restrict__ pA, const float* __restrict__ pB,
+                                          const float4* __restrict__ nA, const float* __restrict__ nB,
+                                          int w, int h, int gx, int gy, float du, float dv) {
+    int xa, ya;
+    float fx, fy;
+    bl_split(gx, du, w, xa, fx);
+    bl_split(gy, dv, h, ya, fy);
+    const float4* r0 = nA + (size_t)ya * w + xa;
+    const float* b0 = nB + (size_t)ya * w + xa;
+    const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r0 + w), q11 = __ldg(r0 + w + 1);
+    const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b0 + w), b11 = __ldg(b0 + w + 1);
+    const size_t o = (size_t)gy * w + gx;
+    const float4 pa = __ldg(pA + o);
+    const float pb = __ldg(pB + o);
+    const float ofx = 1.f - fx, ofy = 1.f - fy;
+#define BL(c) ((q00.c * ofx + q01.c * fx) * ofy + (q10.c * ofx + q11.c * fx) * fy)
+    const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
+#undef BL
+    const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
+    const float a11 = 0.5f * (pa.x + na11);
+    const float a12 = 0.5f * (pa.y + na12);
+    const float a22 = 0.5f * (pa.z + na22);
+    const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
+    const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
+    GTerms t;
+    t.g11 = a11 * a11 + a12 * a12;
+    t.g12 = (a11 + a22) * a12;
+    t.g22 = a12 * a12 + a22 * a22;
+    t.h1 = a11 * db1 + a12 * db2;
+    t.h2 = a12 * db1 + a22 * db2;
+    return t;
 }
 
 // One CTA per FX x FY output tile of one pair (FNT threads, 2 CTAs per SM).
@@ -341,50 +394,34 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     const bool sh = info[p].shifted != 0;
     const float4* nA = (sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo;
     const float* nB = (sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-    // phase 1: normal-equation products over tile + halo (flow.hpp:212-232); one warp per row
-    for (int hy = warp; hy < HH; hy += FNT / 32) {
-        const int gy = y0 - R + hy;
-        for (int hx = lane; hx < HW; hx += 32) {
-            const int gx = x0 - R + hx;
-            float g11 = 0.f, g12 = 0.f, g22 = 0.f, h1 = 0.f, h2 = 0.f;
-            if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-                const float2 pr = prior_at(g, a, pair_off, gx, gy);
-                const float du = pr.x, dv = pr.y;
-                int xa, ya;
-                float fx, fy;
-                bl_split(gx, du, w, xa, fx);
-                bl_split(gy, dv, h, ya, fy);
-                const float4* r0 = nA + (size_t)ya * w + xa;
-                const float* b0 = nB + (size_t)ya * w + xa;
-                const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r0 + w), q11 = __ldg(r0 + w + 1);
-                const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b0 + w), b11 = __ldg(b0 + w + 1);
-                const float ofx = 1.f - fx, ofy = 1.f - fy;
-#define BL(c) ((q00.c * ofx + q01.c * fx) * ofy + (q10.c * ofx + q11.c * fx) * fy)
-                const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
-#undef BL
-                const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
-                const size_t o = (size_t)gy * w + gx;
-                const float4 pa = __ldg(pA + o);
-                const float pb = __ldg(pB + o);
-                const float a11 = 0.5f * (pa.x + na11);
-                const float a12 = 0.5f * (pa.y + na12);
-                const float a22 = 0.5f * (pa.z + na22);
-                const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
-                const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
-                g11 = a11 * a11 + a12 * a12;
-                g12 = (a11 + a22) * a12;
-                g22 = a12 * a12 + a22 * a22;
-                h1 = a11 * db1 + a12 * db2;
-                h2 = a12 * db1 + a22 * db2;
+    // phase 1: normal-equation products over tile + halo; two independent pixels per step so
+    // each thread keeps ~20 gathers in flight
+    for (int i0 = threadIdx.x; i0 < PL; i0 += 2 * FNT) {
+        GTerms t[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int i = i0 + k * FNT;
+            t[k] = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+            if (i < PL) {
+                const int hy = i / HW, hx = i - hy * HW;
+                const int gx = x0 - R + hx, gy = y0 - R + hy;
+                if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
+                    const float2 pr = prior_at(g, a, pair_off, gx, gy);
+                    t[k] = g_terms(pA, pB, nA, nB, w, h, gx, gy, pr.x, pr.y);
+                }
             }
-            const int i = hy * HW + hx;
-            G[i] = g11;
-            G[PL + i] = g12;
-            G[2 * PL + i] = g22;
-            G[3 * PL + i] = h1;
-            G[4 * PL + i] = h2;
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int i = i0 + k * FNT;
+            if (i < PL) {
+                G[i] = t[k].g11;
+                G[PL + i] = t[k].g12;
+                G[2 * PL + i] = t[k].g22;
+                G[3 * PL + i] = t[k].h1;
+                G[4 * PL + i] = t[k].h2;
+            }
         }
     }
     __syncthreads();
@@ -444,14 +481,21 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     __syncthreads();
     // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
     // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
+    __shared__ float rcx[FX], rcy[FY];
+    if (threadIdx.x < FX) {
+        const int x = x0 + threadIdx.x;
+        rcx[threadIdx.x] = __frcp_rn((float)(min(w - 1, x + R) - max(0, x - R) + 1));
+    } else if (threadIdx.x < FX + FY) {
+        const int y = y0 + threadIdx.x - FX;
+        rcy[threadIdx.x - FX] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
+    }
+    __syncthreads();
     float2* out = a.flow_out + pair_off + lo;
     for (int i = threadIdx.x; i < FX * FY; i += FNT) {
         const int ty = i / FX, tx = i - ty * FX;
         const int x = x0 + tx, y = y0 + ty;
         if (x >= w || y >= h) continue;
-        const int cx = min(w - 1, x + R) - max(0, x - R) + 1;
-        const int cy = min(h - 1, y + R) - max(0, y - R) + 1;
-        const float inv = 1.f / (float)(cx * cy);
+        const float inv = rcx[tx] * rcy[ty];
         const int si = ty * HW + tx;
         const float g11 = G[si] * inv, g12 = G[PL + si] * inv, g22 = G[2 * PL + si] * inv;
         const float h1 = G[3 * PL + si] * inv, h2 = G[4 * PL + si] * inv;
@@ -463,8 +507,9 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         if (!(det > 1e-9f * frob2)) {
             r = prior_at(g, a, pair_off, x, y);
         } else {
-            r.x = (g22 * h1 - g12 * h2) / det;
-            r.y = (g11 * h2 - g12 * h1) / det;
+            const float rd = __frcp_rn(det);
+            r.x = (g22 * h1 - g12 * h2) * rd;
+            r.y = (g11 * h2 - g12 * h1) * rd;
         }
         out[(size_t)y * w + x] = r;
     }
@@ -596,7 +641,17 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
         for (int it = 0; it < P.iterations; ++it) {
             IterArgs a;
             a.l = l;
-            a.mode = it > 0 ? 1 : (l == g.L - 1 ? 0 : 2);
+            a.mode = (it == 0 && l == g.L - 1) ? 0 : 1;
+            if (it == 0 && l < g.L - 1) {
+                // upscale the coarser estimate into this level of the same buffer (flow.hpp:318-337)
+                const float fx = (float)((double)g.lw[l] / g.lw[l + 1]);
+                const float fy = (float)((double)g.lh[l] / g.lh[l + 1]);
+                dim3 ug(cdiv(g.lw[l], 32), cdiv(g.lh[l], 8), n_pairs);
+                k_upsample<<<ug, 256, 0, s>>>(g, l, buf[cur], buf[cur], fx, fy,
+                                              (float)(1.0 / ((double)g.lw[l] / g.lw[l + 1])),
+                                              (float)(1.0 / ((double)g.lh[l] / g.lh[l + 1])));
+                FROI_LAUNCH_CHECK();
+            }
             a.flow_in = buf[cur];
             a.flow_out = buf[1 - cur];
             switch (R) {  // window_size 3..15 (the reference default is 15)

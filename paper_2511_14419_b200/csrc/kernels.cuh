@@ -96,8 +96,8 @@ struct DevParams {
 // ---------------------------------------------------------------- launchers
 // k_denoise.cu
 void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw, void* d_den,
-                    unsigned long long* d_sums, const double* d_spatial, const double* d_lut,
-                    int n_slots, cudaStream_t s);
+                    unsigned long long* d_sums, const double* h_spatial, const double* d_lut,
+                    int n_slots, cudaStream_t s);  // h_spatial: host copy of the spatial weights
 
 // k_register.cu
 void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long long* d_sums,

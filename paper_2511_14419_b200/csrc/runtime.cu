@@ -220,6 +220,7 @@ struct froi_ctx {
     size_t device_bytes = 0;
     // constants
     double *d_spatial = nullptr, *d_lut = nullptr, *d_wx = nullptr, *d_wy = nullptr;
+    std::vector<double> h_spatial;
     double2 *d_tw_row = nullptr, *d_tw_col = nullptr, *d_itw_row = nullptr, *d_itw_col = nullptr;
     // frame slots
     uint8_t* d_raw = nullptr;
@@ -347,6 +348,7 @@ void ctx_alloc(froi_ctx* c) {
         std::vector<double> wx(g.pw), wy(g.ph);
         for (int x = 0; x < g.pw; ++x) wx[x] = 0.5 - 0.5 * std::cos(2.0 * kPi * x / g.pw);
         for (int y = 0; y < g.ph; ++y) wy[y] = 0.5 - 0.5 * std::cos(2.0 * kPi * y / g.ph);
+        c->h_spatial = spatial;
         c->d_spatial = dalloc<double>(spatial.size(), &t);
         c->d_lut = dalloc<double>(lut.size(), &t);
         c->d_wx = dalloc<double>(wx.size(), &t);
@@ -524,7 +526,7 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
     cudaEvent_t* ev = c->ev;
     FROI_CUDA(cudaEventRecord(ev[0], s));
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
-    launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->d_spatial, c->d_lut, nf, s);
+    launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, nf, s);
     FROI_CUDA(cudaEventRecord(ev[1], s));
     launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
     FROI_CUDA(cudaEventRecord(ev[2], s));
@@ -1055,7 +1057,7 @@ void taps_copy_den(froi_ctx* c, int n) {  // den := raw, sums (denoise disabled)
     DevParams d = c->dp;
     d.denoise_enabled = 0;
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * n, c->stream));
-    launch_denoise(c->g, d, c->d_frame_raw[0], c->d_den, c->d_sums, c->d_spatial, c->d_lut, n, c->stream);
+    launch_denoise(c->g, d, c->d_frame_raw[0], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, n, c->stream);
 }
 
 void taps_set_info(froi_ctx* c, int dx, int dy) {
@@ -1100,7 +1102,7 @@ int froi_denoise(froi_ctx* c, const uint16_t* in, uint16_t* out) {
     const uint16_t* fr[1] = {in};
     taps_upload(c, fr, 1);
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long), c->stream));
-    launch_denoise(c->g, c->dp, c->d_frame_raw[0], c->d_den, c->d_sums, c->d_spatial, c->d_lut, 1, c->stream);
+    launch_denoise(c->g, c->dp, c->d_frame_raw[0], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, 1, c->stream);
     const size_t px = (size_t)c->g.W * c->g.H;
     std::vector<uint8_t> h(c->frame_bytes);
     FROI_CUDA(cudaMemcpyAsync(h.data(), c->d_den, c->frame_bytes, cudaMemcpyDeviceToHost, c->stream));
