@@ -299,14 +299,15 @@ __global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuf
 }
 
 // One CTA per (pair, query): narrow the prefix after a histogram pass, or sort the collected
-// candidates after a collect pass.
-__global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
+// candidates (<= kSelCap keys, bitonic in shared memory) after a collect pass.
+constexpr int SCT = 1024;
+
+__global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
     extern __shared__ unsigned long long cs[];  // kSelCap candidates
     const int p = blockIdx.x / nq, q = blockIdx.x % nq;
     SelState* sp = b.sel + p * kMaxQueries + q;
     __shared__ SelState s;
-    __shared__ unsigned int part[256];
-    __shared__ unsigned long long lo_pos, hi_pos;
+    __shared__ unsigned int part[SCT];
     if (threadIdx.x == 0) s = *sp;
     __syncthreads();
     if (s.mode == SEL_DONE) return;
@@ -316,11 +317,11 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
         int np2 = 1;
         while (np2 < (int)n) np2 <<= 1;
         const unsigned long long* src = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
-        for (int i = threadIdx.x; i < np2; i += 256) cs[i] = i < (int)n ? src[i] : ~0ull;
+        for (int i = threadIdx.x; i < np2; i += SCT) cs[i] = i < (int)n ? src[i] : ~0ull;
         __syncthreads();
         for (int k = 2; k <= np2; k <<= 1)
             for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < np2; i += 256) {
+                for (int i = threadIdx.x; i < np2; i += SCT) {
                     const int ixj = i ^ j;
                     if (ixj > i) {
                         const bool up = (i & k) == 0;
@@ -335,23 +336,21 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
             }
         if (threadIdx.x == 0) {
             const unsigned long long r = cs[s.rank];
-            unsigned long long lo = 0, hi = n;  // lower_bound
+            unsigned long long lo = 0, hi = n;  // lower_bound(r)
             while (lo < hi) {
                 const unsigned long long mid = (lo + hi) / 2;
                 if (cs[mid] < r) lo = mid + 1; else hi = mid;
             }
-            lo_pos = lo;
+            unsigned long long lo2 = lo;  // upper_bound(r)
             hi = n;
-            unsigned long long lo2 = lo;
             while (lo2 < hi) {
                 const unsigned long long mid = (lo2 + hi) / 2;
                 if (cs[mid] <= r) lo2 = mid + 1; else hi = mid;
             }
-            hi_pos = lo2;
             SelState ns = s;
             ns.result = r;
-            ns.count_lt = (s.k0 - s.rank) + lo_pos;
-            ns.count_eq = hi_pos - lo_pos;
+            ns.count_lt = (s.k0 - s.rank) + lo;
+            ns.count_eq = lo2 - lo;
             ns.mode = SEL_DONE;
             *sp = ns;
             *cc = 0;
@@ -359,7 +358,7 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
         return;
     }
     unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
-    constexpr int PER = kSelBins / 256;
+    constexpr int PER = kSelBins / SCT;
     unsigned int loc[PER];
     unsigned int tot = 0;
     for (int j = 0; j < PER; ++j) {
@@ -368,7 +367,7 @@ __global__ void __launch_bounds__(256) k_sel_scan(MaskBuffers b, int nq) {
     }
     part[threadIdx.x] = tot;
     __syncthreads();
-    for (int o = 1; o < 256; o <<= 1) {
+    for (int o = 1; o < SCT; o <<= 1) {
         const unsigned int v = threadIdx.x >= o ? part[threadIdx.x - o] : 0u;
         __syncthreads();
         part[threadIdx.x] += v;
@@ -936,7 +935,7 @@ int grid_for(long long work, int per_block) {
     return (int)(b < 1 ? 1 : b);
 }
 
-constexpr int kSelPasses = 6;  // worst case: 64 key bits / 11, collect + sort, ties early
+constexpr int kSelPasses = 6;  // worst case: 64 key bits / 11; typically 2 (+ the fused first)
 
 size_t scan_smem() { return sizeof(unsigned long long) * kSelCap; }
 
@@ -964,12 +963,12 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
     k_sel_init_a<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, (unsigned long long)(0.01 * (double)(n - 1)),
                                        (unsigned long long)(0.99 * (double)(n - 1)));
     k_mag_grad<T><<<dim3(2 * bpp, n_pairs), PNT_MG, 0, s>>>(g, P, b);
-    k_sel_scan<<<n_pairs * 4, 256, scan_smem(), s>>>(b, 4);
+    k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
     *launches += 3;
     for (int it = 0; it < kSelPasses; ++it) {
         k_sel_pass_a<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, b);
-        k_sel_scan<<<n_pairs * 4, 256, scan_smem(), s>>>(b, 4);
+        k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }
@@ -987,7 +986,7 @@ void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n
     ++*launches;
     for (int it = 0; it < kSelPasses + 1; ++it) {
         k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, map);
-        k_sel_scan<<<n_pairs, 256, scan_smem(), s>>>(b, 1);
+        k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }

@@ -21,7 +21,7 @@ constexpr int kMaxLevels = 16;
 constexpr int kSelBits = 11;  // radix-select digit width
 constexpr int kSelBins = 1 << kSelBits;
 constexpr int kMaxQueries = 4;
-constexpr int kSelCap = 8192;  // candidates sorted in shared memory once a radix bin is this small
+constexpr int kSelCap = 16384;  // candidates sorted in shared memory once a radix bin is this small
 enum SelMode { SEL_HIST = 0, SEL_COLLECT = 1, SEL_DONE = 2 };
 
 struct Geom {
