@@ -31,9 +31,9 @@ struct PairPix {
     int grad_src;
     const double* lut;  // shared-memory v/maxval table for 8-bit frames (nullptr: convert)
 
-    __device__ __forceinline__ double fmag(int x, int y) const {
+    __device__ __forceinline__ float fmag(int x, int y) const {
         const float2 f = flow[(size_t)y * W + x];
-        return (double)hypotf_glibc(f.x, f.y);
+        return hypotf_glibc(f.x, f.y);
     }
     // normalize_frame(apply_shift(raw, s)) at clamped coordinates
     __device__ __forceinline__ double img(int x, int y) const {
@@ -49,8 +49,8 @@ struct PairPix {
             gx = dmul(0.5, dsub(img(x + 1, y), img(x - 1, y)));
             gy = dmul(0.5, dsub(img(x, y + 1), img(x, y - 1)));
         } else {
-            gx = dmul(0.5, dsub(fmag(min(x + 1, W - 1), y), fmag(max(x - 1, 0), y)));
-            gy = dmul(0.5, dsub(fmag(x, min(y + 1, H - 1)), fmag(x, max(y - 1, 0))));
+            gx = dmul(0.5, dsub((double)fmag(min(x + 1, W - 1), y), (double)fmag(max(x - 1, 0), y)));
+            gy = dmul(0.5, dsub((double)fmag(x, min(y + 1, H - 1)), (double)fmag(x, max(y - 1, 0))));
         }
         return hypot_glibc(gx, gy);
     }
@@ -86,6 +86,15 @@ __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P
 // pass of phase A is fused into the producer that materialises |flow| and |grad I|.
 constexpr int SNT = 512;
 
+// |flow| keys: the float's own bit pattern in the high word (monotone for non-negative floats,
+// no float->double conversion per element); |grad I| and S keys: the double's bit pattern.
+__device__ __forceinline__ unsigned long long fkey(float f) {
+    return f == 0.f ? 0ull : ((unsigned long long)__float_as_uint(f) << 32);
+}
+__device__ __forceinline__ double ffromkey(unsigned long long k) {
+    return (double)__uint_as_float((unsigned int)(k >> 32));
+}
+
 __device__ __forceinline__ void sel_digit(int bits_done, int& shift, int& width) {
     width = min(kSelBits, 64 - bits_done);
     shift = 64 - bits_done - width;
@@ -109,7 +118,7 @@ struct SrcProduce {
         const double gg = px.grad(x, y);
         fm[i] = f;
         gr[i] = gg;
-        k[0] = k[1] = dkey((double)f);
+        k[0] = k[1] = fkey(f);
         k[2] = k[3] = dkey(gg);
     }
 };
@@ -120,7 +129,7 @@ struct SrcBufA {
     static constexpr int NQ = 4;
     __device__ __forceinline__ void keys(long long i, int, int, const bool* act,
                                          unsigned long long* k) const {
-        if (act[0] || act[1]) k[0] = k[1] = dkey((double)fm[i]);
+        if (act[0] || act[1]) k[0] = k[1] = fkey(fm[i]);
         if (act[2] || act[3]) k[2] = k[3] = dkey(gr[i]);
     }
 };
@@ -444,8 +453,8 @@ __global__ void k_sel_init_b(MaskBuffers b, unsigned long long n, unsigned long 
     PairInfo& I = b.info[p];
     if (from_stats) {
         const SelState* s = b.sel + p * kMaxQueries;
-        I.fmag_lo = dfromkey(s[0].result);
-        I.fmag_hi = dfromkey(s[1].result);
+        I.fmag_lo = ffromkey(s[0].result);
+        I.fmag_hi = ffromkey(s[1].result);
         I.grad_lo = dfromkey(s[2].result);
         I.grad_hi = dfromkey(s[3].result);
         const double df = dsub(I.fmag_hi, I.fmag_lo), dg = dsub(I.grad_hi, I.grad_lo);
