@@ -1,0 +1,116 @@
+"""BASELINE configurations end to end against the CPU oracle.
+
+Contract: shifts and confidences bit-identical; the mask stage
+bit-exact given the GPU flow; flow within max |d| <= 2e-2 px and mean EPE <= 1e-3 px of the fp64
+reference; end-to-end mask mismatch <= 1e-4 per frame.  Mismatch rates are printed (pytest -s)
+and recorded in DESIGN.md.
+"""
+import os
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FLOW_MAX_ABS = 2e-2
+FLOW_MEAN_EPE = 1e-3
+MASK_MISMATCH_MAX = 1e-4
+
+
+def _apply_shift(f, dx, dy):
+    h, w = f.shape
+    return f[np.clip(np.arange(h) + dy, 0, h - 1)][:, np.clip(np.arange(w) + dx, 0, w - 1)]
+
+
+def _oracle_extract(args):
+    frames, depth, params = args
+    from oracle.oracle_py import Oracle
+    return Oracle("port").extract_roi(frames, depth, params, workers=os.cpu_count() or 1)
+
+
+def _oracle_flow(args):
+    a, b, depth, params = args
+    from oracle.oracle_py import Oracle
+    return Oracle("port").compute_flow(a, b, depth, params)
+
+
+def check_config(gpu, oracle, frames, depth, params, label):
+    from paper_2511_14419_b200.params import ExtractInfo
+    info = ExtractInfo()
+    got = gpu.extract_roi(frames, params, info=info, depth=depth)
+    want, shifts, fracs = _oracle_extract((frames, depth, params))
+    assert [(s.dx, s.dy, s.confidence) for s in info.shifts] == \
+        [(s.dx, s.dy, s.confidence) for s in shifts], label
+    n, h, w = frames.shape
+    mism = [float((got[t] != want[t]).mean()) for t in range(n)]
+    den = [oracle.denoise(frames[t], depth, params) for t in range(n)]
+    flow_err = []
+    for t in range(1, n):
+        s = shifts[t]
+        nxt = _apply_shift(den[t], s.dx, s.dy)
+        gu, gv = gpu.compute_flow(den[t - 1], nxt, params, depth=depth)
+        ou, ov = oracle.compute_flow(den[t - 1], nxt, depth, params)
+        du, dv = gu.astype(np.float64) - ou, gv.astype(np.float64) - ov
+        flow_err.append((float(max(np.abs(du).max(), np.abs(dv).max())), float(np.hypot(du, dv).mean())))
+        m, _ = oracle.mask_from_flow(gu, gv, frames[t], depth, s.dx, s.dy, params)
+        if params.roi.adjacent_factor == 0:
+            assert np.array_equal(m, got[t]), f"{label}: mask stage differs at frame {t}"
+    print(f"{label}: mask mismatch per frame {mism}; flow (max|d|, mean EPE) {flow_err}")
+    for mx, mean in flow_err:
+        assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (label, mx, mean)
+    assert max(mism) <= MASK_MISMATCH_MAX, (label, mism)
+    return mism, flow_err
+
+
+@pytest.fixture(scope="module")
+def synth():
+    from paper_2511_14419_b200 import synth as S
+    return S
+
+
+def test_c1_single_pair_512(gpu, oracle, synth):
+    cfg = synth.config("C1")
+    check_config(gpu, oracle, synth.well_frames(cfg, 0, 2), 8, cfg.params, "C1")
+
+
+def test_c2_sequence_prefix_1024(gpu, oracle, synth):
+    cfg = synth.config("C2")
+    check_config(gpu, oracle, synth.well_frames(cfg, 0, 4), 8, cfg.params, "C2[0:4]")
+
+
+def test_c3_wells_1024(gpu, oracle, synth):
+    cfg = synth.config("C3")
+    for well in (0, 17):
+        check_config(gpu, oracle, synth.well_frames(cfg, well, 3), 8, cfg.params, f"C3 well {well}")
+
+
+def test_c4_16bit_deep_pyramid_2048(gpu, oracle, synth):
+    cfg = synth.config("C4")
+    check_config(gpu, oracle, synth.well_frames(cfg, 0, 2), 16, cfg.params, "C4")
+
+
+@pytest.mark.parametrize("variant", ["C5-zero", "C5-dense", "C5-low"])
+def test_c5_robustness(gpu, oracle, synth, variant):
+    cfg = synth.config(variant)
+    frames = synth.well_frames(cfg, 0, 2)
+    mism, flow_err = check_config(gpu, oracle, frames, 8, cfg.params, variant)
+    if variant == "C5-zero":
+        u, v = gpu.compute_flow(frames[0], frames[1])
+        assert not np.any(u) and not np.any(v)  # identical frames: exactly zero flow
+        assert max(mism) == 0.0
+
+
+def test_c5_parameter_grid(gpu, synth):
+    """roi_threshold x close_radius x pyramid_levels on one 1024^2 pair (18 runs)."""
+    cfg = synth.scaled(synth.config("C2"), seed=5003)
+    frames = synth.well_frames(cfg, 0, 2)
+    grid = synth.c5_grid()
+    with ProcessPoolExecutor(max_workers=min(len(grid), os.cpu_count() or 1)) as ex:
+        wants = list(ex.map(_oracle_extract, [(frames, 8, p) for _, p in grid]))
+    rates = {}
+    for (key, p), (want, shifts, _) in zip(grid, wants):
+        got = gpu.extract_roi(frames, p, depth=8)
+        rates[key] = float(max((got[t] != want[t]).mean() for t in range(2)))
+    print("C5 grid mask mismatch:", rates)
+    assert max(rates.values()) <= MASK_MISMATCH_MAX, rates
