@@ -265,3 +265,10 @@ class _PairDebug(ctypes.Structure):
                     grad_hi=self.grad_hi, target=t.target, boundary=t.boundary,
                     count_greater=t.count_greater, count_equal=t.count_equal,
                     ties_admitted=t.ties_admitted, degenerate=t.degenerate)
+
+
+def extract_roi_job(args):
+    """Process-pool helper (spawn-safe): (frames, depth, params[, workers]) -> extract_roi result."""
+    frames, depth, params = args[:3]
+    workers = args[3] if len(args) > 3 else (os.cpu_count() or 1)
+    return Oracle("port").extract_roi(frames, depth, params, workers=workers)

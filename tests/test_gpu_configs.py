@@ -24,15 +24,8 @@ def _apply_shift(f, dx, dy):
 
 
 def _oracle_extract(args):
-    frames, depth, params = args
-    from oracle.oracle_py import Oracle
-    return Oracle("port").extract_roi(frames, depth, params, workers=os.cpu_count() or 1)
-
-
-def _oracle_flow(args):
-    a, b, depth, params = args
-    from oracle.oracle_py import Oracle
-    return Oracle("port").compute_flow(a, b, depth, params)
+    from oracle.oracle_py import extract_roi_job
+    return extract_roi_job(args)
 
 
 def check_config(gpu, oracle, frames, depth, params, label):
@@ -106,8 +99,12 @@ def test_c5_parameter_grid(gpu, synth):
     cfg = synth.scaled(synth.config("C2"), seed=5003)
     frames = synth.well_frames(cfg, 0, 2)
     grid = synth.c5_grid()
-    with ProcessPoolExecutor(max_workers=min(len(grid), os.cpu_count() or 1)) as ex:
-        wants = list(ex.map(_oracle_extract, [(frames, 8, p) for _, p in grid]))
+    import multiprocessing
+
+    from oracle.oracle_py import extract_roi_job
+    with ProcessPoolExecutor(max_workers=min(len(grid), os.cpu_count() or 1),
+                             mp_context=multiprocessing.get_context("spawn")) as ex:
+        wants = list(ex.map(extract_roi_job, [(frames, 8, p, 1) for _, p in grid]))
     rates = {}
     for (key, p), (want, shifts, _) in zip(grid, wants):
         got = gpu.extract_roi(frames, p, depth=8)
