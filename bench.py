@@ -325,8 +325,9 @@ def run_ours(args) -> None:
 
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
+        # ~10 s of the reference on every host thread: 8 pairs per thread of one C3 well
         cores = os.cpu_count() or 1
-        frames = max(3, min(cores + 1, 65))
+        frames = max(3, min(8 * cores + 1, 450))
         r = cpu_reference(frames, 0, 1, 0, cores)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 

@@ -222,6 +222,11 @@ def extract_roi(seq, params: ExtractParams | None = None, workers: int = 1,
     return masks[0]
 
 
+def shard_wells(n_wells: int, devices: list[int]) -> dict:
+    """Well w -> device devices[w mod len(devices)]; wells stay whole."""
+    return {d: [w for w in range(n_wells) if w % len(devices) == k] for k, d in enumerate(devices)}
+
+
 def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth: int | None = None,
                   devices: list[int] | None = None, layout: str = "bytes"):
     """Independent wells [wells, n, h, w], sharded well-wise over ``devices`` (one host thread
@@ -243,7 +248,7 @@ def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth
         except Exception as e:  # first error re-raised like parallel_for (parallel.hpp:31-48)
             errors.append(e)
 
-    shards = {d: [i for i in range(nw) if i % len(devices) == k] for k, d in enumerate(devices)}
+    shards = shard_wells(nw, devices)
     threads = [threading.Thread(target=work, args=(d, ws)) for d, ws in shards.items() if ws]
     for t in threads:
         t.start()
