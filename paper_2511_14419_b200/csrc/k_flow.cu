@@ -332,11 +332,38 @@ __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, siz
     return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * g.lw[a.l] + x];
 }
 
+// Packed fp32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2): two independent lanes per instruction.
+__device__ __forceinline__ void fma2(float& dx, float& dy, float ax, float ay, float bx, float by,
+                                     float cx, float cy) {
+    asm("{.reg .b64 a, b, c, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
+        "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(dx), "=f"(dy)
+        : "f"(ax), "f"(ay), "f"(bx), "f"(by), "f"(cx), "f"(cy));
+}
+__device__ __forceinline__ void mul2(float& dx, float& dy, float ax, float ay, float bx, float by) {
+    asm("{.reg .b64 a, b, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(dx), "=f"(dy)
+        : "f"(ax), "f"(ay), "f"(bx), "f"(by));
+}
+__device__ __forceinline__ void add2(float& dx, float& dy, float ax, float ay, float bx, float by) {
+    asm("{.reg .b64 a, b, d;\n\t"
+        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
+        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
+        : "=f"(dx), "=f"(dy)
+        : "f"(ax), "f"(ay), "f"(bx), "f"(by));
+}
+
 // Normal-equation products G of one pixel (flow.hpp:212-232).
 struct GTerms {
     float g11, g12, g22, h1, h2;
 };
 
+// Bilinear weights w00..w11 make every interpolated channel one FMUL + three FFMA (packed for the
+// (a11,a12) and (a22,bx) channel pairs).  fx = fy = 0 (or 1 at the far border) keeps exactly the
+// corner value, so identical frames still give exactly zero flow.
 __device__ __forceinline__ GTerms g_terms(const float4* __restrict__ pA, const float* __restrict__ pB,
                                           const float4* __restrict__ nA, const float* __restrict__ nB,
                                           int w, int h, int gx, int gy, float du, float dv) {
@@ -344,29 +371,45 @@ __device__ __forceinline__ GTerms g_terms(const float4* __restrict__ pA, const f
     float fx, fy;
     bl_split(gx, du, w, xa, fx);
     bl_split(gy, dv, h, ya, fy);
-    const float4* r0 = nA + (size_t)ya * w + xa;
-    const float* b0 = nB + (size_t)ya * w + xa;
-    const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r0 + w), q11 = __ldg(r0 + w + 1);
-    const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b0 + w), b11 = __ldg(b0 + w + 1);
-    const size_t o = (size_t)gy * w + gx;
+    const int i0 = ya * w + xa;
+    const float4* r0 = nA + i0;
+    const float4* r1 = r0 + w;
+    const float* b0 = nB + i0;
+    const float* b1 = b0 + w;
+    const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r1), q11 = __ldg(r1 + 1);
+    const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b1), b11 = __ldg(b1 + 1);
+    const int o = gy * w + gx;
     const float4 pa = __ldg(pA + o);
     const float pb = __ldg(pB + o);
     const float ofx = 1.f - fx, ofy = 1.f - fy;
-#define BL(c) ((q00.c * ofx + q01.c * fx) * ofy + (q10.c * ofx + q11.c * fx) * fy)
-    const float na11 = BL(x), na12 = BL(y), na22 = BL(z), nbx = BL(w);
-#undef BL
-    const float nby = (b00 * ofx + b01 * fx) * ofy + (b10 * ofx + b11 * fx) * fy;
-    const float a11 = 0.5f * (pa.x + na11);
-    const float a12 = 0.5f * (pa.y + na12);
-    const float a22 = 0.5f * (pa.z + na22);
-    const float db1 = -0.5f * (nbx - pa.w) + a11 * du + a12 * dv;
-    const float db2 = -0.5f * (nby - pb) + a12 * du + a22 * dv;
+    float w00, w01, w10, w11;
+    mul2(w00, w01, ofx, fx, ofy, ofy);
+    mul2(w10, w11, ofx, fx, fy, fy);
+    float n11, n12, n22, nbx;
+    mul2(n11, n12, q00.x, q00.y, w00, w00);
+    fma2(n11, n12, q01.x, q01.y, w01, w01, n11, n12);
+    fma2(n11, n12, q10.x, q10.y, w10, w10, n11, n12);
+    fma2(n11, n12, q11.x, q11.y, w11, w11, n11, n12);
+    mul2(n22, nbx, q00.z, q00.w, w00, w00);
+    fma2(n22, nbx, q01.z, q01.w, w01, w01, n22, nbx);
+    fma2(n22, nbx, q10.z, q10.w, w10, w10, n22, nbx);
+    fma2(n22, nbx, q11.z, q11.w, w11, w11, n22, nbx);
+    const float nby = fmaf(b11, w11, fmaf(b10, w10, fmaf(b01, w01, b00 * w00)));
+    float a11, a12, a22, e1;
+    add2(a11, a12, pa.x, pa.y, n11, n12);
+    mul2(a11, a12, a11, a12, 0.5f, 0.5f);
+    add2(a22, e1, pa.z, -pa.w, n22, nbx);          // (pa.z + n22, nbx - pa.w)
+    mul2(a22, e1, a22, e1, 0.5f, -0.5f);           // a22, -0.5 (nbx - bx_prev)
+    const float e2 = -0.5f * (nby - pb);
+    float db1, db2;
+    fma2(db1, db2, a11, a12, du, du, e1, e2);      // + A d (first column)
+    fma2(db1, db2, a12, a22, dv, dv, db1, db2);    // + A d (second column)
     GTerms t;
-    t.g11 = a11 * a11 + a12 * a12;
+    mul2(t.g11, t.g22, a11, a22, a11, a22);
+    fma2(t.g11, t.g22, a12, a12, a12, a12, t.g11, t.g22);
     t.g12 = (a11 + a22) * a12;
-    t.g22 = a12 * a12 + a22 * a22;
-    t.h1 = a11 * db1 + a12 * db2;
-    t.h2 = a12 * db1 + a22 * db2;
+    mul2(t.h1, t.h2, a11, a12, db1, db1);
+    fma2(t.h1, t.h2, a12, a22, db2, db2, t.h1, t.h2);
     return t;
 }
 
@@ -491,8 +534,8 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     }
     __syncthreads();
     float2* out = a.flow_out + pair_off + lo;
-    for (int i = threadIdx.x; i < FX * FY; i += FNT) {
-        const int ty = i / FX, tx = i - ty * FX;
+    const int tx = threadIdx.x % FX;
+    for (int ty = threadIdx.x / FX; ty < FY; ty += FNT / FX) {
         const int x = x0 + tx, y = y0 + ty;
         if (x >= w || y >= h) continue;
         const float inv = rcx[tx] * rcy[ty];
@@ -507,11 +550,11 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         if (!(det > 1e-9f * frob2)) {
             r = prior_at(g, a, pair_off, x, y);
         } else {
-            const float rd = __frcp_rn(det);
+            const float rd = __fdividef(1.f, det);
             r.x = (g22 * h1 - g12 * h2) * rd;
             r.y = (g11 * h2 - g12 * h1) * rd;
         }
-        out[(size_t)y * w + x] = r;
+        out[y * w + x] = r;
     }
 }
 
