@@ -361,30 +361,47 @@ struct GTerms {
     float g11, g12, g22, h1, h2;
 };
 
-// Bilinear weights w00..w11 make every interpolated channel one FMUL + three FFMA (packed for the
-// (a11,a12) and (a22,bx) channel pairs).  fx = fy = 0 (or 1 at the far border) keeps exactly the
-// corner value, so identical frames still give exactly zero flow.
-__device__ __forceinline__ GTerms g_terms(const float4* __restrict__ pA, const float* __restrict__ pB,
-                                          const float4* __restrict__ nA, const float* __restrict__ nB,
-                                          int w, int h, int gx, int gy, float du, float dv) {
+// Gathered operands of one pixel's normal-equation products.
+struct GLoad {
+    float4 q00, q01, q10, q11, pa;
+    float b00, b01, b10, b11, pb, fx, fy;
+};
+
+// Issue every gather of one pixel (no branches, so the loads of several pixels overlap).
+__device__ __forceinline__ void g_load(GLoad& o, const float4* __restrict__ pA,
+                                       const float* __restrict__ pB, const float4* __restrict__ nA,
+                                       const float* __restrict__ nB, int w, int h, int gx, int gy,
+                                       float du, float dv) {
     int xa, ya;
-    float fx, fy;
-    bl_split(gx, du, w, xa, fx);
-    bl_split(gy, dv, h, ya, fy);
+    bl_split(gx, du, w, xa, o.fx);
+    bl_split(gy, dv, h, ya, o.fy);
     const int i0 = ya * w + xa;
     const float4* r0 = nA + i0;
     const float4* r1 = r0 + w;
     const float* b0 = nB + i0;
     const float* b1 = b0 + w;
-    const float4 q00 = __ldg(r0), q01 = __ldg(r0 + 1), q10 = __ldg(r1), q11 = __ldg(r1 + 1);
-    const float b00 = __ldg(b0), b01 = __ldg(b0 + 1), b10 = __ldg(b1), b11 = __ldg(b1 + 1);
-    const int o = gy * w + gx;
-    const float4 pa = __ldg(pA + o);
-    const float pb = __ldg(pB + o);
-    const float ofx = 1.f - fx, ofy = 1.f - fy;
+    o.q00 = __ldg(r0);
+    o.q01 = __ldg(r0 + 1);
+    o.q10 = __ldg(r1);
+    o.q11 = __ldg(r1 + 1);
+    o.b00 = __ldg(b0);
+    o.b01 = __ldg(b0 + 1);
+    o.b10 = __ldg(b1);
+    o.b11 = __ldg(b1 + 1);
+    const int c = gy * w + gx;
+    o.pa = __ldg(pA + c);
+    o.pb = __ldg(pB + c);
+}
+
+// Bilinear weights w00..w11 make every interpolated channel one FMUL + three FFMA (packed for the
+// (a11,a12) and (a22,bx) channel pairs).  fx = fy = 0 (or 1 at the far border) keeps exactly the
+// corner value, so identical frames still give exactly zero flow.
+__device__ __forceinline__ GTerms g_terms(const GLoad& o, float du, float dv) {
+    const float4 q00 = o.q00, q01 = o.q01, q10 = o.q10, q11 = o.q11, pa = o.pa;
+    const float ofx = 1.f - o.fx, ofy = 1.f - o.fy;
     float w00, w01, w10, w11;
-    mul2(w00, w01, ofx, fx, ofy, ofy);
-    mul2(w10, w11, ofx, fx, fy, fy);
+    mul2(w00, w01, ofx, o.fx, ofy, ofy);
+    mul2(w10, w11, ofx, o.fx, o.fy, o.fy);
     float n11, n12, n22, nbx;
     mul2(n11, n12, q00.x, q00.y, w00, w00);
     fma2(n11, n12, q01.x, q01.y, w01, w01, n11, n12);
@@ -394,13 +411,13 @@ __device__ __forceinline__ GTerms g_terms(const float4* __restrict__ pA, const f
     fma2(n22, nbx, q01.z, q01.w, w01, w01, n22, nbx);
     fma2(n22, nbx, q10.z, q10.w, w10, w10, n22, nbx);
     fma2(n22, nbx, q11.z, q11.w, w11, w11, n22, nbx);
-    const float nby = fmaf(b11, w11, fmaf(b10, w10, fmaf(b01, w01, b00 * w00)));
+    const float nby = fmaf(o.b11, w11, fmaf(o.b10, w10, fmaf(o.b01, w01, o.b00 * w00)));
     float a11, a12, a22, e1;
     add2(a11, a12, pa.x, pa.y, n11, n12);
     mul2(a11, a12, a11, a12, 0.5f, 0.5f);
     add2(a22, e1, pa.z, -pa.w, n22, nbx);          // (pa.z + n22, nbx - pa.w)
     mul2(a22, e1, a22, e1, 0.5f, -0.5f);           // a22, -0.5 (nbx - bx_prev)
-    const float e2 = -0.5f * (nby - pb);
+    const float e2 = -0.5f * (nby - o.pb);
     float db1, db2;
     fma2(db1, db2, a11, a12, du, du, e1, e2);      // + A d (first column)
     fma2(db1, db2, a12, a22, dv, dv, db1, db2);    // + A d (second column)
@@ -424,12 +441,13 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const int* __restrict__ next,
                                                       const PairInfo* __restrict__ info) {
     extern __shared__ float smem_f[];
-    constexpr int HW = FX + 2 * R, HH = FY + 2 * R, PL = HW * HH;
+    // smem rows are SW = HW + 1 floats apart (odd stride: the row-wise box pass is conflict-free)
+    constexpr int HW = FX + 2 * R, HH = FY + 2 * R, SW = HW + 1, PL = SW * HH, NPX = HW * HH;
     const int p = blockIdx.z;
     const int l = a.l;
     const int w = g.lw[l], h = g.lh[l];
     const int x0 = blockIdx.x * FX, y0 = blockIdx.y * FY;
-    float* G = smem_f;  // 5 planes [HH][HW]; reused in place for the box sums
+    float* G = smem_f;  // 5 planes [HH][SW]; reused in place for the box sums
     const size_t pair_off = (size_t)p * g.lsum;
     const size_t lo = g.loff[l];
     const float4* pA = exA_f + (size_t)prev[p] * g.lsum + lo;
@@ -440,30 +458,42 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
 
     // phase 1: normal-equation products over tile + halo; two independent pixels per step so
     // each thread keeps ~20 gathers in flight
-    for (int i0 = threadIdx.x; i0 < PL; i0 += 2 * FNT) {
-        GTerms t[2];
+    const float2* fin = a.flow_in + pair_off + lo;
+    for (int i0 = threadIdx.x; i0 < NPX; i0 += 2 * FNT) {
+        // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
+        int gx[2], gy[2];
+        bool ok[2];
+        float2 pr[2];
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
-            const int i = i0 + k * FNT;
-            t[k] = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
-            if (i < PL) {
-                const int hy = i / HW, hx = i - hy * HW;
-                const int gx = x0 - R + hx, gy = y0 - R + hy;
-                if (gx >= 0 && gx < w && gy >= 0 && gy < h) {
-                    const float2 pr = prior_at(g, a, pair_off, gx, gy);
-                    t[k] = g_terms(pA, pB, nA, nB, w, h, gx, gy, pr.x, pr.y);
-                }
-            }
+            const int i = min(i0 + k * FNT, NPX - 1);
+            const int hy = i / HW, hx = i - hy * HW;
+            const int ux = x0 - R + hx, uy = y0 - R + hy;
+            ok[k] = i0 + k * FNT < NPX && ux >= 0 && ux < w && uy >= 0 && uy < h;
+            gx[k] = clampi(ux, 0, w - 1);
+            gy[k] = clampi(uy, 0, h - 1);
         }
+        // one asm statement issues both prior loads before either pixel's dependent index math
+        pr[0] = pr[1] = make_float2(0.f, 0.f);
+        if (a.mode)
+            asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
+                         : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
+                         : "l"(fin + gy[0] * w + gx[0]), "l"(fin + gy[1] * w + gx[1]));
+        GLoad ld[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) g_load(ld[k], pA, pB, nA, nB, w, h, gx[k], gy[k], pr[k].x, pr[k].y);
 #pragma unroll
         for (int k = 0; k < 2; ++k) {
             const int i = i0 + k * FNT;
-            if (i < PL) {
-                G[i] = t[k].g11;
-                G[PL + i] = t[k].g12;
-                G[2 * PL + i] = t[k].g22;
-                G[3 * PL + i] = t[k].h1;
-                G[4 * PL + i] = t[k].h2;
+            GTerms t = g_terms(ld[k], pr[k].x, pr[k].y);
+            if (!ok[k]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+            if (i < NPX) {
+                const int si = i + i / HW;  // hy * SW + hx
+                G[si] = t.g11;
+                G[PL + si] = t.g12;
+                G[2 * PL + si] = t.g22;
+                G[3 * PL + si] = t.h1;
+                G[4 * PL + si] = t.h2;
             }
         }
     }
@@ -478,11 +508,11 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         const float* col = G + c * PL + hx;
         float acc = 0.f;
 #pragma unroll
-        for (int j = 0; j <= 2 * R; ++j) acc += col[j * HW];
+        for (int j = 0; j <= 2 * R; ++j) acc += col[j * SW];
         acc_r[0] = acc;
 #pragma unroll
         for (int j = 1; j < FY; ++j) {
-            acc += col[(j + 2 * R) * HW] - col[(j - 1) * HW];
+            acc += col[(j + 2 * R) * SW] - col[(j - 1) * SW];
             acc_r[j] = acc;
         }
     }
@@ -491,7 +521,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         const int c = vt / HW, hx = vt - c * HW;
         float* col = G + c * PL + hx;
 #pragma unroll
-        for (int j = 0; j < FY; ++j) col[j * HW] = acc_r[j];
+        for (int j = 0; j < FY; ++j) col[j * SW] = acc_r[j];
     }
     __syncthreads();
     // phase 3: horizontal running sums along each of the 5*FY rows, in 32-wide segments
@@ -500,8 +530,8 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     if (hact) {
         const int c = threadIdx.x / (FY * NSEG);
         const int rem = threadIdx.x - c * FY * NSEG;
-        const int ty = rem / NSEG, sg = rem - ty * NSEG;
-        const float* row = G + c * PL + ty * HW + sg * 32;
+        const int sg = rem / FY, ty = rem - sg * FY;  // a warp walks 32 rows of one segment
+        const float* row = G + c * PL + ty * SW + sg * 32;
         float acc = 0.f;
 #pragma unroll
         for (int j = 0; j <= 2 * R; ++j) acc += row[j];
@@ -516,8 +546,8 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     if (hact) {
         const int c = threadIdx.x / (FY * NSEG);
         const int rem = threadIdx.x - c * FY * NSEG;
-        const int ty = rem / NSEG, sg = rem - ty * NSEG;
-        float* row = G + c * PL + ty * HW + sg * 32;
+        const int sg = rem / FY, ty = rem - sg * FY;
+        float* row = G + c * PL + ty * SW + sg * 32;
 #pragma unroll
         for (int j = 0; j < 32; ++j) row[j] = acc_r[j];
     }
@@ -539,7 +569,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         const int x = x0 + tx, y = y0 + ty;
         if (x >= w || y >= h) continue;
         const float inv = rcx[tx] * rcy[ty];
-        const int si = ty * HW + tx;
+        const int si = ty * SW + tx;
         const float g11 = G[si] * inv, g12 = G[PL + si] * inv, g22 = G[2 * PL + si] * inv;
         const float h1 = G[3 * PL + si] * inv, h2 = G[4 * PL + si] * inv;
         const float q = g12 * g12;
@@ -561,7 +591,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
 template <int R>
 void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                  const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R) * (FY + 2 * R);
+    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * (FY + 2 * R);
     static bool attr = false;
     if (!attr) {
         FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
