@@ -160,6 +160,163 @@ __global__ void __launch_bounds__(NT) k_denoise(int W, int H, int maxval, int en
     if ((tid & 31) == 0 && sum) atomicAdd(sums + slot, sum);
 }
 
+// 8-bit frames, median radius 1, bilateral radius 2 (the defaults).  A persistent CTA walks
+// 32x32 tiles with the next tile's raw pixels in flight in registers.
+//   median     each thread walks a column of the median tile: every raw row triple is sorted
+//              once (min3 / max3 / sum) and the 3x3 median is med3(max of lows, med3 of mids,
+//              min of highs) over the last three sorted triples (exact for integers).
+//   bilateral  each thread filters 4 consecutive rows of one column from a 5x5 register window
+//              (circular, 5 new medians per output), with the range weights in a 16-way
+//              replicated table indexed by the signed difference (lane & 15 picks the copy, so a
+//              warp's 64-bit lookups never bank-conflict beyond the 2-wavefront minimum).
+// Same fp64 operations in the same order as k_denoise.
+constexpr int QX = 32, QY = 32, QNT = 256, QRPT = QY / (QNT / QX), QREP = 16;
+constexpr int QRW = QX + 6, QRH = QY + 6, QMW = QX + 4, QMH = QY + 4;
+
+size_t qsmem_bytes() {
+    return sizeof(double) * (511 * QREP + QMW * QMH) + sizeof(int) * (QRW * QRH + QMW * QMH);
+}
+
+__device__ __forceinline__ int med3i(int a, int b, int c) {
+    return a + b + c - min(min(a, b), c) - max(max(a, b), c);
+}
+
+__global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int maxval, int n_slots,
+                                                            const void* const* frame_raw, uint8_t* den,
+                                                            unsigned long long* sums,
+                                                            const __grid_constant__ Spatial sp_w,
+                                                            const double* lut_g) {
+    constexpr int R1 = 3;
+    extern __shared__ __align__(16) unsigned char smem[];
+    double* lut_s = (double*)smem;                  // [511][QREP], index d + 255
+    double* medd_s = lut_s + 511 * QREP;            // QMH * QMW medians as double
+    int* raw_s = (int*)(medd_s + QMW * QMH);        // QRH * QRW
+    int* med_s = raw_s + QRW * QRH;                 // QMH * QMW medians * (QREP * 8)
+    const int tid = threadIdx.y * QX + threadIdx.x;
+    for (int i = tid; i < 511 * QREP; i += QNT) lut_s[i] = lut_g[min(abs(i / QREP - 255), maxval)];
+    // byte address of this lane's copy of entry d = 0; + (m_n - m_c) * QREP * 8 selects d
+    const char* lut0 = (const char*)(lut_s + 255 * QREP + (threadIdx.x & (QREP - 1)));
+    const int tiles_x = (W + QX - 1) / QX, tiles_y = (H + QY - 1) / QY;
+    const int per_slot = tiles_x * tiles_y;
+    const double B52 = 4503599627370496.0;
+    const int n_tiles = per_slot * n_slots;
+    constexpr int NRAW = (QRW * QRH + QNT - 1) / QNT;
+    // this thread's raw-tile positions are the same for every tile: (ry, rx) packed once
+    int rpos[NRAW];
+#pragma unroll
+    for (int k = 0; k < NRAW; ++k) {
+        const int i = tid + k * QNT, ry = i / QRW;
+        rpos[k] = i < QRW * QRH ? (ry << 16) | (i - ry * QRW) : -1;
+    }
+    auto fetch = [&](int t, int* v) {
+        const int slot = t / per_slot, tr = t - slot * per_slot;
+        const int by = tr / tiles_x, bx = tr - by * tiles_x;
+        const uint8_t* src = (const uint8_t*)frame_raw[slot];
+        const int gy0 = by * QY - R1, gx0 = bx * QX - R1;
+#pragma unroll
+        for (int k = 0; k < NRAW; ++k) {
+            v[k] = 0;
+            if (rpos[k] >= 0) {
+                const int gy = clampi(gy0 + (rpos[k] >> 16), 0, H - 1);
+                const int gx = clampi(gx0 + (rpos[k] & 0xffff), 0, W - 1);
+                v[k] = __ldg(src + gy * W + gx);
+            }
+        }
+    };
+    int rv[NRAW];
+    if (blockIdx.x < n_tiles) fetch(blockIdx.x, rv);
+    const int lane = threadIdx.x, grp = threadIdx.y;
+    for (int t = blockIdx.x; t < n_tiles; t += gridDim.x) {
+        const int slot = t / per_slot, tr = t - slot * per_slot;
+        const int by = tr / tiles_x, bx = tr - by * tiles_x;
+        const int x0 = bx * QX, y0 = by * QY;
+        __syncthreads();  // previous tile's bilateral is done with med_s / medd_s
+#pragma unroll
+        for (int k = 0; k < NRAW; ++k)
+            if (tid + k * QNT < QRW * QRH) raw_s[tid + k * QNT] = rv[k];
+        __syncthreads();
+        if (t + (int)gridDim.x < n_tiles) fetch(t + gridDim.x, rv);  // in flight during this tile
+        // medians at clamped centres (denoise.hpp:32-43): columns lane (+32 for lanes 0..3),
+        // rows [grp*QMH/8, (grp+1)*QMH/8)
+        for (int pass = 0; pass < 2; ++pass) {
+            const int mx = lane + 32 * pass;
+            if (mx >= QMW) break;
+            const int cx = clampi(x0 - 2 + mx, 0, W - 1) - (x0 - R1);  // raw_s column of the centre
+            const int rb = grp * QMH / 8, re = (grp + 1) * QMH / 8;
+            // sorted triple of raw_s row r around the centre column
+            auto tri = [&](int r, int& l, int& md, int& h) {
+                const int* q = raw_s + r * QRW + cx;
+                const int a = q[-1], b = q[0], c = q[1];
+                l = min(min(a, b), c);
+                h = max(max(a, b), c);
+                md = a + b + c - l - h;
+            };
+            // the clamped centre row advances by 0 or 1 per median row
+            int prev = clampi(y0 - 2 + rb, 0, H - 1) - (y0 - R1);
+            int l0, m0, h0, l1, m1, h1, l2, m2, h2;
+            tri(prev - 1, l0, m0, h0);
+            tri(prev, l1, m1, h1);
+            tri(prev + 1, l2, m2, h2);
+            int m = med3i(max(max(l0, l1), l2), med3i(m0, m1, m2), min(min(h0, h1), h2));
+            for (int my = rb; my < re; ++my) {
+                const int cy = clampi(y0 - 2 + my, 0, H - 1) - (y0 - R1);
+                if (cy != prev) {
+                    l0 = l1; m0 = m1; h0 = h1;
+                    l1 = l2; m1 = m2; h1 = h2;
+                    tri(cy + 1, l2, m2, h2);
+                    m = med3i(max(max(l0, l1), l2), med3i(m0, m1, m2), min(min(h0, h1), h2));
+                    prev = cy;
+                }
+                med_s[my * QMW + mx] = m * (QREP * 8);
+                medd_s[my * QMW + mx] = dsub(__hiloint2double(0x43300000, m), B52);
+            }
+        }
+        __syncthreads();
+        const int ty0 = grp * QRPT;
+        int mw[5][5];
+        double md[5][5];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int dx = 0; dx < 5; ++dx) {
+                mw[j][dx] = med_s[(ty0 + j) * QMW + lane + dx];
+                md[j][dx] = medd_s[(ty0 + j) * QMW + lane + dx];
+            }
+        unsigned long long sum = 0;
+#pragma unroll
+        for (int r = 0; r < QRPT; ++r) {
+            const int ns = (r + 4) % 5;  // slot of the new bottom row
+#pragma unroll
+            for (int dx = 0; dx < 5; ++dx) {
+                mw[ns][dx] = med_s[(ty0 + r + 4) * QMW + lane + dx];
+                md[ns][dx] = medd_s[(ty0 + r + 4) * QMW + lane + dx];
+            }
+            const char* lc = lut0 - mw[(r + 2) % 5][2];
+            double num = 0.0, dn = 0.0;
+#pragma unroll
+            for (int dy = 0; dy < 5; ++dy)
+#pragma unroll
+                for (int dx = 0; dx < 5; ++dx) {
+                    const double lw = *(const double*)(lc + mw[(r + dy) % 5][dx]);
+                    const double wgt = dmul(sp_w.w[dy * 5 + dx], lw);
+                    num = dadd(num, dmul(wgt, md[(r + dy) % 5][dx]));
+                    dn = dadd(dn, wgt);
+                }
+            double q = ddiv(num, dn);
+            q = (q < 0.0) ? 0.0 : q;
+            q = ((double)maxval < q) ? (double)maxval : q;
+            const int outv = (int)round(q);
+            const int x = x0 + lane, y = y0 + ty0 + r;
+            if (x < W && y < H) {
+                den[(size_t)slot * W * H + (size_t)y * W + x] = (uint8_t)outv;
+                sum += (unsigned long long)outv;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+        if ((tid & 31) == 0 && sum) atomicAdd(sums + slot, sum);
+    }
+}
+
 }  // namespace
 
 void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw, void* d_den,
@@ -175,6 +332,20 @@ void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw,
     Spatial sp{};
     for (int i = 0; i < side * side; ++i) sp.w[i] = h_spatial[i];
     const bool fast = mr == 1 && br == 2;
+    if (fast && p.denoise_enabled && g.sample_bytes == 1 && g.maxval <= 255) {
+        const size_t qsmem = qsmem_bytes();
+        static bool attr = false;
+        if (!attr) {
+            FROI_CUDA(cudaFuncSetAttribute(k_denoise_u8_m1b2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
+            attr = true;
+        }
+        const long long tiles = (long long)cdiv(g.W, QX) * cdiv(g.H, QY) * n_slots;
+        const int blocks = (int)std::min<long long>(tiles, 148 * 2);
+        k_denoise_u8_m1b2<<<blocks, dim3(QX, QNT / QX), qsmem, s>>>(g.W, g.H, g.maxval, n_slots, d_frame_raw,
+                                                                   (uint8_t*)d_den, d_sums, sp, d_lut);
+        FROI_LAUNCH_CHECK();
+        return;
+    }
     if (g.sample_bytes == 1) {
         auto k = fast ? k_denoise<uint8_t, 1, 2> : k_denoise<uint8_t, 0, 0>;
         if (smem > 48 * 1024)

@@ -104,25 +104,46 @@ __device__ __forceinline__ bool sel_match(unsigned long long key, const SelState
     return s.bits_done == 0 || (key >> (64 - s.bits_done)) == (s.prefix >> (64 - s.bits_done));
 }
 
-// Key sources.  Phase A: |flow| for queries 0,1 and |grad I| for 2,3 (producer or buffers).
-// Phase B: saliency for query 0, computed from the buffers, or read from a given map (tap).
-template <typename T>
-struct SrcProduce {
-    PairPix<T> px;
-    float* fm;
-    double* gr;
-    static constexpr int NQ = 4;
-    __device__ __forceinline__ void keys(long long i, int x, int y, const bool* act,
-                                         unsigned long long* k) const {
-        const float f = hypotf_glibc(px.flow[i].x, px.flow[i].y);
-        const double gg = px.grad(x, y);
-        fm[i] = f;
-        gr[i] = gg;
-        k[0] = k[1] = fkey(f);
-        k[2] = k[3] = dkey(gg);
-    }
-};
+// Exponent-window first digit: for a non-negative key, bin 1 + 64*(e - e0) + (top 6 mantissa
+// bits) over the 30 octaves [2^-25, 2^5), bin 0 below (zero included), bin kFpwBins-1 above.  A
+// regular bin is exactly the key prefix sign|exponent|6 mantissa bits (18 bits for a double, 15
+// for an fkey), so one pass resolves the 1/64 of an octave holding the rank -- typically few
+// enough keys to collect directly.  Ranks in the two open bins fall back to radix digits.
+constexpr int kFpwOct = 30, kFpwBins = 2 + 64 * kFpwOct;
+static_assert(kFpwBins <= kSelBins, "exponent window must fit the histogram");
 
+__device__ __forceinline__ int fpw_bin(unsigned long long k, int kind) {
+    int e, m;
+    if (kind == 1) {
+        e = (int)((k >> 52) & 0x7ff) - (1023 - 25);
+        m = (int)((k >> 46) & 63);
+    } else {
+        e = (int)((k >> 55) & 0xff) - (127 - 25);
+        m = (int)((k >> 49) & 63);
+    }
+    if (e < 0) return 0;
+    if (e >= kFpwOct) return kFpwBins - 1;
+    return 1 + 64 * e + m;
+}
+
+// prefix and its length for a regular bin
+__device__ __forceinline__ unsigned long long fpw_prefix(int bin, int kind, int& bits) {
+    const unsigned long long e = (unsigned long long)((bin - 1) >> 6), m = (unsigned long long)((bin - 1) & 63);
+    if (kind == 1) {
+        bits = 18;
+        return ((e + 1023 - 25) << 52) | (m << 46);
+    }
+    bits = 15;
+    return ((e + 127 - 25) << 55) | (m << 49);
+}
+
+__device__ __forceinline__ unsigned int sel_bin(unsigned long long k, const SelState& s, int shift, int width) {
+    if (s.bits_done == 0 && s.fpw) return (unsigned int)fpw_bin(k, s.fpw);
+    return (unsigned int)((k >> shift) & ((1u << width) - 1u));
+}
+
+// Key sources.  Phase A: |flow| for queries 0,1 and |grad I| for 2,3 (materialised buffers).
+// Phase B: saliency for query 0, computed from the buffers, or read from a given map (tap).
 struct SrcBufA {
     const float* fm;
     const double* gr;
@@ -226,7 +247,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                 }
             } else {
                 // histogram update; a warp whose matching keys share one bin adds once
-                const unsigned int bin = (unsigned int)((k[q] >> sh[q]) & ((1u << wd[q]) - 1u));
+                const unsigned int bin = sel_bin(k[q], st[q], sh[q], wd[q]);
                 const unsigned int bal = __ballot_sync(0xffffffffu, m);
                 if (bal) {
                     const int leader = __ffs(bal) - 1;
@@ -273,20 +294,100 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
 // Phase-A producer: |flow| (glibc hypotf) and |grad I| materialised + the first radix pass.
 constexpr int PNT_MG = 256;
 
+// warp-aggregated shared histogram increment (one atomic when the warp's keys share a bin)
+__device__ __forceinline__ void hist_add(unsigned int* h, bool m, unsigned int bin, int lane) {
+    const unsigned int bal = __ballot_sync(0xffffffffu, m);
+    if (!bal) return;
+    const int leader = __ffs(bal) - 1;
+    const unsigned int b0 = __shfl_sync(0xffffffffu, bin, leader);
+    if (__all_sync(0xffffffffu, !m || bin == b0)) {
+        if (lane == leader) atomicAdd(&h[b0], (unsigned int)__popc(bal));
+    } else if (m) {
+        atomicAdd(&h[bin], 1u);
+    }
+}
+
+// Row-blocked: each CTA owns whole rows of one pair (32-bit indexing).  Queries 0/1 (|flow|
+// percentiles) and 2/3 (|grad I|) share their first-pass histograms, so two are built (the
+// exponent-window digit) and added to both queries of each pair.
 template <typename T>
-__global__ void __launch_bounds__(PNT_MG) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
+__global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
     __shared__ double lut[256];
+    __shared__ unsigned int hist[2][kFpwBins];
+    __shared__ unsigned long long smn[2], smx[2];
     const int p = blockIdx.y;
     const PairInfo I = b.info[p];
-    SrcProduce<T> src;
-    src.px = make_pix<T>(g, P, b, I, p);
+    PairPix<T> px = make_pix<T>(g, P, b, I, p);
     if (sizeof(T) == 1) {
-        for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dmul((double)v, src.px.inv_maxval);
-        src.px.lut = lut;  // filled before the first barrier inside sel_pass_body
+        for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = dmul((double)v, px.inv_maxval);
+        px.lut = lut;
     }
-    src.fm = b.fm + (size_t)p * g.W * g.H;
-    src.gr = b.gr + (size_t)p * g.W * g.H;
-    sel_pass_body(g, b, p, src, true);
+    for (int i = threadIdx.x; i < 2 * kFpwBins; i += blockDim.x) (&hist[0][0])[i] = 0u;
+    if (threadIdx.x < 2) {
+        smn[threadIdx.x] = ~0ull;
+        smx[threadIdx.x] = 0ull;
+    }
+    __syncthreads();
+    const int W = g.W, H = g.H;
+    float* fm = b.fm + (size_t)p * W * H;
+    double* gr = b.gr + (size_t)p * W * H;
+    const int rows = (H + gridDim.x - 1) / gridDim.x;
+    const int y0 = blockIdx.x * rows, y1 = min(H, y0 + rows);
+    const int lane = threadIdx.x & 31;
+    unsigned long long mnf = ~0ull, mxf = 0ull, mng = ~0ull, mxg = 0ull;
+    for (int y = y0; y < y1; ++y) {
+        const int row = y * W;
+        for (int xb = 0; xb < W; xb += PNT_MG) {
+            const int x = xb + threadIdx.x;
+            const bool v = x < W;
+            unsigned long long kf = 0, kg = 0;
+            if (v) {
+                const float2 fl = px.flow[row + x];
+                const float f = hypotf_glibc(fl.x, fl.y);
+                const double gg = px.grad(x, y);
+                fm[row + x] = f;
+                gr[row + x] = gg;
+                kf = fkey(f);
+                kg = dkey(gg);
+                mnf = min(mnf, kf);
+                mxf = max(mxf, kf);
+                mng = min(mng, kg);
+                mxg = max(mxg, kg);
+            }
+            hist_add(hist[0], v, (unsigned int)fpw_bin(kf, 2), lane);
+            hist_add(hist[1], v, (unsigned int)fpw_bin(kg, 1), lane);
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        mnf = min(mnf, __shfl_xor_sync(0xffffffffu, mnf, o));
+        mxf = max(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
+        mng = min(mng, __shfl_xor_sync(0xffffffffu, mng, o));
+        mxg = max(mxg, __shfl_xor_sync(0xffffffffu, mxg, o));
+    }
+    if (lane == 0) {
+        atomicMin(&smn[0], mnf);
+        atomicMax(&smx[0], mxf);
+        atomicMin(&smn[1], mng);
+        atomicMax(&smx[1], mxg);
+    }
+    __syncthreads();
+    unsigned int* gh = b.hist + (size_t)p * kMaxQueries * kSelBins;
+    for (int i = threadIdx.x; i < kFpwBins; i += blockDim.x) {
+        const unsigned int hf = hist[0][i], hg = hist[1][i];
+        if (hf) {
+            atomicAdd(gh + i, hf);
+            atomicAdd(gh + kSelBins + i, hf);
+        }
+        if (hg) {
+            atomicAdd(gh + 2 * kSelBins + i, hg);
+            atomicAdd(gh + 3 * kSelBins + i, hg);
+        }
+    }
+    if (threadIdx.x < 4) {
+        const int k = threadIdx.x >> 1;
+        atomicMin(&b.sel[p * kMaxQueries + threadIdx.x].mn, smn[k]);
+        atomicMax(&b.sel[p * kMaxQueries + threadIdx.x].mx, smx[k]);
+    }
 }
 
 __global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
@@ -392,11 +493,22 @@ __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
                 int shift, width;
                 sel_digit(s.bits_done, shift, width);
                 SelState n = s;
+                const bool fp = s.bits_done == 0 && s.fpw;
+                n.fpw = 0;
                 if (s.mn == s.mx) {  // every key of the prefix group equals the answer
                     n.mode = SEL_DONE;
                     n.result = s.mn;
                     n.count_lt = s.k0 - s.rank;
                     n.count_eq = s.count;
+                } else if (fp && (bin == 0 || bin == kFpwBins - 1)) {
+                    // outside the exponent window: radix digits from the top
+                } else if (fp) {
+                    int bits;
+                    n.prefix = fpw_prefix(bin, s.fpw, bits);
+                    n.rank = r - c;
+                    n.count = loc[j];
+                    n.bits_done = bits;
+                    if (n.count <= (unsigned long long)kSelCap) n.mode = SEL_COLLECT;
                 } else {
                     n.prefix = s.prefix | ((unsigned long long)bin << shift);
                     n.rank = r - c;
@@ -422,7 +534,8 @@ __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
     for (int j = 0; j < PER; ++j) gh[threadIdx.x * PER + j] = 0u;
 }
 
-__device__ __forceinline__ SelState sel_init(unsigned long long k0, unsigned long long n, bool done) {
+__device__ __forceinline__ SelState sel_init(unsigned long long k0, unsigned long long n, bool done,
+                                             int fpw) {
     SelState s;
     s.prefix = 0;
     s.rank = k0;
@@ -435,6 +548,7 @@ __device__ __forceinline__ SelState sel_init(unsigned long long k0, unsigned lon
     s.count_eq = 0;
     s.bits_done = 0;
     s.mode = done ? SEL_DONE : SEL_HIST;
+    s.fpw = fpw;
     return s;
 }
 
@@ -442,7 +556,8 @@ __global__ void k_sel_init_a(MaskBuffers b, unsigned long long n, unsigned long 
                              unsigned long long ihi) {
     const int p = blockIdx.x;
     if (threadIdx.x < kMaxQueries)
-        b.sel[p * kMaxQueries + threadIdx.x] = sel_init((threadIdx.x & 1) ? ihi : ilo, n, false);
+        b.sel[p * kMaxQueries + threadIdx.x] = sel_init((threadIdx.x & 1) ? ihi : ilo, n, false,
+                                                        threadIdx.x < 2 ? 2 : 1);
 }
 
 // robust_normalize parameters (roi.hpp:47-63), then the threshold query (roi.hpp:114-120).
@@ -465,7 +580,7 @@ __global__ void k_sel_init_b(MaskBuffers b, unsigned long long n, unsigned long 
     }
     I.target = target;
     // (target-1)-th largest == (n-target)-th smallest
-    b.sel[p * kMaxQueries] = sel_init(target ? n - target : 0, n, target == 0);
+    b.sel[p * kMaxQueries] = sel_init(target ? n - target : 0, n, target == 0, from_stats ? 1 : 0);
     for (int q = 1; q < kMaxQueries; ++q) b.sel[p * kMaxQueries + q].mode = SEL_DONE;
 }
 

@@ -69,6 +69,8 @@ struct SelState {
     unsigned long long count_eq; // on completion: elements equal to the result
     int bits_done;
     int mode;                    // SelMode
+    int fpw;                     // first pass digit while bits_done == 0: 0 radix, 1 / 2 the
+                                 // exponent-window digit of a double / fkey (float) key
 };
 
 // Per-batch device tables.
