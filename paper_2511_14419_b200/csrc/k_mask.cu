@@ -82,8 +82,9 @@ __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P
 // Exact k-th order statistics over 64-bit keys (IEEE bit patterns of non-negative doubles).
 // Each query walks MSD digits of 11 bits with integer histograms; a pass also records min/max of
 // the keys still matching the prefix (all equal -> done), and once the selected bin holds at most
-// kSelCap keys the next pass collects them and k_sel_scan sorts them in shared memory.  The first
-// pass of phase A is fused into the producer that materialises |flow| and |grad I|.
+// kSelCap keys the next pass collects them and k_sel_scan finishes them in shared memory.  The
+// first pass uses an exponent-window digit; for phase A it is fused into the producer that
+// materialises |flow| and |grad I|.
 constexpr int SNT = 512;
 
 // |flow| keys: the float's own bit pattern in the high word (monotone for non-negative floats,
@@ -100,58 +101,63 @@ __device__ __forceinline__ void sel_digit(int bits_done, int& shift, int& width)
     shift = 64 - bits_done - width;
 }
 
-__device__ __forceinline__ bool sel_match(unsigned long long key, const SelState& s) {
-    return s.bits_done == 0 || (key >> (64 - s.bits_done)) == (s.prefix >> (64 - s.bits_done));
-}
 
-// Exponent-window first digit: for a non-negative key, bin 1 + 64*(e - e0) + (top 6 mantissa
-// bits) over the 30 octaves [2^-25, 2^5), bin 0 below (zero included), bin kFpwBins-1 above.  A
-// regular bin is exactly the key prefix sign|exponent|6 mantissa bits (18 bits for a double, 15
-// for an fkey), so one pass resolves the 1/64 of an octave holding the rank -- typically few
+// Exponent-window first digit: for a non-negative key, bin 1 + 128*(e - e0) + (top 7 mantissa
+// bits) over the 31 octaves [2^-26, 2^5), bin 0 below (zero included), bin kFpwBins-1 above.  A
+// regular bin is exactly the key prefix sign|exponent|7 mantissa bits (19 bits for a double, 16
+// for an fkey), so one pass resolves the 1/128 of an octave holding the rank -- typically few
 // enough keys to collect directly.  Ranks in the two open bins fall back to radix digits.
-constexpr int kFpwOct = 30, kFpwBins = 2 + 64 * kFpwOct;
-static_assert(kFpwBins <= kSelBins, "exponent window must fit the histogram");
+constexpr int kFpwOct = 31, kFpwSub = 7, kFpwBins = 2 + (kFpwOct << kFpwSub);
+static_assert(kFpwBins <= kHistBins, "exponent window must fit the histogram");
 
 __device__ __forceinline__ int fpw_bin(unsigned long long k, int kind) {
     int e, m;
     if (kind == 1) {
-        e = (int)((k >> 52) & 0x7ff) - (1023 - 25);
-        m = (int)((k >> 46) & 63);
+        e = (int)((k >> 52) & 0x7ff) - (1023 - 26);
+        m = (int)((k >> (52 - kFpwSub)) & ((1 << kFpwSub) - 1));
     } else {
-        e = (int)((k >> 55) & 0xff) - (127 - 25);
-        m = (int)((k >> 49) & 63);
+        e = (int)((k >> 55) & 0xff) - (127 - 26);
+        m = (int)((k >> (55 - kFpwSub)) & ((1 << kFpwSub) - 1));
     }
     if (e < 0) return 0;
     if (e >= kFpwOct) return kFpwBins - 1;
-    return 1 + 64 * e + m;
+    return 1 + (e << kFpwSub) + m;
 }
 
 // prefix and its length for a regular bin
 __device__ __forceinline__ unsigned long long fpw_prefix(int bin, int kind, int& bits) {
-    const unsigned long long e = (unsigned long long)((bin - 1) >> 6), m = (unsigned long long)((bin - 1) & 63);
+    const unsigned long long e = (unsigned long long)((bin - 1) >> kFpwSub);
+    const unsigned long long m = (unsigned long long)((bin - 1) & ((1 << kFpwSub) - 1));
     if (kind == 1) {
-        bits = 18;
-        return ((e + 1023 - 25) << 52) | (m << 46);
+        bits = 12 + kFpwSub;
+        return ((e + 1023 - 26) << 52) | (m << (52 - kFpwSub));
     }
-    bits = 15;
-    return ((e + 127 - 25) << 55) | (m << 49);
-}
-
-__device__ __forceinline__ unsigned int sel_bin(unsigned long long k, const SelState& s, int shift, int width) {
-    if (s.bits_done == 0 && s.fpw) return (unsigned int)fpw_bin(k, s.fpw);
-    return (unsigned int)((k >> shift) & ((1u << width) - 1u));
+    bits = 9 + kFpwSub;
+    return ((e + 127 - 26) << 55) | (m << (55 - kFpwSub));
 }
 
 // Key sources.  Phase A: |flow| for queries 0,1 and |grad I| for 2,3 (materialised buffers).
 // Phase B: saliency for query 0, computed from the buffers, or read from a given map (tap).
+// keys4 reads elements i..i+3 (i % 4 == 0, plane size % 4 == 0) with vector loads.
 struct SrcBufA {
     const float* fm;
     const double* gr;
     static constexpr int NQ = 4;
-    __device__ __forceinline__ void keys(long long i, int, int, const bool* act,
-                                         unsigned long long* k) const {
-        if (act[0] || act[1]) k[0] = k[1] = fkey(fm[i]);
-        if (act[2] || act[3]) k[2] = k[3] = dkey(gr[i]);
+    __device__ __forceinline__ void keys(long long i, unsigned long long* k) const {
+        k[0] = k[1] = fkey(fm[i]);
+        k[2] = k[3] = dkey(gr[i]);
+    }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
+        const float4 f = __ldg((const float4*)(fm + i));
+        const double2 g0 = __ldg((const double2*)(gr + i)), g1 = __ldg((const double2*)(gr + i + 2));
+        k[0][0] = k[1][0] = fkey(f.x);
+        k[0][1] = k[1][1] = fkey(f.y);
+        k[0][2] = k[1][2] = fkey(f.z);
+        k[0][3] = k[1][3] = fkey(f.w);
+        k[2][0] = k[3][0] = dkey(g0.x);
+        k[2][1] = k[3][1] = dkey(g0.y);
+        k[2][2] = k[3][2] = dkey(g1.x);
+        k[2][3] = k[3][3] = dkey(g1.y);
     }
 };
 
@@ -168,8 +174,14 @@ struct SrcSal {
     double w, w1;
     static constexpr int NQ = 1;
     __device__ __forceinline__ double value(long long i) const { return sal_from(I, w, w1, fm[i], gr[i]); }
-    __device__ __forceinline__ void keys(long long i, int, int, const bool*, unsigned long long* k) const {
-        k[0] = dkey(value(i));
+    __device__ __forceinline__ void keys(long long i, unsigned long long* k) const { k[0] = dkey(value(i)); }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
+        const float4 f = __ldg((const float4*)(fm + i));
+        const double2 g0 = __ldg((const double2*)(gr + i)), g1 = __ldg((const double2*)(gr + i + 2));
+        k[0][0] = dkey(sal_from(I, w, w1, f.x, g0.x));
+        k[0][1] = dkey(sal_from(I, w, w1, f.y, g0.y));
+        k[0][2] = dkey(sal_from(I, w, w1, f.z, g1.x));
+        k[0][3] = dkey(sal_from(I, w, w1, f.w, g1.y));
     }
 };
 
@@ -177,97 +189,140 @@ struct SrcMap {
     const double* map;
     static constexpr int NQ = 1;
     __device__ __forceinline__ double value(long long i) const { return map[i]; }
-    __device__ __forceinline__ void keys(long long i, int, int, const bool*, unsigned long long* k) const {
-        k[0] = dkey(map[i]);
+    __device__ __forceinline__ void keys(long long i, unsigned long long* k) const { k[0] = dkey(map[i]); }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
+        const double2 g0 = __ldg((const double2*)(map + i)), g1 = __ldg((const double2*)(map + i + 2));
+        k[0][0] = dkey(g0.x);
+        k[0][1] = dkey(g0.y);
+        k[0][2] = dkey(g1.x);
+        k[0][3] = dkey(g1.y);
     }
 };
 
-// One pass of every active query of one pair over a contiguous pixel range.
+// warp-aggregated shared histogram increment (one atomic when the warp's keys share a bin);
+// every lane of the warp must call it
+__device__ __forceinline__ void hist_add(unsigned int* h, bool m, unsigned int bin, int lane) {
+    const unsigned int bal = __ballot_sync(0xffffffffu, m);
+    if (!bal) return;
+    const int leader = __ffs(bal) - 1;
+    const unsigned int b0 = __shfl_sync(0xffffffffu, bin, leader);
+    if (__all_sync(0xffffffffu, !m || bin == b0)) {
+        if (lane == leader) atomicAdd(&h[b0], (unsigned int)__popc(bal));
+    } else if (m) {
+        atomicAdd(&h[bin], 1u);
+    }
+}
+
+// One pass of every active query of one pair over a contiguous range of the pair's pixels, four
+// consecutive pixels per thread: histogram of the next digit (exponent window first for
+// single-query sources) for queries in HIST mode, warp-aggregated candidate append for queries in
+// COLLECT mode.  All threads of the CTA run the same number of iterations (warp votes inside).
 template <class Src>
-__device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src, bool produce) {
+__device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src) {
     constexpr int NQ = Src::NQ;
-    __shared__ unsigned int hist[NQ][kSelBins];
+    constexpr int NB = NQ == 1 ? kHistBins : kSelBins;
+    __shared__ unsigned int hist[NQ][NB];
     __shared__ SelState st[NQ];
     __shared__ unsigned long long smn[NQ], smx[NQ];
-    __shared__ int any_active;
     if (threadIdx.x < NQ) {
         st[threadIdx.x] = b.sel[p * kMaxQueries + threadIdx.x];
         smn[threadIdx.x] = ~0ull;
         smx[threadIdx.x] = 0ull;
     }
-    for (int i = threadIdx.x; i < NQ * kSelBins; i += blockDim.x) (&hist[0][0])[i] = 0;
     __syncthreads();
-    if (threadIdx.x == 0) {
-        int a = 0;
-        for (int q = 0; q < NQ; ++q) a |= st[q].mode != SEL_DONE;
-        any_active = a;
-    }
-    __syncthreads();
-    if (!any_active && !produce) return;
-    bool act[NQ], col[NQ];
-    int sh[NQ], wd[NQ];
-    unsigned long long lmn[NQ], lmx[NQ];
+    bool anyh = false, anyc = false;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        act[q] = st[q].mode != SEL_DONE;
-        col[q] = st[q].mode == SEL_COLLECT;
+        anyh |= st[q].mode == SEL_HIST;
+        anyc |= st[q].mode == SEL_COLLECT;
+    }
+    if (!anyh && !anyc) return;
+    if (anyh) {
+        for (int i = threadIdx.x; i < NQ * NB; i += blockDim.x) (&hist[0][0])[i] = 0;
+        __syncthreads();
+    }
+    bool hq[NQ], cq[NQ];
+    int sh[NQ], wd[NQ], fp[NQ], ms[NQ];
+    unsigned long long mp[NQ], lmn[NQ], lmx[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        hq[q] = st[q].mode == SEL_HIST;
+        cq[q] = st[q].mode == SEL_COLLECT;
         sel_digit(st[q].bits_done, sh[q], wd[q]);
+        fp[q] = (NQ == 1 && st[q].bits_done == 0) ? st[q].fpw : 0;
+        ms[q] = 64 - st[q].bits_done;  // keys match when key >> ms == prefix >> ms (ms < 64)
+        mp[q] = ms[q] < 64 ? st[q].prefix >> ms[q] : 0ull;
         lmn[q] = ~0ull;
         lmx[q] = 0ull;
     }
     const long long n = (long long)g.W * g.H;
-    const long long per = cdiv<long long>(n, gridDim.x);
+    const bool vec = (n & 3) == 0;
+    const long long per = cdiv<long long>(cdiv<long long>(n, gridDim.x), 4) * 4;
     const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
     const int lane = threadIdx.x & 31;
-    for (long long base = i0; base < i1; base += blockDim.x) {
-        const long long i = base + threadIdx.x;
-        const bool valid = i < i1;
-        unsigned long long k[NQ];
-        if (valid) {
-            const int y = (int)(i / g.W), x = (int)(i - (long long)y * g.W);
-            src.keys(i, x, y, act, k);
+    for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
+        const long long base = base0 + 4ll * threadIdx.x;
+        unsigned long long k[NQ][4];
+        bool v[4];
+        if (vec && base + 3 < i1) {
+            src.keys4(base, k);
+            v[0] = v[1] = v[2] = v[3] = true;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                v[e] = base + e < i1;
+                unsigned long long t[NQ];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) t[q] = 0;
+                if (v[e]) src.keys(base + e, t);
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) k[q][e] = t[q];
+            }
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            if (!act[q]) continue;
-            const bool m = valid && sel_match(k[q], st[q]);
-            if (col[q]) {
-                // warp-aggregated append of the remaining candidates
-                const unsigned int bal = __ballot_sync(0xffffffffu, m);
-                if (bal) {
-                    unsigned int basei = 0;
-                    const int leader = __ffs(bal) - 1;
-                    if (lane == leader) basei = atomicAdd(b.cand_count + p * kMaxQueries + q, __popc(bal));
-                    basei = __shfl_sync(0xffffffffu, basei, leader);
+            if (hq[q]) {
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    const bool m = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
+                    const unsigned int bin = fp[q] ? (unsigned int)fpw_bin(k[q][e], fp[q])
+                                                   : (unsigned int)((k[q][e] >> sh[q]) & ((1u << wd[q]) - 1u));
+                    hist_add(hist[q], m, bin, lane);
                     if (m) {
-                        const unsigned int idx = basei + __popc(bal & ((1u << lane) - 1u));
-                        if (idx < (unsigned)kSelCap)
-                            b.cand[((size_t)p * kMaxQueries + q) * kSelCap + idx] = k[q];
+                        lmn[q] = min(lmn[q], k[q][e]);
+                        lmx[q] = max(lmx[q], k[q][e]);
                     }
                 }
-            } else {
-                // histogram update; a warp whose matching keys share one bin adds once
-                const unsigned int bin = sel_bin(k[q], st[q], sh[q], wd[q]);
-                const unsigned int bal = __ballot_sync(0xffffffffu, m);
-                if (bal) {
-                    const int leader = __ffs(bal) - 1;
-                    const unsigned int b0 = __shfl_sync(0xffffffffu, bin, leader);
-                    if (__all_sync(0xffffffffu, !m || bin == b0)) {
-                        if (lane == leader) atomicAdd(&hist[q][b0], (unsigned int)__popc(bal));
-                    } else if (m) {
-                        atomicAdd(&hist[q][bin], 1u);
-                    }
+            } else if (cq[q]) {
+                bool m[4], any = false;
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    m[e] = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
+                    any |= m[e];
                 }
-                if (m) {
-                    lmn[q] = min(lmn[q], k[q]);
-                    lmx[q] = max(lmx[q], k[q]);
+                if (__any_sync(0xffffffffu, any)) {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const unsigned int bal = __ballot_sync(0xffffffffu, m[e]);
+                        if (!bal) continue;
+                        unsigned int basei = 0;
+                        const int leader = __ffs(bal) - 1;
+                        if (lane == leader) basei = atomicAdd(b.cand_count + p * kMaxQueries + q, __popc(bal));
+                        basei = __shfl_sync(0xffffffffu, basei, leader);
+                        if (m[e]) {
+                            const unsigned int idx = basei + __popc(bal & ((1u << lane) - 1u));
+                            if (idx < (unsigned)kSelCap)
+                                b.cand[((size_t)p * kMaxQueries + q) * kSelCap + idx] = k[q][e];
+                        }
+                    }
                 }
             }
         }
     }
+    if (!anyh) return;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        if (!act[q] || col[q]) continue;
+        if (!hq[q]) continue;
         unsigned long long a = lmn[q], c = lmx[q];
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -280,9 +335,9 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     }
     __syncthreads();
     for (int q = 0; q < NQ; ++q) {
-        if (!act[q] || col[q]) continue;
-        unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
-        for (int i = threadIdx.x; i < kSelBins; i += blockDim.x)
+        if (!hq[q]) continue;
+        unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kHistBins;
+        for (int i = threadIdx.x; i < NB; i += blockDim.x)
             if (hist[q][i]) atomicAdd(gh + i, hist[q][i]);
         if (threadIdx.x == 0) {
             atomicMin(&b.sel[p * kMaxQueries + q].mn, smn[q]);
@@ -291,21 +346,8 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     }
 }
 
-// Phase-A producer: |flow| (glibc hypotf) and |grad I| materialised + the first radix pass.
+// Phase-A producer: |flow| (glibc hypotf) and |grad I| materialised + the first pass.
 constexpr int PNT_MG = 256;
-
-// warp-aggregated shared histogram increment (one atomic when the warp's keys share a bin)
-__device__ __forceinline__ void hist_add(unsigned int* h, bool m, unsigned int bin, int lane) {
-    const unsigned int bal = __ballot_sync(0xffffffffu, m);
-    if (!bal) return;
-    const int leader = __ffs(bal) - 1;
-    const unsigned int b0 = __shfl_sync(0xffffffffu, bin, leader);
-    if (__all_sync(0xffffffffu, !m || bin == b0)) {
-        if (lane == leader) atomicAdd(&h[b0], (unsigned int)__popc(bal));
-    } else if (m) {
-        atomicAdd(&h[bin], 1u);
-    }
-}
 
 // Row-blocked: each CTA owns whole rows of one pair (32-bit indexing).  Queries 0/1 (|flow|
 // percentiles) and 2/3 (|grad I|) share their first-pass histograms, so two are built (the
@@ -371,16 +413,16 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
         atomicMax(&smx[1], mxg);
     }
     __syncthreads();
-    unsigned int* gh = b.hist + (size_t)p * kMaxQueries * kSelBins;
+    unsigned int* gh = b.hist + (size_t)p * kMaxQueries * kHistBins;
     for (int i = threadIdx.x; i < kFpwBins; i += blockDim.x) {
         const unsigned int hf = hist[0][i], hg = hist[1][i];
         if (hf) {
             atomicAdd(gh + i, hf);
-            atomicAdd(gh + kSelBins + i, hf);
+            atomicAdd(gh + kHistBins + i, hf);
         }
         if (hg) {
-            atomicAdd(gh + 2 * kSelBins + i, hg);
-            atomicAdd(gh + 3 * kSelBins + i, hg);
+            atomicAdd(gh + 2 * kHistBins + i, hg);
+            atomicAdd(gh + 3 * kHistBins + i, hg);
         }
     }
     if (threadIdx.x < 4) {
@@ -390,26 +432,26 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     }
 }
 
-__global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
+__global__ void __launch_bounds__(SNT, 1) k_sel_pass_a(Geom g, MaskBuffers b) {
     const int p = blockIdx.y;
     SrcBufA src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H};
-    sel_pass_body(g, b, p, src, false);
+    sel_pass_body(g, b, p, src);
 }
 
 __global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map) {
     const int p = blockIdx.y;
     if (map) {
         SrcMap src{map};
-        sel_pass_body(g, b, p, src, false);
+        sel_pass_body(g, b, p, src);
     } else {
         SrcSal src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H, b.info[p],
                    P.flow_weight, 1.0 - P.flow_weight};
-        sel_pass_body(g, b, p, src, false);
+        sel_pass_body(g, b, p, src);
     }
 }
 
-// One CTA per (pair, query): narrow the prefix after a histogram pass, or sort the collected
-// candidates (<= kSelCap keys, bitonic in shared memory) after a collect pass.
+// One CTA per (pair, query): narrow the prefix after a histogram pass, or finish a collected
+// group (<= kSelCap keys, all sharing the prefix) by an 8-bit-digit radix select in shared memory.
 constexpr int SCT = 1024;
 
 __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
@@ -422,53 +464,73 @@ __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
     __syncthreads();
     if (s.mode == SEL_DONE) return;
     if (s.mode == SEL_COLLECT) {
+        __shared__ unsigned int h8[256];
+        __shared__ unsigned long long s_pfx, s_r;
+        __shared__ unsigned int s_cnt;
         unsigned int* cc = b.cand_count + p * kMaxQueries + q;
-        const unsigned int n = min((unsigned int)kSelCap, *cc);
-        int np2 = 1;
-        while (np2 < (int)n) np2 <<= 1;
+        const int n = (int)min((unsigned int)kSelCap, *cc);
         const unsigned long long* src = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
-        for (int i = threadIdx.x; i < np2; i += SCT) cs[i] = i < (int)n ? src[i] : ~0ull;
+        for (int i = threadIdx.x; i < n; i += SCT) cs[i] = src[i];
+        if (threadIdx.x == 0) {
+            s_pfx = s.prefix;
+            s_r = s.rank;
+            s_cnt = (unsigned int)n;
+        }
         __syncthreads();
-        for (int k = 2; k <= np2; k <<= 1)
-            for (int j = k >> 1; j > 0; j >>= 1) {
-                for (int i = threadIdx.x; i < np2; i += SCT) {
-                    const int ixj = i ^ j;
-                    if (ixj > i) {
-                        const bool up = (i & k) == 0;
-                        const unsigned long long a = cs[i], c = cs[ixj];
-                        if ((a > c) == up) {
-                            cs[i] = c;
-                            cs[ixj] = a;
+        for (int bd = s.bits_done; bd < 64;) {
+            const int w = min(8, 64 - bd), sh = 64 - bd - w;
+            if (threadIdx.x < 256) h8[threadIdx.x] = 0u;
+            __syncthreads();
+            const unsigned long long pf = s_pfx;
+            for (int i = threadIdx.x; i < n; i += SCT) {
+                const unsigned long long k = cs[i];
+                if (bd == 0 || (k >> (64 - bd)) == (pf >> (64 - bd)))
+                    atomicAdd(&h8[(unsigned int)(k >> sh) & ((1u << w) - 1u)], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x < 32) {
+                const int lane = threadIdx.x;
+                unsigned int c8[8], sum = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    c8[j] = h8[lane * 8 + j];
+                    sum += c8[j];
+                }
+                unsigned int incl = sum;
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned int t = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= o) incl += t;
+                }
+                const unsigned long long r = s_r;
+                unsigned long long c = incl - sum;
+                if (r >= c && r < (unsigned long long)incl) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        if (r >= c && r < c + c8[j]) {
+                            s_pfx = pf | ((unsigned long long)(lane * 8 + j) << sh);
+                            s_r = r - c;
+                            s_cnt = c8[j];
                         }
+                        c += c8[j];
                     }
                 }
-                __syncthreads();
             }
+            __syncthreads();
+            bd += w;
+        }
         if (threadIdx.x == 0) {
-            const unsigned long long r = cs[s.rank];
-            unsigned long long lo = 0, hi = n;  // lower_bound(r)
-            while (lo < hi) {
-                const unsigned long long mid = (lo + hi) / 2;
-                if (cs[mid] < r) lo = mid + 1; else hi = mid;
-            }
-            unsigned long long lo2 = lo;  // upper_bound(r)
-            hi = n;
-            while (lo2 < hi) {
-                const unsigned long long mid = (lo2 + hi) / 2;
-                if (cs[mid] <= r) lo2 = mid + 1; else hi = mid;
-            }
             SelState ns = s;
-            ns.result = r;
-            ns.count_lt = (s.k0 - s.rank) + lo;
-            ns.count_eq = lo2 - lo;
+            ns.result = s_pfx;
+            ns.count_lt = s.k0 - s_r;
+            ns.count_eq = s_cnt;
             ns.mode = SEL_DONE;
             *sp = ns;
             *cc = 0;
         }
         return;
     }
-    unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kSelBins;
-    constexpr int PER = kSelBins / SCT;
+    unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kHistBins;
+    constexpr int PER = kHistBins / SCT;
     unsigned int loc[PER];
     unsigned int tot = 0;
     for (int j = 0; j < PER; ++j) {

@@ -20,6 +20,7 @@ namespace froi {
 constexpr int kMaxLevels = 16;
 constexpr int kSelBits = 11;  // radix-select digit width
 constexpr int kSelBins = 1 << kSelBits;
+constexpr int kHistBins = 4096;  // per-query global histogram stride (radix digit or exponent window)
 constexpr int kMaxQueries = 4;
 constexpr int kSelCap = 16384;  // candidates sorted in shared memory once a radix bin is this small
 enum SelMode { SEL_HIST = 0, SEL_COLLECT = 1, SEL_DONE = 2 };
@@ -139,7 +140,7 @@ struct MaskBuffers {
     long long flow_stride;        // elements between pairs
     const void** raw;             // [pair] raw frame t pointer (T)
     SelState* sel;                // [pair][kMaxQueries]
-    unsigned int* hist;           // [pair][kMaxQueries][kSelBins]
+    unsigned int* hist;           // [pair][kMaxQueries][kHistBins]
     unsigned long long* cand;     // [pair][kMaxQueries][kSelCap]
     unsigned int* cand_count;     // [pair][kMaxQueries]
     float* fm;                    // [pair][H*W] |flow| (FlowField::mag)

@@ -386,8 +386,8 @@ void ctx_alloc(froi_ctx* c) {
     c->d_flow0 = dalloc<float2>((size_t)g.lsum * P, &t);
     c->d_flow1 = dalloc<float2>((size_t)g.lsum * P, &t);
     c->d_sel = dalloc<SelState>((size_t)kMaxQueries * P, &t);
-    c->d_hist = dalloc<unsigned int>((size_t)kMaxQueries * kSelBins * P, &t);
-    FROI_CUDA(cudaMemset(c->d_hist, 0, sizeof(unsigned int) * (size_t)kMaxQueries * kSelBins * P));
+    c->d_hist = dalloc<unsigned int>((size_t)kMaxQueries * kHistBins * P, &t);
+    FROI_CUDA(cudaMemset(c->d_hist, 0, sizeof(unsigned int) * (size_t)kMaxQueries * kHistBins * P));
     c->d_cand = dalloc<unsigned long long>((size_t)kMaxQueries * kSelCap * P, &t);
     c->d_cand_count = dalloc<unsigned int>((size_t)kMaxQueries * P, &t);
     FROI_CUDA(cudaMemset(c->d_cand_count, 0, sizeof(unsigned int) * (size_t)kMaxQueries * P));
