@@ -221,13 +221,20 @@ template <class Src>
 __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src) {
     constexpr int NQ = Src::NQ;
     constexpr int NB = NQ == 1 ? kHistBins : kSelBins;
-    __shared__ unsigned int hist[NQ][NB];
+    constexpr int CB = NQ == 1 ? 2048 : 1024;
+    // dynamic shared memory (pass_smem): COLLECT staging [NQ][CB] keys, then HIST [NQ][NB] bins
+    extern __shared__ __align__(16) unsigned char dsm[];
+    unsigned long long (*cbuf)[CB] = reinterpret_cast<unsigned long long (*)[CB]>(dsm);
+    unsigned int (*hist)[NB] = reinterpret_cast<unsigned int (*)[NB]>(dsm + sizeof(unsigned long long) * NQ * CB);
     __shared__ SelState st[NQ];
     __shared__ unsigned long long smn[NQ], smx[NQ];
+    // COLLECT: candidates staged per block in shared memory (one global reservation per query)
+    __shared__ unsigned int ccnt[NQ], cbase[NQ];
     if (threadIdx.x < NQ) {
         st[threadIdx.x] = b.sel[p * kMaxQueries + threadIdx.x];
         smn[threadIdx.x] = ~0ull;
         smx[threadIdx.x] = 0ull;
+        ccnt[threadIdx.x] = 0u;
     }
     __syncthreads();
     bool anyh = false, anyc = false;
@@ -307,16 +314,36 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                         if (!bal) continue;
                         unsigned int basei = 0;
                         const int leader = __ffs(bal) - 1;
-                        if (lane == leader) basei = atomicAdd(b.cand_count + p * kMaxQueries + q, __popc(bal));
+                        if (lane == leader) basei = atomicAdd(&ccnt[q], __popc(bal));
                         basei = __shfl_sync(0xffffffffu, basei, leader);
                         if (m[e]) {
                             const unsigned int idx = basei + __popc(bal & ((1u << lane) - 1u));
-                            if (idx < (unsigned)kSelCap)
-                                b.cand[((size_t)p * kMaxQueries + q) * kSelCap + idx] = k[q][e];
+                            if (idx < (unsigned)CB) {
+                                cbuf[q][idx] = k[q][e];
+                            } else {  // staging full: straight to the global list
+                                const unsigned int gi = atomicAdd(b.cand_count + p * kMaxQueries + q, 1u);
+                                if (gi < (unsigned)kSelCap)
+                                    b.cand[((size_t)p * kMaxQueries + q) * kSelCap + gi] = k[q][e];
+                            }
                         }
                     }
                 }
             }
+        }
+    }
+    if (anyc) {
+        __syncthreads();
+        if (threadIdx.x < NQ && cq[threadIdx.x]) {
+            const unsigned int c = min(ccnt[threadIdx.x], (unsigned int)CB);
+            cbase[threadIdx.x] = c ? atomicAdd(b.cand_count + p * kMaxQueries + threadIdx.x, c) : 0u;
+        }
+        __syncthreads();
+        for (int q = 0; q < NQ; ++q) {
+            if (!cq[q]) continue;
+            const unsigned int c = min(ccnt[q], (unsigned int)CB);
+            unsigned long long* dst = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
+            for (unsigned int i = threadIdx.x; i < c; i += blockDim.x)
+                if (cbase[q] + i < (unsigned)kSelCap) dst[cbase[q] + i] = cbuf[q][i];
         }
     }
     if (!anyh) return;
@@ -432,7 +459,7 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     }
 }
 
-__global__ void __launch_bounds__(SNT, 1) k_sel_pass_a(Geom g, MaskBuffers b) {
+__global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
     const int p = blockIdx.y;
     SrcBufA src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H};
     sel_pass_body(g, b, p, src);
@@ -448,6 +475,10 @@ __global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuf
                    P.flow_weight, 1.0 - P.flow_weight};
         sel_pass_body(g, b, p, src);
     }
+}
+
+constexpr size_t pass_smem(int nq) {
+    return (sizeof(unsigned long long) * (nq == 1 ? 2048 : 1024) + sizeof(unsigned int) * (nq == 1 ? kHistBins : kSelBins)) * nq;
 }
 
 // One CTA per (pair, query): narrow the prefix after a histogram pass, or finish a collected
@@ -1128,6 +1159,8 @@ size_t scan_smem() { return sizeof(unsigned long long) * kSelCap; }
 void set_scan_smem() {
     static bool done = false;
     if (!done) {
+        FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(4)));
+        FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(1)));
         FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
         done = true;
     }
@@ -1153,7 +1186,7 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
     FROI_LAUNCH_CHECK();
     *launches += 3;
     for (int it = 0; it < kSelPasses; ++it) {
-        k_sel_pass_a<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, b);
+        k_sel_pass_a<<<dim3(bpp, n_pairs), SNT, pass_smem(4), s>>>(g, b);
         k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
         FROI_LAUNCH_CHECK();
         *launches += 2;
@@ -1171,7 +1204,7 @@ void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n
     FROI_LAUNCH_CHECK();
     ++*launches;
     for (int it = 0; it < kSelPasses + 1; ++it) {
-        k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, 0, s>>>(g, P, b, map);
+        k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, pass_smem(1), s>>>(g, P, b, map);
         k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1);
         FROI_LAUNCH_CHECK();
         *launches += 2;
