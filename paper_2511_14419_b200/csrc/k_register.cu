@@ -35,52 +35,74 @@ __device__ __forceinline__ void bfly(double2& u, double2& v, const double2 w) {
     u = nu;
 }
 
-// In-place radix-2 stages over `ncol` interleaved transforms of length n (element i of
-// transform c at a[i*ncol + c]); input already bit-reversed.  tw: stage with half-length h
-// uses tw[h-1 .. 2h-2] (the reference's w sequence for len = 2h).  Two consecutive stages are
-// fused per pass on groups {i, i+h, i+2h, i+3h} held in registers: the butterflies and their
-// operands are exactly the reference's, only the number of shared-memory round trips halves.
-__device__ __forceinline__ void fft_stages(double2* a, int n, int log2n, int ncol,
-                                           const double2* tw) {
-    int s = 0;
-    for (; s + 1 < log2n; s += 2) {
-        const int h = 1 << s;
-        const int ng = (n >> 2) * ncol;
-        for (int j = threadIdx.x; j < ng; j += blockDim.x) {
-            const int c = j % ncol;
-            const int b = j / ncol;
-            const int k = b & (h - 1);
-            const int i = ((b >> s) << (s + 2)) + k;
-            double2* p0 = a + i * ncol + c;
-            double2 e0 = p0[0], e1 = p0[h * ncol], e2 = p0[2 * h * ncol], e3 = p0[3 * h * ncol];
-            const double2 w1 = tw[h - 1 + k];
-            bfly(e0, e1, w1);
-            bfly(e2, e3, w1);
-            bfly(e0, e2, tw[2 * h - 1 + k]);
-            bfly(e1, e3, tw[2 * h - 1 + k + h]);
-            p0[0] = e0;
-            p0[h * ncol] = e1;
-            p0[2 * h * ncol] = e2;
-            p0[3 * h * ncol] = e3;
+// Shared-memory slot of element i: pad slots every 16 and every 128 elements keep every radix-16
+// pass and the bit-reversed scatter (interleave index fastest across lanes) at the 4-wavefront
+// minimum for 16-byte elements, for rows and column blocks alike (checked offline for n = 2^8..2^12).
+__device__ __forceinline__ int pd(int i) { return i + (i >> 4) + (i >> 7); }
+__host__ __device__ constexpr int padded(int n) { return n + (n >> 4) + (n >> 7) + 1; }
+
+// Q consecutive radix-2 stages (half-lengths h, 2h, .., h*2^(Q-1), h = 2^s) over groups of
+// 2^Q elements {i + m*h} held in registers, for `1 << lc` interleaved transforms of length n
+// (element i of transform c at a[pd(i) << lc | c]).  Every butterfly is the reference's
+// (fft.hpp:32-35) with its operands and twiddle tw[hq - 1 + k] (the w sequence for
+// len = 2hq); only the number of shared-memory round trips changes.
+template <int Q>
+__device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
+                                         const double2* __restrict__ tw) {
+    constexpr int G = 1 << Q;
+    const int h = 1 << s;
+    const int ng = (n >> Q) << lc;
+    for (int j = threadIdx.x; j < ng; j += blockDim.x) {
+        const int c = j & ((1 << lc) - 1), b = j >> lc;
+        const int k = b & (h - 1);
+        const int i = ((b >> s) << (s + Q)) + k;
+        double2 e[G];
+#pragma unroll
+        for (int m = 0; m < G; ++m) e[m] = a[(pd(i + m * h) << lc) | c];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int hq = h << q;
+#pragma unroll
+            for (int m = 0; m < G; ++m) {
+                if (m & (1 << q)) continue;
+                const int kq = k + (m & ((1 << q) - 1)) * h;
+                bfly(e[m], e[m | (1 << q)], __ldg(tw + hq - 1 + kq));
+            }
         }
-        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < G; ++m) a[(pd(i + m * h) << lc) | c] = e[m];
     }
-    if (s < log2n) {  // odd log2n: one trailing radix-2 stage
-        const int h = 1 << s;
-        const int nb = (n >> 1) * ncol;
-        for (int j = threadIdx.x; j < nb; j += blockDim.x) {
-            const int c = j % ncol;
-            const int b = j / ncol;
-            const int k = b & (h - 1);
-            const int i1 = ((b >> s) << (s + 1)) + k;
-            double2 u = a[i1 * ncol + c], v = a[(i1 + h) * ncol + c];
-            bfly(u, v, tw[h - 1 + k]);
-            a[i1 * ncol + c] = u;
-            a[(i1 + h) * ncol + c] = v;
-        }
-        __syncthreads();
+    __syncthreads();
+}
+
+// All log2n stages, QM per pass; input already bit-reversed.
+template <int QM>
+__device__ __forceinline__ void fft_stages(double2* a, int n, int log2n, int lc,
+                                           const double2* __restrict__ tw) {
+    int s = 0;
+    for (; s + QM <= log2n; s += QM) fft_pass<QM>(a, n, s, lc, tw);
+    switch (log2n - s) {
+        case 3: fft_pass<3>(a, n, s, lc, tw); break;
+        case 2: fft_pass<2>(a, n, s, lc, tw); break;
+        case 1: fft_pass<1>(a, n, s, lc, tw); break;
+        default: break;
     }
 }
+#ifndef FFT_Q_ROWS
+#define FFT_Q_ROWS 4
+#endif
+#ifndef FFT_Q_COLS
+#define FFT_Q_COLS 4
+#endif
+#ifndef FFT_Q_XPOW
+#define FFT_Q_XPOW 3
+#endif
+// stages per shared-memory pass: radix-16 for the plain transforms; radix-8 (~70 registers,
+// 3 CTAs per SM) where the cross-power prologue needs the occupancy
+constexpr int kQRows = FFT_Q_ROWS, kQCols = FFT_Q_COLS, kQXpow = FFT_Q_XPOW;
+
+// Rows per CTA for the row transforms: 256 threads, one radix-16 group per thread.
+__host__ __device__ constexpr int rows_lc(int log2n) { return log2n >= 12 ? 0 : (log2n >= 8 ? 12 - log2n : 4); }
 
 template <typename T>
 __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int ph, int log2pw,
@@ -92,43 +114,44 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
                                                      double2* __restrict__ spec) {
     extern __shared__ double2 sm[];
     double2* a = sm;
-    double2* tws = sm + pw;
-    const int y = blockIdx.x, slot = blockIdx.y;
+    const int lc = rows_lc(log2pw), R = 1 << lc;
+    const int y0 = blockIdx.x * R, slot = blockIdx.y;
     const T* f = den + (size_t)slot * W * H;
     // windowed_spectrum_input (registration.hpp:26-42): exact integer sum, then one division
     const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
-    const int sy = min(y, H - 1);
-    const double wyv = wy[y];
-    for (int x = threadIdx.x; x < pw; x += NT) {
-        const int sx = min(x, W - 1);
-        const double v = dmul(dmul(dsub((double)f[(size_t)sy * W + sx], mean), wx[x]), wyv);
-        a[brev(x, log2pw)] = make_double2(v, 0.0);
+    for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
+        const int r = e & (R - 1), x = e >> lc;
+        const int y = y0 + r;
+        if (y >= ph) continue;
+        const int sy = min(y, H - 1), sx = min(x, W - 1);
+        const double v = dmul(dmul(dsub((double)f[(size_t)sy * W + sx], mean), wx[x]), wy[y]);
+        a[(pd(brev(x, log2pw)) << lc) | r] = make_double2(v, 0.0);
     }
-    for (int i = threadIdx.x; i < pw - 1; i += NT) tws[i] = tw[i];
     __syncthreads();
-    fft_stages(a, pw, log2pw, 1, tws);
-    double2* out = spec + ((size_t)slot * ph + y) * pw;
-    for (int x = threadIdx.x; x < pw; x += NT) out[x] = a[x];
+    fft_stages<kQRows>(a, pw, log2pw, lc, tw);
+    for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
+        const int r = e & (R - 1), x = e >> lc;
+        if (y0 + r < ph) spec[((size_t)slot * ph + y0 + r) * pw + x] = a[(pd(x) << lc) | r];
+    }
 }
 
-__global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int cb,
+__global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int lcb,
                                                  const double2* __restrict__ tw,
                                                  double2* __restrict__ spec) {
     extern __shared__ double2 sm[];
     double2* a = sm;
-    double2* tws = sm + (size_t)ph * cb;
+    const int cb = 1 << lcb;
     const int slot = blockIdx.y, c0 = blockIdx.x * cb;
     double2* base = spec + (size_t)slot * ph * pw + c0;
-    for (int i = threadIdx.x; i < ph * cb; i += NT) {
-        const int r = i / cb, c = i - r * cb;
-        a[brev(r, log2ph) * cb + c] = base[(size_t)r * pw + c];
+    for (int i = threadIdx.x; i < (ph << lcb); i += NT) {
+        const int r = i >> lcb, c = i & (cb - 1);
+        a[(pd(brev(r, log2ph)) << lcb) | c] = base[(size_t)r * pw + c];
     }
-    for (int i = threadIdx.x; i < ph - 1; i += NT) tws[i] = tw[i];
     __syncthreads();
-    fft_stages(a, ph, log2ph, cb, tws);
-    for (int i = threadIdx.x; i < ph * cb; i += NT) {
-        const int r = i / cb, c = i - r * cb;
-        base[(size_t)r * pw + c] = a[r * cb + c];
+    fft_stages<kQCols>(a, ph, log2ph, lcb, tw);
+    for (int i = threadIdx.x; i < (ph << lcb); i += NT) {
+        const int r = i >> lcb, c = i & (cb - 1);
+        base[(size_t)r * pw + c] = a[(pd(r) << lcb) | c];
     }
 }
 
@@ -140,30 +163,35 @@ __global__ void __launch_bounds__(NT) k_xpow_rows_inv(int pw, int ph, int log2pw
                                                       double2* __restrict__ cols) {
     extern __shared__ double2 sm[];
     double2* a = sm;
-    double2* tws = sm + pw;
-    const int y = blockIdx.x, p = blockIdx.y;
-    const double2* fa = spec + ((size_t)prev[p] * ph + y) * pw;
-    const double2* fb = spec + ((size_t)next[p] * ph + y) * pw;
-    for (int x = threadIdx.x; x < pw; x += NT) {
-        const double2 A = fa[x], B = fb[x];
+    const int lc = rows_lc(log2pw), R = 1 << lc;
+    const int y0 = blockIdx.x * R, p = blockIdx.y;
+    const double2* fa = spec + (size_t)prev[p] * ph * pw;
+    const double2* fb = spec + (size_t)next[p] * ph * pw;
+    for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
+        const int r = e & (R - 1), x = e >> lc;
+        const int y = y0 + r;
+        if (y >= ph) continue;
+        const double2 A = fa[(size_t)y * pw + x], B = fb[(size_t)y * pw + x];
         // c = conj(A) * B (registration.hpp:61-65); |c| = std::abs -> glibc hypot
         const double nai = -A.y;
         const double re = dsub(dmul(A.x, B.x), dmul(nai, B.y));
         const double im = dadd(dmul(A.x, B.y), dmul(nai, B.x));
         const double m = hypot_glibc(re, im);
-        double2 r = make_double2(0.0, 0.0);
-        if (m > 1e-12) r = make_double2(ddiv(re, m), ddiv(im, m));
-        a[brev(x, log2pw)] = r;
+        double2 rr = make_double2(0.0, 0.0);
+        if (m > 1e-12) rr = make_double2(ddiv(re, m), ddiv(im, m));
+        a[(pd(brev(x, log2pw)) << lc) | r] = rr;
     }
-    for (int i = threadIdx.x; i < pw - 1; i += NT) tws[i] = itw[i];
     __syncthreads();
-    fft_stages(a, pw, log2pw, 1, tws);
+    fft_stages<kQXpow>(a, pw, log2pw, lc, itw);
     const double inv = ddiv(1.0, (double)pw);
     const int nc = 2 * M + 1;
-    for (int ci = threadIdx.x; ci < nc; ci += NT) {
+    for (int e = threadIdx.x; e < nc * R; e += NT) {
+        const int r = e % R, ci = e / R;
+        const int y = y0 + r;
+        if (y >= ph) continue;
         const int dx = ci - M;
         const int x = dx < 0 ? dx + pw : dx;
-        const double2 v = a[x];
+        const double2 v = a[(pd(x) << lc) | r];
         cols[((size_t)p * nc + ci) * ph + y] = make_double2(dmul(v.x, inv), dmul(v.y, inv));
     }
 }
@@ -174,19 +202,17 @@ __global__ void __launch_bounds__(NT) k_inv_cols(int ph, int log2ph, int M,
                                                  double* __restrict__ surf) {
     extern __shared__ double2 sm[];
     double2* a = sm;
-    double2* tws = sm + ph;
     const int ci = blockIdx.x, p = blockIdx.y;
     const int nc = 2 * M + 1;
     const double2* src = cols + ((size_t)p * nc + ci) * ph;
-    for (int y = threadIdx.x; y < ph; y += NT) a[brev(y, log2ph)] = src[y];
-    for (int i = threadIdx.x; i < ph - 1; i += NT) tws[i] = itw[i];
+    for (int y = threadIdx.x; y < ph; y += NT) a[pd(brev(y, log2ph))] = src[y];
     __syncthreads();
-    fft_stages(a, ph, log2ph, 1, tws);
+    fft_stages<3>(a, ph, log2ph, 0, itw);
     const double inv = ddiv(1.0, (double)ph);
     for (int r = threadIdx.x; r < nc; r += NT) {
         const int dy = r - M;
         const int y = dy < 0 ? dy + ph : dy;
-        surf[(size_t)p * nc * nc + (size_t)r * nc + ci] = dmul(a[y].x, inv);
+        surf[(size_t)p * nc * nc + (size_t)r * nc + ci] = dmul(a[pd(y)].x, inv);
     }
 }
 
@@ -264,11 +290,13 @@ void set_smem(K kernel, size_t bytes) {
         FROI_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
 }
 
-int column_block(const Geom& g) {
-    int cb = 4096 / g.ph;  // 64 KB of column data per CTA
-    if (cb < 1) cb = 1;
-    if (cb > g.pw) cb = g.pw;
-    return cb;
+// log2 of the columns per CTA: 4 for 1024-row spectra (~70 KB of padded column data)
+int column_lcb(const Geom& g) {
+    int lcb = 12 - g.log2ph;
+    if (lcb < 0) lcb = 0;
+    if (lcb > 4) lcb = 4;
+    while (lcb > 0 && (1 << lcb) > g.pw) --lcb;
+    return lcb;
 }
 
 }  // namespace
@@ -277,21 +305,23 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
                         const double* d_wx, const double* d_wy, const double2* d_tw_row,
                         const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s) {
     if (n_slots <= 0) return;
-    const size_t smem_r = sizeof(double2) * (2 * (size_t)g.pw);
+    const int lr = rows_lc(g.log2pw);
+    const size_t smem_r = sizeof(double2) * ((size_t)padded(g.pw) << lr);
+    const int row_blocks = cdiv(g.ph, 1 << lr);
     if (g.sample_bytes == 1) {
         set_smem(k_fft_rows_fwd<uint8_t>, smem_r);
-        k_fft_rows_fwd<uint8_t><<<dim3(g.ph, n_slots), NT, smem_r, s>>>(
+        k_fft_rows_fwd<uint8_t><<<dim3(row_blocks, n_slots), NT, smem_r, s>>>(
             g.W, g.H, g.pw, g.ph, g.log2pw, (const uint8_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
     } else {
         set_smem(k_fft_rows_fwd<uint16_t>, smem_r);
-        k_fft_rows_fwd<uint16_t><<<dim3(g.ph, n_slots), NT, smem_r, s>>>(
+        k_fft_rows_fwd<uint16_t><<<dim3(row_blocks, n_slots), NT, smem_r, s>>>(
             g.W, g.H, g.pw, g.ph, g.log2pw, (const uint16_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
     }
     FROI_LAUNCH_CHECK();
-    const int cb = column_block(g);
-    const size_t smem_c = sizeof(double2) * ((size_t)g.ph * cb + g.ph);
+    const int lcb = column_lcb(g);
+    const size_t smem_c = sizeof(double2) * ((size_t)padded(g.ph) << lcb);
     set_smem(k_fft_cols, smem_c);
-    k_fft_cols<<<dim3(g.pw / cb, n_slots), NT, smem_c, s>>>(g.pw, g.ph, g.log2ph, cb, d_tw_col, d_spec);
+    k_fft_cols<<<dim3(g.pw >> lcb, n_slots), NT, smem_c, s>>>(g.pw, g.ph, g.log2ph, lcb, d_tw_col, d_spec);
     FROI_LAUNCH_CHECK();
 }
 
@@ -301,12 +331,13 @@ void launch_register_pairs(const Geom& g, const DevParams& p, const double2* d_s
                            PairInfo* d_info, int n_pairs, cudaStream_t s) {
     if (n_pairs <= 0) return;
     const int M = p.max_shift;
-    const size_t smem_r = sizeof(double2) * (2 * (size_t)g.pw);
+    const int lr = rows_lc(g.log2pw);
+    const size_t smem_r = sizeof(double2) * ((size_t)padded(g.pw) << lr);
     set_smem(k_xpow_rows_inv, smem_r);
-    k_xpow_rows_inv<<<dim3(g.ph, n_pairs), NT, smem_r, s>>>(g.pw, g.ph, g.log2pw, M, d_spec, d_prev,
-                                                            d_next, d_itw_row, d_cols);
+    k_xpow_rows_inv<<<dim3(cdiv(g.ph, 1 << lr), n_pairs), NT, smem_r, s>>>(g.pw, g.ph, g.log2pw, M, d_spec,
+                                                                         d_prev, d_next, d_itw_row, d_cols);
     FROI_LAUNCH_CHECK();
-    const size_t smem_c = sizeof(double2) * (2 * (size_t)g.ph);
+    const size_t smem_c = sizeof(double2) * (size_t)padded(g.ph);
     set_smem(k_inv_cols, smem_c);
     k_inv_cols<<<dim3(2 * M + 1, n_pairs), NT, smem_c, s>>>(g.ph, g.log2ph, M, d_cols, d_itw_col, d_surf);
     FROI_LAUNCH_CHECK();
