@@ -430,7 +430,33 @@ __device__ __forceinline__ GTerms g_terms(const GLoad& o, float du, float dv) {
     return t;
 }
 
-// One CTA per FX x FY output tile of one pair (FNT threads, 2 CTAs per SM).
+// One CTA per strip of `nr` vertically stacked FX x FY output tiles of one pair (FNT threads,
+// 2 CTAs per SM).  The products G live in a ring of RG rows per plane: each tile computes only
+// the FY rows its window adds (the first tile also the 2R rows above), the 2R overlap rows stay
+// resident, so the halo overhead is (FX+2R)/FX x (FY*nr+2R)/(FY*nr) instead of
+// (FX+2R)/FX x (FY+2R)/FY.  Ring slots: row r of the strip (relative to its first halo row) sits
+// in slot r % RG; tile k's box sums overwrite slots of rows [FY*k, FY*k+FY), which no later tile
+// reads.  RG = 48 >= FY + 2R keeps the footprint at ~76 KB, leaving the L1 room the gathers need.
+constexpr int RG = 48;
+
+// vertical (2R+1)-row running sums down one ring column (FY outputs, rows from slot BOFF on),
+// written in place one step behind: a thread owns its column, and output j-1 overwrites row j-1
+// only after row j-1 was subtracted for output j
+template <int R, int BOFF, int SW>
+__device__ __forceinline__ void vsum_inplace(float* col) {
+    float acc = 0.f;
+#pragma unroll
+    for (int j = 0; j <= 2 * R; ++j) acc += col[((BOFF + j) % RG) * SW];
+    float pv = acc;
+#pragma unroll
+    for (int j = 1; j < FY; ++j) {
+        acc += col[((BOFF + j + 2 * R) % RG) * SW] - col[((BOFF + j - 1) % RG) * SW];
+        col[((BOFF + j - 1) % RG) * SW] = pv;
+        pv = acc;
+    }
+    col[((BOFF + FY - 1) % RG) * SW] = pv;
+}
+
 template <int R>
 __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const float4* __restrict__ exA_f,
@@ -439,15 +465,16 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const float* __restrict__ exB_p,
                                                       const int* __restrict__ prev,
                                                       const int* __restrict__ next,
-                                                      const PairInfo* __restrict__ info) {
+                                                      const PairInfo* __restrict__ info, int nr) {
     extern __shared__ float smem_f[];
-    // smem rows are SW = HW + 1 floats apart (odd stride: the row-wise box pass is conflict-free)
-    constexpr int HW = FX + 2 * R, HH = FY + 2 * R, SW = HW + 1, PL = SW * HH, NPX = HW * HH;
+    // ring rows are SW = HW + 1 floats apart (odd stride: the row-wise box pass is conflict-free)
+    constexpr int HW = FX + 2 * R, SW = HW + 1, PL = SW * RG;
+    static_assert(FY + 2 * R <= RG && FY == 32 && RG == 48, "ring layout");
     const int p = blockIdx.z;
     const int l = a.l;
     const int w = g.lw[l], h = g.lh[l];
-    const int x0 = blockIdx.x * FX, y0 = blockIdx.y * FY;
-    float* G = smem_f;  // 5 planes [HH][SW]; reused in place for the box sums
+    const int x0 = blockIdx.x * FX, ys = blockIdx.y * FY * nr;
+    float* G = smem_f;  // 5 planes [RG][SW]
     const size_t pair_off = (size_t)p * g.lsum;
     const size_t lo = g.loff[l];
     const float4* pA = exA_f + (size_t)prev[p] * g.lsum + lo;
@@ -455,150 +482,151 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     const bool sh = info[p].shifted != 0;
     const float4* nA = (sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo;
     const float* nB = (sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo;
-
-    // phase 1: normal-equation products over tile + halo; two independent pixels per step so
-    // each thread keeps ~20 gathers in flight
     const float2* fin = a.flow_in + pair_off + lo;
-    for (int i0 = threadIdx.x; i0 < NPX; i0 += 2 * FNT) {
-        // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
-        int gx[2], gy[2];
-        bool ok[2];
-        float2 pr[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int i = min(i0 + k * FNT, NPX - 1);
-            const int hy = i / HW, hx = i - hy * HW;
-            const int ux = x0 - R + hx, uy = y0 - R + hy;
-            ok[k] = i0 + k * FNT < NPX && ux >= 0 && ux < w && uy >= 0 && uy < h;
-            gx[k] = clampi(ux, 0, w - 1);
-            gy[k] = clampi(uy, 0, h - 1);
-        }
-        // one asm statement issues both prior loads before either pixel's dependent index math
-        pr[0] = pr[1] = make_float2(0.f, 0.f);
-        if (a.mode)
-            asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
-                         : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
-                         : "l"(fin + gy[0] * w + gx[0]), "l"(fin + gy[1] * w + gx[1]));
-        GLoad ld[2];
-#pragma unroll
-        for (int k = 0; k < 2; ++k) g_load(ld[k], pA, pB, nA, nB, w, h, gx[k], gy[k], pr[k].x, pr[k].y);
-#pragma unroll
-        for (int k = 0; k < 2; ++k) {
-            const int i = i0 + k * FNT;
-            GTerms t = g_terms(ld[k], pr[k].x, pr[k].y);
-            if (!ok[k]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
-            if (i < NPX) {
-                const int si = i + i / HW;  // hy * SW + hx
-                G[si] = t.g11;
-                G[PL + si] = t.g12;
-                G[2 * PL + si] = t.g22;
-                G[3 * PL + si] = t.h1;
-                G[4 * PL + si] = t.h2;
-            }
-        }
-    }
-    __syncthreads();
-    // phase 2: vertical (2R+1)-row running sums down each of the 5*HW columns (FY outputs each),
-    // held in registers and written back in place after every column has been read
-    float acc_r[FY];
-    const int vt = threadIdx.x;
-    const bool vact = vt < 5 * HW;
-    if (vact) {
-        const int c = vt / HW, hx = vt - c * HW;
-        const float* col = G + c * PL + hx;
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 0; j <= 2 * R; ++j) acc += col[j * SW];
-        acc_r[0] = acc;
-#pragma unroll
-        for (int j = 1; j < FY; ++j) {
-            acc += col[(j + 2 * R) * SW] - col[(j - 1) * SW];
-            acc_r[j] = acc;
-        }
-    }
-    __syncthreads();
-    if (vact) {
-        const int c = vt / HW, hx = vt - c * HW;
-        float* col = G + c * PL + hx;
-#pragma unroll
-        for (int j = 0; j < FY; ++j) col[j * SW] = acc_r[j];
-    }
-    __syncthreads();
-    // phase 3: horizontal running sums along each of the 5*FY rows, in 32-wide segments
-    constexpr int NSEG = FX / 32;
-    const bool hact = threadIdx.x < 5 * FY * NSEG;
-    if (hact) {
-        const int c = threadIdx.x / (FY * NSEG);
-        const int rem = threadIdx.x - c * FY * NSEG;
-        const int sg = rem / FY, ty = rem - sg * FY;  // a warp walks 32 rows of one segment
-        const float* row = G + c * PL + ty * SW + sg * 32;
-        float acc = 0.f;
-#pragma unroll
-        for (int j = 0; j <= 2 * R; ++j) acc += row[j];
-        acc_r[0] = acc;
-#pragma unroll
-        for (int j = 1; j < 32; ++j) {
-            acc += row[j + 2 * R] - row[j - 1];
-            acc_r[j] = acc;
-        }
-    }
-    __syncthreads();
-    if (hact) {
-        const int c = threadIdx.x / (FY * NSEG);
-        const int rem = threadIdx.x - c * FY * NSEG;
-        const int sg = rem / FY, ty = rem - sg * FY;
-        float* row = G + c * PL + ty * SW + sg * 32;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) row[j] = acc_r[j];
-    }
-    __syncthreads();
-    // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
-    // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
+    float2* out = a.flow_out + pair_off + lo;
     __shared__ float rcx[FX], rcy[FY];
     if (threadIdx.x < FX) {
         const int x = x0 + threadIdx.x;
         rcx[threadIdx.x] = __frcp_rn((float)(min(w - 1, x + R) - max(0, x - R) + 1));
-    } else if (threadIdx.x < FX + FY) {
-        const int y = y0 + threadIdx.x - FX;
-        rcy[threadIdx.x - FX] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
     }
-    __syncthreads();
-    float2* out = a.flow_out + pair_off + lo;
-    const int tx = threadIdx.x % FX;
-    for (int ty = threadIdx.x / FX; ty < FY; ty += FNT / FX) {
-        const int x = x0 + tx, y = y0 + ty;
-        if (x >= w || y >= h) continue;
-        const float inv = rcx[tx] * rcy[ty];
-        const int si = ty * SW + tx;
-        const float g11 = G[si] * inv, g12 = G[PL + si] * inv, g22 = G[2 * PL + si] * inv;
-        const float h1 = G[3 * PL + si] * inv, h2 = G[4 * PL + si] * inv;
-        const float q = g12 * g12;
-        const float qe = fmaf(g12, g12, -q);
-        const float det = fmaf(g11, g22, -q) - qe;
-        const float frob2 = fmaf(g11, g11, fmaf(2.f * g12, g12, g22 * g22));
-        float2 r;
-        if (!(det > 1e-9f * frob2)) {
-            r = prior_at(g, a, pair_off, x, y);
-        } else {
-            const float rd = __fdividef(1.f, det);
-            r.x = (g22 * h1 - g12 * h2) * rd;
-            r.y = (g11 * h2 - g12 * h1) * rd;
+    for (int k = 0; k < nr; ++k) {
+        const int y0 = ys + k * FY;
+        if (y0 >= h) break;
+        // phase 1: normal-equation products of the rows this tile adds; two independent pixels
+        // per step so each thread keeps ~20 gathers in flight
+        const int r0 = k == 0 ? 0 : FY * k + 2 * R;
+        const int npx = (k == 0 ? FY + 2 * R : FY) * HW;
+        for (int i0 = threadIdx.x; i0 < npx; i0 += 2 * FNT) {
+            // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
+            int gx[2], gy[2], si[2];
+            bool ok[2];
+            float2 pr[2];
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                const int i = min(i0 + kk * FNT, npx - 1);
+                const int hy = i / HW, hx = i - hy * HW;
+                const int ux = x0 - R + hx, uy = ys - R + r0 + hy;
+                ok[kk] = i0 + kk * FNT < npx && ux >= 0 && ux < w && uy >= 0 && uy < h;
+                gx[kk] = clampi(ux, 0, w - 1);
+                gy[kk] = clampi(uy, 0, h - 1);
+                si[kk] = ((r0 + hy) % RG) * SW + hx;
+            }
+            // one asm statement issues both prior loads before either pixel's dependent index math
+            pr[0] = pr[1] = make_float2(0.f, 0.f);
+            if (a.mode)
+                asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
+                             : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
+                             : "l"(fin + gy[0] * w + gx[0]), "l"(fin + gy[1] * w + gx[1]));
+            GLoad ld[2];
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) g_load(ld[kk], pA, pB, nA, nB, w, h, gx[kk], gy[kk], pr[kk].x, pr[kk].y);
+#pragma unroll
+            for (int kk = 0; kk < 2; ++kk) {
+                GTerms t = g_terms(ld[kk], pr[kk].x, pr[kk].y);
+                if (!ok[kk]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+                if (i0 + kk * FNT < npx) {
+                    G[si[kk]] = t.g11;
+                    G[PL + si[kk]] = t.g12;
+                    G[2 * PL + si[kk]] = t.g22;
+                    G[3 * PL + si[kk]] = t.h1;
+                    G[4 * PL + si[kk]] = t.h2;
+                }
+            }
         }
-        out[y * w + x] = r;
+        if (threadIdx.x < FY) {
+            const int y = y0 + threadIdx.x;
+            rcy[threadIdx.x] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
+        }
+        __syncthreads();
+        // phase 2: vertical running sums down each of the 5*HW ring columns (FY outputs each),
+        // in place over this tile's first FY ring rows
+        const int b0 = (FY * k) % RG;  // 0, 32 or 16
+        if (threadIdx.x < 5 * HW) {
+            const int vc = threadIdx.x / HW, vx = threadIdx.x - vc * HW;
+            float* col = G + vc * PL + vx;
+            if (b0 == 0) vsum_inplace<R, 0, SW>(col);
+            else if (b0 == 32) vsum_inplace<R, 32, SW>(col);
+            else vsum_inplace<R, 16, SW>(col);
+        }
+        __syncthreads();
+        // phase 3: horizontal running sums along each of the 5*FY rows in 32-wide segments, in
+        // place one step behind; a segment first takes the 2R inputs it shares with the next
+        // segment into registers, so after one barrier every thread owns what it overwrites
+        constexpr int NSEG = FX / 32;
+        const bool hact = threadIdx.x < 5 * FY * NSEG;
+        const int hc = threadIdx.x / (FY * NSEG);
+        const int hrem = threadIdx.x - hc * FY * NSEG;
+        const int hsg = hrem / FY, hty = hrem - hsg * FY;  // a warp walks 32 rows of one segment
+        float* hrow = G + hc * PL + ((b0 + hty) % RG) * SW + hsg * 32;
+        float tail[2 * R];
+        if (hact) {
+#pragma unroll
+            for (int j = 0; j < 2 * R; ++j) tail[j] = hrow[32 + j];
+        }
+        __syncthreads();
+        if (hact) {
+            float acc = 0.f;
+#pragma unroll
+            for (int j = 0; j <= 2 * R; ++j) acc += hrow[j];
+            float pv = acc;
+#pragma unroll
+            for (int j = 1; j < 32; ++j) {
+                const float in = j + 2 * R < 32 ? hrow[j + 2 * R] : tail[j + 2 * R - 32];
+                acc += in - hrow[j - 1];
+                hrow[j - 1] = pv;
+                pv = acc;
+            }
+            hrow[31] = pv;
+        }
+        __syncthreads();
+        // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
+        // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
+        const int tx = threadIdx.x % FX;
+        for (int ty = threadIdx.x / FX; ty < FY; ty += FNT / FX) {
+            const int x = x0 + tx, y = y0 + ty;
+            if (x >= w || y >= h) continue;
+            const float inv = rcx[tx] * rcy[ty];
+            const int sidx = ((b0 + ty) % RG) * SW + tx;
+            const float g11 = G[sidx] * inv, g12 = G[PL + sidx] * inv, g22 = G[2 * PL + sidx] * inv;
+            const float h1 = G[3 * PL + sidx] * inv, h2 = G[4 * PL + sidx] * inv;
+            const float q = g12 * g12;
+            const float qe = fmaf(g12, g12, -q);
+            const float det = fmaf(g11, g22, -q) - qe;
+            const float frob2 = fmaf(g11, g11, fmaf(2.f * g12, g12, g22 * g22));
+            float2 r;
+            if (!(det > 1e-9f * frob2)) {
+                r = prior_at(g, a, pair_off, x, y);
+            } else {
+                const float rd = __fdividef(1.f, det);
+                r.x = (g22 * h1 - g12 * h2) * rd;
+                r.y = (g11 * h2 - g12 * h1) * rd;
+            }
+            out[y * w + x] = r;
+        }
+        __syncthreads();  // ring rows and rcy are rewritten by the next tile
     }
+}
+
+// tiles per strip: as tall as possible while the grid still fills ~4 CTAs per SM
+int strip_tiles(const Geom& g, int l, int n_pairs) {
+    const int tx = cdiv(g.lw[l], FX), ty = cdiv(g.lh[l], FY);
+    int nr = 4;
+    while (nr > 1 && (long long)tx * cdiv(ty, nr) * n_pairs < 4 * 148) nr >>= 1;
+    return nr;
 }
 
 template <int R>
 void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                  const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * (FY + 2 * R);
+    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * RG;
     static bool attr = false;
     if (!attr) {
         FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY), n_pairs);
-    k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info);
+    const int nr = strip_tiles(g, a.l, n_pairs);
+    dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY * nr), n_pairs);
+    k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info, nr);
     FROI_LAUNCH_CHECK();
 }
 
