@@ -27,13 +27,26 @@ template <typename T>
 struct FrameSrc {  // normalize_frame(apply_shift(den, s)) at level 0
     const T* f;
     int W, H, dx, dy;
-    double inv;  // 1.0 / maxval
+    double inv;        // 1.0 / maxval
+    const float* lut;  // 8-bit frames: the 256 values (float)(v * inv) in shared memory
     __device__ __forceinline__ float at(int x, int y) const {
         const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
         const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
-        return (float)((double)f[(size_t)sy * W + sx] * inv);
+        const int v = f[sy * W + sx];
+        return sizeof(T) == 1 ? lut[v] : (float)((double)v * inv);
     }
 };
+
+// shared-memory table of normalize_frame's (float)(v / maxval) for 8-bit frames; callers
+// synchronise before the first use (the tile loaders below start with a barrier-free fill, then
+// every path reaches a __syncthreads() before reading the input tile)
+template <typename T>
+__device__ __forceinline__ const float* frame_lut(float* lut, double inv) {
+    if (sizeof(T) != 1) return nullptr;
+    for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = (float)((double)v * inv);
+    __syncthreads();
+    return lut;
+}
 
 struct ImageSrc {
     const float* f;
@@ -46,10 +59,12 @@ struct ImageSrc {
 // ------------------------------------------------------------------ polynomial expansion
 constexpr int PX = 32, PY = 16, PNT = 256;
 
-template <typename Src, bool kDebug>
-__device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r,
+// RC > 0: compile-time radius (unrolled taps, weights as constant-bank operands); 0: runtime.
+template <typename Src, bool kDebug, int RC = 0>
+__device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r_rt,
                                              const DevParams& P, float4* outA, float* outB,
                                              float* dbg_planes, float* smem) {
+    const int r = RC > 0 ? RC : r_rt;
     const int x0 = blockIdx.x * PX, y0 = blockIdx.y * PY;
     const int sw = PX + 2 * r, sh = PY + 2 * r;
     float* s_in = smem;               // sh * sw
@@ -67,6 +82,7 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
         const int yy = i / PX, xx = i - yy * PX;
         const float* row = s_in + yy * sw + xx;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
         for (int t = 0; t <= 2 * r; ++t) {
             const float v = row[t];
             a0 += P.g0[t] * v;
@@ -84,6 +100,7 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
         const int x = x0 + xx, y = y0 + yy;
         if (x >= w || y >= h) continue;
         float s1 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
+#pragma unroll
         for (int t = 0; t <= 2 * r; ++t) {
             const float r0 = s_r[(yy + t) * PX + xx];
             const float r1 = s_r[sh * PX + (yy + t) * PX + xx];
@@ -119,31 +136,36 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
 }
 
 // Frame slots: level-0 expansion from the denoised frame (unshifted).
-template <typename T>
+template <typename T, int RC>
 __global__ void __launch_bounds__(PNT) k_polyexp_frame(Geom g, DevParams P, const T* den,
                                                        float4* exA, float* exB) {
     extern __shared__ float smem_f[];
+    __shared__ float lut[256];
     const int slot = blockIdx.z;
-    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, 1.0 / g.maxval};
-    polyexp_tile<FrameSrc<T>, false>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)slot * g.lsum,
-                                     exB + (size_t)slot * g.lsum, nullptr, smem_f);
+    const double inv = 1.0 / g.maxval;
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, frame_lut<T>(lut, inv)};
+    polyexp_tile<FrameSrc<T>, false, RC>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)slot * g.lsum,
+                                         exB + (size_t)slot * g.lsum, nullptr, smem_f);
 }
 
 // Pair slots: level-0 expansion of apply_shift(den[t], s) when s != 0.
-template <typename T>
+template <typename T, int RC>
 __global__ void __launch_bounds__(PNT) k_polyexp_shifted(Geom g, DevParams P, const T* den,
                                                          const int* next, const PairInfo* info,
                                                          float4* exA, float* exB) {
     extern __shared__ float smem_f[];
+    __shared__ float lut[256];
     const int p = blockIdx.z;
     const PairInfo I = info[p];
     if (!I.shifted) return;
-    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, 1.0 / g.maxval};
-    polyexp_tile<FrameSrc<T>, false>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)p * g.lsum,
-                                     exB + (size_t)p * g.lsum, nullptr, smem_f);
+    const double inv = 1.0 / g.maxval;
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, frame_lut<T>(lut, inv)};
+    polyexp_tile<FrameSrc<T>, false, RC>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)p * g.lsum,
+                                         exB + (size_t)p * g.lsum, nullptr, smem_f);
 }
 
 // Levels >= 1 from a float pyramid image (frame slots if info == nullptr, else pair slots).
+template <int RC>
 __global__ void __launch_bounds__(PNT) k_polyexp_level(Geom g, DevParams P, int l,
                                                        const float* pyr, long long pyr_stride,
                                                        const PairInfo* info, float4* exA,
@@ -153,7 +175,7 @@ __global__ void __launch_bounds__(PNT) k_polyexp_level(Geom g, DevParams P, int 
     if (info && !info[z].shifted) return;
     const long long poff = g.loff[l] - g.loff[1];
     ImageSrc src{pyr + (size_t)z * pyr_stride + poff, g.lw[l], g.lh[l]};
-    polyexp_tile<ImageSrc, false>(src, g.lw[l], g.lh[l], P.poly_radius, P,
+    polyexp_tile<ImageSrc, false, RC>(src, g.lw[l], g.lh[l], P.poly_radius, P,
                                   exA + (size_t)z * g.lsum + g.loff[l],
                                   exB + (size_t)z * g.lsum + g.loff[l], nullptr, smem_f);
 }
@@ -195,6 +217,19 @@ __device__ __forceinline__ void pyr_tile(const Src& src, int w, int h, int tw, i
     float* s_in = smem;             // ih * iw
     float* s_rb = s_in + ih * iw;   // ih * RW
     float* s_bl = s_rb + ih * RW;   // RH * RW
+    // bilinear() taps of this tile's output columns and rows, computed once (same fp64 rule)
+    __shared__ int s_ix0[QX], s_ix1[QX], s_iy0[QY], s_iy1[QY];
+    __shared__ float s_fx[QX], s_fy[QY];
+    if (threadIdx.x < QX) {
+        double fd;
+        bl_index((ox0 + threadIdx.x + 0.5) * sx - 0.5, w, s_ix0[threadIdx.x], s_ix1[threadIdx.x], fd);
+        s_fx[threadIdx.x] = (float)fd;
+    } else if (threadIdx.x < QX + QY) {
+        const int t = threadIdx.x - QX;
+        double fd;
+        bl_index((oy0 + t + 0.5) * sy - 0.5, h, s_iy0[t], s_iy1[t], fd);
+        s_fy[t] = (float)fd;
+    }
     for (int i = threadIdx.x; i < ih * iw; i += QNT) {
         const int yy = i / iw, xx = i - yy * iw;
         s_in[i] = src.at(xa - 3 + xx, ya - 3 + yy);
@@ -219,13 +254,10 @@ __device__ __forceinline__ void pyr_tile(const Src& src, int w, int h, int tw, i
         const int yy = i / QX, xx = i - yy * QX;
         const int x = ox0 + xx, y = oy0 + yy;
         if (x >= tw || y >= th) continue;
-        int x0, x1, y0, y1;
-        double fx, fy;
-        bl_index((x + 0.5) * sx - 0.5, w, x0, x1, fx);
-        bl_index((y + 0.5) * sy - 0.5, h, y0, y1, fy);
+        const int x0 = s_ix0[xx], x1 = s_ix1[xx], y0 = s_iy0[yy], y1 = s_iy1[yy];
         const float* r0 = s_bl + (y0 - ya) * RW;
         const float* r1 = s_bl + (y1 - ya) * RW;
-        const float ffx = (float)fx, ffy = (float)fy;
+        const float ffx = s_fx[xx], ffy = s_fy[yy];
         const float top = r0[x0 - xa] * (1.f - ffx) + r0[x1 - xa] * ffx;
         const float bot = r1[x0 - xa] * (1.f - ffx) + r1[x1 - xa] * ffx;
         out[(size_t)y * tw + x] = top * (1.f - ffy) + bot * ffy;
@@ -237,7 +269,9 @@ __global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T
                                                     int rwmax, int rhmax) {
     extern __shared__ float smem_f[];
     const int slot = blockIdx.z;
-    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, 1.0 / g.maxval};
+    __shared__ float lut[256];
+    const double inv = 1.0 / g.maxval;
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, frame_lut<T>(lut, inv)};
     pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)slot * (g.lsum - g.loff[1]),
              smem_f, rwmax, rhmax);
 }
@@ -250,7 +284,9 @@ __global__ void __launch_bounds__(QNT) k_pyr0_shifted(Geom g, DevParams P, const
     const int p = blockIdx.z;
     const PairInfo I = info[p];
     if (!I.shifted) return;
-    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, 1.0 / g.maxval};
+    __shared__ float lut[256];
+    const double inv = 1.0 / g.maxval;
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, frame_lut<T>(lut, inv)};
     pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)p * (g.lsum - g.loff[1]),
              smem_f, rwmax, rhmax);
 }
@@ -649,6 +685,16 @@ size_t pyr_smem(int rwmax, int rhmax) {
 
 }  // namespace
 
+// the default poly_n = 5 (radius 2) runs fully unrolled; other radii take the runtime loops
+#define FROI_POLY_RC(P, ...)            \
+    if ((P).poly_radius == 2) {         \
+        constexpr int RC = 2;           \
+        __VA_ARGS__;                    \
+    } else {                            \
+        constexpr int RC = 0;           \
+        __VA_ARGS__;                    \
+    }
+
 void launch_expand_frames(const Geom& g, const DevParams& P, const FlowBuffers& b, int n_slots,
                           cudaStream_t s) {
     if (n_slots <= 0) return;
@@ -657,11 +703,11 @@ void launch_expand_frames(const Geom& g, const DevParams& P, const FlowBuffers& 
     {
         dim3 grid(cdiv(g.W, PX), cdiv(g.H, PY), n_slots);
         if (g.sample_bytes == 1) {
-            set_smem(k_polyexp_frame<uint8_t>, pe);
-            k_polyexp_frame<uint8_t><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, b.exA_f, b.exB_f);
+            FROI_POLY_RC(P, set_smem(k_polyexp_frame<uint8_t, RC>, pe);
+                         k_polyexp_frame<uint8_t, RC><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, b.exA_f, b.exB_f))
         } else {
-            set_smem(k_polyexp_frame<uint16_t>, pe);
-            k_polyexp_frame<uint16_t><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, b.exA_f, b.exB_f);
+            FROI_POLY_RC(P, set_smem(k_polyexp_frame<uint16_t, RC>, pe);
+                         k_polyexp_frame<uint16_t, RC><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, b.exA_f, b.exB_f))
         }
         FROI_LAUNCH_CHECK();
     }
@@ -683,10 +729,10 @@ void launch_expand_frames(const Geom& g, const DevParams& P, const FlowBuffers& 
             k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_f, nullptr, rwmax, rhmax);
         }
         FROI_LAUNCH_CHECK();
-        set_smem(k_polyexp_level, pe);
         dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_slots);
-        k_polyexp_level<<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_f, g.lsum - g.loff[1], nullptr,
-                                            b.exA_f, b.exB_f);
+        FROI_POLY_RC(P, set_smem(k_polyexp_level<RC>, pe);
+                     k_polyexp_level<RC><<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_f, g.lsum - g.loff[1],
+                                                             nullptr, b.exA_f, b.exB_f))
         FROI_LAUNCH_CHECK();
     }
 }
@@ -698,11 +744,13 @@ void launch_expand_shifted(const Geom& g, const DevParams& P, const FlowBuffers&
     {
         dim3 grid(cdiv(g.W, PX), cdiv(g.H, PY), n_pairs);
         if (g.sample_bytes == 1) {
-            set_smem(k_polyexp_shifted<uint8_t>, pe);
-            k_polyexp_shifted<uint8_t><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, d_next, d_info, b.exA_p, b.exB_p);
+            FROI_POLY_RC(P, set_smem(k_polyexp_shifted<uint8_t, RC>, pe);
+                         k_polyexp_shifted<uint8_t, RC><<<grid, PNT, pe, s>>>(g, P, (const uint8_t*)b.den, d_next,
+                                                                              d_info, b.exA_p, b.exB_p))
         } else {
-            set_smem(k_polyexp_shifted<uint16_t>, pe);
-            k_polyexp_shifted<uint16_t><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, d_next, d_info, b.exA_p, b.exB_p);
+            FROI_POLY_RC(P, set_smem(k_polyexp_shifted<uint16_t, RC>, pe);
+                         k_polyexp_shifted<uint16_t, RC><<<grid, PNT, pe, s>>>(g, P, (const uint16_t*)b.den, d_next,
+                                                                               d_info, b.exA_p, b.exB_p))
         }
         FROI_LAUNCH_CHECK();
     }
@@ -724,10 +772,10 @@ void launch_expand_shifted(const Geom& g, const DevParams& P, const FlowBuffers&
             k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_p, d_info, rwmax, rhmax);
         }
         FROI_LAUNCH_CHECK();
-        set_smem(k_polyexp_level, pe);
         dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_pairs);
-        k_polyexp_level<<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_p, g.lsum - g.loff[1], d_info,
-                                            b.exA_p, b.exB_p);
+        FROI_POLY_RC(P, set_smem(k_polyexp_level<RC>, pe);
+                     k_polyexp_level<RC><<<eg, PNT, pe, s>>>(g, P, l + 1, b.pyr_p, g.lsum - g.loff[1],
+                                                             d_info, b.exA_p, b.exB_p))
         FROI_LAUNCH_CHECK();
     }
 }
