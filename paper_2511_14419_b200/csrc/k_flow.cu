@@ -397,6 +397,12 @@ struct GTerms {
     float g11, g12, g22, h1, h2;
 };
 
+template <typename P>
+__device__ __forceinline__ P* opaque(P* p) {
+    asm("mov.b64 %0, %0;" : "+l"(p));
+    return p;
+}
+
 // Gathered operands of one pixel's normal-equation products.
 struct GLoad {
     float4 q00, q01, q10, q11, pa;
@@ -411,11 +417,12 @@ __device__ __forceinline__ void g_load(GLoad& o, const float4* __restrict__ pA,
     int xa, ya;
     bl_split(gx, du, w, xa, o.fx);
     bl_split(gy, dv, h, ya, o.fy);
-    const int i0 = ya * w + xa;
+    // unsigned 32-bit element offsets: one wide multiply-add per address, no sign extension
+    const unsigned i0 = (unsigned)(ya * w + xa), i1 = i0 + (unsigned)w;
     const float4* r0 = nA + i0;
-    const float4* r1 = r0 + w;
+    const float4* r1 = nA + i1;
     const float* b0 = nB + i0;
-    const float* b1 = b0 + w;
+    const float* b1 = nB + i1;
     o.q00 = __ldg(r0);
     o.q01 = __ldg(r0 + 1);
     o.q10 = __ldg(r1);
@@ -424,7 +431,7 @@ __device__ __forceinline__ void g_load(GLoad& o, const float4* __restrict__ pA,
     o.b01 = __ldg(b0 + 1);
     o.b10 = __ldg(b1);
     o.b11 = __ldg(b1 + 1);
-    const int c = gy * w + gx;
+    const unsigned c = (unsigned)(gy * w + gx);
     o.pa = __ldg(pA + c);
     o.pb = __ldg(pB + c);
 }
@@ -513,13 +520,15 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     float* G = smem_f;  // 5 planes [RG][SW]
     const size_t pair_off = (size_t)p * g.lsum;
     const size_t lo = g.loff[l];
-    const float4* pA = exA_f + (size_t)prev[p] * g.lsum + lo;
-    const float* pB = exB_f + (size_t)prev[p] * g.lsum + lo;
+    // opaque() keeps each plane base a single 64-bit value, so a gather address is one wide
+    // multiply-add of its unsigned 32-bit element offset (no re-association with the level offset)
+    const float4* pA = opaque(exA_f + (size_t)prev[p] * g.lsum + lo);
+    const float* pB = opaque(exB_f + (size_t)prev[p] * g.lsum + lo);
     const bool sh = info[p].shifted != 0;
-    const float4* nA = (sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo;
-    const float* nB = (sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo;
-    const float2* fin = a.flow_in + pair_off + lo;
-    float2* out = a.flow_out + pair_off + lo;
+    const float4* nA = opaque((sh ? exA_p + pair_off : exA_f + (size_t)next[p] * g.lsum) + lo);
+    const float* nB = opaque((sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo);
+    const float2* fin = opaque(a.flow_in + pair_off + lo);
+    float2* out = opaque(a.flow_out + pair_off + lo);
     __shared__ float rcx[FX], rcy[FY];
     if (threadIdx.x < FX) {
         const int x = x0 + threadIdx.x;
@@ -552,7 +561,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             if (a.mode)
                 asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
                              : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
-                             : "l"(fin + gy[0] * w + gx[0]), "l"(fin + gy[1] * w + gx[1]));
+                             : "l"(fin + (unsigned)(gy[0] * w + gx[0])), "l"(fin + (unsigned)(gy[1] * w + gx[1])));
             GLoad ld[2];
 #pragma unroll
             for (int kk = 0; kk < 2; ++kk) g_load(ld[kk], pA, pB, nA, nB, w, h, gx[kk], gy[kk], pr[kk].x, pr[kk].y);
