@@ -397,12 +397,6 @@ struct GTerms {
     float g11, g12, g22, h1, h2;
 };
 
-template <typename P>
-__device__ __forceinline__ P* opaque(P* p) {
-    asm("mov.b64 %0, %0;" : "+l"(p));
-    return p;
-}
-
 // Gathered operands of one pixel's normal-equation products.
 struct GLoad {
     float4 q00, q01, q10, q11, pa;

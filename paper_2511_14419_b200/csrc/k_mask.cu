@@ -32,14 +32,14 @@ struct PairPix {
     const double* lut;  // shared-memory v/maxval table for 8-bit frames (nullptr: convert)
 
     __device__ __forceinline__ float fmag(int x, int y) const {
-        const float2 f = flow[(size_t)y * W + x];
+        const float2 f = flow[y * W + x];
         return hypotf_glibc(f.x, f.y);
     }
     // normalize_frame(apply_shift(raw, s)) at clamped coordinates
     __device__ __forceinline__ double img(int x, int y) const {
         const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
         const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
-        const int v = raw[(size_t)sy * W + sx];
+        const int v = raw[sy * W + sx];
         return lut ? lut[v] : dmul((double)v, inv_maxval);
     }
     // gradient_magnitude (roi.hpp:65-74)
@@ -66,7 +66,7 @@ template <typename T>
 __device__ __forceinline__ PairPix<T> make_pix(const Geom& g, const DevParams& P,
                                                const MaskBuffers& b, const PairInfo& I, int p) {
     PairPix<T> px;
-    px.flow = b.flow + (size_t)p * b.flow_stride;
+    px.flow = opaque(b.flow + (size_t)p * b.flow_stride);
     px.raw = (const T*)b.raw[p];
     px.W = g.W;
     px.H = g.H;
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     }
     __syncthreads();
     const int W = g.W, H = g.H;
-    float* fm = b.fm + (size_t)p * W * H;
-    double* gr = b.gr + (size_t)p * W * H;
+    float* fm = opaque(b.fm + (size_t)p * W * H);
+    double* gr = opaque(b.gr + (size_t)p * W * H);
     const int rows = (H + gridDim.x - 1) / gridDim.x;
     const int y0 = blockIdx.x * rows, y1 = min(H, y0 + rows);
     const int lane = threadIdx.x & 31;
@@ -461,7 +461,7 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
 
 __global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
     const int p = blockIdx.y;
-    SrcBufA src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H};
+    SrcBufA src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H)};
     sel_pass_body(g, b, p, src);
 }
 
@@ -471,7 +471,7 @@ __global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuf
         SrcMap src{map};
         sel_pass_body(g, b, p, src);
     } else {
-        SrcSal src{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H, b.info[p],
+        SrcSal src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H), b.info[p],
                    P.flow_weight, 1.0 - P.flow_weight};
         sel_pass_body(g, b, p, src);
     }
@@ -709,7 +709,7 @@ __device__ __forceinline__ Src make_thr_src(const Geom& g, const DevParams& P, c
 template <>
 __device__ __forceinline__ SrcSal make_thr_src<SrcSal>(const Geom& g, const DevParams& P,
                                                        const MaskBuffers& b, int p, const double*) {
-    return SrcSal{b.fm + (size_t)p * g.W * g.H, b.gr + (size_t)p * g.W * g.H, b.info[p],
+    return SrcSal{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H), b.info[p],
                   P.flow_weight, 1.0 - P.flow_weight};
 }
 template <>
