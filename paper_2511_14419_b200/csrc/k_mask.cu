@@ -40,7 +40,7 @@ struct PairPix {
         const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
         const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
         const int v = raw[sy * W + sx];
-        return lut ? lut[v] : dmul((double)v, inv_maxval);
+        return sizeof(T) == 1 ? lut[v] : dmul((double)v, inv_maxval);  // 8-bit: shared table (k_mag_grad)
     }
     // gradient_magnitude (roi.hpp:65-74)
     __device__ __forceinline__ double grad(int x, int y) const {
