@@ -404,27 +404,60 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     const int y0 = blockIdx.x * rows, y1 = min(H, y0 + rows);
     const int lane = threadIdx.x & 31;
     unsigned long long mnf = ~0ull, mxf = 0ull, mng = ~0ull, mxg = 0ull;
+    // NPX pixels per thread per step: all their loads (flow, the four gradient neighbours) are
+    // issued before any of their arithmetic, so each thread keeps ~NPX*5 loads in flight
+    constexpr int NPX = 4;
+    const float2* __restrict__ flw = px.flow;
+    const T* __restrict__ raw = px.raw;
     for (int y = y0; y < y1; ++y) {
         const int row = y * W;
-        for (int xb = 0; xb < W; xb += PNT_MG) {
-            const int x = xb + threadIdx.x;
-            const bool v = x < W;
-            unsigned long long kf = 0, kg = 0;
-            if (v) {
-                const float2 fl = px.flow[row + x];
-                const float f = hypotf_glibc(fl.x, fl.y);
-                const double gg = px.grad(x, y);
-                fm[row + x] = f;
-                gr[row + x] = gg;
-                kf = fkey(f);
-                kg = dkey(gg);
-                mnf = min(mnf, kf);
-                mxf = max(mxf, kf);
-                mng = min(mng, kg);
-                mxg = max(mxg, kg);
+        const int sy = clampi(y + px.dy, 0, H - 1);
+        const int sym = clampi(clampi(y - 1, 0, H - 1) + px.dy, 0, H - 1);
+        const int syp = clampi(clampi(y + 1, 0, H - 1) + px.dy, 0, H - 1);
+        for (int xb = 0; xb < W; xb += NPX * PNT_MG) {
+            float2 fl[NPX];
+            int vl[NPX], vr[NPX], vu[NPX], vd[NPX];
+#pragma unroll
+            for (int k = 0; k < NPX; ++k) {
+                const int x = min(xb + threadIdx.x + k * PNT_MG, W - 1);
+                fl[k] = __ldg(flw + row + x);
+                if (sizeof(T) == 1 && P.gradient_source == 0) {
+                    const int sx = clampi(x + px.dx, 0, W - 1);
+                    const int sxm = clampi(clampi(x - 1, 0, W - 1) + px.dx, 0, W - 1);
+                    const int sxp = clampi(clampi(x + 1, 0, W - 1) + px.dx, 0, W - 1);
+                    vl[k] = __ldg(raw + sy * W + sxm);
+                    vr[k] = __ldg(raw + sy * W + sxp);
+                    vu[k] = __ldg(raw + sym * W + sx);
+                    vd[k] = __ldg(raw + syp * W + sx);
+                }
             }
-            hist_add(hist[0], v, (unsigned int)fpw_bin(kf, 2), lane);
-            hist_add(hist[1], v, (unsigned int)fpw_bin(kg, 1), lane);
+#pragma unroll
+            for (int k = 0; k < NPX; ++k) {
+                const int x = xb + threadIdx.x + k * PNT_MG;
+                const bool v = x < W;
+                unsigned long long kf = 0, kg = 0;
+                if (v) {
+                    const float f = hypotf_glibc(fl[k].x, fl[k].y);
+                    double gg;
+                    if (sizeof(T) == 1 && P.gradient_source == 0) {
+                        const double gx = dmul(0.5, dsub(lut[vr[k]], lut[vl[k]]));
+                        const double gy = dmul(0.5, dsub(lut[vd[k]], lut[vu[k]]));
+                        gg = hypot_glibc(gx, gy);
+                    } else {
+                        gg = px.grad(x, y);
+                    }
+                    fm[row + x] = f;
+                    gr[row + x] = gg;
+                    kf = fkey(f);
+                    kg = dkey(gg);
+                    mnf = min(mnf, kf);
+                    mxf = max(mxf, kf);
+                    mng = min(mng, kg);
+                    mxg = max(mxg, kg);
+                }
+                hist_add(hist[0], v, (unsigned int)fpw_bin(kf, 2), lane);
+                hist_add(hist[1], v, (unsigned int)fpw_bin(kg, 1), lane);
+            }
         }
     }
     for (int o = 16; o > 0; o >>= 1) {
