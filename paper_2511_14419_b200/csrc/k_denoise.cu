@@ -174,7 +174,7 @@ constexpr int QX = 32, QY = 32, QNT = 256, QRPT = QY / (QNT / QX), QREP = 16;
 constexpr int QRW = QX + 6, QRH = QY + 6, QMW = QX + 4, QMH = QY + 4;
 
 size_t qsmem_bytes() {
-    return sizeof(double) * (511 * QREP + QMW * QMH) + sizeof(int) * (QRW * QRH + QMW * QMH);
+    return sizeof(double) * (511 * QREP) + sizeof(int) * (QRW * QRH + QMW * QMH);
 }
 
 __device__ __forceinline__ int med3i(int a, int b, int c) {
@@ -189,8 +189,7 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
     constexpr int R1 = 3;
     extern __shared__ __align__(16) unsigned char smem[];
     double* lut_s = (double*)smem;                  // [511][QREP], index d + 255
-    double* medd_s = lut_s + 511 * QREP;            // QMH * QMW medians as double
-    int* raw_s = (int*)(medd_s + QMW * QMH);        // QRH * QRW
+    int* raw_s = (int*)(lut_s + 511 * QREP);        // QRH * QRW
     int* med_s = raw_s + QRW * QRH;                 // QMH * QMW medians * (QREP * 8)
     const int tid = threadIdx.y * QX + threadIdx.x;
     for (int i = tid; i < 511 * QREP; i += QNT) lut_s[i] = lut_g[min(abs(i / QREP - 255), maxval)];
@@ -230,7 +229,7 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
         const int slot = t / per_slot, tr = t - slot * per_slot;
         const int by = tr / tiles_x, bx = tr - by * tiles_x;
         const int x0 = bx * QX, y0 = by * QY;
-        __syncthreads();  // previous tile's bilateral is done with med_s / medd_s
+        __syncthreads();  // previous tile's bilateral is done with med_s
 #pragma unroll
         for (int k = 0; k < NRAW; ++k)
             if (tid + k * QNT < QRW * QRH) raw_s[tid + k * QNT] = rv[k];
@@ -268,48 +267,53 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
                     prev = cy;
                 }
                 med_s[my * QMW + mx] = m * (QREP * 8);
-                medd_s[my * QMW + mx] = dsub(__hiloint2double(0x43300000, m), B52);
             }
         }
         __syncthreads();
         const int ty0 = grp * QRPT;
-        int mw[5][5];
-        double md[5][5];
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int dx = 0; dx < 5; ++dx) {
-                mw[j][dx] = med_s[(ty0 + j) * QMW + lane + dx];
-                md[j][dx] = medd_s[(ty0 + j) * QMW + lane + dx];
-            }
+        // Two output rows per pass, their four accumulation chains interleaved: window rows
+        // ty0+r .. ty0+r+5 are walked once; row r takes j = 0..4 and row r+1 takes j = 1..5, each
+        // in the reference's dy-major / dx-minor order, and each median is converted to double
+        // once for both (2^52 bias, one DADD).
         unsigned long long sum = 0;
+        const double dmax = (double)maxval;
 #pragma unroll
-        for (int r = 0; r < QRPT; ++r) {
-            const int ns = (r + 4) % 5;  // slot of the new bottom row
+        for (int r = 0; r < QRPT; r += 2) {
+            int mw[6][5];
 #pragma unroll
-            for (int dx = 0; dx < 5; ++dx) {
-                mw[ns][dx] = med_s[(ty0 + r + 4) * QMW + lane + dx];
-                md[ns][dx] = medd_s[(ty0 + r + 4) * QMW + lane + dx];
-            }
-            const char* lc = lut0 - mw[(r + 2) % 5][2];
-            double num = 0.0, dn = 0.0;
+            for (int j = 0; j < 6; ++j)
 #pragma unroll
-            for (int dy = 0; dy < 5; ++dy)
+                for (int dx = 0; dx < 5; ++dx) mw[j][dx] = med_s[(ty0 + r + j) * QMW + lane + dx];
+            const char* lc0 = lut0 - mw[2][2];
+            const char* lc1 = lut0 - mw[3][2];
+            double num0 = 0.0, dn0 = 0.0, num1 = 0.0, dn1 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 6; ++j)
 #pragma unroll
                 for (int dx = 0; dx < 5; ++dx) {
-                    const double lw = *(const double*)(lc + mw[(r + dy) % 5][dx]);
-                    const double wgt = dmul(sp_w.w[dy * 5 + dx], lw);
-                    num = dadd(num, dmul(wgt, md[(r + dy) % 5][dx]));
-                    dn = dadd(dn, wgt);
+                    const double v = dsub(__hiloint2double(0x43300000, (int)((unsigned)mw[j][dx] / (QREP * 8))), B52);
+                    if (j <= 4) {
+                        const double w0 = dmul(sp_w.w[j * 5 + dx], *(const double*)(lc0 + mw[j][dx]));
+                        num0 = dadd(num0, dmul(w0, v));
+                        dn0 = dadd(dn0, w0);
+                    }
+                    if (j >= 1) {
+                        const double w1 = dmul(sp_w.w[(j - 1) * 5 + dx], *(const double*)(lc1 + mw[j][dx]));
+                        num1 = dadd(num1, dmul(w1, v));
+                        dn1 = dadd(dn1, w1);
+                    }
                 }
-            double q = ddiv(num, dn);
-            q = (q < 0.0) ? 0.0 : q;
-            q = ((double)maxval < q) ? (double)maxval : q;
-            const int outv = (int)round(q);
-            const int x = x0 + lane, y = y0 + ty0 + r;
-            if (x < W && y < H) {
-                den[(size_t)slot * W * H + (size_t)y * W + x] = (uint8_t)outv;
-                sum += (unsigned long long)outv;
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                double q = ddiv(k ? num1 : num0, k ? dn1 : dn0);
+                q = (q < 0.0) ? 0.0 : q;
+                q = (dmax < q) ? dmax : q;
+                const int outv = (int)round(q);
+                const int x = x0 + lane, y = y0 + ty0 + r + k;
+                if (x < W && y < H) {
+                    den[(size_t)slot * W * H + (size_t)y * W + x] = (uint8_t)outv;
+                    sum += (unsigned long long)outv;
+                }
             }
         }
         for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
