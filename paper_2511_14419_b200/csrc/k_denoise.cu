@@ -271,41 +271,44 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
         }
         __syncthreads();
         const int ty0 = grp * QRPT;
-        // Two output rows per pass, their four accumulation chains interleaved: window rows
-        // ty0+r .. ty0+r+5 are walked once; row r takes j = 0..4 and row r+1 takes j = 1..5, each
-        // in the reference's dy-major / dx-minor order, and each median is converted to double
-        // once for both (2^52 bias, one DADD).
+        // NR output rows per pass, their 2*NR accumulation chains interleaved: window rows
+        // ty0+r .. ty0+r+NR+3 are walked once; output row r+k takes j = k..k+4, each in the
+        // reference's dy-major / dx-minor order, and each median is converted to double once
+        // for all of them (2^52 bias, one DADD).
+        constexpr int NR = 4;
         unsigned long long sum = 0;
         const double dmax = (double)maxval;
 #pragma unroll
-        for (int r = 0; r < QRPT; r += 2) {
-            int mw[6][5];
+        for (int r = 0; r < QRPT; r += NR) {
+            int mw[NR + 4][5];
 #pragma unroll
-            for (int j = 0; j < 6; ++j)
+            for (int j = 0; j < NR + 4; ++j)
 #pragma unroll
                 for (int dx = 0; dx < 5; ++dx) mw[j][dx] = med_s[(ty0 + r + j) * QMW + lane + dx];
-            const char* lc0 = lut0 - mw[2][2];
-            const char* lc1 = lut0 - mw[3][2];
-            double num0 = 0.0, dn0 = 0.0, num1 = 0.0, dn1 = 0.0;
+            const char* lc[NR];
+            double num[NR], dn[NR];
 #pragma unroll
-            for (int j = 0; j < 6; ++j)
+            for (int k = 0; k < NR; ++k) {
+                lc[k] = lut0 - mw[k + 2][2];
+                num[k] = 0.0;
+                dn[k] = 0.0;
+            }
+#pragma unroll
+            for (int j = 0; j < NR + 4; ++j)
 #pragma unroll
                 for (int dx = 0; dx < 5; ++dx) {
                     const double v = dsub(__hiloint2double(0x43300000, (int)((unsigned)mw[j][dx] / (QREP * 8))), B52);
-                    if (j <= 4) {
-                        const double w0 = dmul(sp_w.w[j * 5 + dx], *(const double*)(lc0 + mw[j][dx]));
-                        num0 = dadd(num0, dmul(w0, v));
-                        dn0 = dadd(dn0, w0);
-                    }
-                    if (j >= 1) {
-                        const double w1 = dmul(sp_w.w[(j - 1) * 5 + dx], *(const double*)(lc1 + mw[j][dx]));
-                        num1 = dadd(num1, dmul(w1, v));
-                        dn1 = dadd(dn1, w1);
+#pragma unroll
+                    for (int k = 0; k < NR; ++k) {
+                        if (j < k || j > k + 4) continue;
+                        const double w = dmul(sp_w.w[(j - k) * 5 + dx], *(const double*)(lc[k] + mw[j][dx]));
+                        num[k] = dadd(num[k], dmul(w, v));
+                        dn[k] = dadd(dn[k], w);
                     }
                 }
 #pragma unroll
-            for (int k = 0; k < 2; ++k) {
-                double q = ddiv(k ? num1 : num0, k ? dn1 : dn0);
+            for (int k = 0; k < NR; ++k) {
+                double q = ddiv(num[k], dn[k]);
                 q = (q < 0.0) ? 0.0 : q;
                 q = (dmax < q) ? dmax : q;
                 const int outv = (int)round(q);
