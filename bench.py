@@ -350,6 +350,11 @@ def run_ours(args) -> None:
                                   "frac": mb["total"] * pairs_per_s / 1e9 / pk["hbm_gbs"],
                                   "pairs_per_s_per_gpu": pairs_per_s},
             "stage_share": stage_frac,
+            # device time inside the per-stage events vs the step's wall-clock events: the rest is
+            # host-side gaps between batches
+            "stage_ms_per_step": sum(kt_sum.get(x, 0) for x in (
+                "denoise_ns", "fft_forward_ns", "expand_ns", "register_ns", "expand_shifted_ns",
+                "flow_iter_ns", "mask_ns")) / 1e6 / max(1, args.steps),
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "../../include/froi/froi.h"
@@ -261,7 +262,9 @@ struct froi_ctx {
     size_t tables_bytes = 0;
     cudaEvent_t tables_free[2] = {nullptr, nullptr};
     int tb = 0;
-    PairInfo* h_info = nullptr;  // pinned [Pcap]
+    PairInfo* h_info = nullptr;  // pinned, one entry per pair of the current call
+    size_t h_info_cap = 0;
+    std::vector<std::array<cudaEvent_t, 8>> bev;  // stage events of each batch of a call
     // sequence-level output buffer (PBM) for host outputs
     uint8_t* d_seq_out = nullptr;
     size_t seq_out_cap = 0;
@@ -418,6 +421,7 @@ void ctx_alloc(froi_ctx* c) {
         FROI_CUDA(cudaEventCreateWithFlags(&c->tables_free[i], cudaEventDisableTiming));
     }
     FROI_CUDA(cudaMallocHost((void**)&c->h_info, sizeof(PairInfo) * P));
+    c->h_info_cap = P;
     for (int i = 0; i < 8; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
 }
@@ -445,6 +449,8 @@ void ctx_free(froi_ctx* c) {
     if (c->h_info) cudaFreeHost(c->h_info);
     for (auto& e : c->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& a : c->bev)
+        for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->well_ready) cudaEventDestroy(e);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
@@ -476,8 +482,10 @@ struct PairJob {
 
 // Runs one batch of pairs.  frames given on device; output PBM masks written at out_index of
 // out_pbm (device).  h_stats_pairs receives the PairInfo of each pair (host, after sync).
+// One batch of pairs, enqueued without a host synchronisation: its PairInfo rows are copied to
+// h_info[info_off ..] and its stage events are batch event set `bi` (read by finish_batches).
 void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t j1, uint8_t* out_pbm,
-               std::vector<PairInfo>& infos) {
+               size_t bi, size_t info_off) {
     const Geom& g = c->g;
     const int n_pairs = int(j1 - j0);
     cudaStream_t s = c->stream;
@@ -523,7 +531,7 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
             FROI_CUDA(cudaStreamWaitEvent(s, jobs[j].ready, 0));
             waited = jobs[j].ready;
         }
-    cudaEvent_t* ev = c->ev;
+    cudaEvent_t* ev = c->bev[bi].data();
     FROI_CUDA(cudaEventRecord(ev[0], s));
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
     launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, nf, s);
@@ -545,29 +553,57 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
     mb.out_pbm = out_pbm;
     launch_mask_stage(g, c->dp, mb, n_pairs, s, &c->launches);
     FROI_CUDA(cudaEventRecord(ev[7], s));
-    FROI_CUDA(cudaMemcpyAsync(c->h_info, c->d_info, sizeof(PairInfo) * n_pairs, cudaMemcpyDeviceToHost, s));
-    FROI_CUDA(cudaStreamSynchronize(s));
-    float ms[7];
-    for (int i = 0; i < 7; ++i) FROI_CUDA(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
-    auto ns = [](float m) { return (uint64_t)((double)m * 1e6); };
-    c->times.denoise_ns += ns(ms[0]);
-    c->times.flow_ns += ns(ms[1] + ms[2] + ms[3] + ms[4] + ms[5]);
-    c->times.roi_ns += ns(ms[6]);
+    FROI_CUDA(cudaMemcpyAsync(c->h_info + info_off, c->d_info, sizeof(PairInfo) * n_pairs,
+                              cudaMemcpyDeviceToHost, s));
     froi_kernel_times& K = c->ktimes;
-    K.denoise_ns += ns(ms[0]);
-    K.fft_forward_ns += ns(ms[1]);
-    K.expand_ns += ns(ms[2]);
-    K.register_ns += ns(ms[3]);
-    K.expand_shifted_ns += ns(ms[4]);
-    K.flow_iter_ns += ns(ms[5]);
-    K.mask_ns += ns(ms[6]);
     K.pairs += n_pairs;
     K.frames += nf;
     K.flow_iter_launches += (uint64_t)g.L * c->dp.iterations;
     K.batches += 1;
     // launches: denoise 1, fft 2, expand (1 + 2(L-1)) x2, register 3, flow L*iters (+ mask stage)
     c->launches += 1 + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations;
-    for (int p = 0; p < n_pairs; ++p) infos.push_back(c->h_info[p]);
+}
+
+// Enqueue every batch of `jobs`, then synchronise once: stage times from each batch's events,
+// PairInfo rows in job order.
+void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm,
+                 std::vector<PairInfo>& infos) {
+    const size_t nb = (jobs.size() + c->Pcap - 1) / c->Pcap;
+    if (c->h_info_cap < jobs.size()) {
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+        FROI_CUDA(cudaFreeHost(c->h_info));
+        c->h_info = nullptr;
+        c->h_info_cap = 0;
+        FROI_CUDA(cudaMallocHost((void**)&c->h_info, sizeof(PairInfo) * jobs.size()));
+        c->h_info_cap = jobs.size();
+    }
+    while (c->bev.size() < nb) {
+        std::array<cudaEvent_t, 8> a;
+        for (auto& e : a) FROI_CUDA(cudaEventCreate(&e));
+        c->bev.push_back(a);
+    }
+    for (size_t b = 0; b < nb; ++b) {
+        const size_t j0 = b * c->Pcap, j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
+        run_batch(c, jobs, j0, j1, out_pbm, b, j0);
+    }
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    auto ns = [](float m) { return (uint64_t)((double)m * 1e6); };
+    froi_kernel_times& K = c->ktimes;
+    for (size_t b = 0; b < nb; ++b) {
+        float ms[7];
+        for (int i = 0; i < 7; ++i) FROI_CUDA(cudaEventElapsedTime(&ms[i], c->bev[b][i], c->bev[b][i + 1]));
+        c->times.denoise_ns += ns(ms[0]);
+        c->times.flow_ns += ns(ms[1] + ms[2] + ms[3] + ms[4] + ms[5]);
+        c->times.roi_ns += ns(ms[6]);
+        K.denoise_ns += ns(ms[0]);
+        K.fft_forward_ns += ns(ms[1]);
+        K.expand_ns += ns(ms[2]);
+        K.register_ns += ns(ms[3]);
+        K.expand_shifted_ns += ns(ms[4]);
+        K.flow_iter_ns += ns(ms[5]);
+        K.mask_ns += ns(ms[6]);
+    }
+    infos.insert(infos.end(), c->h_info, c->h_info + jobs.size());
 }
 
 void fill_stats(const Geom& g, const PairInfo& I, froi_frame_stats* st) {
@@ -642,10 +678,7 @@ void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int 
     c->times = froi_stage_times{};
     c->ktimes = froi_kernel_times{};
     c->launches = 0;
-    for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap) {
-        const size_t j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
-        run_batch(c, jobs, j0, j1, d_out, infos);
-    }
+    run_batches(c, jobs, d_out, infos);
     // frame 0 borrows frame 1's mask (roi.hpp:348)
     const size_t mb = (size_t)g.H * g.SB;
     for (int w = 0; w < n_wells; ++w)
@@ -1008,8 +1041,7 @@ int froi_stream_push(froi_ctx* c, const void* frames, int frames_on_device, int 
     c->ktimes = froi_kernel_times{};
     c->launches = 0;
     std::vector<PairInfo> infos;
-    for (size_t j0 = 0; j0 < jobs.size(); j0 += c->Pcap)
-        run_batch(c, jobs, j0, std::min(jobs.size(), j0 + (size_t)c->Pcap), d_out, infos);
+    run_batches(c, jobs, d_out, infos);
     if (first)
         for (int w = 0; w < nw; ++w)
             FROI_CUDA(cudaMemcpyAsync(d_out + mb * ((size_t)w * chunk), d_out + mb * ((size_t)w * chunk + 1), mb,
