@@ -264,7 +264,78 @@ __device__ __forceinline__ void pyr_tile(const Src& src, int w, int h, int tw, i
     }
 }
 
-template <typename T>
+// Exact 2:1 levels (w == 2 tw, h == 2 th; the default pyramid): bilinear() then always reads
+// blurred pixels (2x, 2x+1) x (2y, 2y+1) with fraction 0.5, so the tile is fixed: a 32x16 output
+// tile blurs a 64x32 block from a 70x38 input block.  Same blur order and resample expression as
+// pyr_tile; loops and divisions are compile-time, the column blur walks 8 rows per thread.
+constexpr int Q2X = 32, Q2Y = 16, Q2W = 2 * Q2X + 6, Q2H = 2 * Q2Y + 6;
+
+template <typename Src>
+__device__ __forceinline__ void pyr2_tile(const Src& src, int tw, int th, const float* kblur,
+                                          float* out, float* smem) {
+    float* s_in = smem;                  // Q2H x Q2W input (edge-clamped by the source)
+    float* s_rb = s_in + Q2H * Q2W;      // Q2H x 64 row-blurred
+    float* s_bl = s_rb + Q2H * 2 * Q2X;  // 32 x 64 blurred
+    const int ox0 = blockIdx.x * Q2X, oy0 = blockIdx.y * Q2Y;
+    const int ix0 = 2 * ox0 - 3, iy0 = 2 * oy0 - 3;
+    const int tid = threadIdx.x;
+    for (int i = tid; i < Q2H * Q2W; i += QNT) {
+        const int yy = i / Q2W, xx = i - yy * Q2W;
+        s_in[i] = src.at(ix0 + xx, iy0 + yy);
+    }
+    __syncthreads();
+    float k[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) k[t] = kblur[t];
+    // row blur: two adjacent columns per thread from 8 loads
+    for (int i = tid; i < Q2H * Q2X; i += QNT) {
+        const int yy = i / Q2X, xx = 2 * (i - yy * Q2X);
+        const float* row = s_in + yy * Q2W + xx;
+        float v[8];
+#pragma unroll
+        for (int t = 0; t < 8; ++t) v[t] = row[t];
+        float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+        for (int t = 0; t < 7; ++t) {
+            a0 += k[t] * v[t];
+            a1 += k[t] * v[t + 1];
+        }
+        s_rb[yy * 2 * Q2X + xx] = a0;
+        s_rb[yy * 2 * Q2X + xx + 1] = a1;
+    }
+    __syncthreads();
+    // column blur: 8 consecutive rows of one column per thread from 14 loads
+    {
+        const int xx = tid & (2 * Q2X - 1), yb = (tid >> 6) * 8;
+        float v[14];
+#pragma unroll
+        for (int t = 0; t < 14; ++t) v[t] = s_rb[(yb + t) * 2 * Q2X + xx];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            float acc = 0.f;
+#pragma unroll
+            for (int t = 0; t < 7; ++t) acc += k[t] * v[r + t];
+            s_bl[(yb + r) * 2 * Q2X + xx] = acc;
+        }
+    }
+    __syncthreads();
+    // resample: fraction 0.5 on both axes (pyr_tile's expression with ffx = ffy = 0.5)
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2) {
+        const int xx = tid & (Q2X - 1), yy = (tid >> 5) + 8 * k2;
+        const int x = ox0 + xx, y = oy0 + yy;
+        if (x >= tw || y >= th) continue;
+        const float* r0 = s_bl + (2 * yy) * 2 * Q2X + 2 * xx;
+        const float* r1 = r0 + 2 * Q2X;
+        const float f = 0.5f;
+        const float top = r0[0] * (1.f - f) + r0[1] * f;
+        const float bot = r1[0] * (1.f - f) + r1[1] * f;
+        out[(size_t)y * tw + x] = top * (1.f - f) + bot * f;
+    }
+}
+constexpr size_t pyr2_smem() { return sizeof(float) * (Q2H * Q2W + Q2H * 2 * Q2X + 2 * Q2Y * 2 * Q2X); }
+
+template <typename T, bool HALF>
 __global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T* den, float* pyr,
                                                     int rwmax, int rhmax) {
     extern __shared__ float smem_f[];
@@ -272,11 +343,12 @@ __global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T
     __shared__ float lut[256];
     const double inv = 1.0 / g.maxval;
     FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, frame_lut<T>(lut, inv)};
-    pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)slot * (g.lsum - g.loff[1]),
-             smem_f, rwmax, rhmax);
+    float* dst = pyr + (size_t)slot * (g.lsum - g.loff[1]);
+    if (HALF) pyr2_tile(src, g.lw[1], g.lh[1], P.blur, dst, smem_f);
+    else pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, dst, smem_f, rwmax, rhmax);
 }
 
-template <typename T>
+template <typename T, bool HALF>
 __global__ void __launch_bounds__(QNT) k_pyr0_shifted(Geom g, DevParams P, const T* den,
                                                       const int* next, const PairInfo* info,
                                                       float* pyr, int rwmax, int rhmax) {
@@ -287,10 +359,12 @@ __global__ void __launch_bounds__(QNT) k_pyr0_shifted(Geom g, DevParams P, const
     __shared__ float lut[256];
     const double inv = 1.0 / g.maxval;
     FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, frame_lut<T>(lut, inv)};
-    pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, pyr + (size_t)p * (g.lsum - g.loff[1]),
-             smem_f, rwmax, rhmax);
+    float* dst = pyr + (size_t)p * (g.lsum - g.loff[1]);
+    if (HALF) pyr2_tile(src, g.lw[1], g.lh[1], P.blur, dst, smem_f);
+    else pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, dst, smem_f, rwmax, rhmax);
 }
 
+template <bool HALF>
 __global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, float* pyr,
                                                    const PairInfo* info, int rwmax, int rhmax) {
     // level l -> l+1, l >= 1
@@ -299,8 +373,9 @@ __global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, f
     if (info && !info[z].shifted) return;
     float* base = pyr + (size_t)z * (g.lsum - g.loff[1]);
     ImageSrc src{base + (g.loff[l] - g.loff[1]), g.lw[l], g.lh[l]};
-    pyr_tile(src, g.lw[l], g.lh[l], g.lw[l + 1], g.lh[l + 1], P.blur,
-             base + (g.loff[l + 1] - g.loff[1]), smem_f, rwmax, rhmax);
+    float* dst = base + (g.loff[l + 1] - g.loff[1]);
+    if (HALF) pyr2_tile(src, g.lw[l + 1], g.lh[l + 1], P.blur, dst, smem_f);
+    else pyr_tile(src, g.lw[l], g.lh[l], g.lw[l + 1], g.lh[l + 1], P.blur, dst, smem_f, rwmax, rhmax);
 }
 
 // ------------------------------------------------------------------ flow iteration
@@ -688,6 +763,17 @@ size_t pyr_smem(int rwmax, int rhmax) {
 
 }  // namespace
 
+// exact 2:1 pyramid step (the fixed-tile kernel), else the general resample
+bool is_half(const Geom& g, int l) { return g.lw[l] == 2 * g.lw[l + 1] && g.lh[l] == 2 * g.lh[l + 1]; }
+#define FROI_HALF(h, ...)        \
+    if (h) {                     \
+        constexpr bool HF = true;  \
+        __VA_ARGS__;             \
+    } else {                     \
+        constexpr bool HF = false; \
+        __VA_ARGS__;             \
+    }
+
 // the default poly_n = 5 (radius 2) runs fully unrolled; other radii take the runtime loops
 #define FROI_POLY_RC(P, ...)            \
     if ((P).poly_radius == 2) {         \
@@ -717,20 +803,23 @@ void launch_expand_frames(const Geom& g, const DevParams& P, const FlowBuffers& 
     for (int l = 0; l + 1 < g.L; ++l) {
         int rwmax, rhmax;
         pyr_bounds(g, l, rwmax, rhmax);
-        const size_t ps = pyr_smem(rwmax, rhmax);
-        dim3 grid(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_slots);
-        if (l == 0) {
-            if (g.sample_bytes == 1) {
-                set_smem(k_pyr0_frame<uint8_t>, ps);
-                k_pyr0_frame<uint8_t><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, b.pyr_f, rwmax, rhmax);
+        const bool half = is_half(g, l);
+        const size_t ps = half ? pyr2_smem() : pyr_smem(rwmax, rhmax);
+        const dim3 grid = half ? dim3(cdiv(g.lw[l + 1], Q2X), cdiv(g.lh[l + 1], Q2Y), n_slots)
+                               : dim3(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_slots);
+        FROI_HALF(half,
+            if (l == 0) {
+                if (g.sample_bytes == 1) {
+                    set_smem(k_pyr0_frame<uint8_t, HF>, ps);
+                    k_pyr0_frame<uint8_t, HF><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, b.pyr_f, rwmax, rhmax);
+                } else {
+                    set_smem(k_pyr0_frame<uint16_t, HF>, ps);
+                    k_pyr0_frame<uint16_t, HF><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, b.pyr_f, rwmax, rhmax);
+                }
             } else {
-                set_smem(k_pyr0_frame<uint16_t>, ps);
-                k_pyr0_frame<uint16_t><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, b.pyr_f, rwmax, rhmax);
-            }
-        } else {
-            set_smem(k_pyr_level, ps);
-            k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_f, nullptr, rwmax, rhmax);
-        }
+                set_smem(k_pyr_level<HF>, ps);
+                k_pyr_level<HF><<<grid, QNT, ps, s>>>(g, P, l, b.pyr_f, nullptr, rwmax, rhmax);
+            })
         FROI_LAUNCH_CHECK();
         dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_slots);
         FROI_POLY_RC(P, set_smem(k_polyexp_level<RC>, pe);
@@ -760,20 +849,23 @@ void launch_expand_shifted(const Geom& g, const DevParams& P, const FlowBuffers&
     for (int l = 0; l + 1 < g.L; ++l) {
         int rwmax, rhmax;
         pyr_bounds(g, l, rwmax, rhmax);
-        const size_t ps = pyr_smem(rwmax, rhmax);
-        dim3 grid(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_pairs);
-        if (l == 0) {
-            if (g.sample_bytes == 1) {
-                set_smem(k_pyr0_shifted<uint8_t>, ps);
-                k_pyr0_shifted<uint8_t><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
+        const bool half = is_half(g, l);
+        const size_t ps = half ? pyr2_smem() : pyr_smem(rwmax, rhmax);
+        const dim3 grid = half ? dim3(cdiv(g.lw[l + 1], Q2X), cdiv(g.lh[l + 1], Q2Y), n_pairs)
+                               : dim3(cdiv(g.lw[l + 1], QX), cdiv(g.lh[l + 1], QY), n_pairs);
+        FROI_HALF(half,
+            if (l == 0) {
+                if (g.sample_bytes == 1) {
+                    set_smem(k_pyr0_shifted<uint8_t, HF>, ps);
+                    k_pyr0_shifted<uint8_t, HF><<<grid, QNT, ps, s>>>(g, P, (const uint8_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
+                } else {
+                    set_smem(k_pyr0_shifted<uint16_t, HF>, ps);
+                    k_pyr0_shifted<uint16_t, HF><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
+                }
             } else {
-                set_smem(k_pyr0_shifted<uint16_t>, ps);
-                k_pyr0_shifted<uint16_t><<<grid, QNT, ps, s>>>(g, P, (const uint16_t*)b.den, d_next, d_info, b.pyr_p, rwmax, rhmax);
-            }
-        } else {
-            set_smem(k_pyr_level, ps);
-            k_pyr_level<<<grid, QNT, ps, s>>>(g, P, l, b.pyr_p, d_info, rwmax, rhmax);
-        }
+                set_smem(k_pyr_level<HF>, ps);
+                k_pyr_level<HF><<<grid, QNT, ps, s>>>(g, P, l, b.pyr_p, d_info, rwmax, rhmax);
+            })
         FROI_LAUNCH_CHECK();
         dim3 eg(cdiv(g.lw[l + 1], PX), cdiv(g.lh[l + 1], PY), n_pairs);
         FROI_POLY_RC(P, set_smem(k_polyexp_level<RC>, pe);
