@@ -77,6 +77,72 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
         s_in[i] = src.at(x0 - r + xx, y0 - r + yy) - c0;
     }
     __syncthreads();
+    if (RC == 2 && !kDebug) {
+        // radius 2: same arithmetic per output, loads shared between neighbours -- row pass two
+        // adjacent columns from 6 loads, column pass two adjacent rows from 18 loads
+        constexpr int SW = PX + 4, SH = PY + 4;
+        float g0[5], g1[5], g2[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            g0[t] = P.g0[t];
+            g1[t] = P.g1[t];
+            g2[t] = P.g2[t];
+        }
+        for (int i = tid; i < SH * (PX / 2); i += PNT) {
+            const int yy = i / (PX / 2), xx = 2 * (i - yy * (PX / 2));
+            const float* row = s_in + yy * SW + xx;
+            float v[6];
+#pragma unroll
+            for (int t = 0; t < 6; ++t) v[t] = row[t];
+#pragma unroll
+            for (int k = 0; k < 2; ++k) {
+                float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+                for (int t = 0; t < 5; ++t) {
+                    a0 += g0[t] * v[t + k];
+                    a1 += g1[t] * v[t + k];
+                    a2 += g2[t] * v[t + k];
+                }
+                s_r[yy * PX + xx + k] = a0;
+                s_r[SH * PX + yy * PX + xx + k] = a1;
+                s_r[2 * SH * PX + yy * PX + xx + k] = a2;
+            }
+        }
+        __syncthreads();
+        const float inv_m20 = P.poly_moments[0], inv_m22 = P.poly_moments[1];
+        const float i01 = P.poly_moments[3], i11 = P.poly_moments[4], i12 = P.poly_moments[5];
+        const int xx = tid & (PX - 1), yb = (tid / PX) * 2;
+        float q0[6], q1[6], q2[6];
+#pragma unroll
+        for (int t = 0; t < 6; ++t) {
+            q0[t] = s_r[(yb + t) * PX + xx];
+            q1[t] = s_r[SH * PX + (yb + t) * PX + xx];
+            q2[t] = s_r[2 * SH * PX + (yb + t) * PX + xx];
+        }
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+            const int x = x0 + xx, y = y0 + yb + k;
+            if (x >= w || y >= h) continue;
+            float s1 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
+#pragma unroll
+            for (int t = 0; t < 5; ++t) {
+                s1 += g0[t] * q0[t + k];
+                sx += g0[t] * q1[t + k];
+                sy += g1[t] * q0[t + k];
+                sxx += g0[t] * q2[t + k];
+                syy += g2[t] * q0[t + k];
+                sxy += g1[t] * q1[t + k];
+            }
+            const float bx = sx * inv_m20, by = sy * inv_m20;
+            const float a12 = 0.5f * sxy * inv_m22;
+            const float a11 = i01 * s1 + i11 * sxx + i12 * syy;
+            const float a22 = i01 * s1 + i12 * sxx + i11 * syy;
+            const int o = y * w + x;
+            outA[o] = make_float4(a11, a12, a22, bx);
+            outB[o] = by;
+        }
+        return;
+    }
     // correlate_rows with g0, g1, g2 (flow.hpp:55-70)
     for (int i = tid; i < sh * PX; i += PNT) {
         const int yy = i / PX, xx = i - yy * PX;
