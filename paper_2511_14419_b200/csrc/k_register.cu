@@ -143,9 +143,21 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
     const int cb = 1 << lcb;
     const int slot = blockIdx.y, c0 = blockIdx.x * cb;
     double2* base = spec + (size_t)slot * ph * pw + c0;
-    for (int i = threadIdx.x; i < (ph << lcb); i += NT) {
-        const int r = i >> lcb, c = i & (cb - 1);
-        a[(pd(brev(r, log2ph)) << lcb) | c] = base[(size_t)r * pw + c];
+    // batches of UB loads in flight per thread before their shared-memory scatter
+    constexpr int UB = 8;
+    const int n = ph << lcb;
+    for (int i0 = threadIdx.x; i0 < n; i0 += NT * UB) {
+        double2 v[UB];
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int i = i0 + u * NT;
+            if (i < n) v[u] = __ldg(base + (size_t)(i >> lcb) * pw + (i & (cb - 1)));
+        }
+#pragma unroll
+        for (int u = 0; u < UB; ++u) {
+            const int i = i0 + u * NT;
+            if (i < n) a[(pd(brev(i >> lcb, log2ph)) << lcb) | (i & (cb - 1))] = v[u];
+        }
     }
     __syncthreads();
     fft_stages<kQCols>(a, ph, log2ph, lcb, tw);
