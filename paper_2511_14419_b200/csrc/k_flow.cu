@@ -19,6 +19,8 @@
 // level-0 image is never materialised.
 #include "kernels.cuh"
 
+#include <type_traits>
+
 namespace froi {
 namespace {
 
@@ -676,43 +678,55 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         // per step so each thread keeps ~20 gathers in flight
         const int r0 = k == 0 ? 0 : FY * k + 2 * R;
         const int npx = (k == 0 ? FY + 2 * R : FY) * HW;
-        for (int i0 = threadIdx.x; i0 < npx; i0 += 2 * FNT) {
-            // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
-            int gx[2], gy[2], si[2];
-            bool ok[2];
-            float2 pr[2];
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-                const int i = min(i0 + kk * FNT, npx - 1);
-                const int hy = i / HW, hx = i - hy * HW;
-                const int ux = x0 - R + hx, uy = ys - R + r0 + hy;
-                ok[kk] = i0 + kk * FNT < npx && ux >= 0 && ux < w && uy >= 0 && uy < h;
-                gx[kk] = clampi(ux, 0, w - 1);
-                gy[kk] = clampi(uy, 0, h - 1);
-                si[kk] = ((r0 + hy) % RG) * SW + hx;
-            }
-            // one asm statement issues both prior loads before either pixel's dependent index math
-            pr[0] = pr[1] = make_float2(0.f, 0.f);
-            if (a.mode)
-                asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
-                             : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
-                             : "l"(fin + (unsigned)(gy[0] * w + gx[0])), "l"(fin + (unsigned)(gy[1] * w + gx[1])));
-            GLoad ld[2];
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) g_load(ld[kk], pA, pB, nA, nB, w, h, gx[kk], gy[kk], pr[kk].x, pr[kk].y);
-#pragma unroll
-            for (int kk = 0; kk < 2; ++kk) {
-                GTerms t = g_terms(ld[kk], pr[kk].x, pr[kk].y);
-                if (!ok[kk]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
-                if (i0 + kk * FNT < npx) {
-                    G[si[kk]] = t.g11;
-                    G[PL + si[kk]] = t.g12;
-                    G[2 * PL + si[kk]] = t.g22;
-                    G[3 * PL + si[kk]] = t.h1;
-                    G[4 * PL + si[kk]] = t.h2;
+        auto phase1 = [&](auto in_tag) {
+            constexpr bool IN = decltype(in_tag)::value;
+            for (int i0 = threadIdx.x; i0 < npx; i0 += 2 * FNT) {
+                // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
+                int gx[2], gy[2], si[2];
+                bool ok[2];
+                float2 pr[2];
+    #pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    const int i = min(i0 + kk * FNT, npx - 1);
+                    const int hy = i / HW, hx = i - hy * HW;
+                    const int ux = x0 - R + hx, uy = ys - R + r0 + hy;
+                    if (IN) {  // the whole block of rows and columns lies inside the image
+                        ok[kk] = i0 + kk * FNT < npx;
+                        gx[kk] = ux;
+                        gy[kk] = uy;
+                    } else {
+                        ok[kk] = i0 + kk * FNT < npx && ux >= 0 && ux < w && uy >= 0 && uy < h;
+                        gx[kk] = clampi(ux, 0, w - 1);
+                        gy[kk] = clampi(uy, 0, h - 1);
+                    }
+                    si[kk] = ((r0 + hy) % RG) * SW + hx;
+                }
+                // one asm statement issues both prior loads before either pixel's dependent index math
+                pr[0] = pr[1] = make_float2(0.f, 0.f);
+                if (a.mode)
+                    asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
+                                 : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
+                                 : "l"(fin + (unsigned)(gy[0] * w + gx[0])), "l"(fin + (unsigned)(gy[1] * w + gx[1])));
+                GLoad ld[2];
+    #pragma unroll
+                for (int kk = 0; kk < 2; ++kk) g_load(ld[kk], pA, pB, nA, nB, w, h, gx[kk], gy[kk], pr[kk].x, pr[kk].y);
+    #pragma unroll
+                for (int kk = 0; kk < 2; ++kk) {
+                    GTerms t = g_terms(ld[kk], pr[kk].x, pr[kk].y);
+                    if (!ok[kk]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+                    if (i0 + kk * FNT < npx) {
+                        G[si[kk]] = t.g11;
+                        G[PL + si[kk]] = t.g12;
+                        G[2 * PL + si[kk]] = t.g22;
+                        G[3 * PL + si[kk]] = t.h1;
+                        G[4 * PL + si[kk]] = t.h2;
+                    }
                 }
             }
-        }
+        };
+        const int ry0 = ys - R + r0, ry1 = ry0 + npx / HW;
+        if (x0 - R >= 0 && x0 + FX + R <= w && ry0 >= 0 && ry1 <= h) phase1(std::true_type{});
+        else phase1(std::false_type{});
         if (threadIdx.x < FY) {
             const int y = y0 + threadIdx.x;
             rcy[threadIdx.x] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
