@@ -488,21 +488,40 @@ __device__ __forceinline__ void bl_split(int i, float d, int n, int& i0, float& 
 __global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* __restrict__ coarse,
                                                   float2* __restrict__ fine, float fx, float fy,
                                                   float rfx, float rfy) {
+    // 32 x 32 fine pixels per CTA, four rows per thread with all 16 coarse loads issued first
+    constexpr int NY = 4;
     const int p = blockIdx.z;
     const int w = g.lw[l], h = g.lh[l], cw = g.lw[l + 1], ch = g.lh[l + 1];
-    const int x = blockIdx.x * 32 + (threadIdx.x & 31), y = blockIdx.y * 8 + (threadIdx.x >> 5);
-    if (x >= w || y >= h) return;
+    const int x = blockIdx.x * 32 + (threadIdx.x & 31);
     const float2* c = coarse + (size_t)p * g.lsum + g.loff[l + 1];
-    const float sx = (x + 0.5f) * rfx - 0.5f, sy = (y + 0.5f) * rfy - 0.5f;
-    int x0, y0;
-    float ax, ay;
+    float2* f = fine + (size_t)p * g.lsum + g.loff[l];
+    const float sx = (x + 0.5f) * rfx - 0.5f;
+    int x0;
+    float ax;
     bl_split(0, sx, cw, x0, ax);
-    bl_split(0, sy, ch, y0, ay);
-    const float2 a = c[(size_t)y0 * cw + x0], b = c[(size_t)y0 * cw + x0 + 1];
-    const float2 d = c[(size_t)(y0 + 1) * cw + x0], e = c[(size_t)(y0 + 1) * cw + x0 + 1];
-    const float u = ((a.x * (1.f - ax) + b.x * ax) * (1.f - ay) + (d.x * (1.f - ax) + e.x * ax) * ay) * fx;
-    const float v = ((a.y * (1.f - ax) + b.y * ax) * (1.f - ay) + (d.y * (1.f - ax) + e.y * ax) * ay) * fy;
-    fine[(size_t)p * g.lsum + g.loff[l] + (size_t)y * w + x] = make_float2(u, v);
+    float2 q[NY][4];
+    float ay[NY];
+#pragma unroll
+    for (int k = 0; k < NY; ++k) {
+        const int y = min(blockIdx.y * 32 + (threadIdx.x >> 5) + 8 * k, h - 1);
+        const float sy = (y + 0.5f) * rfy - 0.5f;
+        int y0;
+        bl_split(0, sy, ch, y0, ay[k]);
+        const float2* r0 = c + y0 * cw + x0;
+        q[k][0] = __ldg(r0);
+        q[k][1] = __ldg(r0 + 1);
+        q[k][2] = __ldg(r0 + cw);
+        q[k][3] = __ldg(r0 + cw + 1);
+    }
+#pragma unroll
+    for (int k = 0; k < NY; ++k) {
+        const int y = blockIdx.y * 32 + (threadIdx.x >> 5) + 8 * k;
+        if (x >= w || y >= h) continue;
+        const float2 a = q[k][0], b = q[k][1], d = q[k][2], e = q[k][3];
+        const float u = ((a.x * (1.f - ax) + b.x * ax) * (1.f - ay[k]) + (d.x * (1.f - ax) + e.x * ax) * ay[k]) * fx;
+        const float v = ((a.y * (1.f - ax) + b.y * ax) * (1.f - ay[k]) + (d.y * (1.f - ax) + e.y * ax) * ay[k]) * fy;
+        f[y * w + x] = make_float2(u, v);
+    }
 }
 
 __device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, size_t pair_off,
@@ -970,7 +989,7 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
                 // upscale the coarser estimate into this level of the same buffer (flow.hpp:318-337)
                 const float fx = (float)((double)g.lw[l] / g.lw[l + 1]);
                 const float fy = (float)((double)g.lh[l] / g.lh[l + 1]);
-                dim3 ug(cdiv(g.lw[l], 32), cdiv(g.lh[l], 8), n_pairs);
+                dim3 ug(cdiv(g.lw[l], 32), cdiv(g.lh[l], 32), n_pairs);
                 k_upsample<<<ug, 256, 0, s>>>(g, l, buf[cur], buf[cur], fx, fy,
                                               (float)(1.0 / ((double)g.lw[l] / g.lw[l + 1])),
                                               (float)(1.0 / ((double)g.lh[l] / g.lh[l + 1])));
