@@ -146,8 +146,13 @@ int froi_ctx_stage_times(const froi_ctx* ctx, froi_stage_times* out);
 int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out);
 /* Per-kernel-group device times of the last extract call. */
 int froi_ctx_kernel_times(const froi_ctx* ctx, froi_kernel_times* out);
-/* The context's CUDA stream (cudaStream_t), for callers that time or order work around it. */
+/* The context's CUDA stream (cudaStream_t), for callers that time or order work around it.
+ * Extract calls end with all their work ordered on this stream (and the host synchronised). */
 int froi_ctx_stream(const froi_ctx* ctx, void** stream_out);
+/* Execution lanes (1 or 2, default 2 or $FROI_LANES): with 2, the batches of one call alternate
+ * between two buffer sets on two streams so their kernels overlap; outputs are identical.
+ * Per-stage times (froi_ctx_kernel_times) are exact kernel durations only with 1 lane. */
+int froi_ctx_set_lanes(froi_ctx* ctx, int lanes);
 
 /* ---- stage entry: extract_roi (roi.hpp:309-364) ----
  * Host frames: n_frames frames of width*height samples; frame f starts at

@@ -35,6 +35,7 @@ SIGNATURES = {
     "froi_ctx_launch_count": (_I, [_P, ctypes.POINTER(ctypes.c_uint64)]),
     "froi_ctx_kernel_times": (_I, [_P, ctypes.POINTER(CKernelTimes)]),
     "froi_ctx_stream": (_I, [_P, ctypes.POINTER(_P)]),
+    "froi_ctx_set_lanes": (_I, [_P, ctypes.c_int]),
     "froi_extract_roi": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),
     "froi_extract_wells": (_I, [_P, _P, _I, _SZ, _I, _I, _I, _P, _P]),
     "froi_extract_wells_device": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),

@@ -11,6 +11,7 @@
 // weights, Hann windows, FFT twiddle recurrence) are computed here with the same libm calls and
 // expression order as the reference; this file is compiled with -ffp-contract=off.
 #include <cmath>
+#include <cstdlib>
 #include <complex>
 #include <cstring>
 #include <mutex>
@@ -210,6 +211,11 @@ T* dalloc(size_t count, size_t* total) {
 
 }  // namespace
 
+static int default_lanes() {
+    const char* e = getenv("FROI_LANES");
+    return (e && atoi(e) == 1) ? 1 : 2;
+}
+
 struct froi_ctx {
     int device = 0;
     froi_params params{};
@@ -262,6 +268,11 @@ struct froi_ctx {
     size_t tables_bytes = 0;
     cudaEvent_t tables_free[2] = {nullptr, nullptr};
     int tb = 0;
+    // second execution lane (own buffers and stream, same constants): batches of one call
+    // alternate between the lanes so one lane's kernels fill the other's tails and small launches
+    froi_ctx* lane = nullptr;
+    int lanes = default_lanes();
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     PairInfo* h_info = nullptr;  // pinned, one entry per pair of the current call
     size_t h_info_cap = 0;
     std::vector<std::array<cudaEvent_t, 8>> bev;  // stage events of each batch of a call
@@ -428,6 +439,13 @@ void ctx_alloc(froi_ctx* c) {
 
 void ctx_free(froi_ctx* c) {
     cudaSetDevice(c->device);
+    if (c->lane) {
+        ctx_free(c->lane);
+        delete c->lane;
+        c->lane = nullptr;
+    }
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamSynchronize(c->stream);
     void* ptrs[] = {c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
@@ -484,8 +502,8 @@ struct PairJob {
 // out_pbm (device).  h_stats_pairs receives the PairInfo of each pair (host, after sync).
 // One batch of pairs, enqueued without a host synchronisation: its PairInfo rows are copied to
 // h_info[info_off ..] and its stage events are batch event set `bi` (read by finish_batches).
-void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t j1, uint8_t* out_pbm,
-               size_t bi, size_t info_off) {
+void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, size_t j0, size_t j1,
+               uint8_t* out_pbm, size_t bi, size_t info_off) {
     const Geom& g = c->g;
     const int n_pairs = int(j1 - j0);
     cudaStream_t s = c->stream;
@@ -531,7 +549,7 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
             FROI_CUDA(cudaStreamWaitEvent(s, jobs[j].ready, 0));
             waited = jobs[j].ready;
         }
-    cudaEvent_t* ev = c->bev[bi].data();
+    cudaEvent_t* ev = owner->bev[bi].data();
     FROI_CUDA(cudaEventRecord(ev[0], s));
     FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
     launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, nf, s);
@@ -551,17 +569,46 @@ void run_batch(froi_ctx* c, const std::vector<PairJob>& jobs, size_t j0, size_t 
     MaskBuffers mb = c->mask_buffers(tb);
     mb.flow = cur ? c->d_flow1 : c->d_flow0;
     mb.out_pbm = out_pbm;
-    launch_mask_stage(g, c->dp, mb, n_pairs, s, &c->launches);
+    launch_mask_stage(g, c->dp, mb, n_pairs, s, &owner->launches);
     FROI_CUDA(cudaEventRecord(ev[7], s));
-    FROI_CUDA(cudaMemcpyAsync(c->h_info + info_off, c->d_info, sizeof(PairInfo) * n_pairs,
+    FROI_CUDA(cudaMemcpyAsync(owner->h_info + info_off, c->d_info, sizeof(PairInfo) * n_pairs,
                               cudaMemcpyDeviceToHost, s));
-    froi_kernel_times& K = c->ktimes;
+    froi_kernel_times& K = owner->ktimes;
     K.pairs += n_pairs;
     K.frames += nf;
     K.flow_iter_launches += (uint64_t)g.L * c->dp.iterations;
     K.batches += 1;
     // launches: denoise 1, fft 2, expand (1 + 2(L-1)) x2, register 3, flow L*iters (+ mask stage)
-    c->launches += 1 + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations;
+    owner->launches += 1 + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations;
+}
+
+// The second lane, created on first use with the owner's device, parameters and capacity.
+// One lane (froi_ctx_set_lanes or FROI_LANES=1) keeps every batch on the owner's stream.
+froi_ctx* lane_of(froi_ctx* c) {
+    if (c->lanes < 2) return nullptr;
+    if (!c->lane) {
+        froi_ctx* l = new froi_ctx();
+        try {
+            l->device = c->device;
+            l->params = c->params;
+            l->g = c->g;
+            l->dp = c->dp;
+            l->Pcap = c->Pcap;
+            l->Fcap = c->Fcap;
+            FROI_CUDA(cudaStreamCreateWithFlags(&l->stream, cudaStreamNonBlocking));
+            ctx_alloc(l);
+        } catch (...) {
+            ctx_free(l);
+            delete l;
+            throw;
+        }
+        c->lane = l;
+        FROI_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+        FROI_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
+    }
+    c->lane->dp = c->dp;  // set_params may have changed the run-time parameters
+    c->lane->params = c->params;
+    return c->lane;
 }
 
 // Enqueue every batch of `jobs`, then synchronise once: stage times from each batch's events,
@@ -582,9 +629,20 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         for (auto& e : a) FROI_CUDA(cudaEventCreate(&e));
         c->bev.push_back(a);
     }
+    froi_ctx* lane = nb >= 2 ? lane_of(c) : nullptr;
+    if (lane) {
+        // the lane starts after everything already ordered on the owner's stream
+        FROI_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+        FROI_CUDA(cudaStreamWaitEvent(lane->stream, c->ev_fork, 0));
+    }
     for (size_t b = 0; b < nb; ++b) {
         const size_t j0 = b * c->Pcap, j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
-        run_batch(c, jobs, j0, j1, out_pbm, b, j0);
+        run_batch((lane && (b & 1)) ? lane : c, c, jobs, j0, j1, out_pbm, b, j0);
+    }
+    if (lane) {
+        // later work on the owner's stream (frame-0 copies, ensemble, delivery) follows both lanes
+        FROI_CUDA(cudaEventRecord(c->ev_join, lane->stream));
+        FROI_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     FROI_CUDA(cudaStreamSynchronize(c->stream));
     auto ns = [](float m) { return (uint64_t)((double)m * 1e6); };
@@ -878,6 +936,13 @@ int froi_ctx_kernel_times(const froi_ctx* ctx, froi_kernel_times* out) {
 int froi_ctx_stream(const froi_ctx* ctx, void** stream_out) {
     if (!ctx || !stream_out) return fail(1, "null argument");
     *stream_out = (void*)ctx->stream;
+    return 0;
+}
+
+int froi_ctx_set_lanes(froi_ctx* ctx, int lanes) {
+    if (!ctx) return fail(1, "null context");
+    if (lanes != 1 && lanes != 2) return fail(1, "lanes must be 1 or 2");
+    ctx->lanes = lanes;
     return 0;
 }
 

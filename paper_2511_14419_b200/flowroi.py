@@ -119,6 +119,10 @@ class Context:
         _native.check(_native.lib.froi_ctx_kernel_times(self._h, ctypes.byref(t)))
         return t.as_dict()
 
+    def set_lanes(self, lanes: int) -> None:
+        """1 or 2 execution lanes (two overlap consecutive batches; outputs are identical)."""
+        _native.check(_native.lib.froi_ctx_set_lanes(self._h, int(lanes)))
+
     def stream(self) -> int:
         s = ctypes.c_void_p()
         _native.check(_native.lib.froi_ctx_stream(self._h, ctypes.byref(s)))

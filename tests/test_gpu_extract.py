@@ -157,3 +157,21 @@ def test_streaming_matches_whole_sequence(gpu):
                                                    0, out.ctypes.data, 0, None))
         got.append(out)
     assert np.array_equal(np.concatenate(got), whole)
+
+
+def test_two_lanes_identical(gpu):
+    """Two execution lanes (consecutive batches on two buffer sets / streams) give the same
+    masks and stats byte for byte as one lane, for a call spanning several batches and wells."""
+    from paper_2511_14419_b200 import flowroi
+    from paper_2511_14419_b200.params import ExtractParams
+    n, size = 13, 96
+    wells = np.stack([np.stack([cyclic_shift(textured_frame(size, size, 8, 70 + w), t, (t * w) % 3)
+                                for t in range(n)]) for w in range(2)]).astype(np.uint8)
+    out = {}
+    for lanes in (1, 2):
+        ctx = flowroi.Context(size, size, 8, ExtractParams(), max_pairs=4)
+        ctx.set_lanes(lanes)
+        masks, stats = ctx.extract_wells(wells, layout="pbm")
+        out[lanes] = (masks, [(s.dx, s.dy, s.confidence, s.mask_count) for s in stats])
+    assert np.array_equal(out[1][0], out[2][0])
+    assert out[1][1] == out[2][1]
