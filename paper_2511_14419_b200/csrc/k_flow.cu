@@ -697,50 +697,85 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         // per step so each thread keeps ~20 gathers in flight
         const int r0 = k == 0 ? 0 : FY * k + 2 * R;
         const int npx = (k == 0 ? FY + 2 * R : FY) * HW;
+        // Each thread takes two vertically adjacent halo pixels (rows 2rp, 2rp+1 of the block).
+        // When the lower pixel's bilinear top row is the upper pixel's bottom row (the common case
+        // for a smooth flow) those four corners are reused from registers instead of re-gathered.
         auto phase1 = [&](auto in_tag) {
             constexpr bool IN = decltype(in_tag)::value;
-            for (int i0 = threadIdx.x; i0 < npx; i0 += 2 * FNT) {
-                // branch-free: out-of-image halo pixels load a clamped neighbour and store zeros
-                int gx[2], gy[2], si[2];
-                bool ok[2];
-                float2 pr[2];
-    #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    const int i = min(i0 + kk * FNT, npx - 1);
-                    const int hy = i / HW, hx = i - hy * HW;
-                    const int ux = x0 - R + hx, uy = ys - R + r0 + hy;
-                    if (IN) {  // the whole block of rows and columns lies inside the image
-                        ok[kk] = i0 + kk * FNT < npx;
-                        gx[kk] = ux;
-                        gy[kk] = uy;
-                    } else {
-                        ok[kk] = i0 + kk * FNT < npx && ux >= 0 && ux < w && uy >= 0 && uy < h;
-                        gx[kk] = clampi(ux, 0, w - 1);
-                        gy[kk] = clampi(uy, 0, h - 1);
-                    }
-                    si[kk] = ((r0 + hy) % RG) * SW + hx;
+            const int npp = npx / 2;
+            for (int ip = threadIdx.x; ip < npp; ip += FNT) {
+                const int rp = ip / HW, hx = ip - rp * HW;
+                const int ux = x0 - R + hx, uy = ys - R + r0 + 2 * rp;
+                int gx, gyA, gyB;
+                bool okA, okB;
+                if (IN) {  // the whole block of rows and columns lies inside the image
+                    gx = ux;
+                    gyA = uy;
+                    gyB = uy + 1;
+                    okA = okB = true;
+                } else {
+                    const bool okx = ux >= 0 && ux < w;
+                    okA = okx && uy >= 0 && uy < h;
+                    okB = okx && uy + 1 >= 0 && uy + 1 < h;
+                    gx = clampi(ux, 0, w - 1);
+                    gyA = clampi(uy, 0, h - 1);
+                    gyB = clampi(uy + 1, 0, h - 1);
                 }
-                // one asm statement issues both prior loads before either pixel's dependent index math
-                pr[0] = pr[1] = make_float2(0.f, 0.f);
+                const int siA = ((r0 + 2 * rp) % RG) * SW + hx, siB = ((r0 + 2 * rp + 1) % RG) * SW + hx;
+                float2 prA = make_float2(0.f, 0.f), prB = make_float2(0.f, 0.f);
                 if (a.mode)
                     asm volatile("ld.global.nc.v2.f32 {%0, %1}, [%4];\n\tld.global.nc.v2.f32 {%2, %3}, [%5];"
-                                 : "=f"(pr[0].x), "=f"(pr[0].y), "=f"(pr[1].x), "=f"(pr[1].y)
-                                 : "l"(fin + (unsigned)(gy[0] * w + gx[0])), "l"(fin + (unsigned)(gy[1] * w + gx[1])));
-                GLoad ld[2];
-    #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) g_load(ld[kk], pA, pB, nA, nB, w, h, gx[kk], gy[kk], pr[kk].x, pr[kk].y);
-    #pragma unroll
-                for (int kk = 0; kk < 2; ++kk) {
-                    GTerms t = g_terms(ld[kk], pr[kk].x, pr[kk].y);
-                    if (!ok[kk]) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
-                    if (i0 + kk * FNT < npx) {
-                        G[si[kk]] = t.g11;
-                        G[PL + si[kk]] = t.g12;
-                        G[2 * PL + si[kk]] = t.g22;
-                        G[3 * PL + si[kk]] = t.h1;
-                        G[4 * PL + si[kk]] = t.h2;
-                    }
+                                 : "=f"(prA.x), "=f"(prA.y), "=f"(prB.x), "=f"(prB.y)
+                                 : "l"(fin + (unsigned)(gyA * w + gx)), "l"(fin + (unsigned)(gyB * w + gx)));
+                GLoad lA, lB;
+                int xaA, yaA, xaB, yaB;
+                bl_split(gx, prA.x, w, xaA, lA.fx);
+                bl_split(gyA, prA.y, h, yaA, lA.fy);
+                bl_split(gx, prB.x, w, xaB, lB.fx);
+                bl_split(gyB, prB.y, h, yaB, lB.fy);
+                const unsigned iA0 = (unsigned)(yaA * w + xaA), iA1 = iA0 + (unsigned)w;
+                const unsigned iB0 = (unsigned)(yaB * w + xaB), iB1 = iB0 + (unsigned)w;
+                lA.q00 = __ldg(nA + iA0);
+                lA.q01 = __ldg(nA + iA0 + 1);
+                lA.q10 = __ldg(nA + iA1);
+                lA.q11 = __ldg(nA + iA1 + 1);
+                lA.b00 = __ldg(nB + iA0);
+                lA.b01 = __ldg(nB + iA0 + 1);
+                lA.b10 = __ldg(nB + iA1);
+                lA.b11 = __ldg(nB + iA1 + 1);
+                lB.q10 = __ldg(nA + iB1);
+                lB.q11 = __ldg(nA + iB1 + 1);
+                lB.b10 = __ldg(nB + iB1);
+                lB.b11 = __ldg(nB + iB1 + 1);
+                if (iB0 == iA1) {
+                    lB.q00 = lA.q10;
+                    lB.q01 = lA.q11;
+                    lB.b00 = lA.b10;
+                    lB.b01 = lA.b11;
+                } else {
+                    lB.q00 = __ldg(nA + iB0);
+                    lB.q01 = __ldg(nA + iB0 + 1);
+                    lB.b00 = __ldg(nB + iB0);
+                    lB.b01 = __ldg(nB + iB0 + 1);
                 }
+                const unsigned cA = (unsigned)(gyA * w + gx), cB = (unsigned)(gyB * w + gx);
+                lA.pa = __ldg(pA + cA);
+                lA.pb = __ldg(pB + cA);
+                lB.pa = __ldg(pA + cB);
+                lB.pb = __ldg(pB + cB);
+                GTerms tA = g_terms(lA, prA.x, prA.y), tB = g_terms(lB, prB.x, prB.y);
+                if (!okA) tA = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+                if (!okB) tB = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+                G[siA] = tA.g11;
+                G[PL + siA] = tA.g12;
+                G[2 * PL + siA] = tA.g22;
+                G[3 * PL + siA] = tA.h1;
+                G[4 * PL + siA] = tA.h2;
+                G[siB] = tB.g11;
+                G[PL + siB] = tB.g12;
+                G[2 * PL + siB] = tB.g22;
+                G[3 * PL + siB] = tB.h1;
+                G[4 * PL + siB] = tB.h2;
             }
         };
         const int ry0 = ys - R + r0, ry1 = ry0 + npx / HW;
