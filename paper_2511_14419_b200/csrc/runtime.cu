@@ -613,8 +613,10 @@ froi_ctx* lane_of(froi_ctx* c) {
 
 // Enqueue every batch of `jobs`, then synchronise once: stage times from each batch's events,
 // PairInfo rows in job order.
+// host_pbm (nullable, pinned): each batch's PBM masks are copied to the same offsets of host_pbm
+// on the batch's lane right after its mask stage, overlapping the later batches.
 void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm,
-                 std::vector<PairInfo>& infos) {
+                 std::vector<PairInfo>& infos, uint8_t* host_pbm = nullptr) {
     const size_t nb = (jobs.size() + c->Pcap - 1) / c->Pcap;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
@@ -635,9 +637,20 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         FROI_CUDA(cudaEventRecord(c->ev_fork, c->stream));
         FROI_CUDA(cudaStreamWaitEvent(lane->stream, c->ev_fork, 0));
     }
+    const size_t mb = (size_t)c->g.H * c->g.SB;
     for (size_t b = 0; b < nb; ++b) {
         const size_t j0 = b * c->Pcap, j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
-        run_batch((lane && (b & 1)) ? lane : c, c, jobs, j0, j1, out_pbm, b, j0);
+        froi_ctx* x = (lane && (b & 1)) ? lane : c;
+        run_batch(x, c, jobs, j0, j1, out_pbm, b, j0);
+        if (host_pbm) {
+            long long lo = jobs[j0].out_index, hi = lo;
+            for (size_t j = j0; j < j1; ++j) {
+                lo = std::min(lo, jobs[j].out_index);
+                hi = std::max(hi, jobs[j].out_index);
+            }
+            FROI_CUDA(cudaMemcpyAsync(host_pbm + mb * lo, out_pbm + mb * lo, mb * (size_t)(hi - lo + 1),
+                                      cudaMemcpyDeviceToHost, x->stream));
+        }
     }
     if (lane) {
         // later work on the owner's stream (frame-0 copies, ensemble, delivery) follows both lanes
@@ -718,7 +731,8 @@ void check_frames_range(froi_ctx* c, const void* frames, int sample_bytes, size_
 
 // Whole wells: frames on device (well-major, contiguous in ctx sample type).
 void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int n_wells, int n_frames,
-                       uint8_t* d_out, std::vector<PairInfo>& infos, const cudaEvent_t* ready = nullptr) {
+                       uint8_t* d_out, std::vector<PairInfo>& infos, const cudaEvent_t* ready = nullptr,
+                       uint8_t* host_pbm = nullptr) {
     // ready (nullable): per (well, frame) event after which the frame is resident
     const Geom& g = c->g;
     std::vector<PairJob> jobs;
@@ -736,7 +750,7 @@ void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int 
     c->times = froi_stage_times{};
     c->ktimes = froi_kernel_times{};
     c->launches = 0;
-    run_batches(c, jobs, d_out, infos);
+    run_batches(c, jobs, d_out, infos, host_pbm);
     // frame 0 borrows frame 1's mask (roi.hpp:348)
     const size_t mb = (size_t)g.H * g.SB;
     for (int w = 0; w < n_wells; ++w)
@@ -1007,9 +1021,22 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
     }
     ensure_seq_out(c, mb * nm);
     std::vector<PairInfo> infos;
+    // PBM into pinned memory without the ensemble: masks stream back batch by batch
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, masks_out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();  // a pageable pointer may leave an error behind
+    const bool stream_back = layout == FROI_MASK_PBM && c->params.adjacent_factor == 0 && pinned;
     extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos,
-                      direct ? ready.data() : nullptr);
-    deliver_masks(c, c->d_seq_out, nm, layout, masks_out);
+                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr);
+    if (stream_back) {
+        // only frame 0 of each well (a copy of frame 1's mask, made after the batches) is left
+        for (int w = 0; w < n_wells; ++w)
+            FROI_CUDA(cudaMemcpyAsync(masks_out + mb * ((size_t)w * n_frames), c->d_seq_out + mb * ((size_t)w * n_frames),
+                                      mb, cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    } else {
+        deliver_masks(c, c->d_seq_out, nm, layout, masks_out);
+    }
     stats_for_wells(c, infos, n_wells, n_frames, stats_out);
     ABI_CATCH
 }

@@ -175,3 +175,20 @@ def test_two_lanes_identical(gpu):
         out[lanes] = (masks, [(s.dx, s.dy, s.confidence, s.mask_count) for s in stats])
     assert np.array_equal(out[1][0], out[2][0])
     assert out[1][1] == out[2][1]
+
+
+def test_pinned_pbm_streamed_back_identical(gpu):
+    """PBM masks into pinned host memory are copied back batch by batch during the call (frame 0
+    of each well at the end); the bytes equal the pageable-memory path."""
+    import torch
+    from paper_2511_14419_b200 import flowroi
+    from paper_2511_14419_b200.params import CFrameStats, ExtractParams
+    n, size = 13, 96
+    wells = np.stack([np.stack([cyclic_shift(textured_frame(size, size, 8, 90 + w), t, (t * w) % 3)
+                                for t in range(n)]) for w in range(2)]).astype(np.uint8)
+    ctx = flowroi.Context(size, size, 8, ExtractParams(), max_pairs=4)
+    want, _ = ctx.extract_wells(wells, layout="pbm")
+    pinned = torch.zeros((2, n, size, (size + 7) // 8), dtype=torch.uint8, pin_memory=True)
+    stats = (CFrameStats * (2 * n))()
+    ctx.extract_wells_into(wells, pinned.numpy(), stats)
+    assert np.array_equal(pinned.numpy(), want)
