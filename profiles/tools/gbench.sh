@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage: scratch/gbench.sh <logname> [bench args]
+# usage: profiles/tools/gbench.sh <logname> [bench args]
 LOG=$1; shift
 (timeout 2400 /usr/local/graft/bin/gpurun --timeout 900 -- "timeout 300 python -m pytest tests -m gpu -q -p no:cacheprovider --tb=short 2>&1 | tail -5; timeout 600 python bench.py $* 2>&1 | tail -3" > gpurun_out/$LOG.log 2>&1)
 tail -12 gpurun_out/$LOG.log | python -c "

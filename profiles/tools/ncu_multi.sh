@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage (on the box): scratch/ncu_multi.sh tag kernel1 kernel2 ...
+# usage (on the box): profiles/tools/ncu_multi.sh tag kernel1 kernel2 ...
 TAG=$1; shift
 python bench.py --steps 1 --warmup 3 --frames 33 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 for k in "$@"; do

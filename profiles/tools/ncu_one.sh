@@ -1,5 +1,5 @@
 #!/bin/bash
-# usage (on the box): scratch/ncu_one.sh tag "kernel:skip" ...
+# usage (on the box): profiles/tools/ncu_one.sh tag "kernel:skip" ...
 TAG=$1; shift
 python bench.py --steps 1 --warmup 3 --frames 33 --no-cpu-baseline --no-e2e > gpurun_out/${TAG}_plain.log 2>&1 || exit 1
 for ks in "$@"; do
