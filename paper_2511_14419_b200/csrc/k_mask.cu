@@ -217,8 +217,12 @@ __device__ __forceinline__ void hist_add(unsigned int* h, bool m, unsigned int b
 // consecutive pixels per thread: histogram of the next digit (exponent window first for
 // single-query sources) for queries in HIST mode, warp-aggregated candidate append for queries in
 // COLLECT mode.  All threads of the CTA run the same number of iterations (warp votes inside).
+// write_bits (single-query sources, W % 32 == 0): a COLLECT pass also writes the threshold words
+// of every pixel outside the boundary bin (above -> 1, below -> 0; the bin's candidates are 0
+// until k_thr_fixup) and records each candidate's pixel index.
 template <class Src>
-__device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src) {
+__device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src,
+                              bool write_bits = false) {
     constexpr int NQ = Src::NQ;
     constexpr int NB = NQ == 1 ? kHistBins : kSelBins;
     constexpr int CB = NQ == 1 ? 2048 : 1024;
@@ -226,6 +230,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     extern __shared__ __align__(16) unsigned char dsm[];
     unsigned long long (*cbuf)[CB] = reinterpret_cast<unsigned long long (*)[CB]>(dsm);
     unsigned int (*hist)[NB] = reinterpret_cast<unsigned int (*)[NB]>(dsm + sizeof(unsigned long long) * NQ * CB);
+    unsigned int* cidx = reinterpret_cast<unsigned int*>(dsm + (sizeof(unsigned long long) * CB + sizeof(unsigned int) * NB) * NQ);
     __shared__ SelState st[NQ];
     __shared__ unsigned long long smn[NQ], smx[NQ];
     // COLLECT: candidates staged per block in shared memory (one global reservation per query)
@@ -264,7 +269,10 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     }
     const long long n = (long long)g.W * g.H;
     const bool vec = (n & 3) == 0;
-    const long long per = cdiv<long long>(cdiv<long long>(n, gridDim.x), 4) * 4;
+    const bool bits = NQ == 1 && write_bits && cq[0];
+    // word-aligned block ranges when writing bits (every warp step covers 4 whole words)
+    const long long gran = bits ? 4ll * blockDim.x : 4ll;
+    const long long per = cdiv<long long>(cdiv<long long>(n, gridDim.x), gran) * gran;
     const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
     const int lane = threadIdx.x & 31;
     for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
@@ -302,10 +310,21 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                 }
             } else if (cq[q]) {
                 bool m[4], any = false;
+                unsigned int nib = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
                     m[e] = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
                     any |= m[e];
+                    if (v[e] && ms[q] < 64 && (k[q][e] >> ms[q]) > mp[q]) nib |= 1u << e;
+                }
+                if (bits) {
+                    // lane l holds bits 4(l%8)..+3 of word (base0 + 128 w_l)/32 + l/8
+                    unsigned int word = nib << (4 * (lane & 7));
+                    word |= __shfl_xor_sync(0xffffffffu, word, 1);
+                    word |= __shfl_xor_sync(0xffffffffu, word, 2);
+                    word |= __shfl_xor_sync(0xffffffffu, word, 4);
+                    if ((lane & 7) == 0 && base < i1)
+                        b.bits_thr[(size_t)p * g.H * g.WW + (size_t)(base >> 5)] = word;
                 }
                 if (__any_sync(0xffffffffu, any)) {
 #pragma unroll
@@ -320,10 +339,13 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                             const unsigned int idx = basei + __popc(bal & ((1u << lane) - 1u));
                             if (idx < (unsigned)CB) {
                                 cbuf[q][idx] = k[q][e];
+                                if (bits) cidx[idx] = (unsigned int)(base + e);
                             } else {  // staging full: straight to the global list
                                 const unsigned int gi = atomicAdd(b.cand_count + p * kMaxQueries + q, 1u);
-                                if (gi < (unsigned)kSelCap)
+                                if (gi < (unsigned)kSelCap) {
                                     b.cand[((size_t)p * kMaxQueries + q) * kSelCap + gi] = k[q][e];
+                                    if (bits) b.cand_idx[(size_t)p * kSelCap + gi] = (unsigned int)(base + e);
+                                }
                             }
                         }
                     }
@@ -343,7 +365,10 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
             const unsigned int c = min(ccnt[q], (unsigned int)CB);
             unsigned long long* dst = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
             for (unsigned int i = threadIdx.x; i < c; i += blockDim.x)
-                if (cbase[q] + i < (unsigned)kSelCap) dst[cbase[q] + i] = cbuf[q][i];
+                if (cbase[q] + i < (unsigned)kSelCap) {
+                    dst[cbase[q] + i] = cbuf[q][i];
+                    if (bits) b.cand_idx[(size_t)p * kSelCap + cbase[q] + i] = cidx[i];
+                }
         }
     }
     if (!anyh) return;
@@ -498,27 +523,29 @@ __global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
     sel_pass_body(g, b, p, src);
 }
 
-__global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map) {
+__global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map,
+                                                   int write_bits) {
     const int p = blockIdx.y;
     if (map) {
         SrcMap src{map};
-        sel_pass_body(g, b, p, src);
+        sel_pass_body(g, b, p, src, write_bits != 0);
     } else {
         SrcSal src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H), b.info[p],
                    P.flow_weight, 1.0 - P.flow_weight};
-        sel_pass_body(g, b, p, src);
+        sel_pass_body(g, b, p, src, write_bits != 0);
     }
 }
 
 constexpr size_t pass_smem(int nq) {
-    return (sizeof(unsigned long long) * (nq == 1 ? 2048 : 1024) + sizeof(unsigned int) * (nq == 1 ? kHistBins : kSelBins)) * nq;
+    return (sizeof(unsigned long long) * (nq == 1 ? 2048 : 1024) + sizeof(unsigned int) * (nq == 1 ? kHistBins : kSelBins)) * nq +
+           (nq == 1 ? sizeof(unsigned int) * 2048 : 0);
 }
 
 // One CTA per (pair, query): narrow the prefix after a histogram pass, or finish a collected
 // group (<= kSelCap keys, all sharing the prefix) by an 8-bit-digit radix select in shared memory.
 constexpr int SCT = 1024;
 
-__global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
+__global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq, int bits = 0) {
     extern __shared__ unsigned long long cs[];  // kSelCap candidates
     const int p = blockIdx.x / nq, q = blockIdx.x % nq;
     SelState* sp = b.sel + p * kMaxQueries + q;
@@ -590,6 +617,10 @@ __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq) {
             ns.mode = SEL_DONE;
             *sp = ns;
             *cc = 0;
+            if (bits) {  // the collect pass that fed this select wrote the threshold words
+                b.info[p].bits_ready = 1;
+                b.info[p].n_cand = (unsigned int)n;
+            }
         }
         return;
     }
@@ -705,6 +736,8 @@ __global__ void k_sel_init_b(MaskBuffers b, unsigned long long n, unsigned long 
         I.grad_inv = I.grad_zero ? 0.0 : ddiv(1.0, dg);
     }
     I.target = target;
+    I.bits_ready = 0;
+    I.n_cand = 0;
     // (target-1)-th largest == (n-target)-th smallest
     b.sel[p * kMaxQueries] = sel_init(target ? n - target : 0, n, target == 0, from_stats ? 1 : 0);
     for (int q = 1; q < kMaxQueries; ++q) b.sel[p * kMaxQueries + q].mode = SEL_DONE;
@@ -757,7 +790,7 @@ __global__ void __launch_bounds__(TNT) k_thr_count(Geom g, DevParams P, MaskBuff
                                                    const double* map) {
     const int p = blockIdx.y, chunk = blockIdx.x;
     const PairInfo& I = b.info[p];
-    if (I.thr_mode != 3) return;
+    if (I.thr_mode != 3 || I.bits_ready) return;
     __shared__ unsigned long long se;
     if (threadIdx.x == 0) se = 0;
     __syncthreads();
@@ -776,7 +809,7 @@ __global__ void __launch_bounds__(TNT) k_thr_count(Geom g, DevParams P, MaskBuff
 // Exclusive scan of the per-chunk tie counts (thr_mode 3 only).
 __global__ void __launch_bounds__(1024) k_thr_scan(MaskBuffers b, int nch) {
     const int p = blockIdx.x;
-    if (b.info[p].thr_mode != 3) return;
+    if (b.info[p].thr_mode != 3 || b.info[p].bits_ready) return;
     __shared__ unsigned long long seq[1024];
     unsigned long long* tc = b.tie_cnt + (size_t)p * nch;
     const int per = cdiv(nch, 1024);
@@ -810,6 +843,7 @@ __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuff
                                                    const double* map) {
     const int p = blockIdx.y, chunk = blockIdx.x;
     const PairInfo I = b.info[p];
+    if (I.bits_ready) return;  // written by the collect pass, settled by k_thr_fixup
     const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
     uint32_t* out = b.bits_thr + (size_t)p * g.H * g.WW;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -867,6 +901,61 @@ __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuff
         }
         __syncthreads();
     }
+}
+
+// Settles the boundary bin's candidates after phase B's collect pass wrote every other pixel's
+// threshold bit (one CTA per pair): mode 0 admits S >= boundary, mode 2 S > 0, mode 3 S >
+// boundary plus the first `need` tied pixels in row-major order (their indices sorted here).
+constexpr int FXT = 1024;
+
+__global__ void __launch_bounds__(FXT) k_thr_fixup(const Geom g, MaskBuffers b) {
+    extern __shared__ unsigned int tie_idx[];  // kSelCap
+    __shared__ unsigned int n_tie;
+    const int p = blockIdx.x;
+    const PairInfo I = b.info[p];
+    if (!I.bits_ready) return;
+    if (threadIdx.x == 0) n_tie = 0;
+    __syncthreads();
+    const unsigned int n = I.n_cand;
+    const unsigned long long* keys = b.cand + (size_t)p * kMaxQueries * kSelCap;
+    const unsigned int* idx = b.cand_idx + (size_t)p * kSelCap;
+    uint32_t* bits = b.bits_thr + (size_t)p * g.H * g.WW;
+    const unsigned long long kb = dkey(I.boundary);
+    for (unsigned int i = threadIdx.x; i < n; i += FXT) {
+        const unsigned long long k = keys[i];
+        bool on;
+        if (I.thr_mode == 0) on = k >= kb;
+        else if (I.thr_mode == 2) on = k > 0ull;
+        else {
+            on = k > kb;
+            if (k == kb) tie_idx[atomicAdd(&n_tie, 1u)] = idx[i];
+        }
+        if (on) atomicOr(bits + (idx[i] >> 5), 1u << (idx[i] & 31));
+    }
+    if (I.thr_mode != 3) return;
+    __syncthreads();
+    const unsigned int nt = n_tie;
+    int np2 = 1;
+    while (np2 < (int)nt) np2 <<= 1;
+    for (int i = nt + threadIdx.x; i < np2; i += FXT) tie_idx[i] = 0xffffffffu;
+    __syncthreads();
+    for (int k2 = 2; k2 <= np2; k2 <<= 1)
+        for (int j = k2 >> 1; j > 0; j >>= 1) {
+            for (int i = threadIdx.x; i < np2; i += FXT) {
+                const int ixj = i ^ j;
+                if (ixj > i) {
+                    const bool up = (i & k2) == 0;
+                    const unsigned int a = tie_idx[i], c = tie_idx[ixj];
+                    if ((a > c) == up) {
+                        tie_idx[i] = c;
+                        tie_idx[ixj] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    for (unsigned int i = threadIdx.x; i < nt && i < I.need; i += FXT)
+        atomicOr(bits + (tie_idx[i] >> 5), 1u << (tie_idx[i] & 31));
 }
 
 // ------------------------------------------------------------------ morphology
@@ -1195,6 +1284,8 @@ void set_scan_smem() {
         FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(4)));
         FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(1)));
         FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+        FROI_CUDA(cudaFuncSetAttribute(k_thr_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)(sizeof(unsigned int) * kSelCap)));
         done = true;
     }
 }
@@ -1236,15 +1327,22 @@ void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n
     k_sel_init_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, target, from_stats ? 1 : 0);
     FROI_LAUNCH_CHECK();
     ++*launches;
+    // threshold words fused into the collect pass when rows are whole 32-bit words
+    const int bits = g.W % 32 == 0 ? 1 : 0;
     for (int it = 0; it < kSelPasses + 1; ++it) {
-        k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, pass_smem(1), s>>>(g, P, b, map);
-        k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1);
+        k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, pass_smem(1), s>>>(g, P, b, map, bits);
+        k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1, bits);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }
     k_sel_finish_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n);
     FROI_LAUNCH_CHECK();
     ++*launches;
+    if (bits) {
+        k_thr_fixup<<<n_pairs, FXT, sizeof(unsigned int) * kSelCap, s>>>(g, b);
+        FROI_LAUNCH_CHECK();
+        ++*launches;
+    }
 }
 
 template <class Src>

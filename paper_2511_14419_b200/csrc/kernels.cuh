@@ -57,6 +57,10 @@ struct PairInfo {
     unsigned int mask_count;
     unsigned int components;
     unsigned int pad1;
+    // threshold words already written by phase B's collect pass (all pixels outside the boundary
+    // bin); the bin's n_cand candidates are settled by k_thr_fixup
+    int bits_ready;
+    unsigned int n_cand;
 };
 
 struct SelState {
@@ -143,6 +147,7 @@ struct MaskBuffers {
     unsigned int* hist;           // [pair][kMaxQueries][kHistBins]
     unsigned long long* cand;     // [pair][kMaxQueries][kSelCap]
     unsigned int* cand_count;     // [pair][kMaxQueries]
+    unsigned int* cand_idx;       // [pair][kSelCap] pixel index of each phase-B candidate
     float* fm;                    // [pair][H*W] |flow| (FlowField::mag)
     double* gr;                   // [pair][H*W] |grad I|
     unsigned long long* tie_cnt;  // [pair][chunks][2]

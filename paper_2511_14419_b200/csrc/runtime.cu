@@ -250,6 +250,7 @@ struct froi_ctx {
     unsigned int* d_hist = nullptr;
     unsigned long long* d_cand = nullptr;
     unsigned int* d_cand_count = nullptr;
+    unsigned int* d_cand_idx = nullptr;
     float* d_fm = nullptr;
     double* d_gr = nullptr;
     unsigned long long* d_tie = nullptr;
@@ -306,6 +307,7 @@ struct froi_ctx {
         b.hist = d_hist;
         b.cand = d_cand;
         b.cand_count = d_cand_count;
+        b.cand_idx = d_cand_idx;
         b.fm = d_fm;
         b.gr = d_gr;
         b.tie_cnt = d_tie;
@@ -404,6 +406,7 @@ void ctx_alloc(froi_ctx* c) {
     FROI_CUDA(cudaMemset(c->d_hist, 0, sizeof(unsigned int) * (size_t)kMaxQueries * kHistBins * P));
     c->d_cand = dalloc<unsigned long long>((size_t)kMaxQueries * kSelCap * P, &t);
     c->d_cand_count = dalloc<unsigned int>((size_t)kMaxQueries * P, &t);
+    c->d_cand_idx = dalloc<unsigned int>((size_t)kSelCap * P, &t);
     FROI_CUDA(cudaMemset(c->d_cand_count, 0, sizeof(unsigned int) * (size_t)kMaxQueries * P));
     c->d_fm = dalloc<float>(px * P, &t);
     c->d_gr = dalloc<double>(px * P, &t);
@@ -450,7 +453,7 @@ void ctx_free(froi_ctx* c) {
     void* ptrs[] = {c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
-                    c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
+                    c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_cand_idx, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
                     c->d_bits_clean, c->d_bits_keep, c->d_run_x0, c->d_run_x1, c->d_run_n, c->d_run_par, c->d_run_area,
                     c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry, c->d_arena};
     for (void* p : ptrs)

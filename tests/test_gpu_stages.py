@@ -210,6 +210,13 @@ def test_threshold_bit_exact(gpu, oracle):
         # fewer positive values than the target: keep the positive ones
         sparse = np.where(r > 0.9, r, 0.0)
         assert np.array_equal(gpu.threshold_mask(sparse, 0.5), oracle.threshold_mask(sparse, 0.5))
+    # widths that are whole 32-bit words take the fused path (threshold words written by the
+    # collect pass, boundary-bin candidates settled afterwards): plain, heavy ties, sparse
+    for shape in ((96, 128), (256, 256)):
+        r = gen.random(shape)
+        for t in (0.05, 0.2, 0.5):
+            for m in (r, np.floor(r * 7) / 7, np.floor(r * 300) / 300, np.where(r > 0.9, r, 0.0)):
+                assert np.array_equal(gpu.threshold_mask(m, t), oracle.threshold_mask(m, t)), (shape, t)
 
 
 @pytest.mark.parametrize("ro,rc,min_area", [(1, 1, 20), (0, 0, 20), (1, 2, 12), (2, 3, 0), (1, 1, 1)])
