@@ -1195,23 +1195,35 @@ __device__ __forceinline__ bool bit_at(const uint32_t* m, int WW, int x, int y) 
 
 // Area filter result (keep mask or the cleaned mask) + unshift_mask + PBM packing + pixel count.
 // One thread per PBM byte.
+// 8 source bits at columns sx0 .. sx0+7 of one packed row (0 outside [0, W)), bit k = column sx0+k
+__device__ __forceinline__ unsigned int src_bits8(const uint32_t* row, int WW, int W, int sx0) {
+    const int wi = sx0 >> 5, sh = sx0 & 31;  // floor division also for negative sx0
+    const uint32_t lo = (wi >= 0 && wi < WW) ? row[wi] : 0u;
+    const uint32_t hi = (wi + 1 >= 0 && wi + 1 < WW) ? row[wi + 1] : 0u;
+    unsigned int v = (unsigned int)(((((unsigned long long)hi) << 32) | lo) >> sh) & 0xffu;
+    const int valid = W - sx0;  // columns >= W are outside
+    if (valid < 8) v &= valid <= 0 ? 0u : ((1u << valid) - 1u);
+    return v;
+}
+
+// unshift_mask (registration.hpp:111-121) fused with the PBM packing: output byte (y, x0..x0+7)
+// takes source columns x0-dx .. x0-dx+7 of source row y-dy (zero outside), MSB first.
 __global__ void __launch_bounds__(256) k_output(Geom g, DevParams P, MaskBuffers b, int use_ccl) {
     const int p = blockIdx.y;
     const PairInfo I = b.info[p];
-    const long long nbytes = (long long)g.H * g.SB;
+    const int nbytes = g.H * g.SB;
     const uint32_t* m = (use_ccl ? b.bits_keep : b.bits_clean) + (size_t)p * g.H * g.WW;
     uint8_t* out = b.out_pbm + (size_t)b.out_index[p] * nbytes;
     unsigned int cnt = 0;
-    for (long long bi = blockIdx.x * 256LL + threadIdx.x; bi < nbytes; bi += (long long)gridDim.x * 256) {
-        const int y = (int)(bi / g.SB), x0 = (int)(bi % g.SB) * 8;
-        unsigned int byte = 0;
+    for (int bi = blockIdx.x * 256 + threadIdx.x; bi < nbytes; bi += gridDim.x * 256) {
+        const int y = bi / g.SB, x0 = (bi - y * g.SB) * 8;
         const int sy = y - I.dy;
+        unsigned int byte = 0;
         if (sy >= 0 && sy < g.H) {
-            for (int k = 0; k < 8; ++k) {
-                const int x = x0 + k, sx = x - I.dx;
-                if (x >= g.W || sx < 0 || sx >= g.W) continue;
-                if (bit_at(m, g.WW, sx, sy)) byte |= 0x80u >> k;
-            }
+            unsigned int v = src_bits8(m + (size_t)sy * g.WW, g.WW, g.W, x0 - I.dx);
+            const int outw = g.W - x0;  // output columns beyond W stay 0
+            if (outw < 8) v &= outw <= 0 ? 0u : ((1u << outw) - 1u);
+            byte = __brev(v) >> 24;  // column x0 -> bit 7
         }
         out[bi] = (uint8_t)byte;
         cnt += __popc(byte);
