@@ -30,25 +30,14 @@ struct FrameSrc {  // normalize_frame(apply_shift(den, s)) at level 0
     const T* f;
     int W, H, dx, dy;
     double inv;        // 1.0 / maxval
-    const float* lut;  // 8-bit frames: the 256 values (float)(v * inv) in shared memory
+    const float* lut;  // 8-bit frames: the 256 values (float)(v * inv), global (L1-resident)
     __device__ __forceinline__ float at(int x, int y) const {
         const int sx = clampi(clampi(x, 0, W - 1) + dx, 0, W - 1);
         const int sy = clampi(clampi(y, 0, H - 1) + dy, 0, H - 1);
         const int v = f[sy * W + sx];
-        return sizeof(T) == 1 ? lut[v] : (float)((double)v * inv);
+        return sizeof(T) == 1 ? __ldg(lut + v) : (float)((double)v * inv);
     }
 };
-
-// shared-memory table of normalize_frame's (float)(v / maxval) for 8-bit frames; callers
-// synchronise before the first use (the tile loaders below start with a barrier-free fill, then
-// every path reaches a __syncthreads() before reading the input tile)
-template <typename T>
-__device__ __forceinline__ const float* frame_lut(float* lut, double inv) {
-    if (sizeof(T) != 1) return nullptr;
-    for (int v = threadIdx.x; v < 256; v += blockDim.x) lut[v] = (float)((double)v * inv);
-    __syncthreads();
-    return lut;
-}
 
 struct ImageSrc {
     const float* f;
@@ -208,10 +197,9 @@ template <typename T, int RC>
 __global__ void __launch_bounds__(PNT) k_polyexp_frame(Geom g, DevParams P, const T* den,
                                                        float4* exA, float* exB) {
     extern __shared__ float smem_f[];
-    __shared__ float lut[256];
     const int slot = blockIdx.z;
     const double inv = 1.0 / g.maxval;
-    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, frame_lut<T>(lut, inv)};
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, P.norm_lut};
     polyexp_tile<FrameSrc<T>, false, RC>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)slot * g.lsum,
                                          exB + (size_t)slot * g.lsum, nullptr, smem_f);
 }
@@ -222,12 +210,11 @@ __global__ void __launch_bounds__(PNT) k_polyexp_shifted(Geom g, DevParams P, co
                                                          const int* next, const PairInfo* info,
                                                          float4* exA, float* exB) {
     extern __shared__ float smem_f[];
-    __shared__ float lut[256];
     const int p = blockIdx.z;
     const PairInfo I = info[p];
     if (!I.shifted) return;
     const double inv = 1.0 / g.maxval;
-    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, frame_lut<T>(lut, inv)};
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, P.norm_lut};
     polyexp_tile<FrameSrc<T>, false, RC>(src, g.W, g.H, P.poly_radius, P, exA + (size_t)p * g.lsum,
                                          exB + (size_t)p * g.lsum, nullptr, smem_f);
 }
@@ -408,9 +395,8 @@ __global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T
                                                     int rwmax, int rhmax) {
     extern __shared__ float smem_f[];
     const int slot = blockIdx.z;
-    __shared__ float lut[256];
     const double inv = 1.0 / g.maxval;
-    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, frame_lut<T>(lut, inv)};
+    FrameSrc<T> src{den + (size_t)slot * g.W * g.H, g.W, g.H, 0, 0, inv, P.norm_lut};
     float* dst = pyr + (size_t)slot * (g.lsum - g.loff[1]);
     if (HALF) pyr2_tile(src, g.lw[1], g.lh[1], P.blur, dst, smem_f);
     else pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, dst, smem_f, rwmax, rhmax);
@@ -424,9 +410,8 @@ __global__ void __launch_bounds__(QNT) k_pyr0_shifted(Geom g, DevParams P, const
     const int p = blockIdx.z;
     const PairInfo I = info[p];
     if (!I.shifted) return;
-    __shared__ float lut[256];
     const double inv = 1.0 / g.maxval;
-    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, frame_lut<T>(lut, inv)};
+    FrameSrc<T> src{den + (size_t)next[p] * g.W * g.H, g.W, g.H, I.dx, I.dy, inv, P.norm_lut};
     float* dst = pyr + (size_t)p * (g.lsum - g.loff[1]);
     if (HALF) pyr2_tile(src, g.lw[1], g.lh[1], P.blur, dst, smem_f);
     else pyr_tile(src, g.W, g.H, g.lw[1], g.lh[1], P.blur, dst, smem_f, rwmax, rhmax);

@@ -1228,8 +1228,16 @@ __global__ void __launch_bounds__(256) k_output(Geom g, DevParams P, MaskBuffers
         out[bi] = (uint8_t)byte;
         cnt += __popc(byte);
     }
+    // one atomic per CTA (per-warp atomics on one counter per pair serialise)
+    __shared__ unsigned int wsum[8];
     for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-    if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&b.info[p].mask_count, cnt);
+    if ((threadIdx.x & 31) == 0) wsum[threadIdx.x >> 5] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int t = 0;
+        for (int k = 0; k < 8; ++k) t += wsum[k];
+        if (t) atomicAdd(&b.info[p].mask_count, t);
+    }
 }
 
 __global__ void k_reset_counts(MaskBuffers b) {
@@ -1390,7 +1398,7 @@ void run_cleanup_output(const Geom& g, const DevParams& P, const MaskBuffers& b,
         FROI_LAUNCH_CHECK();
         *launches += 4;
     }
-    k_output<<<dim3(grid_for((long long)g.H * g.SB, 256), n_pairs), 256, 0, s>>>(g, Q, b, use_ccl ? 1 : 0);
+    k_output<<<dim3(grid_for((long long)g.H * g.SB, 4096), n_pairs), 256, 0, s>>>(g, Q, b, use_ccl ? 1 : 0);
     FROI_LAUNCH_CHECK();
     ++*launches;
 }

@@ -98,6 +98,8 @@ struct DevParams {
     // roi
     double roi_threshold, flow_weight;
     int min_area, open_radius, close_radius, gradient_source, max_shift;
+    // 8-bit frames: normalize_frame's (float)(v * (1.0/maxval)) for v = 0..255 (device, context)
+    const float* norm_lut;
 };
 
 // ---------------------------------------------------------------- launchers

@@ -227,6 +227,7 @@ struct froi_ctx {
     size_t device_bytes = 0;
     // constants
     double *d_spatial = nullptr, *d_lut = nullptr, *d_wx = nullptr, *d_wy = nullptr;
+    float* d_norm_lut = nullptr;
     std::vector<double> h_spatial;
     double2 *d_tw_row = nullptr, *d_tw_col = nullptr, *d_itw_row = nullptr, *d_itw_col = nullptr;
     // frame slots
@@ -365,6 +366,14 @@ void ctx_alloc(froi_ctx* c) {
         for (int x = 0; x < g.pw; ++x) wx[x] = 0.5 - 0.5 * std::cos(2.0 * kPi * x / g.pw);
         for (int y = 0; y < g.ph; ++y) wy[y] = 0.5 - 0.5 * std::cos(2.0 * kPi * y / g.ph);
         c->h_spatial = spatial;
+        {
+            std::vector<float> nl(256, 0.f);
+            const double inv = 1.0 / g.maxval;
+            for (int v = 0; v < 256 && v <= g.maxval; ++v) nl[v] = (float)((double)v * inv);
+            c->d_norm_lut = dalloc<float>(256, &t);
+            FROI_CUDA(cudaMemcpy(c->d_norm_lut, nl.data(), 256 * sizeof(float), cudaMemcpyHostToDevice));
+            c->dp.norm_lut = c->d_norm_lut;
+        }
         c->d_spatial = dalloc<double>(spatial.size(), &t);
         c->d_lut = dalloc<double>(lut.size(), &t);
         c->d_wx = dalloc<double>(wx.size(), &t);
@@ -450,7 +459,7 @@ void ctx_free(froi_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    void* ptrs[] = {c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
+    void* ptrs[] = {c->d_norm_lut, c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_cand_idx, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
@@ -935,6 +944,7 @@ int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p) {
                        "create a new context");
     ctx->params = *p;
     ctx->dp = make_dev_params(*p);
+    ctx->dp.norm_lut = ctx->d_norm_lut;
     return 0;
 }
 
