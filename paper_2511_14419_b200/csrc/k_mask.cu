@@ -302,7 +302,11 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                     const bool m = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
                     const unsigned int bin = fp[q] ? (unsigned int)fpw_bin(k[q][e], fp[q])
                                                    : (unsigned int)((k[q][e] >> sh[q]) & ((1u << wd[q]) - 1u));
-                    hist_add(hist[q], m, bin, lane);
+                    if (fp[q]) {  // exponent-window bins are spread out: plain shared atomics
+                        if (m) atomicAdd(&hist[q][bin], 1u);
+                    } else {
+                        hist_add(hist[q], m, bin, lane);
+                    }
                     if (m) {
                         lmn[q] = min(lmn[q], k[q][e]);
                         lmx[q] = max(lmx[q], k[q][e]);
@@ -480,8 +484,10 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                     mng = min(mng, kg);
                     mxg = max(mxg, kg);
                 }
-                hist_add(hist[0], v, (unsigned int)fpw_bin(kf, 2), lane);
-                hist_add(hist[1], v, (unsigned int)fpw_bin(kg, 1), lane);
+                if (v) {  // exponent-window bins are spread out: plain shared atomics
+                    atomicAdd(&hist[0][fpw_bin(kf, 2)], 1u);
+                    atomicAdd(&hist[1][fpw_bin(kg, 1)], 1u);
+                }
             }
         }
     }
