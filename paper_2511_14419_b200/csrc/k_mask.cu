@@ -432,7 +432,9 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     const int rows = (H + gridDim.x - 1) / gridDim.x;
     const int y0 = blockIdx.x * rows, y1 = min(H, y0 + rows);
     const int lane = threadIdx.x & 31;
-    unsigned long long mnf = ~0ull, mxf = 0ull, mng = ~0ull, mxg = 0ull;
+    // extremes tracked on the values (the keys are monotone in them), keyed after the loop
+    float mnf = __int_as_float(0x7f800000), mxf = 0.f;
+    double mng = __longlong_as_double(0x7ff0000000000000ll), mxg = 0.0;
     // NPX pixels per thread per step: all their loads (flow, the four gradient neighbours) are
     // issued before any of their arithmetic, so each thread keeps ~NPX*5 loads in flight
     constexpr int NPX = 4;
@@ -479,10 +481,10 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                     gr[row + x] = gg;
                     kf = fkey(f);
                     kg = dkey(gg);
-                    mnf = min(mnf, kf);
-                    mxf = max(mxf, kf);
-                    mng = min(mng, kg);
-                    mxg = max(mxg, kg);
+                    mnf = fminf(mnf, f);
+                    mxf = fmaxf(mxf, f);
+                    mng = gg < mng ? gg : mng;
+                    mxg = gg > mxg ? gg : mxg;
                 }
                 if (v) {  // exponent-window bins are spread out: plain shared atomics
                     atomicAdd(&hist[0][fpw_bin(kf, 2)], 1u);
@@ -491,17 +493,20 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
             }
         }
     }
+    unsigned long long kmnf = mnf == __int_as_float(0x7f800000) ? ~0ull : fkey(mnf), kmxf = fkey(mxf);
+    unsigned long long kmng = mng == __longlong_as_double(0x7ff0000000000000ll) ? ~0ull : dkey(mng);
+    unsigned long long kmxg = dkey(mxg);
     for (int o = 16; o > 0; o >>= 1) {
-        mnf = min(mnf, __shfl_xor_sync(0xffffffffu, mnf, o));
-        mxf = max(mxf, __shfl_xor_sync(0xffffffffu, mxf, o));
-        mng = min(mng, __shfl_xor_sync(0xffffffffu, mng, o));
-        mxg = max(mxg, __shfl_xor_sync(0xffffffffu, mxg, o));
+        kmnf = min(kmnf, __shfl_xor_sync(0xffffffffu, kmnf, o));
+        kmxf = max(kmxf, __shfl_xor_sync(0xffffffffu, kmxf, o));
+        kmng = min(kmng, __shfl_xor_sync(0xffffffffu, kmng, o));
+        kmxg = max(kmxg, __shfl_xor_sync(0xffffffffu, kmxg, o));
     }
     if (lane == 0) {
-        atomicMin(&smn[0], mnf);
-        atomicMax(&smx[0], mxf);
-        atomicMin(&smn[1], mng);
-        atomicMax(&smx[1], mxg);
+        atomicMin(&smn[0], kmnf);
+        atomicMax(&smx[0], kmxf);
+        atomicMin(&smn[1], kmng);
+        atomicMax(&smx[1], kmxg);
     }
     __syncthreads();
     unsigned int* gh = b.hist + (size_t)p * kMaxQueries * kHistBins;
