@@ -119,13 +119,32 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
     const T* f = den + (size_t)slot * W * H;
     // windowed_spectrum_input (registration.hpp:26-42): exact integer sum, then one division
     const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
-    for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
-        const int r = e & (R - 1), x = e >> lc;
+    if (sizeof(T) == 1 && W == pw && H == ph && (W & 15) == 0 && (R << log2pw) == 16 * NT) {
+        // 8-bit frames without padding: each thread reads 16 consecutive samples of one row with
+        // one 128-bit load, then converts and scatters them to their bit-reversed slots
+        const int r = threadIdx.x / (pw / 16), x0 = (threadIdx.x % (pw / 16)) * 16;
         const int y = y0 + r;
-        if (y >= ph) continue;
-        const int sy = min(y, H - 1), sx = min(x, W - 1);
-        const double v = dmul(dmul(dsub((double)f[(size_t)sy * W + sx], mean), wx[x]), wy[y]);
-        a[(pd(brev(x, log2pw)) << lc) | r] = make_double2(v, 0.0);
+        if (y < ph) {
+            const uint4 raw = __ldg((const uint4*)(f + (size_t)y * W + x0));
+            const double wyv = __ldg(wy + y);
+            const unsigned int wds[4] = {raw.x, raw.y, raw.z, raw.w};
+#pragma unroll
+            for (int k = 0; k < 16; ++k) {
+                const int x = x0 + k;
+                const double sv = (double)((wds[k >> 2] >> (8 * (k & 3))) & 0xffu);
+                const double val = dmul(dmul(dsub(sv, mean), __ldg(wx + x)), wyv);
+                a[(pd(brev(x, log2pw)) << lc) | r] = make_double2(val, 0.0);
+            }
+        }
+    } else {
+        for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
+            const int r = e & (R - 1), x = e >> lc;
+            const int y = y0 + r;
+            if (y >= ph) continue;
+            const int sy = min(y, H - 1), sx = min(x, W - 1);
+            const double v = dmul(dmul(dsub((double)f[(size_t)sy * W + sx], mean), wx[x]), wy[y]);
+            a[(pd(brev(x, log2pw)) << lc) | r] = make_double2(v, 0.0);
+        }
     }
     __syncthreads();
     fft_stages<kQRows>(a, pw, log2pw, lc, tw);
