@@ -16,6 +16,9 @@
 #include "flowroi/roi.hpp"
 #include "flowroi/synthetic.hpp"
 #include "froi/flowroi_gpu.hpp"
+#ifdef FROI_HAVE_JSON
+#include "froi/flowroi_gpu_pipeline.hpp"
+#endif
 
 using namespace flowroi;
 
@@ -57,8 +60,49 @@ static int run_case(const char* name, int cells, int frames, int size, int depth
     return (shifts_equal == seq.size() && double(mism) / double(total) <= 1e-4) ? 0 : 1;
 }
 
+#ifdef FROI_HAVE_JSON
+// compress_sequence (pipeline.hpp:137-153) with the CPU stage vs the pipelined GPU stage: one
+// .froi file per frame, identical wherever the masks are identical; shifts identical.
+static int run_pipeline_case(const char* name, int cells, int frames, int size, std::uint64_t seed,
+                             int adjacent, int chunk) {
+    SyntheticSpec spec;
+    spec.n_cells = cells;
+    spec.n_frames = frames;
+    spec.width = spec.height = size;
+    spec.seed = seed;
+    auto [seq, truth] = generate_synthetic(spec);
+    PipelineConfig cfg;
+    cfg.workers = 4;
+    cfg.roi.adjacent_factor = adjacent;
+    const CompressResult cpu = compress_sequence(seq, cfg);
+    const CompressResult gpu = flowroi_gpu::compress_sequence(seq, cfg, chunk);
+    std::size_t frames_equal = 0, files_equal = 0, shifts_equal = 0, mism = 0, total = 0;
+    for (std::size_t t = 0; t < seq.size(); ++t) {
+        std::size_t m = 0;
+        for (std::size_t i = 0; i < cpu.masks[t].size(); ++i) m += cpu.masks[t].bits[i] != gpu.masks[t].bits[i];
+        mism += m;
+        total += cpu.masks[t].size();
+        frames_equal += m == 0;
+        files_equal += cpu.files[t] == gpu.files[t];
+        shifts_equal += cpu.info.shifts[t].dx == gpu.info.shifts[t].dx &&
+                        cpu.info.shifts[t].dy == gpu.info.shifts[t].dy &&
+                        cpu.info.shifts[t].confidence == gpu.info.shifts[t].confidence;
+    }
+    std::printf("{\"pipeline_case\": \"%s\", \"frames\": %zu, \"chunk\": %d, \"mask_mismatch\": %.3e, "
+                "\"frames_identical\": %zu, \"files_identical\": %zu, \"shifts_identical\": %zu, "
+                "\"gpu_wall_s\": %.3f, \"cpu_wall_s\": %.3f, \"gpu_encode_ns\": %llu}\n",
+                name, seq.size(), chunk, double(mism) / double(total), frames_equal, files_equal, shifts_equal,
+                gpu.wall_seconds, cpu.wall_seconds, (unsigned long long)gpu.stages.encode_ns);
+    return (shifts_equal == seq.size() && files_equal >= frames_equal && double(mism) / double(total) <= 1e-4) ? 0 : 1;
+}
+#endif
+
 int main() {
     int bad = 0;
+#ifdef FROI_HAVE_JSON
+    bad += run_pipeline_case("pipeline-160-chunk4", 5, 11, 160, 31, 0, 4);
+    bad += run_pipeline_case("pipeline-128-ensemble", 4, 6, 128, 32, 1, 4);
+#endif
     ExtractParams p;
     bad += run_case("synthetic-160", 5, 6, 160, 8, 77, p);
     bad += run_case("synthetic-256-16bit", 8, 4, 256, 16, 12, p);

@@ -28,3 +28,8 @@ def test_dropin_against_reference_and_encoder():
         # wherever the masks agree, the reference encoder produces identical files
         assert c["encoded_identical"] >= c["frames_identical"]
     assert lines[-1]["errors_mapped"] == 2
+    # compress_sequence with the pipelined GPU stage, when built with json
+    for c in [c for c in lines if "pipeline_case" in c]:
+        assert c["shifts_identical"] == c["frames"]
+        assert c["mask_mismatch"] <= 1e-4
+        assert c["files_identical"] >= c["frames_identical"]
