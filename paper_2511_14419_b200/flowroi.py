@@ -467,3 +467,75 @@ def mask_from_flow(u: np.ndarray, v: np.ndarray, raw: np.ndarray, dx: int = 0, d
                                                       ctypes.byref(st)), "mask_from_flow")
     return mask, dict(mask_count=st.mask_count, components=st.components,
                       raw_fraction=st.raw_fraction)
+
+
+# ---------------------------------------------------------------- wire formats and the report
+def save_flo(path: str, u: np.ndarray, v: np.ndarray) -> None:
+    """FLO1 flow dump (``save_flo``, flow.hpp:347-366): b"FLO1", u32 LE width and height, then
+    row-major (u, v) pairs as f32 LE."""
+    u32 = np.ascontiguousarray(u, dtype="<f4")
+    v32 = np.ascontiguousarray(v, dtype="<f4")
+    if u32.shape != v32.shape or u32.ndim != 2:
+        raise DataError("save_flo: u and v must be 2-D arrays of one shape")
+    h, w = u32.shape
+    inter = np.empty((h, w, 2), "<f4")
+    inter[..., 0] = u32
+    inter[..., 1] = v32
+    try:
+        with open(path, "wb") as f:
+            f.write(b"FLO1" + np.array([w, h], "<u4").tobytes() + inter.tobytes())
+    except OSError as e:
+        raise DataError(f"cannot write {path}: {e}") from e
+
+
+def load_flo(path: str) -> tuple[np.ndarray, np.ndarray]:
+    """Reads a FLO1 file (``load_flo``, flow.hpp:368-389) -> (u, v) float32 arrays."""
+    try:
+        data = open(path, "rb").read()
+    except OSError as e:
+        raise DataError(f"cannot open {path}") from e
+    if data[:4] != b"FLO1":
+        raise DataError(f"{path}: not a FLO1 file")
+    if len(data) < 12:
+        raise DataError(f"{path}: bad FLO1 header")
+    w, h = (int(x) for x in np.frombuffer(data[4:12], "<u4"))
+    if w <= 0 or h <= 0:
+        raise DataError(f"{path}: bad FLO1 header")
+    if len(data) < 12 + 8 * w * h:
+        raise DataError(f"{path}: truncated FLO1 data")
+    inter = np.frombuffer(data[12:12 + 8 * w * h], "<f4").reshape(h, w, 2)
+    return inter[..., 0].copy(), inter[..., 1].copy()
+
+
+def save_pbm(path: str, mask: np.ndarray, width: int | None = None) -> None:
+    """P4 mask file (``save_pbm``, pgm.hpp:127-138): b"P4\\n<w> <h>\\n" + rows packed MSB first,
+    padded to whole bytes.  `mask` is [h, w] 0/1 bytes, or [h, ceil(w/8)] PBM rows (the
+    FROI_MASK_PBM layout the GPU writes) together with `width`."""
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    if width is None:
+        h, w = m.shape
+        rows = np.packbits(m != 0, axis=1)
+    else:
+        h, w = m.shape[0], int(width)
+        if m.shape[1] != (w + 7) // 8:
+            raise DataError("save_pbm: PBM rows do not match the width")
+        rows = m
+    try:
+        with open(path, "wb") as f:
+            f.write(f"P4\n{w} {h}\n".encode() + rows.tobytes())
+    except OSError as e:
+        raise DataError(f"cannot write {path}: {e}") from e
+
+
+def extract_report_frames(masks: np.ndarray, info: ExtractInfo) -> list[dict]:
+    """The per-frame rows of the extract-roi report (tools/flowroi.cpp:186-196): mask fraction,
+    8-connected component count of the final mask (``label_components``, on the GPU) and the
+    registration shift."""
+    m = np.asarray(masks)
+    rows = []
+    for i in range(m.shape[0]):
+        s = info.shifts[i]
+        rows.append({"index": i, "mask_fraction": float((m[i] != 0).mean()),
+                     "components": int(component_areas(m[i]).size),
+                     "shift": {"dx": int(s.dx), "dy": int(s.dy), "confidence": float(s.confidence)}})
+    return rows

@@ -192,3 +192,20 @@ def test_pinned_pbm_streamed_back_identical(gpu):
     stats = (CFrameStats * (2 * n))()
     ctx.extract_wells_into(wells, pinned.numpy(), stats)
     assert np.array_equal(pinned.numpy(), want)
+
+
+def test_extract_report_frames(gpu, oracle):
+    """Per-frame rows of the extract-roi report (tools/flowroi.cpp:186-196): components of each
+    final mask by the GPU labeller equal the restated label_components; fractions and shifts come
+    straight from the stage."""
+    from paper_2511_14419_b200 import flowroi
+    from paper_2511_14419_b200.params import ExtractInfo, ExtractParams
+    frames = np.stack([cyclic_shift(textured_frame(96, 96, 8, 321), t, t % 2) for t in range(5)]).astype(np.uint8)
+    info = ExtractInfo()
+    masks = flowroi.extract_roi(frames, ExtractParams(), info=info)
+    rows = flowroi.extract_report_frames(masks, info)
+    assert [r["index"] for r in rows] == list(range(5))
+    for r, m in zip(rows, masks):
+        assert r["components"] == oracle.component_areas(m).size
+        assert r["mask_fraction"] == float(m.mean())
+    assert [(r["shift"]["dx"], r["shift"]["dy"]) for r in rows] == [(s.dx, s.dy) for s in info.shifts]
