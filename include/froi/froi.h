@@ -211,6 +211,19 @@ int froi_morph_cleanup(froi_ctx* ctx, uint8_t* mask, int open_radius, int close_
                        int min_area);
 /* label_components (roi.hpp:184-234): component areas (any order) of a W*H mask.
  * areas_out may be NULL to query the count; *n_components receives the count. */
+/* ---- codec side on the GPU ----
+ * Reversible 5/3 DWT of one frame of the context geometry (dwt_forward / dwt_inverse,
+ * dwt.hpp:113-171): DC-shifted int32 coefficients in the canonical in-place layout, bit-identical.
+ * levels < 1 -> usage error; frame smaller than 2^levels -> data error. */
+int froi_dwt_forward(froi_ctx* ctx, const uint16_t* frame, int levels, int32_t* coeffs);
+int froi_dwt_inverse(froi_ctx* ctx, const int32_t* coeffs, int levels, uint16_t* frame);
+/* n device frames (context sample type, packed) -> n device coefficient grids. */
+int froi_dwt_forward_device(froi_ctx* ctx, const void* d_frames, int n, int levels, int32_t* d_coeffs);
+/* RoI coefficient masks (map_mask_to_subbands, codec.hpp:152-171): level 1..levels masks of
+ * ceil-halved extents, concatenated; *out_len receives their total size. */
+int froi_map_mask_to_subbands(froi_ctx* ctx, const uint8_t* mask, int levels, uint8_t* out,
+                              size_t cap, size_t* out_len);
+
 int froi_component_areas(froi_ctx* ctx, const uint8_t* mask, uint32_t* areas_out,
                          size_t areas_capacity, size_t* n_components);
 /* Mask stage of one pair from a given flow (roi.hpp:340-345): saliency against

@@ -1110,3 +1110,125 @@ double oracle_hypot_restated(double x, double y) {
     hh -= (t1 + t2) / (2.0 * hh);
     return hh;
 }
+
+
+/* ======================================================================== 5/3 DWT (codec side) */
+/* lift_53_forward / lift_53_inverse (dwt.hpp:36-63): whole-sample symmetric extension; >> on
+ * negative int32 is the arithmetic (floor) shift the reference relies on (C++20). */
+static int dwt_r(int i, int n) { return i + 1 < n ? i + 1 : n - 2; }
+static int dwt_l(int i) { return i > 0 ? i - 1 : 1; }
+
+static void lift53(int32_t* x, int n, int inverse) {
+    if (n < 2) return;
+    if (!inverse) {
+        for (int i = 1; i < n; i += 2) x[i] -= (x[i - 1] + x[dwt_r(i, n)]) >> 1;
+        for (int i = 0; i < n; i += 2) x[i] += (x[dwt_l(i)] + x[dwt_r(i, n)] + 2) >> 2;
+    } else {
+        for (int i = 0; i < n; i += 2) x[i] -= (x[dwt_l(i)] + x[dwt_r(i, n)] + 2) >> 2;
+        for (int i = 1; i < n; i += 2) x[i] += (x[i - 1] + x[dwt_r(i, n)]) >> 1;
+    }
+}
+
+/* evens to the front half (ceil), odds behind (dwt.hpp:65-83), or back */
+static void dwt_shuffle(const int32_t* x, int n, int32_t* out, int interleave) {
+    const int half = (n + 1) / 2;
+    for (int i = 0; i < n; ++i) {
+        const int j = (i % 2 == 0) ? i / 2 : half + i / 2;
+        if (interleave) out[i] = x[j];
+        else out[j] = x[i];
+    }
+}
+
+static int dwt_extent(int n, int level) {
+    for (int l = 0; l < level; ++l) n = (n + 1) / 2;
+    return n;
+}
+
+int oracle_dwt_forward(const uint16_t* frame, int w, int h, int depth, int levels, int32_t* g) {
+    if (levels < 1) return 1;
+    if (w < (1 << levels) || h < (1 << levels)) return 2;
+    const int32_t dc = 1 << (depth - 1);
+    for (size_t i = 0; i < (size_t)w * h; ++i) g[i] = (int32_t)frame[i] - dc;
+    const int nmax = w > h ? w : h;
+    int32_t* line = (int32_t*)malloc(sizeof(int32_t) * nmax);
+    int32_t* scr = (int32_t*)malloc(sizeof(int32_t) * nmax);
+    for (int l = 0; l < levels; ++l) {
+        const int lw = dwt_extent(w, l), lh = dwt_extent(h, l);
+        for (int y = 0; y < lh; ++y) {
+            memcpy(line, g + (size_t)y * w, sizeof(int32_t) * lw);
+            lift53(line, lw, 0);
+            dwt_shuffle(line, lw, scr, 0);
+            memcpy(g + (size_t)y * w, scr, sizeof(int32_t) * lw);
+        }
+        for (int x = 0; x < lw; ++x) {
+            for (int y = 0; y < lh; ++y) line[y] = g[(size_t)y * w + x];
+            lift53(line, lh, 0);
+            dwt_shuffle(line, lh, scr, 0);
+            for (int y = 0; y < lh; ++y) g[(size_t)y * w + x] = scr[y];
+        }
+    }
+    free(line);
+    free(scr);
+    return 0;
+}
+
+int oracle_dwt_inverse(const int32_t* coeffs, int w, int h, int depth, int levels, uint16_t* frame) {
+    if (levels < 1) return 1;
+    int32_t* g = (int32_t*)malloc(sizeof(int32_t) * (size_t)w * h);
+    memcpy(g, coeffs, sizeof(int32_t) * (size_t)w * h);
+    const int nmax = w > h ? w : h;
+    int32_t* line = (int32_t*)malloc(sizeof(int32_t) * nmax);
+    int32_t* scr = (int32_t*)malloc(sizeof(int32_t) * nmax);
+    for (int l = levels - 1; l >= 0; --l) {
+        const int lw = dwt_extent(w, l), lh = dwt_extent(h, l);
+        for (int x = 0; x < lw; ++x) {
+            for (int y = 0; y < lh; ++y) line[y] = g[(size_t)y * w + x];
+            dwt_shuffle(line, lh, scr, 1);
+            lift53(scr, lh, 1);
+            for (int y = 0; y < lh; ++y) g[(size_t)y * w + x] = scr[y];
+        }
+        for (int y = 0; y < lh; ++y) {
+            memcpy(line, g + (size_t)y * w, sizeof(int32_t) * lw);
+            dwt_shuffle(line, lw, scr, 1);
+            lift53(scr, lw, 1);
+            memcpy(g + (size_t)y * w, scr, sizeof(int32_t) * lw);
+        }
+    }
+    /* clamp_to_depth(double(c + dc)) (core.hpp): integers clamp to [0, maxval] */
+    const int32_t dc = 1 << (depth - 1), mx = (int32_t)((1u << depth) - 1u);
+    for (size_t i = 0; i < (size_t)w * h; ++i) {
+        const int32_t v = g[i] + dc;
+        frame[i] = (uint16_t)(v < 0 ? 0 : (v > mx ? mx : v));
+    }
+    free(g);
+    free(line);
+    free(scr);
+    return 0;
+}
+
+size_t oracle_map_mask_to_subbands(const uint8_t* mask, int w, int h, int levels, uint8_t* out) {
+    int any = 0;
+    for (size_t i = 0; i < (size_t)w * h && !any; ++i) any = mask[i] != 0;
+    const uint8_t* cur = mask;
+    int cw = w, ch = h;
+    size_t off = 0;
+    uint8_t* down = NULL;
+    for (int l = 1; l <= levels; ++l) {
+        const int nw = (cw + 1) / 2, nh = (ch + 1) / 2;
+        free(down);
+        down = (uint8_t*)calloc((size_t)nw * nh, 1);
+        if (any)
+            for (int y = 0; y < ch; ++y)
+                for (int x = 0; x < cw; ++x)
+                    if (cur[(size_t)y * cw + x]) down[(size_t)(y / 2) * nw + x / 2] = 1;
+        uint8_t* lev = out + off;
+        if (any) morph_square(down, nw, nh, 2, 0, lev);
+        else memcpy(lev, down, (size_t)nw * nh);
+        cur = lev;
+        cw = nw;
+        ch = nh;
+        off += (size_t)nw * nh;
+    }
+    free(down);
+    return off;
+}

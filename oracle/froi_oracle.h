@@ -79,6 +79,12 @@ int oracle_mask_from_flow(const float* u, const float* v, const uint16_t* raw_fr
                           oracle_pair_debug* dbg);
 /* extract_roi (roi.hpp:309-364).  frames: n*w*h samples; masks: n*w*h bytes;
  * shifts (nullable): n entries; raw_fractions (nullable): n entries. workers <= 1: serial. */
+/* Reversible 5/3 DWT (dwt.hpp:113-171) in the canonical in-place layout, DC-shifted int32. */
+int oracle_dwt_forward(const uint16_t* frame, int w, int h, int depth, int levels, int32_t* coeffs);
+int oracle_dwt_inverse(const int32_t* coeffs, int w, int h, int depth, int levels, uint16_t* frame);
+/* map_mask_to_subbands (codec.hpp:152-171): level masks concatenated, level 1 first. */
+size_t oracle_map_mask_to_subbands(const uint8_t* mask, int w, int h, int levels, uint8_t* out);
+
 int oracle_extract_roi(const uint16_t* frames, int n, int w, int h, int depth,
                        const froi_params* p, int workers, uint8_t* masks, froi_shift* shifts,
                        double* raw_fractions);

@@ -172,6 +172,46 @@ class Oracle:
         f(_ptr(m), _I(w), _I(h), _I(open_radius), _I(close_radius), _I(min_area))
         return m
 
+    # ---- dwt.hpp / codec.hpp (the codec side)
+    def dwt_forward(self, frame: np.ndarray, depth: int, levels: int) -> np.ndarray:
+        f = np.ascontiguousarray(frame, dtype=np.uint16)
+        h, w = f.shape
+        out = np.empty((h, w), np.int32)
+        rc = self._fn("dwt_forward")(_ptr(f), _I(w), _I(h), _I(depth), _I(levels), _ptr(out))
+        if rc == 1:
+            raise UsageError("dwt: levels must be >= 1")
+        if rc == 2:
+            raise DataError("dwt: frame too small")
+        if rc:
+            raise RuntimeError("dwt_forward failed")
+        return out
+
+    def dwt_inverse(self, coeffs: np.ndarray, depth: int, levels: int) -> np.ndarray:
+        c = np.ascontiguousarray(coeffs, dtype=np.int32)
+        h, w = c.shape
+        out = np.empty((h, w), np.uint16)
+        if self._fn("dwt_inverse")(_ptr(c), _I(w), _I(h), _I(depth), _I(levels), _ptr(out)):
+            raise RuntimeError("dwt_inverse failed")
+        return out
+
+    def map_mask_to_subbands(self, mask: np.ndarray, levels: int) -> list:
+        m = np.ascontiguousarray(mask, dtype=np.uint8)
+        h, w = m.shape
+        dims, cw, ch = [], w, h
+        for _ in range(levels):
+            cw, ch = (cw + 1) // 2, (ch + 1) // 2
+            dims.append((ch, cw))
+        out = np.zeros(sum(a * b for a, b in dims), np.uint8)
+        rt = ctypes.c_size_t if self.kind == "port" else ctypes.c_long
+        n = self._fn("map_mask_to_subbands", rt)(_ptr(m), _I(w), _I(h), _I(levels), _ptr(out))
+        if n != out.size:
+            raise RuntimeError("map_mask_to_subbands failed")
+        res, off = [], 0
+        for a, b in dims:
+            res.append(out[off:off + a * b].reshape(a, b).copy())
+            off += a * b
+        return res
+
     def component_areas(self, mask: np.ndarray) -> np.ndarray:
         m = np.ascontiguousarray(mask, dtype=np.uint8)
         h, w = m.shape

@@ -10,7 +10,9 @@
 #include <exception>
 #include <vector>
 
+#include "flowroi/codec.hpp"
 #include "flowroi/denoise.hpp"
+#include "flowroi/dwt.hpp"
 #include "flowroi/flow.hpp"
 #include "flowroi/registration.hpp"
 #include "flowroi/roi.hpp"
@@ -151,6 +153,55 @@ int ref_morph_cleanup(uint8_t* mask, int w, int h, int ro, int rc, int min_area)
     const RoiMask r = morph_cleanup(m, ro, rc, min_area);
     std::memcpy(mask, r.bits.data(), r.size());
     SHIM_CATCH
+}
+
+// dwt_forward / dwt_inverse (dwt.hpp:113-171), map_mask_to_subbands (codec.hpp:152-171)
+int ref_dwt_forward(const uint16_t* px, int w, int h, int depth, int levels, int32_t* out) {
+    try {
+        Frame f(w, h, depth);
+        std::memcpy(f.pixels.data(), px, sizeof(uint16_t) * f.size());
+        const SubbandGrid g = dwt_forward(f, levels);
+        std::memcpy(out, g.coeffs.data(), sizeof(int32_t) * g.coeffs.size());
+        return 0;
+    } catch (const usage_error&) {
+        return 1;
+    } catch (const data_error&) {
+        return 2;
+    } catch (...) {
+        return 3;
+    }
+}
+
+int ref_dwt_inverse(const int32_t* coeffs, int w, int h, int depth, int levels, uint16_t* out) {
+    try {
+        SubbandGrid g;
+        g.width = w;
+        g.height = h;
+        g.levels = levels;
+        g.depth = depth;
+        g.coeffs.assign(coeffs, coeffs + std::size_t(w) * h);
+        const Frame f = dwt_inverse(g);
+        std::memcpy(out, f.pixels.data(), sizeof(uint16_t) * f.size());
+        return 0;
+    } catch (...) {
+        return 3;
+    }
+}
+
+long ref_map_mask_to_subbands(const uint8_t* mask, int w, int h, int levels, uint8_t* out) {
+    try {
+        RoiMask m(w, h);
+        std::memcpy(m.bits.data(), mask, m.size());
+        const auto lv = map_mask_to_subbands(m, levels);
+        long off = 0;
+        for (const auto& r : lv) {
+            std::memcpy(out + off, r.bits.data(), r.size());
+            off += long(r.size());
+        }
+        return off;
+    } catch (...) {
+        return -1;
+    }
 }
 
 long ref_label_components(const uint8_t* mask, int w, int h, uint32_t* areas, long cap) {

@@ -36,6 +36,11 @@ SIGNATURES = {
     "froi_ctx_kernel_times": (_I, [_P, ctypes.POINTER(CKernelTimes)]),
     "froi_ctx_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "froi_ctx_set_lanes": (_I, [_P, ctypes.c_int]),
+    "froi_dwt_forward": (_I, [_P, _P, ctypes.c_int, _P]),
+    "froi_dwt_inverse": (_I, [_P, _P, ctypes.c_int, _P]),
+    "froi_dwt_forward_device": (_I, [_P, _P, ctypes.c_int, ctypes.c_int, _P]),
+    "froi_map_mask_to_subbands": (_I, [_P, _P, ctypes.c_int, _P, ctypes.c_size_t,
+                                       ctypes.POINTER(ctypes.c_size_t)]),
     "froi_extract_roi": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),
     "froi_extract_wells": (_I, [_P, _P, _I, _SZ, _I, _I, _I, _P, _P]),
     "froi_extract_wells_device": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),

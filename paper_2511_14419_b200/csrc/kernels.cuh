@@ -117,6 +117,14 @@ void launch_register_pairs(const Geom& g, const DevParams& p, const double2* d_s
                            const double2* d_itw_col, double2* d_cols, double* d_surf,
                            PairInfo* d_info, int n_pairs, cudaStream_t s);
 
+// k_dwt.cu (codec side)
+void launch_dwt_forward(const void* d_frames, int sample_bytes, int W, int H, int depth, int n,
+                        int levels, int32_t* d_coeffs, cudaStream_t s);
+void launch_dwt_inverse(int32_t* d_coeffs, int W, int H, int depth, int n, int levels,
+                        uint16_t* d_frames, cudaStream_t s);
+size_t launch_map_mask_to_subbands(const uint8_t* d_mask, int W, int H, int levels, bool any,
+                                   uint8_t* d_out, cudaStream_t s);
+
 // k_flow.cu
 struct FlowBuffers {
     const void* den;     // frame-slot denoised frames (T)

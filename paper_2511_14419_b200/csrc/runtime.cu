@@ -1375,6 +1375,110 @@ int froi_morph_cleanup(froi_ctx* c, uint8_t* mask, int open_radius, int close_ra
     ABI_CATCH
 }
 
+static int dwt_check(froi_ctx* c, int levels) {
+    if (levels < 1) return fail(1, "dwt: levels must be >= 1");
+    if (c->g.W < (1 << levels) || c->g.H < (1 << levels))
+        return fail(2, "dwt: frame too small for " + std::to_string(levels) + " levels");
+    return 0;
+}
+
+int froi_dwt_forward(froi_ctx* c, const uint16_t* frame, int levels, int32_t* coeffs) {
+    if (!c || !frame || !coeffs) return fail(1, "null argument");
+    if (int rc = dwt_check(c, levels)) return rc;
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)c->g.W * c->g.H;
+    uint16_t* d_in = nullptr;
+    int32_t* d_c = nullptr;
+    FROI_CUDA(cudaMalloc(&d_in, px * sizeof(uint16_t)));
+    FROI_CUDA(cudaMalloc(&d_c, px * sizeof(int32_t)));
+    try {
+        FROI_CUDA(cudaMemcpyAsync(d_in, frame, px * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
+        launch_dwt_forward(d_in, 2, c->g.W, c->g.H, c->g.depth, 1, levels, d_c, c->stream);
+        FROI_CUDA(cudaMemcpyAsync(coeffs, d_c, px * sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        cudaFree(d_in);
+        cudaFree(d_c);
+        throw;
+    }
+    cudaFree(d_in);
+    cudaFree(d_c);
+    ABI_CATCH
+}
+
+int froi_dwt_inverse(froi_ctx* c, const int32_t* coeffs, int levels, uint16_t* frame) {
+    if (!c || !frame || !coeffs) return fail(1, "null argument");
+    if (int rc = dwt_check(c, levels)) return rc;
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)c->g.W * c->g.H;
+    uint16_t* d_out = nullptr;
+    int32_t* d_c = nullptr;
+    FROI_CUDA(cudaMalloc(&d_out, px * sizeof(uint16_t)));
+    FROI_CUDA(cudaMalloc(&d_c, px * sizeof(int32_t)));
+    try {
+        FROI_CUDA(cudaMemcpyAsync(d_c, coeffs, px * sizeof(int32_t), cudaMemcpyHostToDevice, c->stream));
+        launch_dwt_inverse(d_c, c->g.W, c->g.H, c->g.depth, 1, levels, d_out, c->stream);
+        FROI_CUDA(cudaMemcpyAsync(frame, d_out, px * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        cudaFree(d_out);
+        cudaFree(d_c);
+        throw;
+    }
+    cudaFree(d_out);
+    cudaFree(d_c);
+    ABI_CATCH
+}
+
+int froi_dwt_forward_device(froi_ctx* c, const void* d_frames, int n, int levels, int32_t* d_coeffs) {
+    if (!c || !d_frames || !d_coeffs) return fail(1, "null argument");
+    if (n < 1) return fail(2, "need at least one frame");
+    if (int rc = dwt_check(c, levels)) return rc;
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    launch_dwt_forward(d_frames, c->g.sample_bytes, c->g.W, c->g.H, c->g.depth, n, levels, d_coeffs, c->stream);
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
+    ABI_CATCH
+}
+
+int froi_map_mask_to_subbands(froi_ctx* c, const uint8_t* mask, int levels, uint8_t* out, size_t cap,
+                              size_t* out_len) {
+    if (!c || !mask || !out || !out_len) return fail(1, "null argument");
+    if (levels < 1) return fail(1, "map_mask_to_subbands: levels must be >= 1");
+    const int W = c->g.W, H = c->g.H;
+    size_t total = 0;
+    for (int l = 1, w = W, h = H; l <= levels; ++l) {
+        w = (w + 1) / 2;
+        h = (h + 1) / 2;
+        total += (size_t)w * h;
+    }
+    *out_len = total;
+    if (cap < total) return fail(1, "map_mask_to_subbands: output buffer too small");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const size_t px = (size_t)W * H;
+    bool any = false;
+    for (size_t i = 0; i < px && !any; ++i) any = mask[i] != 0;
+    uint8_t *d_m = nullptr, *d_o = nullptr;
+    FROI_CUDA(cudaMalloc(&d_m, px));
+    FROI_CUDA(cudaMalloc(&d_o, total));
+    try {
+        FROI_CUDA(cudaMemcpyAsync(d_m, mask, px, cudaMemcpyHostToDevice, c->stream));
+        launch_map_mask_to_subbands(d_m, W, H, levels, any, d_o, c->stream);
+        FROI_CUDA(cudaMemcpyAsync(out, d_o, total, cudaMemcpyDeviceToHost, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        cudaFree(d_m);
+        cudaFree(d_o);
+        throw;
+    }
+    cudaFree(d_m);
+    cudaFree(d_o);
+    ABI_CATCH
+}
+
 int froi_component_areas(froi_ctx* c, const uint8_t* mask, uint32_t* areas_out, size_t cap,
                          size_t* n_components) {
     if (!c || !mask || !n_components) return fail(1, "null argument");

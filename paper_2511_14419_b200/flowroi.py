@@ -539,3 +539,53 @@ def extract_report_frames(masks: np.ndarray, info: ExtractInfo) -> list[dict]:
                      "components": int(component_areas(m[i]).size),
                      "shift": {"dx": int(s.dx), "dy": int(s.dy), "confidence": float(s.confidence)}})
     return rows
+
+
+# ---------------------------------------------------------------- codec side
+def dwt_forward(frame: np.ndarray, levels: int = 5, depth: int | None = None) -> np.ndarray:
+    """Reversible 5/3 DWT on the GPU (``dwt_forward``, dwt.hpp:113-141): DC-shifted int32
+    coefficients in the canonical in-place layout (coarser levels in the top-left quadrant)."""
+    f = _u16(frame)
+    d = depth or _default_depth(np.asarray(frame))
+    h, w = f.shape
+    ctx = _small_ctx(w, h, d, ExtractParams())
+    out = np.empty((h, w), np.int32)
+    with ctx.lock:
+        _native.check(_native.lib.froi_dwt_forward(ctx.handle, f.ctypes.data, int(levels), out.ctypes.data),
+                      "dwt_forward")
+    return out
+
+
+def dwt_inverse(coeffs: np.ndarray, levels: int = 5, depth: int = 8) -> np.ndarray:
+    """Inverse of ``dwt_forward`` (``dwt_inverse``, dwt.hpp:143-171) -> uint16 frame."""
+    c = np.ascontiguousarray(coeffs, dtype=np.int32)
+    h, w = c.shape
+    ctx = _small_ctx(w, h, depth, ExtractParams())
+    out = np.empty((h, w), np.uint16)
+    with ctx.lock:
+        _native.check(_native.lib.froi_dwt_inverse(ctx.handle, c.ctypes.data, int(levels), out.ctypes.data),
+                      "dwt_inverse")
+    return out
+
+
+def map_mask_to_subbands(mask: np.ndarray, levels: int = 5) -> list[np.ndarray]:
+    """RoI coefficient masks per level (``map_mask_to_subbands``, codec.hpp:152-171), level 1
+    (finest) first: 2x2 OR down-sampling then a radius-2 square dilation, on the GPU."""
+    m = np.ascontiguousarray(mask, dtype=np.uint8)
+    h, w = m.shape
+    dims, cw, ch = [], w, h
+    for _ in range(int(levels)):
+        cw, ch = (cw + 1) // 2, (ch + 1) // 2
+        dims.append((ch, cw))
+    out = np.zeros(sum(a * b for a, b in dims), np.uint8)
+    n = ctypes.c_size_t(0)
+    ctx = _small_ctx(w, h, 8, ExtractParams())
+    with ctx.lock:
+        _native.check(_native.lib.froi_map_mask_to_subbands(ctx.handle, m.ctypes.data, int(levels),
+                                                            out.ctypes.data, out.size, ctypes.byref(n)),
+                      "map_mask_to_subbands")
+    res, off = [], 0
+    for a, b in dims:
+        res.append(out[off:off + a * b].reshape(a, b).copy())
+        off += a * b
+    return res
