@@ -46,15 +46,23 @@ __host__ __device__ constexpr int padded(int n) { return n + (n >> 4) + (n >> 7)
 // (element i of transform c at a[pd(i) << lc | c]).  Every butterfly is the reference's
 // (fft.hpp:32-35) with its operands and twiddle tw[hq - 1 + k] (the w sequence for
 // len = 2hq); only the number of shared-memory round trips changes.
+//
+// prune_m >= 0 (the inverse transforms of the registration, whose outputs are read only at
+// positions [0, M] and [n-M, n)): after stage t the value at position p feeds exactly the final
+// outputs q with q = p mod 2^(t+1), so a group whose positions k + m*h (m < 2^Q) hit no needed
+// residue mod T = h*2^Q is skipped; every input of a computed group is then itself needed, so the
+// outputs read are exactly the reference's.
 template <int Q>
 __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
-                                         const double2* __restrict__ tw) {
+                                         const double2* __restrict__ tw, int prune_m = -1) {
     constexpr int G = 1 << Q;
     const int h = 1 << s;
     const int ng = (n >> Q) << lc;
+    const int T = h << Q;
     for (int j = threadIdx.x; j < ng; j += blockDim.x) {
         const int c = j & ((1 << lc) - 1), b = j >> lc;
         const int k = b & (h - 1);
+        if (prune_m >= 0 && T > 2 * prune_m + 1 && k > prune_m && k + (G - 1) * h < T - prune_m) continue;
         const int i = ((b >> s) << (s + Q)) + k;
         double2 e[G];
 #pragma unroll
@@ -78,13 +86,13 @@ __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
 // All log2n stages, QM per pass; input already bit-reversed.
 template <int QM>
 __device__ __forceinline__ void fft_stages(double2* a, int n, int log2n, int lc,
-                                           const double2* __restrict__ tw) {
+                                           const double2* __restrict__ tw, int prune_m = -1) {
     int s = 0;
-    for (; s + QM <= log2n; s += QM) fft_pass<QM>(a, n, s, lc, tw);
+    for (; s + QM <= log2n; s += QM) fft_pass<QM>(a, n, s, lc, tw, prune_m);
     switch (log2n - s) {
-        case 3: fft_pass<3>(a, n, s, lc, tw); break;
-        case 2: fft_pass<2>(a, n, s, lc, tw); break;
-        case 1: fft_pass<1>(a, n, s, lc, tw); break;
+        case 3: fft_pass<3>(a, n, s, lc, tw, prune_m); break;
+        case 2: fft_pass<2>(a, n, s, lc, tw, prune_m); break;
+        case 1: fft_pass<1>(a, n, s, lc, tw, prune_m); break;
         default: break;
     }
 }
@@ -213,7 +221,7 @@ __global__ void __launch_bounds__(NT) k_xpow_rows_inv(int pw, int ph, int log2pw
         a[(pd(brev(x, log2pw)) << lc) | r] = rr;
     }
     __syncthreads();
-    fft_stages<kQXpow>(a, pw, log2pw, lc, itw);
+    fft_stages<kQXpow>(a, pw, log2pw, lc, itw, M);  // only the 2M+1 wrapped columns are read
     const double inv = ddiv(1.0, (double)pw);
     const int nc = 2 * M + 1;
     for (int e = threadIdx.x; e < nc * R; e += NT) {
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(NT) k_inv_cols(int ph, int log2ph, int M,
     const double2* src = cols + ((size_t)p * nc + ci) * ph;
     for (int y = threadIdx.x; y < ph; y += NT) a[pd(brev(y, log2ph))] = src[y];
     __syncthreads();
-    fft_stages<3>(a, ph, log2ph, 0, itw);
+    fft_stages<3>(a, ph, log2ph, 0, itw, M);  // only the 2M+1 wrapped rows are read
     const double inv = ddiv(1.0, (double)ph);
     for (int r = threadIdx.x; r < nc; r += NT) {
         const int dy = r - M;
