@@ -688,7 +688,11 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         auto phase1 = [&](auto in_tag) {
             constexpr bool IN = decltype(in_tag)::value;
             const int npp = npx / 2;
-            for (int ip = threadIdx.x; ip < npp; ip += FNT) {
+            // whole iterations of pixel pairs; the remainder goes out as single pixels over
+            // twice as many threads (a shorter last step before the barrier)
+            const int full0 = (npp / FNT) * FNT;
+            const int full = 2 * (npp - full0) <= FNT ? full0 : npp;  // remainder fits one step
+            for (int ip = threadIdx.x; ip < full; ip += FNT) {
                 const int rp = ip / HW, hx = ip - rp * HW;
                 const int ux = x0 - R + hx, uy = ys - R + r0 + 2 * rp;
                 int gx, gyA, gyB;
@@ -761,6 +765,33 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                 G[2 * PL + siB] = tB.g22;
                 G[3 * PL + siB] = tB.h1;
                 G[4 * PL + siB] = tB.h2;
+            }
+            for (int q = threadIdx.x; q < 2 * (npp - full); q += FNT) {
+                const int ip = full + (q >> 1);
+                const int rp = ip / HW, hx = ip - rp * HW;
+                const int ux = x0 - R + hx, uy = ys - R + r0 + 2 * rp + (q & 1);
+                int gx, gy;
+                bool ok;
+                if (IN) {
+                    gx = ux;
+                    gy = uy;
+                    ok = true;
+                } else {
+                    ok = ux >= 0 && ux < w && uy >= 0 && uy < h;
+                    gx = clampi(ux, 0, w - 1);
+                    gy = clampi(uy, 0, h - 1);
+                }
+                const float2 pr = a.mode ? __ldg(fin + (unsigned)(gy * w + gx)) : make_float2(0.f, 0.f);
+                GLoad ld;
+                g_load(ld, pA, pB, nA, nB, w, h, gx, gy, pr.x, pr.y);
+                GTerms t = g_terms(ld, pr.x, pr.y);
+                if (!ok) t = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
+                const int si = ((r0 + 2 * rp + (q & 1)) % RG) * SW + hx;
+                G[si] = t.g11;
+                G[PL + si] = t.g12;
+                G[2 * PL + si] = t.g22;
+                G[3 * PL + si] = t.h1;
+                G[4 * PL + si] = t.h2;
             }
         };
         const int ry0 = ys - R + r0, ry1 = ry0 + npx / HW;
