@@ -690,8 +690,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             const int npp = npx / 2;
             // whole iterations of pixel pairs; the remainder goes out as single pixels over
             // twice as many threads (a shorter last step before the barrier)
-            const int full0 = (npp / FNT) * FNT;
-            const int full = 2 * (npp - full0) <= FNT ? full0 : npp;  // remainder fits one step
+            const int full = (npp / FNT) * FNT;
             for (int ip = threadIdx.x; ip < full; ip += FNT) {
                 const int rp = ip / HW, hx = ip - rp * HW;
                 const int ux = x0 - R + hx, uy = ys - R + r0 + 2 * rp;
