@@ -194,31 +194,46 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
     }
 }
 
-__global__ void __launch_bounds__(NT) k_xpow_rows_inv(int pw, int ph, int log2pw, int M,
-                                                      const double2* __restrict__ spec,
-                                                      const int* __restrict__ prev,
-                                                      const int* __restrict__ next,
-                                                      const double2* __restrict__ itw,
-                                                      double2* __restrict__ cols) {
+__global__ void __launch_bounds__(NT, 3) k_xpow_rows_inv(int pw, int ph, int log2pw, int M,
+                                                         const double2* __restrict__ spec,
+                                                         const int* __restrict__ prev,
+                                                         const int* __restrict__ next,
+                                                         const double2* __restrict__ itw,
+                                                         double2* __restrict__ cols) {
     extern __shared__ double2 sm[];
     double2* a = sm;
     const int lc = rows_lc(log2pw), R = 1 << lc;
     const int y0 = blockIdx.x * R, p = blockIdx.y;
     const double2* fa = spec + (size_t)prev[p] * ph * pw;
     const double2* fb = spec + (size_t)next[p] * ph * pw;
-    for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
-        const int r = e & (R - 1), x = e >> lc;
-        const int y = y0 + r;
-        if (y >= ph) continue;
-        const double2 A = fa[(size_t)y * pw + x], B = fb[(size_t)y * pw + x];
-        // c = conj(A) * B (registration.hpp:61-65); |c| = std::abs -> glibc hypot
-        const double nai = -A.y;
-        const double re = dsub(dmul(A.x, B.x), dmul(nai, B.y));
-        const double im = dadd(dmul(A.x, B.y), dmul(nai, B.x));
-        const double m = hypot_glibc(re, im);
-        double2 rr = make_double2(0.0, 0.0);
-        if (m > 1e-12) rr = make_double2(ddiv(re, m), ddiv(im, m));
-        a[(pd(brev(x, log2pw)) << lc) | r] = rr;
+    // XU elements per thread per round, all four 16-byte loads issued before the math so the
+    // spectrum reads overlap instead of each stalling its own cross-power
+    constexpr int XU = 4;
+    const int ne = R << log2pw;
+    for (int e0 = threadIdx.x; e0 < ne; e0 += XU * NT) {
+        double2 A[XU], B[XU];
+#pragma unroll
+        for (int u = 0; u < XU; ++u) {
+            const int e = e0 + u * NT, y = y0 + (e & (R - 1)), x = e >> lc;
+            A[u] = B[u] = make_double2(0.0, 0.0);
+            if (e < ne && y < ph) {
+                A[u] = fa[(size_t)y * pw + x];
+                B[u] = fb[(size_t)y * pw + x];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < XU; ++u) {
+            const int e = e0 + u * NT, r = e & (R - 1), x = e >> lc;
+            if (e >= ne || y0 + r >= ph) continue;
+            // c = conj(A) * B (registration.hpp:61-65); |c| = std::abs -> glibc hypot
+            const double nai = -A[u].y;
+            const double re = dsub(dmul(A[u].x, B[u].x), dmul(nai, B[u].y));
+            const double im = dadd(dmul(A[u].x, B[u].y), dmul(nai, B[u].x));
+            const double m = hypot_glibc(re, im);
+            double2 rr = make_double2(0.0, 0.0);
+            if (m > 1e-12) rr = make_double2(ddiv(re, m), ddiv(im, m));
+            a[(pd(brev(x, log2pw)) << lc) | r] = rr;
+        }
     }
     __syncthreads();
     fft_stages<kQXpow>(a, pw, log2pw, lc, itw, M);  // only the 2M+1 wrapped columns are read
