@@ -129,8 +129,12 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
     const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
     if (sizeof(T) == 1 && W == pw && H == ph && (W & 15) == 0 && (R << log2pw) == 16 * NT) {
         // 8-bit frames without padding: each thread reads 16 consecutive samples of one row with
-        // one 128-bit load, then converts and scatters them to their bit-reversed slots
-        const int r = threadIdx.x / (pw / 16), x0 = (threadIdx.x % (pw / 16)) * 16;
+        // one 128-bit load, then converts and scatters them to their bit-reversed slots.  The
+        // lowest lane bits pick the row, the next 3 - lc the top bits of x (the low bits of the
+        // bit-reversed slot), so every 8-lane phase of a 128-bit store hits 8 distinct bank groups.
+        const int hb = lc >= 3 ? 0 : 3 - lc;
+        const int r = threadIdx.x & (R - 1), u = threadIdx.x >> lc;
+        const int x0 = (u & ((1 << hb) - 1)) * (pw >> hb) + (u >> hb) * 16;
         const int y = y0 + r;
         if (y < ph) {
             const uint4 raw = __ldg((const uint4*)(f + (size_t)y * W + x0));
