@@ -177,17 +177,25 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
     // batches of UB loads in flight per thread before their shared-memory scatter
     constexpr int UB = 8;
     const int n = ph << lcb;
+    // element i -> (row, column): the lowest bits pick the column, the next 3 - lcb the top bits
+    // of the row (= the low bits of its bit-reversed slot), so every 8-lane phase of the 128-bit
+    // scatter hits 8 distinct bank groups; rows are 16*pw bytes apart, so no coalescing is lost
+    const int hb = lcb >= 3 ? 0 : 3 - lcb;
+    auto row_of = [&](int i) {
+        const int u = i >> lcb;
+        return (u & ((1 << hb) - 1)) * (ph >> hb) + (u >> hb);
+    };
     for (int i0 = threadIdx.x; i0 < n; i0 += NT * UB) {
         double2 v[UB];
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
             const int i = i0 + u * NT;
-            if (i < n) v[u] = __ldg(base + (size_t)(i >> lcb) * pw + (i & (cb - 1)));
+            if (i < n) v[u] = __ldg(base + (size_t)row_of(i) * pw + (i & (cb - 1)));
         }
 #pragma unroll
         for (int u = 0; u < UB; ++u) {
             const int i = i0 + u * NT;
-            if (i < n) a[(pd(brev(i >> lcb, log2ph)) << lcb) | (i & (cb - 1))] = v[u];
+            if (i < n) a[(pd(brev(row_of(i), log2ph)) << lcb) | (i & (cb - 1))] = v[u];
         }
     }
     __syncthreads();
