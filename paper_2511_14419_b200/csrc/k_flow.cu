@@ -801,6 +801,18 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             rcy[threadIdx.x] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
         }
         __syncthreads();
+        // the threads phase 2 leaves idle pull the next tile's prior rows into L1, so its
+        // gathers do not start behind an L2/DRAM round trip
+        if (a.mode && k + 1 < nr && threadIdx.x >= 5 * HW) {
+            const int ny0 = ys + FY * (k + 1) + R;
+            const int xs = max(0, x0 - R), xe = min(w, x0 + FX + R);
+            constexpr int NL = (HW * 8 + 127) / 128 + 1;
+            for (int i = threadIdx.x - 5 * HW; i < FY * NL; i += FNT - 5 * HW) {
+                const int row = i / NL, ln = i - row * NL;
+                const int y = ny0 + row, x = xs + ln * 16;
+                if (y < h && x < xe) asm volatile("prefetch.global.L1 [%0];" ::"l"(fin + (size_t)y * w + x));
+            }
+        }
         // phase 2: vertical running sums down each of the 5*HW ring columns (FY outputs each),
         // in place over this tile's first FY ring rows
         const int b0 = (FY * k) % RG;  // 0, 32 or 16
