@@ -856,12 +856,15 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         __syncthreads();
         // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
         // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
-        const int tx = threadIdx.x % FX;
-        for (int ty = threadIdx.x / FX; ty < FY; ty += FNT / FX) {
-            const int x = x0 + tx, y = y0 + ty;
+        const int tx = threadIdx.x % FX, x = x0 + tx;
+        const float icx = rcx[tx];
+#pragma unroll 1
+        for (int j = 0; j < FY / (FNT / FX); ++j) {
+            const int ty = threadIdx.x / FX + j * (FNT / FX), y = y0 + ty;
             if (x >= w || y >= h) continue;
-            const float inv = rcx[tx] * rcy[ty];
-            const int sidx = ((b0 + ty) % RG) * SW + tx;
+            const float inv = icx * rcy[ty];
+            const int rr = b0 + ty;
+            const int sidx = (rr >= RG ? rr - RG : rr) * SW + tx;
             const float g11 = G[sidx] * inv, g12 = G[PL + sidx] * inv, g22 = G[2 * PL + sidx] * inv;
             const float h1 = G[3 * PL + sidx] * inv, h2 = G[4 * PL + sidx] * inv;
             const float q = g12 * g12;
