@@ -201,17 +201,24 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
     const int n_tiles = per_slot * n_slots;
     constexpr int NRAW = (QRW * QRH + QNT - 1) / QNT;
     // this thread's raw-tile positions are the same for every tile: (ry, rx) packed once
-    int rpos[NRAW];
+    int rpos[NRAW], roff[NRAW];
 #pragma unroll
     for (int k = 0; k < NRAW; ++k) {
         const int i = tid + k * QNT, ry = i / QRW;
         rpos[k] = i < QRW * QRH ? (ry << 16) | (i - ry * QRW) : -1;
+        roff[k] = ry * W + (i - ry * QRW);
     }
     auto fetch = [&](int t, int* v) {
         const int slot = t / per_slot, tr = t - slot * per_slot;
         const int by = tr / tiles_x, bx = tr - by * tiles_x;
         const uint8_t* src = (const uint8_t*)frame_raw[slot];
         const int gy0 = by * QY - R1, gx0 = bx * QX - R1;
+        if (gx0 >= 0 && gy0 >= 0 && gx0 + QRW <= W && gy0 + QRH <= H) {  // no clamping
+            const uint8_t* s0 = src + gy0 * W + gx0;
+#pragma unroll
+            for (int k = 0; k < NRAW; ++k) v[k] = rpos[k] >= 0 ? __ldg(s0 + roff[k]) : 0;
+            return;
+        }
 #pragma unroll
         for (int k = 0; k < NRAW; ++k) {
             v[k] = 0;
@@ -235,13 +242,12 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
             if (tid + k * QNT < QRW * QRH) raw_s[tid + k * QNT] = rv[k];
         __syncthreads();
         if (t + (int)gridDim.x < n_tiles) fetch(t + gridDim.x, rv);  // in flight during this tile
-        // medians at clamped centres (denoise.hpp:32-43): columns lane (+32 for lanes 0..3),
-        // rows [grp*QMH/8, (grp+1)*QMH/8)
-        for (int pass = 0; pass < 2; ++pass) {
-            const int mx = lane + 32 * pass;
-            if (mx >= QMW) break;
+        // medians at clamped centres (denoise.hpp:32-43): thread -> (column tid % QMW, run of
+        // rows (tid / QMW) * QMH / 7 ..), one sliding window of sorted row triples per run
+        if (tid < 7 * QMW) {
+            const int mx = tid % QMW, mg = tid / QMW;
             const int cx = clampi(x0 - 2 + mx, 0, W - 1) - (x0 - R1);  // raw_s column of the centre
-            const int rb = grp * QMH / 8, re = (grp + 1) * QMH / 8;
+            const int rb = mg * QMH / 7, re = (mg + 1) * QMH / 7;
             // sorted triple of raw_s row r around the centre column
             auto tri = [&](int r, int& l, int& md, int& h) {
                 const int* q = raw_s + r * QRW + cx;
