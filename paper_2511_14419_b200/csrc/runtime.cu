@@ -627,9 +627,13 @@ froi_ctx* lane_of(froi_ctx* c) {
 // PairInfo rows in job order.
 // host_pbm (nullable, pinned): each batch's PBM masks are copied to the same offsets of host_pbm
 // on the batch's lane right after its mask stage, overlapping the later batches.
+// first (> 0): size of batch 0 when the frames are still arriving from the host, so the GPU
+// starts on a few pairs while the rest of the upload is in flight; later batches are Pcap pairs.
 void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm,
-                 std::vector<PairInfo>& infos, uint8_t* host_pbm = nullptr) {
-    const size_t nb = (jobs.size() + c->Pcap - 1) / c->Pcap;
+                 std::vector<PairInfo>& infos, uint8_t* host_pbm = nullptr, int first = 0) {
+    const size_t P = (size_t)c->Pcap, F = first > 0 && first < c->Pcap ? (size_t)first : P;
+    auto bstart = [&](size_t b) { return b == 0 ? 0 : std::min(jobs.size(), F + (b - 1) * P); };
+    const size_t nb = jobs.size() <= F ? 1 : 1 + (jobs.size() - F + P - 1) / P;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
         FROI_CUDA(cudaFreeHost(c->h_info));
@@ -651,7 +655,7 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
     }
     const size_t mb = (size_t)c->g.H * c->g.SB;
     for (size_t b = 0; b < nb; ++b) {
-        const size_t j0 = b * c->Pcap, j1 = std::min(jobs.size(), j0 + (size_t)c->Pcap);
+        const size_t j0 = bstart(b), j1 = bstart(b + 1);
         froi_ctx* x = (lane && (b & 1)) ? lane : c;
         run_batch(x, c, jobs, j0, j1, out_pbm, b, j0);
         if (host_pbm) {
@@ -744,7 +748,7 @@ void check_frames_range(froi_ctx* c, const void* frames, int sample_bytes, size_
 // Whole wells: frames on device (well-major, contiguous in ctx sample type).
 void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int n_wells, int n_frames,
                        uint8_t* d_out, std::vector<PairInfo>& infos, const cudaEvent_t* ready = nullptr,
-                       uint8_t* host_pbm = nullptr) {
+                       uint8_t* host_pbm = nullptr, int first = 0) {
     // ready (nullable): per (well, frame) event after which the frame is resident
     const Geom& g = c->g;
     std::vector<PairJob> jobs;
@@ -762,7 +766,7 @@ void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int 
     c->times = froi_stage_times{};
     c->ktimes = froi_kernel_times{};
     c->launches = 0;
-    run_batches(c, jobs, d_out, infos, host_pbm);
+    run_batches(c, jobs, d_out, infos, host_pbm, first);
     // frame 0 borrows frame 1's mask (roi.hpp:348)
     const size_t mb = (size_t)g.H * g.SB;
     for (int w = 0; w < n_wells; ++w)
@@ -1003,15 +1007,10 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
         c->arena_cap = need;
     }
     uint8_t* d_frames = c->d_arena;
-    // copy granularity: chunks of Pcap frames, each with an event the consuming batch waits on
+    // copy granularity: a short first chunk (frames 0..first of well 0, all the first batch
+    // needs) then chunks of Pcap frames, each with an event the consuming batches wait on
     const int fchunk = std::max(1, c->Pcap);
-    const int chunks_per_well = (n_frames + fchunk - 1) / fchunk;
-    const size_t n_events = (size_t)n_wells * chunks_per_well;
-    while (c->well_ready.size() < n_events) {
-        cudaEvent_t e;
-        FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        c->well_ready.push_back(e);
-    }
+    const int first = n_frames > 2 ? std::max(1, std::min(c->Pcap / 4, n_frames - 2)) : 0;
     const bool direct = sample_bytes == c->g.sample_bytes && stride == c->frame_bytes;
     std::vector<cudaEvent_t> ready;
     if (direct) {
@@ -1019,15 +1018,22 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
         FROI_CUDA(cudaEventRecord(c->ev[7], c->stream));
         FROI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[7], 0));
         ready.resize((size_t)n_wells * n_frames);
+        size_t ne = 0;
         for (int w = 0; w < n_wells; ++w)
-            for (int k = 0; k < chunks_per_well; ++k) {
-                const int f0 = k * fchunk, f1 = std::min(n_frames, f0 + fchunk);
+            for (int f0 = 0; f0 < n_frames;) {
+                const int f1 = std::min(n_frames, f0 + (w == 0 && f0 == 0 && first ? first + 1 : fchunk));
                 const size_t off = c->frame_bytes * ((size_t)n_frames * w + f0);
                 FROI_CUDA(cudaMemcpyAsync(d_frames + off, (const uint8_t*)frames + off,
                                           c->frame_bytes * (f1 - f0), cudaMemcpyHostToDevice, c->copy_stream));
-                cudaEvent_t e = c->well_ready[(size_t)w * chunks_per_well + k];
+                if (c->well_ready.size() <= ne) {
+                    cudaEvent_t e;
+                    FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    c->well_ready.push_back(e);
+                }
+                cudaEvent_t e = c->well_ready[ne++];
                 FROI_CUDA(cudaEventRecord(e, c->copy_stream));
                 for (int f = f0; f < f1; ++f) ready[(size_t)w * n_frames + f] = e;
+                f0 = f1;
             }
     } else {
         upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
@@ -1040,7 +1046,8 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
     cudaGetLastError();  // a pageable pointer may leave an error behind
     const bool stream_back = layout == FROI_MASK_PBM && c->params.adjacent_factor == 0 && pinned;
     extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos,
-                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr);
+                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr,
+                      direct ? first : 0);
     if (stream_back) {
         // only frame 0 of each well (a copy of frame 1's mask, made after the batches) is left
         for (int w = 0; w < n_wells; ++w)
