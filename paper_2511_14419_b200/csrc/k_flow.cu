@@ -47,6 +47,27 @@ struct ImageSrc {
     }
 };
 
+// Stages an edge-clamped source block into shared memory with U elements per thread in flight:
+// all U source reads (for 8-bit frames a byte load then its table lookup) are issued before any
+// store, instead of one dependent load pair per element.
+template <int NT, int U, typename At>
+__device__ __forceinline__ void stage_block(float* dst, int n, int sw, At at) {
+    for (int i0 = threadIdx.x; i0 < n; i0 += U * NT) {
+        float v[U];
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const int i = i0 + k * NT;
+            if (i < n) {
+                const int yy = i / sw, xx = i - yy * sw;
+                v[k] = at(xx, yy);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k)
+            if (i0 + k * NT < n) dst[i0 + k * NT] = v[k];
+    }
+}
+
 // ------------------------------------------------------------------ polynomial expansion
 constexpr int PX = 32, PY = 16, PNT = 256;
 
@@ -63,10 +84,7 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
     const int tid = threadIdx.x;
     // constant offset: the fit of A and b is invariant to it and it removes cancellation
     const float c0 = src.at(x0, y0);
-    for (int i = tid; i < sh * sw; i += PNT) {
-        const int yy = i / sw, xx = i - yy * sw;
-        s_in[i] = src.at(x0 - r + xx, y0 - r + yy) - c0;
-    }
+    stage_block<PNT, 3>(s_in, sh * sw, sw, [&](int xx, int yy) { return src.at(x0 - r + xx, y0 - r + yy) - c0; });
     __syncthreads();
     if (RC == 2 && !kDebug) {
         // radius 2: same arithmetic per output, loads shared between neighbours -- row pass two
@@ -334,10 +352,7 @@ __device__ __forceinline__ void pyr2_tile(const Src& src, int tw, int th, const 
     const int ox0 = blockIdx.x * Q2X, oy0 = blockIdx.y * Q2Y;
     const int ix0 = 2 * ox0 - 3, iy0 = 2 * oy0 - 3;
     const int tid = threadIdx.x;
-    for (int i = tid; i < Q2H * Q2W; i += QNT) {
-        const int yy = i / Q2W, xx = i - yy * Q2W;
-        s_in[i] = src.at(ix0 + xx, iy0 + yy);
-    }
+    stage_block<QNT, 4>(s_in, Q2H * Q2W, Q2W, [&](int xx, int yy) { return src.at(ix0 + xx, iy0 + yy); });
     __syncthreads();
     float k[7];
 #pragma unroll
