@@ -37,6 +37,15 @@ struct FrameSrc {  // normalize_frame(apply_shift(den, s)) at level 0
         const int v = f[sy * W + sx];
         return sizeof(T) == 1 ? __ldg(lut + v) : (float)((double)v * inv);
     }
+    // [x0, x1) x [y0, y1) needs no clamping (before or after the shift)
+    __device__ __forceinline__ bool inside(int x0, int y0, int x1, int y1) const {
+        return x0 >= 0 && y0 >= 0 && x1 <= W && y1 <= H && x0 + dx >= 0 && y0 + dy >= 0 && x1 + dx <= W &&
+               y1 + dy <= H;
+    }
+    __device__ __forceinline__ const T* base(int x0, int y0) const { return f + (y0 + dy) * W + x0 + dx; }
+    __device__ __forceinline__ float conv(T v) const {
+        return sizeof(T) == 1 ? __ldg(lut + v) : (float)((double)v * inv);
+    }
 };
 
 struct ImageSrc {
@@ -45,6 +54,11 @@ struct ImageSrc {
     __device__ __forceinline__ float at(int x, int y) const {
         return f[(size_t)clampi(y, 0, H - 1) * W + clampi(x, 0, W - 1)];
     }
+    __device__ __forceinline__ bool inside(int x0, int y0, int x1, int y1) const {
+        return x0 >= 0 && y0 >= 0 && x1 <= W && y1 <= H;
+    }
+    __device__ __forceinline__ const float* base(int x0, int y0) const { return f + (size_t)y0 * W + x0; }
+    __device__ __forceinline__ float conv(float v) const { return v; }
 };
 
 // Stages an edge-clamped source block into shared memory with U elements per thread in flight:
@@ -68,6 +82,20 @@ __device__ __forceinline__ void stage_block(float* dst, int n, int sw, At at) {
     }
 }
 
+// The bw x bh source block at (bx0, by0), minus `sub`, into shared memory: without any clamping
+// when the block lies inside the image.
+template <int NT, int U, typename Src>
+__device__ __forceinline__ void stage_src(const Src& src, float* dst, int bx0, int by0, int bw, int bh,
+                                          float sub) {
+    if (src.inside(bx0, by0, bx0 + bw, by0 + bh)) {
+        const auto* b0 = src.base(bx0, by0);
+        const int W = src.W;
+        stage_block<NT, U>(dst, bw * bh, bw, [&](int xx, int yy) { return src.conv(b0[yy * W + xx]) - sub; });
+    } else {
+        stage_block<NT, U>(dst, bw * bh, bw, [&](int xx, int yy) { return src.at(bx0 + xx, by0 + yy) - sub; });
+    }
+}
+
 // ------------------------------------------------------------------ polynomial expansion
 constexpr int PX = 32, PY = 16, PNT = 256;
 
@@ -84,7 +112,7 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
     const int tid = threadIdx.x;
     // constant offset: the fit of A and b is invariant to it and it removes cancellation
     const float c0 = src.at(x0, y0);
-    stage_block<PNT, 3>(s_in, sh * sw, sw, [&](int xx, int yy) { return src.at(x0 - r + xx, y0 - r + yy) - c0; });
+    stage_src<PNT, 3>(src, s_in, x0 - r, y0 - r, sw, sh, c0);
     __syncthreads();
     if (RC == 2 && !kDebug) {
         // radius 2: same arithmetic per output, loads shared between neighbours -- row pass two
@@ -352,7 +380,7 @@ __device__ __forceinline__ void pyr2_tile(const Src& src, int tw, int th, const 
     const int ox0 = blockIdx.x * Q2X, oy0 = blockIdx.y * Q2Y;
     const int ix0 = 2 * ox0 - 3, iy0 = 2 * oy0 - 3;
     const int tid = threadIdx.x;
-    stage_block<QNT, 4>(s_in, Q2H * Q2W, Q2W, [&](int xx, int yy) { return src.at(ix0 + xx, iy0 + yy); });
+    stage_src<QNT, 4>(src, s_in, ix0, iy0, Q2W, Q2H, 0.f);
     __syncthreads();
     float k[7];
 #pragma unroll
