@@ -174,8 +174,6 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
     const int cb = 1 << lcb;
     const int slot = blockIdx.y, c0 = blockIdx.x * cb;
     double2* base = spec + (size_t)slot * ph * pw + c0;
-    // batches of UB loads in flight per thread before their shared-memory scatter
-    constexpr int UB = 8;
     const int n = ph << lcb;
     // element i -> (row, column): the lowest bits pick the column, the next 3 - lcb the top bits
     // of the row (= the low bits of its bit-reversed slot), so every 8-lane phase of the 128-bit
@@ -185,19 +183,14 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
         const int u = i >> lcb;
         return (u & ((1 << hb) - 1)) * (ph >> hb) + (u >> hb);
     };
-    for (int i0 = threadIdx.x; i0 < n; i0 += NT * UB) {
-        double2 v[UB];
-#pragma unroll
-        for (int u = 0; u < UB; ++u) {
-            const int i = i0 + u * NT;
-            if (i < n) v[u] = __ldg(base + (size_t)row_of(i) * pw + (i & (cb - 1)));
-        }
-#pragma unroll
-        for (int u = 0; u < UB; ++u) {
-            const int i = i0 + u * NT;
-            if (i < n) a[(pd(brev(row_of(i), log2ph)) << lcb) | (i & (cb - 1))] = v[u];
-        }
+    // global -> shared without a register round trip (cp.async, 16 B per element): every element
+    // of the column block is in flight at once
+    for (int i = threadIdx.x; i < n; i += NT) {
+        const double2* src = base + (size_t)row_of(i) * pw + (i & (cb - 1));
+        const unsigned dst = (unsigned)__cvta_generic_to_shared(a + ((pd(brev(row_of(i), log2ph)) << lcb) | (i & (cb - 1))));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
+    asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     fft_stages<kQCols>(a, ph, log2ph, lcb, tw);
     for (int i = threadIdx.x; i < (ph << lcb); i += NT) {
