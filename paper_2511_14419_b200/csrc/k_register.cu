@@ -74,13 +74,20 @@ __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
             for (int m = 0; m < G; ++m) {
                 if (m & (1 << q)) continue;
                 const int kq = k + (m & ((1 << q) - 1)) * h;
-                bfly(e[m], e[m | (1 << q)], __ldg(tw + hq - 1 + kq));
+                bfly(e[m], e[m | (1 << q)], tw[hq - 1 + kq]);
             }
         }
 #pragma unroll
         for (int m = 0; m < G; ++m) a[(pd(i + m * h) << lc) | c] = e[m];
     }
     __syncthreads();
+}
+
+// The n - 1 twiddles of a length-n transform into shared memory (dst, behind the data), so the
+// butterflies read them without L1 tag lookups; the caller's barrier publishes them.
+__device__ __forceinline__ const double2* stage_tw(double2* dst, const double2* __restrict__ tw, int n) {
+    for (int i = threadIdx.x; i < n - 1; i += blockDim.x) dst[i] = __ldg(tw + i);
+    return dst;
 }
 
 // All log2n stages, QM per pass; input already bit-reversed.
@@ -127,6 +134,7 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
     const T* f = den + (size_t)slot * W * H;
     // windowed_spectrum_input (registration.hpp:26-42): exact integer sum, then one division
     const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
+    const double2* stw = stage_tw(a + ((size_t)padded(pw) << lc), tw, pw);
     if (sizeof(T) == 1 && W == pw && H == ph && (W & 15) == 0 && (R << log2pw) == 16 * NT) {
         // 8-bit frames without padding: each thread reads 16 consecutive samples of one row with
         // one 128-bit load, then converts and scatters them to their bit-reversed slots.  The
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
         }
     }
     __syncthreads();
-    fft_stages<kQRows>(a, pw, log2pw, lc, tw);
+    fft_stages<kQRows>(a, pw, log2pw, lc, stw);
     for (int e = threadIdx.x; e < (R << log2pw); e += NT) {
         const int r = e & (R - 1), x = e >> lc;
         if (y0 + r < ph) spec[((size_t)slot * ph + y0 + r) * pw + x] = a[(pd(x) << lc) | r];
@@ -190,9 +198,10 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
         const unsigned dst = (unsigned)__cvta_generic_to_shared(a + ((pd(brev(row_of(i), log2ph)) << lcb) | (i & (cb - 1))));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
+    const double2* stw = stage_tw(a + ((size_t)padded(ph) << lcb), tw, ph);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
-    fft_stages<kQCols>(a, ph, log2ph, lcb, tw);
+    fft_stages<kQCols>(a, ph, log2ph, lcb, stw);
     for (int i = threadIdx.x; i < (ph << lcb); i += NT) {
         const int r = i >> lcb, c = i & (cb - 1);
         base[(size_t)r * pw + c] = a[(pd(r) << lcb) | c];
@@ -365,7 +374,7 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
                         const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s) {
     if (n_slots <= 0) return;
     const int lr = rows_lc(g.log2pw);
-    const size_t smem_r = sizeof(double2) * ((size_t)padded(g.pw) << lr);
+    const size_t smem_r = sizeof(double2) * (((size_t)padded(g.pw) << lr) + g.pw);
     const int row_blocks = cdiv(g.ph, 1 << lr);
     if (g.sample_bytes == 1) {
         set_smem(k_fft_rows_fwd<uint8_t>, smem_r);
@@ -378,7 +387,7 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
     }
     FROI_LAUNCH_CHECK();
     const int lcb = column_lcb(g);
-    const size_t smem_c = sizeof(double2) * ((size_t)padded(g.ph) << lcb);
+    const size_t smem_c = sizeof(double2) * (((size_t)padded(g.ph) << lcb) + g.ph);
     set_smem(k_fft_cols, smem_c);
     k_fft_cols<<<dim3(g.pw >> lcb, n_slots), NT, smem_c, s>>>(g.pw, g.ph, g.log2ph, lcb, d_tw_col, d_spec);
     FROI_LAUNCH_CHECK();
