@@ -174,14 +174,14 @@ constexpr int QX = 32, QY = 32, QNT = 256, QRPT = QY / (QNT / QX), QREP = 16;
 constexpr int QRW = QX + 6, QRH = QY + 6, QMW = QX + 4, QMH = QY + 4;
 
 size_t qsmem_bytes() {
-    return sizeof(double) * (511 * QREP) + sizeof(int) * (QRW * QRH + QMW * QMH);
+    return sizeof(double) * (511 * QREP) + sizeof(int) * QMW * QMH + sizeof(uint8_t) * QRW * QRH;
 }
 
 __device__ __forceinline__ int med3i(int a, int b, int c) {
     return a + b + c - min(min(a, b), c) - max(max(a, b), c);
 }
 
-__global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int maxval, int n_slots,
+__global__ void __launch_bounds__(QNT, 3) k_denoise_u8_m1b2(int W, int H, int maxval, int n_slots,
                                                             const void* const* frame_raw, uint8_t* den,
                                                             unsigned long long* sums,
                                                             const __grid_constant__ Spatial sp_w,
@@ -189,8 +189,8 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
     constexpr int R1 = 3;
     extern __shared__ __align__(16) unsigned char smem[];
     double* lut_s = (double*)smem;                  // [511][QREP], index d + 255
-    int* raw_s = (int*)(lut_s + 511 * QREP);        // QRH * QRW
-    int* med_s = raw_s + QRW * QRH;                 // QMH * QMW medians * (QREP * 8)
+    int* med_s = (int*)(lut_s + 511 * QREP);        // QMH * QMW medians * (QREP * 8)
+    uint8_t* raw_s = (uint8_t*)(med_s + QMW * QMH); // QRH * QRW samples
     const int tid = threadIdx.y * QX + threadIdx.x;
     for (int i = tid; i < 511 * QREP; i += QNT) lut_s[i] = lut_g[min(abs(i / QREP - 255), maxval)];
     // byte address of this lane's copy of entry d = 0; + (m_n - m_c) * QREP * 8 selects d
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
         __syncthreads();  // previous tile's bilateral is done with med_s
 #pragma unroll
         for (int k = 0; k < NRAW; ++k)
-            if (tid + k * QNT < QRW * QRH) raw_s[tid + k * QNT] = rv[k];
+            if (tid + k * QNT < QRW * QRH) raw_s[tid + k * QNT] = (uint8_t)rv[k];
         __syncthreads();
         if (t + (int)gridDim.x < n_tiles) fetch(t + gridDim.x, rv);  // in flight during this tile
         // medians at clamped centres (denoise.hpp:32-43): thread -> (column tid % QMW, run of
@@ -250,7 +250,7 @@ __global__ void __launch_bounds__(QNT, 2) k_denoise_u8_m1b2(int W, int H, int ma
             const int rb = mg * QMH / 7, re = (mg + 1) * QMH / 7;
             // sorted triple of raw_s row r around the centre column
             auto tri = [&](int r, int& l, int& md, int& h) {
-                const int* q = raw_s + r * QRW + cx;
+                const uint8_t* q = raw_s + r * QRW + cx;
                 const int a = q[-1], b = q[0], c = q[1];
                 l = min(min(a, b), c);
                 h = max(max(a, b), c);
@@ -353,7 +353,7 @@ void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw,
             attr = true;
         }
         const long long tiles = (long long)cdiv(g.W, QX) * cdiv(g.H, QY) * n_slots;
-        const int blocks = (int)std::min<long long>(tiles, 148 * 2);
+        const int blocks = (int)std::min<long long>(tiles, 148 * 3);
         k_denoise_u8_m1b2<<<blocks, dim3(QX, QNT / QX), qsmem, s>>>(g.W, g.H, g.maxval, n_slots, d_frame_raw,
                                                                    (uint8_t*)d_den, d_sums, sp, d_lut);
         FROI_LAUNCH_CHECK();
