@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(NT, 3) k_xpow_rows_inv(int pw, int ph, int log
     const double2* fb = spec + (size_t)next[p] * ph * pw;
     // XU elements per thread per round, all four 16-byte loads issued before the math so the
     // spectrum reads overlap instead of each stalling its own cross-power
-    constexpr int XU = 4;
+    constexpr int XU = 2;
     const int ne = R << log2pw;
     for (int e0 = threadIdx.x; e0 < ne; e0 += XU * NT) {
         double2 A[XU], B[XU];
@@ -235,18 +235,37 @@ __global__ void __launch_bounds__(NT, 3) k_xpow_rows_inv(int pw, int ph, int log
                 B[u] = fb[(size_t)y * pw + x];
             }
         }
+        // c = conj(A) * B (registration.hpp:61-65); |c| = std::abs -> glibc hypot; c / |c|.
+        // All XU elements go through the branch-free fast paths first (their fp64 chains
+        // interleave); an element a fast path flags is redone with the intrinsics.
+        double2 rr[XU];
+        bool ok[XU];
+#pragma unroll
+        for (int u = 0; u < XU; ++u) {
+            const double nai = -A[u].y;
+            const double re = dsub(dmul(A[u].x, B[u].x), dmul(nai, B[u].y));
+            const double im = dadd(dmul(A[u].x, B[u].y), dmul(nai, B[u].x));
+            bool okh, okx, oky;
+            const double m = hypot_glibc_fast(re, im, okh);
+            const bool big = m > 1e-12;
+            const double mm = big ? m : 1.0;
+            const double r2 = drcp_refined(mm);
+            const double qx = ddiv_fast(re, mm, r2, okx), qy = ddiv_fast(im, mm, r2, oky);
+            rr[u] = big ? make_double2(qx, qy) : make_double2(0.0, 0.0);
+            ok[u] = okh && (!big || (okx && oky));
+        }
 #pragma unroll
         for (int u = 0; u < XU; ++u) {
             const int e = e0 + u * NT, r = e & (R - 1), x = e >> lc;
             if (e >= ne || y0 + r >= ph) continue;
-            // c = conj(A) * B (registration.hpp:61-65); |c| = std::abs -> glibc hypot
-            const double nai = -A[u].y;
-            const double re = dsub(dmul(A[u].x, B[u].x), dmul(nai, B[u].y));
-            const double im = dadd(dmul(A[u].x, B[u].y), dmul(nai, B[u].x));
-            const double m = hypot_glibc(re, im);
-            double2 rr = make_double2(0.0, 0.0);
-            if (m > 1e-12) rr = make_double2(ddiv(re, m), ddiv(im, m));
-            a[(pd(brev(x, log2pw)) << lc) | r] = rr;
+            if (!ok[u]) {
+                const double nai = -A[u].y;
+                const double re = dsub(dmul(A[u].x, B[u].x), dmul(nai, B[u].y));
+                const double im = dadd(dmul(A[u].x, B[u].y), dmul(nai, B[u].x));
+                const double m = hypot_glibc(re, im);
+                rr[u] = m > 1e-12 ? make_double2(ddiv(re, m), ddiv(im, m)) : make_double2(0.0, 0.0);
+            }
+            a[(pd(brev(x, log2pw)) << lc) | r] = rr[u];
         }
     }
     __syncthreads();
