@@ -347,11 +347,8 @@ void launch_denoise(const Geom& g, const DevParams& p, const void** d_frame_raw,
     const bool fast = mr == 1 && br == 2;
     if (fast && p.denoise_enabled && g.sample_bytes == 1 && g.maxval <= 255) {
         const size_t qsmem = qsmem_bytes();
-        static bool attr = false;
-        if (!attr) {
-            FROI_CUDA(cudaFuncSetAttribute(k_denoise_u8_m1b2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
-            attr = true;
-        }
+        // kernel attributes are per device: set on every call (one host thread may drive several)
+        FROI_CUDA(cudaFuncSetAttribute(k_denoise_u8_m1b2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)qsmem));
         const long long tiles = (long long)cdiv(g.W, QX) * cdiv(g.H, QY) * n_slots;
         const int blocks = (int)std::min<long long>(tiles, 148 * 3);
         k_denoise_u8_m1b2<<<blocks, dim3(QX, QNT / QX), qsmem, s>>>(g.W, g.H, g.maxval, n_slots, d_frame_raw,

@@ -940,11 +940,8 @@ template <int R>
 void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                  const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
     const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * RG;
-    static bool attr = false;
-    if (!attr) {
-        FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr = true;
-    }
+    // kernel attributes are per device: set on every call (one host thread may drive several)
+    FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nr = strip_tiles(g, a.l, n_pairs);
     dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY * nr), n_pairs);
     k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info, nr);

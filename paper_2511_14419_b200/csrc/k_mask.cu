@@ -1309,16 +1309,13 @@ constexpr int kSelPasses = 6;  // worst case: 64 key bits / 11; typically 2 (+ t
 
 size_t scan_smem() { return sizeof(unsigned long long) * kSelCap; }
 
+// kernel attributes are per device: set on every call (one host thread may drive several devices)
 void set_scan_smem() {
-    static bool done = false;
-    if (!done) {
-        FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(4)));
-        FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(1)));
-        FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
-        FROI_CUDA(cudaFuncSetAttribute(k_thr_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)(sizeof(unsigned int) * kSelCap)));
-        done = true;
-    }
+    FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(4)));
+    FROI_CUDA(cudaFuncSetAttribute(k_sel_pass_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pass_smem(1)));
+    FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
+    FROI_CUDA(cudaFuncSetAttribute(k_thr_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)(sizeof(unsigned int) * kSelCap)));
 }
 
 int blocks_per_pair(const Geom& g, int n_pairs) {
