@@ -296,6 +296,9 @@ struct froi_ctx {
     uint8_t* d_arena = nullptr;
     size_t arena_cap = 0;
     cudaStream_t copy_stream = nullptr;
+    cudaStream_t d2h_stream = nullptr;       // per-batch mask read-back (host PBM), off the lanes
+    std::vector<cudaEvent_t> d2h_ev;         // batch b's masks are final
+    cudaEvent_t d2h_done = nullptr;
     std::vector<cudaEvent_t> well_ready;
     uint64_t launches = 0;
 
@@ -447,6 +450,8 @@ void ctx_alloc(froi_ctx* c) {
     c->h_info_cap = P;
     for (int i = 0; i < 8; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    FROI_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
+    FROI_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
 }
 
 void ctx_free(froi_ctx* c) {
@@ -482,7 +487,10 @@ void ctx_free(froi_ctx* c) {
     for (auto& a : c->bev)
         for (auto e : a) cudaEventDestroy(e);
     for (auto e : c->well_ready) cudaEventDestroy(e);
+    for (auto e : c->d2h_ev) cudaEventDestroy(e);
+    if (c->d2h_done) cudaEventDestroy(c->d2h_done);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
 
@@ -664,9 +672,21 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
                 lo = std::min(lo, jobs[j].out_index);
                 hi = std::max(hi, jobs[j].out_index);
             }
+            // read back on its own stream, so neither lane waits for the copy
+            while (c->d2h_ev.size() <= b) {
+                cudaEvent_t e;
+                FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                c->d2h_ev.push_back(e);
+            }
+            FROI_CUDA(cudaEventRecord(c->d2h_ev[b], x->stream));
+            FROI_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->d2h_ev[b], 0));
             FROI_CUDA(cudaMemcpyAsync(host_pbm + mb * lo, out_pbm + mb * lo, mb * (size_t)(hi - lo + 1),
-                                      cudaMemcpyDeviceToHost, x->stream));
+                                      cudaMemcpyDeviceToHost, c->d2h_stream));
         }
+    }
+    if (host_pbm) {
+        FROI_CUDA(cudaEventRecord(c->d2h_done, c->d2h_stream));
+        FROI_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
     }
     if (lane) {
         // later work on the owner's stream (frame-0 copies, ensemble, delivery) follows both lanes
