@@ -587,6 +587,21 @@ struct GTerms {
     float g11, g12, g22, h1, h2;
 };
 
+// Streaming reads (the previous frame's coefficients at the pixel itself: read once per tile)
+// bypass L1 allocation, leaving its capacity to the bilinear gathers that do reuse lines.
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+    float4 v;
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+        : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+        : "l"(p));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float* p) {
+    float v;
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+
 // Gathered operands of one pixel's normal-equation products.
 struct GLoad {
     float4 q00, q01, q10, q11, pa;
@@ -616,8 +631,8 @@ __device__ __forceinline__ void g_load(GLoad& o, const float4* __restrict__ pA,
     o.b10 = __ldg(b1);
     o.b11 = __ldg(b1 + 1);
     const unsigned c = (unsigned)(gy * w + gx);
-    o.pa = __ldg(pA + c);
-    o.pb = __ldg(pB + c);
+    o.pa = ld_stream(pA + c);
+    o.pb = ld_stream(pB + c);
 }
 
 // Bilinear weights w00..w11 make every interpolated channel one FMUL + three FFMA (packed for the
@@ -790,10 +805,10 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                     lB.b01 = __ldg(nB + iB0 + 1);
                 }
                 const unsigned cA = (unsigned)(gyA * w + gx), cB = (unsigned)(gyB * w + gx);
-                lA.pa = __ldg(pA + cA);
-                lA.pb = __ldg(pB + cA);
-                lB.pa = __ldg(pA + cB);
-                lB.pb = __ldg(pB + cB);
+                lA.pa = ld_stream(pA + cA);
+                lA.pb = ld_stream(pB + cA);
+                lB.pa = ld_stream(pA + cB);
+                lB.pb = ld_stream(pB + cB);
                 GTerms tA = g_terms(lA, prA.x, prA.y), tB = g_terms(lB, prB.x, prB.y);
                 if (!okA) tA = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
                 if (!okB) tB = GTerms{0.f, 0.f, 0.f, 0.f, 0.f};
