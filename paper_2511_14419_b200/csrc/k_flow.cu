@@ -733,6 +733,17 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         const int x = x0 + threadIdx.x;
         rcx[threadIdx.x] = __frcp_rn((float)(min(w - 1, x + R) - max(0, x - R) + 1));
     }
+    if (a.mode) {
+        // the first tile's prior rows (its later tiles' rows are prefetched during phase 2):
+        // later pair rounds of the first tile then find them in L1
+        const int xs = max(0, x0 - R), xe = min(w, x0 + FX + R);
+        constexpr int NL = (HW * 8 + 127) / 128 + 1;
+        for (int i = threadIdx.x; i < (FY + 2 * R) * NL; i += FNT) {
+            const int row = i / NL, ln = i - row * NL;
+            const int y = ys - R + row, x = xs + ln * 16;
+            if (y >= 0 && y < h && x < xe) asm volatile("prefetch.global.L1 [%0];" ::"l"(fin + (size_t)y * w + x));
+        }
+    }
     for (int k = 0; k < nr; ++k) {
         const int y0 = ys + k * FY;
         if (y0 >= h) break;
