@@ -222,7 +222,12 @@ __device__ __forceinline__ void hist_add(unsigned int* h, bool m, unsigned int b
 // until k_thr_fixup) and records each candidate's pixel index.
 template <class Src>
 __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const Src& src,
-                              bool write_bits = false) {
+                              bool write_bits = false, int bi = -1, int nb = 0) {
+    // this CTA's share of the pair's pixels: block bi of nb (default: blockIdx.x of gridDim.x)
+    if (bi < 0) {
+        bi = blockIdx.x;
+        nb = gridDim.x;
+    }
     constexpr int NQ = Src::NQ;
     constexpr int NB = NQ == 1 ? kHistBins : kSelBins;
     constexpr int CB = NQ == 1 ? 2048 : 1024;
@@ -235,6 +240,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     __shared__ unsigned long long smn[NQ], smx[NQ];
     // COLLECT: candidates staged per block in shared memory (one global reservation per query)
     __shared__ unsigned int ccnt[NQ], cbase[NQ];
+    __syncthreads();  // a previous pass / scan of this CTA (k_sel_rest_*) is done with shared memory
     if (threadIdx.x < NQ) {
         st[threadIdx.x] = b.sel[p * kMaxQueries + threadIdx.x];
         smn[threadIdx.x] = ~0ull;
@@ -272,8 +278,8 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     const bool bits = NQ == 1 && write_bits && cq[0];
     // word-aligned block ranges when writing bits (every warp step covers 4 whole words)
     const long long gran = bits ? 4ll * blockDim.x : 4ll;
-    const long long per = cdiv<long long>(cdiv<long long>(n, gridDim.x), gran) * gran;
-    const long long i0 = blockIdx.x * per, i1 = min(n, i0 + per);
+    const long long per = cdiv<long long>(cdiv<long long>(n, nb), gran) * gran;
+    const long long i0 = bi * per, i1 = min(n, i0 + per);
     const int lane = threadIdx.x & 31;
     for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
         const long long base = base0 + 4ll * threadIdx.x;
@@ -556,12 +562,13 @@ constexpr size_t pass_smem(int nq) {
 // group (<= kSelCap keys, all sharing the prefix) by an 8-bit-digit radix select in shared memory.
 constexpr int SCT = 1024;
 
-__global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq, int bits = 0) {
-    extern __shared__ unsigned long long cs[];  // kSelCap candidates
-    const int p = blockIdx.x / nq, q = blockIdx.x % nq;
+// One (pair, query) step of the selection by a CTA of SCT threads; cs: kSelCap keys of shared
+// memory.  Shared by k_sel_scan (one CTA per query) and k_sel_rest_* (one CTA per pair).
+__device__ void sel_scan_body(const MaskBuffers& b, int p, int q, int bits, unsigned long long* cs) {
     SelState* sp = b.sel + p * kMaxQueries + q;
     __shared__ SelState s;
     __shared__ unsigned int part[SCT];
+    __syncthreads();  // a previous step of this CTA is done with shared memory
     if (threadIdx.x == 0) s = *sp;
     __syncthreads();
     if (s.mode == SEL_DONE) return;
@@ -700,6 +707,53 @@ __global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq, int bit
         }
     }
     for (int j = 0; j < PER; ++j) gh[threadIdx.x * PER + j] = 0u;
+}
+
+__global__ void __launch_bounds__(SCT) k_sel_scan(MaskBuffers b, int nq, int bits = 0) {
+    extern __shared__ unsigned long long cs[];  // kSelCap candidates
+    sel_scan_body(b, blockIdx.x / nq, blockIdx.x % nq, bits, cs);
+}
+
+// The selection's remaining steps, one CTA per pair, looping pass + scans in the CTA until every
+// query is done.  Launched once after the passes that normally finish the selection, so the
+// worst case (long runs of equal keys) needs no extra launches and the common case costs one
+// launch that exits at once.
+template <class Src, int NQ>
+__device__ void sel_rest(const Geom& g, const MaskBuffers& b, int p, const Src& src, bool write_bits) {
+    extern __shared__ unsigned long long cs[];
+    __shared__ int open;
+    for (int it = 0; it < 64; ++it) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int o = 0;
+            for (int q = 0; q < NQ; ++q) o |= b.sel[p * kMaxQueries + q].mode != SEL_DONE;
+            open = o;
+        }
+        __syncthreads();
+        if (!open) return;
+        sel_pass_body(g, b, p, src, write_bits, 0, 1);
+        __syncthreads();
+        for (int q = 0; q < NQ; ++q) sel_scan_body(b, p, q, write_bits ? 1 : 0, cs);
+    }
+}
+
+__global__ void __launch_bounds__(SCT) k_sel_rest_a(Geom g, MaskBuffers b) {
+    const int p = blockIdx.x;
+    SrcBufA src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H)};
+    sel_rest<SrcBufA, 4>(g, b, p, src, false);
+}
+
+__global__ void __launch_bounds__(SCT) k_sel_rest_b(Geom g, DevParams P, MaskBuffers b, const double* map,
+                                                    int write_bits) {
+    const int p = blockIdx.x;
+    if (map) {
+        SrcMap src{map};
+        sel_rest<SrcMap, 1>(g, b, p, src, write_bits != 0);
+    } else {
+        SrcSal src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H), b.info[p],
+                   P.flow_weight, 1.0 - P.flow_weight};
+        sel_rest<SrcSal, 1>(g, b, p, src, write_bits != 0);
+    }
 }
 
 __device__ __forceinline__ SelState sel_init(unsigned long long k0, unsigned long long n, bool done,
@@ -1305,9 +1359,20 @@ int grid_for(long long work, int per_block) {
     return (int)(b < 1 ? 1 : b);
 }
 
-constexpr int kSelPasses = 6;  // worst case: 64 key bits / 11; typically 2 (+ the fused first)
+// grid-wide pass + scan launches per phase that normally finish the selection (after the first
+// pass fused into k_mag_grad for phase A); whatever is left is finished by k_sel_rest_*
+constexpr int kSelPassesA = 1, kSelPassesB = 2;
+// FROI_SEL_GRID_PASSES=n overrides both counts (0: every step through k_sel_rest_*; a test knob)
+int sel_passes(int dflt) {
+    static const int v = [] {
+        const char* e = getenv("FROI_SEL_GRID_PASSES");
+        return e ? atoi(e) : -1;
+    }();
+    return v >= 0 ? v : dflt;
+}
 
 size_t scan_smem() { return sizeof(unsigned long long) * kSelCap; }
+size_t rest_smem() { return std::max(scan_smem(), std::max(pass_smem(4), pass_smem(1))); }
 
 // kernel attributes are per device: set on every call (one host thread may drive several devices)
 void set_scan_smem() {
@@ -1316,6 +1381,8 @@ void set_scan_smem() {
     FROI_CUDA(cudaFuncSetAttribute(k_sel_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)scan_smem()));
     FROI_CUDA(cudaFuncSetAttribute(k_thr_fixup, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)(sizeof(unsigned int) * kSelCap)));
+    FROI_CUDA(cudaFuncSetAttribute(k_sel_rest_a, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rest_smem()));
+    FROI_CUDA(cudaFuncSetAttribute(k_sel_rest_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rest_smem()));
 }
 
 int blocks_per_pair(const Geom& g, int n_pairs) {
@@ -1337,12 +1404,15 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
     k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
     *launches += 3;
-    for (int it = 0; it < kSelPasses; ++it) {
+    for (int it = 0; it < sel_passes(kSelPassesA); ++it) {
         k_sel_pass_a<<<dim3(bpp, n_pairs), SNT, pass_smem(4), s>>>(g, b);
         k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }
+    k_sel_rest_a<<<n_pairs, SCT, rest_smem(), s>>>(g, b);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
 }
 
 // Phase B: the round(t*n)-th largest saliency (or map value) and the tie decision.
@@ -1357,12 +1427,15 @@ void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n
     ++*launches;
     // threshold words fused into the collect pass when rows are whole 32-bit words
     const int bits = g.W % 32 == 0 ? 1 : 0;
-    for (int it = 0; it < kSelPasses + 1; ++it) {
+    for (int it = 0; it < sel_passes(kSelPassesB); ++it) {
         k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, pass_smem(1), s>>>(g, P, b, map, bits);
         k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1, bits);
         FROI_LAUNCH_CHECK();
         *launches += 2;
     }
+    k_sel_rest_b<<<n_pairs, SCT, rest_smem(), s>>>(g, P, b, map, bits);
+    FROI_LAUNCH_CHECK();
+    ++*launches;
     k_sel_finish_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n);
     FROI_LAUNCH_CHECK();
     ++*launches;

@@ -209,3 +209,38 @@ def test_extract_report_frames(gpu, oracle):
         assert r["components"] == oracle.component_areas(m).size
         assert r["mask_fraction"] == float(m.mean())
     assert [(r["shift"]["dx"], r["shift"]["dy"]) for r in rows] == [(s.dx, s.dy) for s in info.shifts]
+
+
+def test_selection_rest_kernels_identical(gpu, tmp_path):
+    """Selection finished entirely by the per-pair k_sel_rest_* kernels (FROI_SEL_GRID_PASSES=0,
+    read once per process, so in a subprocess) gives the same masks and stats as the default
+    grid-wide passes, on a sequence with many exactly equal saliency values (static frames) and
+    a moving one."""
+    import os
+    import subprocess
+    import sys
+    from paper_2511_14419_b200.params import ExtractInfo, ExtractParams
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    static = np.stack([textured_frame(128, 96, 8, 7)] * 4)
+    moving = np.stack([cyclic_shift(textured_frame(128, 96, 8, 9), t, t % 2) for t in range(5)])
+    np.save(tmp_path / "static.npy", static)
+    np.save(tmp_path / "moving.npy", moving)
+    script = (
+        "import sys, numpy as np\n"
+        f"sys.path.insert(0, {root!r})\n"
+        "from paper_2511_14419_b200 import flowroi\n"
+        "from paper_2511_14419_b200.params import ExtractInfo, ExtractParams\n"
+        "for name in ('static', 'moving'):\n"
+        f"    f = np.load({str(tmp_path)!r} + '/' + name + '.npy')\n"
+        "    info = ExtractInfo()\n"
+        "    m = flowroi.extract_roi(f, ExtractParams(), info=info)\n"
+        f"    np.save({str(tmp_path)!r} + '/' + name + '_rest.npy', m)\n"
+        f"    np.save({str(tmp_path)!r} + '/' + name + '_fr.npy', np.array(info.raw_fractions))\n")
+    env = dict(os.environ, FROI_SEL_GRID_PASSES="0")
+    subprocess.run([sys.executable, "-c", script], check=True, env=env, cwd=root)
+    for name, frames in (("static", static), ("moving", moving)):
+        info = ExtractInfo()
+        want = gpu.extract_roi(frames, ExtractParams(), info=info)
+        got = np.load(tmp_path / f"{name}_rest.npy")
+        assert np.array_equal(got, want), name
+        assert np.array_equal(np.load(tmp_path / f"{name}_fr.npy"), np.array(info.raw_fractions)), name
