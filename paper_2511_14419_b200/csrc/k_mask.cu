@@ -451,21 +451,26 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
         const int sy = clampi(y + px.dy, 0, H - 1);
         const int sym = clampi(clampi(y - 1, 0, H - 1) + px.dy, 0, H - 1);
         const int syp = clampi(clampi(y + 1, 0, H - 1) + px.dy, 0, H - 1);
+        // row bases once per row (opaque: each gather is then one 32-bit-offset add)
+        const float2* flr = opaque(flw + (unsigned)row);
+        const T* rs = opaque(raw + (unsigned)(sy * W));
+        const T* rm = opaque(raw + (unsigned)(sym * W));
+        const T* rp = opaque(raw + (unsigned)(syp * W));
         for (int xb = 0; xb < W; xb += NPX * PNT_MG) {
             float2 fl[NPX];
             int vl[NPX], vr[NPX], vu[NPX], vd[NPX];
 #pragma unroll
             for (int k = 0; k < NPX; ++k) {
-                const int x = min(xb + threadIdx.x + k * PNT_MG, W - 1);
-                fl[k] = __ldg(flw + row + x);
+                const int x = min(xb + (int)threadIdx.x + k * PNT_MG, W - 1);
+                fl[k] = __ldg(flr + (unsigned)x);
                 if (sizeof(T) == 1 && P.gradient_source == 0) {
-                    const int sx = clampi(x + px.dx, 0, W - 1);
-                    const int sxm = clampi(clampi(x - 1, 0, W - 1) + px.dx, 0, W - 1);
-                    const int sxp = clampi(clampi(x + 1, 0, W - 1) + px.dx, 0, W - 1);
-                    vl[k] = __ldg(raw + sy * W + sxm);
-                    vr[k] = __ldg(raw + sy * W + sxp);
-                    vu[k] = __ldg(raw + sym * W + sx);
-                    vd[k] = __ldg(raw + syp * W + sx);
+                    const unsigned sx = clampi(x + px.dx, 0, W - 1);
+                    const unsigned sxm = clampi(clampi(x - 1, 0, W - 1) + px.dx, 0, W - 1);
+                    const unsigned sxp = clampi(clampi(x + 1, 0, W - 1) + px.dx, 0, W - 1);
+                    vl[k] = __ldg(rs + sxm);
+                    vr[k] = __ldg(rs + sxp);
+                    vu[k] = __ldg(rm + sx);
+                    vd[k] = __ldg(rp + sx);
                 }
             }
 #pragma unroll
@@ -483,8 +488,8 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                     } else {
                         gg = px.grad(x, y);
                     }
-                    fm[row + x] = f;
-                    gr[row + x] = gg;
+                    fm[(unsigned)(row + x)] = f;
+                    gr[(unsigned)(row + x)] = gg;
                     kf = fkey(f);
                     kg = dkey(gg);
                     mnf = fminf(mnf, f);
