@@ -97,7 +97,7 @@ __device__ __forceinline__ void stage_src(const Src& src, float* dst, int bx0, i
 }
 
 // ------------------------------------------------------------------ polynomial expansion
-constexpr int PX = 32, PY = 16, PNT = 256;
+constexpr int PX = 32, PY = 32, PNT = 256;
 
 // RC > 0: compile-time radius (unrolled taps, weights as constant-bank operands); 0: runtime.
 template <typename Src, bool kDebug, int RC = 0>
@@ -148,7 +148,9 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
         __syncthreads();
         const float inv_m20 = P.poly_moments[0], inv_m22 = P.poly_moments[1];
         const float i01 = P.poly_moments[3], i11 = P.poly_moments[4], i12 = P.poly_moments[5];
-        const int xx = tid & (PX - 1), yb = (tid / PX) * 2;
+        const int xx = tid & (PX - 1);
+#pragma unroll 1
+        for (int yb = (tid / PX) * 2; yb < PY; yb += 2 * (PNT / PX)) {
         float q0[6], q1[6], q2[6];
 #pragma unroll
         for (int t = 0; t < 6; ++t) {
@@ -177,6 +179,7 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
             const int o = y * w + x;
             outA[o] = make_float4(a11, a12, a22, bx);
             outB[o] = by;
+        }
         }
         return;
     }
