@@ -1027,10 +1027,12 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
         c->arena_cap = need;
     }
     uint8_t* d_frames = c->d_arena;
-    // copy granularity: a short first chunk (frames 0..first of well 0, all the first batch
-    // needs) then chunks of Pcap frames, each with an event the consuming batches wait on
+    // copy granularity: a first chunk of Pcap + 1 frames (exactly what the first batch needs)
+    // then chunks of Pcap frames, each with an event the consuming batches wait on.  (A shorter
+    // first batch starts sooner but leaves the two lanes in step for the rest of the call: 3 %
+    // slower on a 450-frame well.)
     const int fchunk = std::max(1, c->Pcap);
-    const int first = n_frames > 2 ? std::max(1, std::min(c->Pcap / 4, n_frames - 2)) : 0;
+    const int first = c->Pcap;
     const bool direct = sample_bytes == c->g.sample_bytes && stride == c->frame_bytes;
     std::vector<cudaEvent_t> ready;
     if (direct) {
@@ -1066,8 +1068,7 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
     cudaGetLastError();  // a pageable pointer may leave an error behind
     const bool stream_back = layout == FROI_MASK_PBM && c->params.adjacent_factor == 0 && pinned;
     extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos,
-                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr,
-                      direct ? first : 0);
+                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr);
     if (stream_back) {
         // only frame 0 of each well (a copy of frame 1's mask, made after the batches) is left
         for (int w = 0; w < n_wells; ++w)
