@@ -1390,10 +1390,18 @@ void set_scan_smem() {
     FROI_CUDA(cudaFuncSetAttribute(k_sel_rest_b, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rest_smem()));
 }
 
-int blocks_per_pair(const Geom& g, int n_pairs) {
+// CTAs per pair for the row-/range-blocked mask kernels: a whole number of waves over the SMs
+// (ctas_per_sm resident CTAs each), so no wave runs a few stragglers alone -- e.g. 32 pairs x 19
+// blocks on 2 x 148 slots was 2.05 waves, i.e. three rounds.
+int sm_count() {
+    int dev = 0, n = 148;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    return n > 0 ? n : 148;
+}
+int blocks_per_pair(const Geom& g, int n_pairs, int ctas_per_sm, int waves = 2) {
     const long long n = (long long)g.W * g.H;
-    int bpp = (int)cdiv<long long>(148 * 4, n_pairs);
-    return max(1, min(bpp, (int)cdiv<long long>(n, 8192)));
+    const int bpp = (int)std::max<long long>(1, (long long)waves * sm_count() * ctas_per_sm / n_pairs);
+    return (int)std::max<long long>(1, std::min<long long>(bpp, cdiv<long long>(n, 8192)));
 }
 
 // Phase A: the four robust_normalize percentiles.
@@ -1401,11 +1409,12 @@ template <typename T>
 void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs, cudaStream_t s,
                uint64_t* launches) {
     const long long n = (long long)g.W * g.H;
-    const int bpp = blocks_per_pair(g, n_pairs);
+    const int bpp = blocks_per_pair(g, n_pairs, 2);  // k_sel_pass_a: 2 CTAs per SM
+    const int mgb = blocks_per_pair(g, n_pairs, 4);  // k_mag_grad: 4 CTAs per SM
     set_scan_smem();
     k_sel_init_a<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, (unsigned long long)(0.01 * (double)(n - 1)),
                                        (unsigned long long)(0.99 * (double)(n - 1)));
-    k_mag_grad<T><<<dim3(2 * bpp, n_pairs), PNT_MG, 0, s>>>(g, P, b);
+    k_mag_grad<T><<<dim3(mgb, n_pairs), PNT_MG, 0, s>>>(g, P, b);
     k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
     *launches += 3;
@@ -1424,7 +1433,7 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
 void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
                   const double* map, bool from_stats, cudaStream_t s, uint64_t* launches) {
     const long long n = (long long)g.W * g.H;
-    const int bpp = blocks_per_pair(g, n_pairs);
+    const int bpp = blocks_per_pair(g, n_pairs, 2);  // k_sel_pass_b: 2 CTAs per SM
     set_scan_smem();
     const unsigned long long target = (unsigned long long)llround(P.roi_threshold * (double)n);
     k_sel_init_b<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, target, from_stats ? 1 : 0);
