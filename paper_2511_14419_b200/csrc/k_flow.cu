@@ -957,12 +957,28 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     }
 }
 
-// tiles per strip: as tall as possible while the grid still fills ~4 CTAs per SM
-int strip_tiles(const Geom& g, int l, int n_pairs) {
+// tiles per strip: the least (rounds of resident CTAs) x (rows each CTA computes, halo included)
+// among strips of 1..8 tiles that still fill every CTA slot (2 per SM) once
+int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
+    static const int sms = [] {
+        int dev = 0, n = 148;
+        if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        return n > 0 ? n : 148;
+    }();
+    const long long slots = 2LL * sms;
     const int tx = cdiv(g.lw[l], FX), ty = cdiv(g.lh[l], FY);
-    int nr = 4;
-    while (nr > 1 && (long long)tx * cdiv(ty, nr) * n_pairs < 4 * 148) nr >>= 1;
-    return nr;
+    int best = 1;
+    long long best_cost = -1;
+    for (int nr = 1; nr <= 8; nr *= 2) {
+        const long long ctas = (long long)tx * cdiv(ty, nr) * n_pairs;
+        if (nr > 1 && ctas < slots) break;
+        const long long cost = cdiv(ctas, slots) * (long long)(FY * std::min(nr, ty) + 2 * R);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = nr;
+        }
+    }
+    return best;
 }
 
 template <int R>
@@ -971,7 +987,7 @@ void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const i
     const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * RG;
     // kernel attributes are per device: set on every call (one host thread may drive several)
     FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int nr = strip_tiles(g, a.l, n_pairs);
+    const int nr = strip_tiles(g, a.l, n_pairs, R);
     dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY * nr), n_pairs);
     k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info, nr);
     FROI_LAUNCH_CHECK();
