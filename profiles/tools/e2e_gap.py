@@ -40,11 +40,10 @@ print('host call 1 lane', timed(lambda: ctx.extract_wells_into(hv.numpy()[None],
 # contention probe: the device call while the copy engine uploads a well on another stream
 ctx.set_lanes(2)
 side = torch.cuda.Stream()
-hv2 = torch.empty_like(hv).pin_memory() if False else hv
 dv2 = torch.empty_like(dv)
 def dev_with_copy():
     with torch.cuda.stream(side):
-        dv2.copy_(hv2, non_blocking=True)
+        dv2.copy_(hv, non_blocking=True)
     ctx.extract_wells_device(dv.data_ptr(), 1, F, dm.data_ptr())
 print('device call + concurrent H2D', timed(dev_with_copy))
 # host call with a pageable mask destination (no per-batch read-back; one copy at the end)
