@@ -244,3 +244,16 @@ def test_selection_rest_kernels_identical(gpu, tmp_path):
         got = np.load(tmp_path / f"{name}_rest.npy")
         assert np.array_equal(got, want), name
         assert np.array_equal(np.load(tmp_path / f"{name}_fr.npy"), np.array(info.raw_fractions)), name
+
+
+@pytest.mark.parametrize("w,h", [(40, 36), (65, 33), (100, 70), (129, 64), (31, 97)])
+def test_extract_odd_shapes(gpu, oracle, w, h):
+    """Ragged shapes: widths that are not multiples of 32 (threshold words without the fused
+    path), of 64 (partial flow tiles, clusters of tiles not filling a row) and pyramids that stop
+    after one or two levels; shifts, masks and stats against the oracle as everywhere else."""
+    from paper_2511_14419_b200.params import ExtractParams
+    p = ExtractParams()
+    p.max_shift = 4
+    f = textured_frame(w, h, 8, w + h)
+    frames = np.stack([cyclic_shift(f, t % 2, t // 2) for t in range(4)])
+    _check_sequence(gpu, oracle, frames, params=p)
