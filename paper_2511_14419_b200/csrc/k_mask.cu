@@ -281,6 +281,14 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     const long long per = cdiv<long long>(cdiv<long long>(n, nb), gran) * gran;
     const long long i0 = bi * per, i1 = min(n, i0 + per);
     const int lane = threadIdx.x & 31;
+    // HI: every active query's prefix lies in the keys' high 32 bits (ms >= 32, e.g. right after
+    // the exponent-window digit): prefix tests on the high word alone
+    bool hi = true;
+#pragma unroll
+    for (int q = 0; q < NQ; ++q)
+        if ((hq[q] || cq[q]) && ms[q] < 32) hi = false;
+    auto main_loop = [&](auto hi_tag) {
+    constexpr bool HI = decltype(hi_tag)::value;
     for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
         const long long base = base0 + 4ll * threadIdx.x;
         unsigned long long k[NQ][4];
@@ -305,7 +313,8 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
             if (hq[q]) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const bool m = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
+                    const bool m = v[e] && (ms[q] >= 64 || (HI ? ((unsigned)(k[q][e] >> 32) >> (ms[q] - 32)) == (unsigned)mp[q]
+                                                               : (k[q][e] >> ms[q]) == mp[q]));
                     const unsigned int bin = fp[q] ? (unsigned int)fpw_bin(k[q][e], fp[q])
                                                    : (unsigned int)((k[q][e] >> sh[q]) & ((1u << wd[q]) - 1u));
                     if (fp[q]) {  // exponent-window bins are spread out: plain shared atomics
@@ -323,9 +332,11 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                 unsigned int nib = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    m[e] = v[e] && (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]);
+                    const unsigned long long kp = HI ? (unsigned long long)((unsigned)(k[q][e] >> 32) >> (ms[q] - 32))
+                                                     : (ms[q] < 64 ? k[q][e] >> ms[q] : 0ull);
+                    m[e] = v[e] && (ms[q] >= 64 || kp == mp[q]);
                     any |= m[e];
-                    if (v[e] && ms[q] < 64 && (k[q][e] >> ms[q]) > mp[q]) nib |= 1u << e;
+                    if (v[e] && ms[q] < 64 && kp > mp[q]) nib |= 1u << e;
                 }
                 if (bits) {
                     // lane l holds bits 4(l%8)..+3 of word (base0 + 128 w_l)/32 + l/8
@@ -363,6 +374,9 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
             }
         }
     }
+    };
+    if (hi) main_loop(std::true_type{});
+    else main_loop(std::false_type{});
     if (anyc) {
         __syncthreads();
         if (threadIdx.x < NQ && cq[threadIdx.x]) {
