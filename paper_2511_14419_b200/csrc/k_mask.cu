@@ -56,8 +56,10 @@ struct PairPix {
     }
 };
 
+// Branch-free: a degenerate range has inv = 0, so t is +-0 -- the same key and the same order as
+// the reference's 0 (keys map -0 to +0; -0 + x == x for x != 0).  `zero` is kept for callers.
 __device__ __forceinline__ double normalize(double v, double lo, double inv, int zero) {
-    if (zero) return 0.0;
+    (void)zero;
     const double t = dmul(dsub(v, lo), inv);
     return t < 0.0 ? 0.0 : (1.0 < t ? 1.0 : t);
 }
@@ -1369,7 +1371,7 @@ __global__ void __launch_bounds__(256) k_saliency_map(Geom g, DevParams P, MaskB
     const SrcSal src = make_thr_src<SrcSal>(g, P, b, 0, nullptr);
     const long long n = (long long)g.W * g.H;
     for (long long i = blockIdx.x * 256LL + threadIdx.x; i < n; i += (long long)gridDim.x * 256)
-        out[i] = src.value(i);
+        out[i] = dadd(src.value(i), 0.0);  // -0 (degenerate range, see normalize) reads as +0
 }
 
 int grid_for(long long work, int per_block) {
