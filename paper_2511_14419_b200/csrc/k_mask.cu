@@ -261,13 +261,13 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
         for (int i = threadIdx.x; i < NQ * NB; i += blockDim.x) (&hist[0][0])[i] = 0;
         __syncthreads();
     }
-    bool hq[NQ], cq[NQ];
+    unsigned hqm = 0u, cqm = 0u;  // queries in HIST / COLLECT mode (bit q)
     int sh[NQ], wd[NQ], fp[NQ], ms[NQ];
     unsigned long long mp[NQ], lmn[NQ], lmx[NQ];
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        hq[q] = st[q].mode == SEL_HIST;
-        cq[q] = st[q].mode == SEL_COLLECT;
+        hqm |= (st[q].mode == SEL_HIST ? 1u : 0u) << q;
+        cqm |= (st[q].mode == SEL_COLLECT ? 1u : 0u) << q;
         sel_digit(st[q].bits_done, sh[q], wd[q]);
         fp[q] = (NQ == 1 && st[q].bits_done == 0) ? st[q].fpw : 0;
         ms[q] = 64 - st[q].bits_done;  // keys match when key >> ms == prefix >> ms (ms < 64)
@@ -275,9 +275,19 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
         lmn[q] = ~0ull;
         lmx[q] = 0ull;
     }
+    // high-word prefix test (HI passes): (hi >> s32) & m32 == p32, with m32 = 0 matching every key
+    // while no digit is fixed yet
+    unsigned s32[NQ], m32[NQ], p32[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const bool all = ms[q] >= 64;
+        s32[q] = all ? 0u : (unsigned)max(0, ms[q] - 32);
+        m32[q] = all ? 0u : ~0u;
+        p32[q] = all ? 0u : (unsigned)mp[q];
+    }
     const long long n = (long long)g.W * g.H;
     const bool vec = (n & 3) == 0;
-    const bool bits = NQ == 1 && write_bits && cq[0];
+    const bool bits = NQ == 1 && write_bits && (cqm & 1u);
     // word-aligned block ranges when writing bits (every warp step covers 4 whole words)
     const long long gran = bits ? 4ll * blockDim.x : 4ll;
     const long long per = cdiv<long long>(cdiv<long long>(n, nb), gran) * gran;
@@ -288,7 +298,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     bool hi = true;
 #pragma unroll
     for (int q = 0; q < NQ; ++q)
-        if ((hq[q] || cq[q]) && ms[q] < 32) hi = false;
+        if ((((hqm >> q) & 1u) || ((cqm >> q) & 1u)) && ms[q] < 32) hi = false;
     auto main_loop = [&](auto hi_tag) {
     constexpr bool HI = decltype(hi_tag)::value;
     for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
@@ -312,11 +322,11 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
         }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-            if (hq[q]) {
+            if (((hqm >> q) & 1u)) {
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const bool m = v[e] && (ms[q] >= 64 || (HI ? ((unsigned)(k[q][e] >> 32) >> (ms[q] - 32)) == (unsigned)mp[q]
-                                                               : (k[q][e] >> ms[q]) == mp[q]));
+                    const bool m = v[e] && (HI ? (((unsigned)(k[q][e] >> 32) >> s32[q]) & m32[q]) == p32[q]
+                                               : (ms[q] >= 64 || (k[q][e] >> ms[q]) == mp[q]));
                     const unsigned int bin = fp[q] ? (unsigned int)fpw_bin(k[q][e], fp[q])
                                                    : (unsigned int)((k[q][e] >> sh[q]) & ((1u << wd[q]) - 1u));
                     if (fp[q]) {  // exponent-window bins are spread out: plain shared atomics
@@ -329,16 +339,16 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
                         lmx[q] = max(lmx[q], k[q][e]);
                     }
                 }
-            } else if (cq[q]) {
+            } else if (((cqm >> q) & 1u)) {
                 bool m[4], any = false;
                 unsigned int nib = 0;
 #pragma unroll
                 for (int e = 0; e < 4; ++e) {
-                    const unsigned long long kp = HI ? (unsigned long long)((unsigned)(k[q][e] >> 32) >> (ms[q] - 32))
+                    const unsigned long long kp = HI ? (unsigned long long)(((unsigned)(k[q][e] >> 32) >> s32[q]) & m32[q])
                                                      : (ms[q] < 64 ? k[q][e] >> ms[q] : 0ull);
-                    m[e] = v[e] && (ms[q] >= 64 || kp == mp[q]);
+                    m[e] = v[e] && (HI ? (unsigned)kp == p32[q] : (ms[q] >= 64 || kp == mp[q]));
                     any |= m[e];
-                    if (v[e] && ms[q] < 64 && kp > mp[q]) nib |= 1u << e;
+                    if (v[e] && ms[q] < 64 && (HI ? (unsigned)kp > p32[q] : kp > mp[q])) nib |= 1u << e;
                 }
                 if (bits) {
                     // lane l holds bits 4(l%8)..+3 of word (base0 + 128 w_l)/32 + l/8
@@ -381,13 +391,13 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     else main_loop(std::false_type{});
     if (anyc) {
         __syncthreads();
-        if (threadIdx.x < NQ && cq[threadIdx.x]) {
+        if (threadIdx.x < NQ && ((cqm >> threadIdx.x) & 1u)) {
             const unsigned int c = min(ccnt[threadIdx.x], (unsigned int)CB);
             cbase[threadIdx.x] = c ? atomicAdd(b.cand_count + p * kMaxQueries + threadIdx.x, c) : 0u;
         }
         __syncthreads();
         for (int q = 0; q < NQ; ++q) {
-            if (!cq[q]) continue;
+            if (!((cqm >> q) & 1u)) continue;
             const unsigned int c = min(ccnt[q], (unsigned int)CB);
             unsigned long long* dst = b.cand + ((size_t)p * kMaxQueries + q) * kSelCap;
             for (unsigned int i = threadIdx.x; i < c; i += blockDim.x)
@@ -400,7 +410,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     if (!anyh) return;
 #pragma unroll
     for (int q = 0; q < NQ; ++q) {
-        if (!hq[q]) continue;
+        if (!((hqm >> q) & 1u)) continue;
         unsigned long long a = lmn[q], c = lmx[q];
         for (int o = 16; o > 0; o >>= 1) {
             a = min(a, __shfl_xor_sync(0xffffffffu, a, o));
@@ -413,7 +423,7 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
     }
     __syncthreads();
     for (int q = 0; q < NQ; ++q) {
-        if (!hq[q]) continue;
+        if (!((hqm >> q) & 1u)) continue;
         unsigned int* gh = b.hist + ((size_t)p * kMaxQueries + q) * kHistBins;
         for (int i = threadIdx.x; i < NB; i += blockDim.x)
             if (hist[q][i]) atomicAdd(gh + i, hist[q][i]);
