@@ -499,10 +499,14 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                     vd[k] = __ldg(rp + sx);
                 }
             }
+            // a whole chunk inside the row (every chunk when W is a multiple of NPX*PNT_MG) runs
+            // without per-pixel validity branches
+            auto consume = [&](auto full_tag) {
+            constexpr bool FULL = decltype(full_tag)::value;
 #pragma unroll
             for (int k = 0; k < NPX; ++k) {
                 const int x = xb + threadIdx.x + k * PNT_MG;
-                const bool v = x < W;
+                const bool v = FULL || x < W;
                 unsigned long long kf = 0, kg = 0;
                 if (v) {
                     const float f = hypotf_glibc(fl[k].x, fl[k].y);
@@ -528,6 +532,9 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                     atomicAdd(&hist[1][fpw_bin(kg, 1)], 1u);
                 }
             }
+            };
+            if (xb + NPX * PNT_MG <= W) consume(std::true_type{});
+            else consume(std::false_type{});
         }
     }
     unsigned long long kmnf = mnf == __int_as_float(0x7f800000) ? ~0ull : fkey(mnf), kmxf = fkey(mxf);
