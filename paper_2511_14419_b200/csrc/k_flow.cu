@@ -731,11 +731,6 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     const float* nB = opaque((sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo);
     const float2* fin = opaque(a.flow_in + pair_off + lo);
     float2* out = opaque(a.flow_out + pair_off + lo);
-    __shared__ float rcx[FX], rcy[FY];
-    if (threadIdx.x < FX) {
-        const int x = x0 + threadIdx.x;
-        rcx[threadIdx.x] = __frcp_rn((float)(min(w - 1, x + R) - max(0, x - R) + 1));
-    }
     if (a.mode) {
         // the first tile's prior rows (its later tiles' rows are prefetched during phase 2):
         // later pair rounds of the first tile then find them in L1
@@ -868,10 +863,6 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         const int ry0 = ys - R + r0, ry1 = ry0 + npx / HW;
         if (x0 - R >= 0 && x0 + FX + R <= w && ry0 >= 0 && ry1 <= h) phase1(std::true_type{});
         else phase1(std::false_type{});
-        if (threadIdx.x < FY) {
-            const int y = y0 + threadIdx.x;
-            rcy[threadIdx.x] = __frcp_rn((float)(min(h - 1, y + R) - max(0, y - R) + 1));
-        }
         __syncthreads();
         // the threads phase 2 leaves idle pull the next tile's prior rows into L1, so its
         // gathers do not start behind an L2/DRAM round trip
@@ -926,19 +917,19 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             hrow[31] = pv;
         }
         __syncthreads();
-        // phase 4: clipped-window means and the 2x2 solve (flow.hpp:242-253).  fp32 with a
-        // compensated determinant (Kahan: the g12^2 rounding error is carried exactly).
+        // phase 4: the 2x2 solve of the clipped-window means (flow.hpp:242-253) on the window
+        // sums: the solution and the det > 1e-9 ||G||^2 test are invariant to the common 1/count
+        // scale, so it is never applied.  fp32 with a compensated determinant (Kahan: the g12^2
+        // rounding error is carried exactly).
         const int tx = threadIdx.x % FX, x = x0 + tx;
-        const float icx = rcx[tx];
 #pragma unroll 1
         for (int j = 0; j < FY / (FNT / FX); ++j) {
             const int ty = threadIdx.x / FX + j * (FNT / FX), y = y0 + ty;
             if (x >= w || y >= h) continue;
-            const float inv = icx * rcy[ty];
             const int rr = b0 + ty;
             const int sidx = (rr >= RG ? rr - RG : rr) * SW + tx;
-            const float g11 = G[sidx] * inv, g12 = G[PL + sidx] * inv, g22 = G[2 * PL + sidx] * inv;
-            const float h1 = G[3 * PL + sidx] * inv, h2 = G[4 * PL + sidx] * inv;
+            const float g11 = G[sidx], g12 = G[PL + sidx], g22 = G[2 * PL + sidx];
+            const float h1 = G[3 * PL + sidx], h2 = G[4 * PL + sidx];
             const float q = g12 * g12;
             const float qe = fmaf(g12, g12, -q);
             const float det = fmaf(g11, g22, -q) - qe;
@@ -953,7 +944,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             }
             out[y * w + x] = r;
         }
-        __syncthreads();  // ring rows and rcy are rewritten by the next tile
+        __syncthreads();  // ring rows are rewritten by the next tile
     }
 }
 
