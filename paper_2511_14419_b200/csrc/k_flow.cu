@@ -657,12 +657,12 @@ __device__ __forceinline__ GTerms g_terms(const GLoad& o, float du, float dv) {
     fma2(n22, nbx, q10.z, q10.w, w10, w10, n22, nbx);
     fma2(n22, nbx, q11.z, q11.w, w11, w11, n22, nbx);
     const float nby = fmaf(o.b11, w11, fmaf(o.b10, w10, fmaf(o.b01, w01, o.b00 * w00)));
+    // A and delta-b at twice the reference's scale (the 1/2 of the averages dropped): every
+    // product below is then exactly 4x, and the solve is scale-invariant, so the flow is unchanged
     float a11, a12, a22, e1;
-    add2(a11, a12, pa.x, pa.y, n11, n12);
-    mul2(a11, a12, a11, a12, 0.5f, 0.5f);
-    add2(a22, e1, pa.z, -pa.w, n22, nbx);          // (pa.z + n22, nbx - pa.w)
-    mul2(a22, e1, a22, e1, 0.5f, -0.5f);           // a22, -0.5 (nbx - bx_prev)
-    const float e2 = -0.5f * (nby - o.pb);
+    add2(a11, a12, pa.x, pa.y, n11, n12);          // 2 a11, 2 a12
+    add2(a22, e1, pa.z, pa.w, n22, -nbx);          // 2 a22, -(nbx - bx_prev)
+    const float e2 = o.pb - nby;
     float db1, db2;
     fma2(db1, db2, a11, a12, du, du, e1, e2);      // + A d (first column)
     fma2(db1, db2, a12, a22, dv, dv, db1, db2);    // + A d (second column)
