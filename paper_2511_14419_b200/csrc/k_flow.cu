@@ -684,6 +684,23 @@ __device__ __forceinline__ GTerms g_terms(const GLoad& o, float du, float dv) {
 // reads.  RG = 48 >= FY + 2R keeps the footprint at ~76 KB, leaving the L1 room the gathers need.
 constexpr int RG = 48;
 
+// Ring row stride SW and plane stride PL (floats).  SW is odd, so phase 3 (a warp walks 32 rows
+// of one column) is conflict-free.  With PAD, SW is also chosen so that 2 SW == HW (mod 32) and
+// PL == HW (mod 32): the phase-1 warps that wrap from one pixel-pair row to the next, and the
+// phase-2 warps that wrap from one plane to the next, then still address 32 consecutive banks.
+constexpr int ring_sw(int hw, bool pad) {
+    int s = hw + 1;
+    if (pad && ((hw / 2) & 1))
+        while (((2 * s - hw) & 31) != 0 || !(s & 1)) ++s;
+    return s;
+}
+constexpr int ring_pl(int hw, bool pad) {
+    int p = ring_sw(hw, pad) * RG;
+    if (pad)
+        while (((p - hw) & 31) != 0) ++p;
+    return p;
+}
+
 // vertical (2R+1)-row running sums down one ring column (FY outputs, rows from slot BOFF on),
 // written in place one step behind: a thread owns its column, and output j-1 overwrites row j-1
 // only after row j-1 was subtracted for output j
@@ -702,7 +719,7 @@ __device__ __forceinline__ void vsum_inplace(float* col) {
     col[((BOFF + FY - 1) % RG) * SW] = pv;
 }
 
-template <int R>
+template <int R, bool PAD>
 __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const float4* __restrict__ exA_f,
                                                       const float* __restrict__ exB_f,
@@ -713,7 +730,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const PairInfo* __restrict__ info, int nr) {
     extern __shared__ float smem_f[];
     // ring rows are SW = HW + 1 floats apart (odd stride: the row-wise box pass is conflict-free)
-    constexpr int HW = FX + 2 * R, SW = HW + 1, PL = SW * RG;
+    constexpr int HW = FX + 2 * R, SW = ring_sw(HW, PAD), PL = ring_pl(HW, PAD);
     static_assert(FY + 2 * R <= RG && FY == 32 && RG == 48, "ring layout");
     const int p = blockIdx.z;
     const int l = a.l;
@@ -972,16 +989,23 @@ int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
     return best;
 }
 
+template <int R, bool PAD>
+void launch_iter_t(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
+                   const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
+    const size_t smem = sizeof(float) * 5 * (size_t)ring_pl(FX + 2 * R, PAD);
+    // kernel attributes are per device: set on every call (one host thread may drive several)
+    FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int nr = strip_tiles(g, a.l, n_pairs, R);
+    dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY * nr), n_pairs);
+    k_flow_iter<R, PAD><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info, nr);
+    FROI_LAUNCH_CHECK();
+}
+
 template <int R>
 void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                  const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 5 * (size_t)(FX + 2 * R + 1) * RG;
-    // kernel attributes are per device: set on every call (one host thread may drive several)
-    FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int nr = strip_tiles(g, a.l, n_pairs, R);
-    dim3 grid(cdiv(g.lw[a.l], FX), cdiv(g.lh[a.l], FY * nr), n_pairs);
-    k_flow_iter<R><<<grid, FNT, smem, s>>>(g, a, b.exA_f, b.exB_f, b.exA_p, b.exB_p, d_prev, d_next, d_info, nr);
-    FROI_LAUNCH_CHECK();
+    // padded ring (A/B on the C3 bench: -2.1 % k_flow_iter time vs SW = HW + 1)
+    launch_iter_t<R, true>(g, a, b, d_prev, d_next, d_info, n_pairs, s);
 }
 
 template <typename K>
