@@ -40,6 +40,17 @@ __device__ __forceinline__ void bfly(double2& u, double2& v, const double2 w) {
 // minimum for 16-byte elements, for rows and column blocks alike (checked offline for n = 2^8..2^12).
 __device__ __forceinline__ int pd(int i) { return i + (i >> 4) + (i >> 7); }
 __host__ __device__ constexpr int padded(int n) { return n + (n >> 4) + (n >> 7) + 1; }
+struct PadStd {
+    static __device__ __forceinline__ int at(int i) { return pd(i); }
+};
+// The cross-power kernel's layout (4 interleaved rows, radix-8 passes, bit-reversed scatter from
+// row-major element order): pads every 8, 256 and 512 elements put every quarter-warp of a
+// 128-bit access on 8 distinct bank groups (checked offline for n = 1024: the standard layout
+// costs 2x the ideal wavefronts on the scatter and 1.25x on the passes).
+struct PadX {
+    static __device__ __forceinline__ int at(int i) { return i + (i >> 3) + (i >> 8) + (i >> 9); }
+};
+__host__ __device__ constexpr int padded_x(int n) { return n + (n >> 3) + (n >> 8) + (n >> 9) + 1; }
 
 // Q consecutive radix-2 stages (half-lengths h, 2h, .., h*2^(Q-1), h = 2^s) over groups of
 // 2^Q elements {i + m*h} held in registers, for `1 << lc` interleaved transforms of length n
@@ -52,7 +63,7 @@ __host__ __device__ constexpr int padded(int n) { return n + (n >> 4) + (n >> 7)
 // outputs q with q = p mod 2^(t+1), so a group whose positions k + m*h (m < 2^Q) hit no needed
 // residue mod T = h*2^Q is skipped; every input of a computed group is then itself needed, so the
 // outputs read are exactly the reference's.
-template <int Q>
+template <int Q, typename Pad = PadStd>
 __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
                                          const double2* __restrict__ tw, int prune_m = -1) {
     constexpr int G = 1 << Q;
@@ -66,7 +77,7 @@ __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
         const int i = ((b >> s) << (s + Q)) + k;
         double2 e[G];
 #pragma unroll
-        for (int m = 0; m < G; ++m) e[m] = a[(pd(i + m * h) << lc) | c];
+        for (int m = 0; m < G; ++m) e[m] = a[(Pad::at(i + m * h) << lc) | c];
 #pragma unroll
         for (int q = 0; q < Q; ++q) {
             const int hq = h << q;
@@ -78,7 +89,7 @@ __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
             }
         }
 #pragma unroll
-        for (int m = 0; m < G; ++m) a[(pd(i + m * h) << lc) | c] = e[m];
+        for (int m = 0; m < G; ++m) a[(Pad::at(i + m * h) << lc) | c] = e[m];
     }
     __syncthreads();
 }
@@ -91,15 +102,15 @@ __device__ __forceinline__ const double2* stage_tw(double2* dst, const double2* 
 }
 
 // All log2n stages, QM per pass; input already bit-reversed.
-template <int QM>
+template <int QM, typename Pad = PadStd>
 __device__ __forceinline__ void fft_stages(double2* a, int n, int log2n, int lc,
                                            const double2* __restrict__ tw, int prune_m = -1) {
     int s = 0;
-    for (; s + QM <= log2n; s += QM) fft_pass<QM>(a, n, s, lc, tw, prune_m);
+    for (; s + QM <= log2n; s += QM) fft_pass<QM, Pad>(a, n, s, lc, tw, prune_m);
     switch (log2n - s) {
-        case 3: fft_pass<3>(a, n, s, lc, tw, prune_m); break;
-        case 2: fft_pass<2>(a, n, s, lc, tw, prune_m); break;
-        case 1: fft_pass<1>(a, n, s, lc, tw, prune_m); break;
+        case 3: fft_pass<3, Pad>(a, n, s, lc, tw, prune_m); break;
+        case 2: fft_pass<2, Pad>(a, n, s, lc, tw, prune_m); break;
+        case 1: fft_pass<1, Pad>(a, n, s, lc, tw, prune_m); break;
         default: break;
     }
 }
@@ -265,11 +276,11 @@ __global__ void __launch_bounds__(NT, 3) k_xpow_rows_inv(int pw, int ph, int log
                 const double m = hypot_glibc(re, im);
                 rr[u] = m > 1e-12 ? make_double2(ddiv(re, m), ddiv(im, m)) : make_double2(0.0, 0.0);
             }
-            a[(pd(brev(x, log2pw)) << lc) | r] = rr[u];
+            a[(PadX::at(brev(x, log2pw)) << lc) | r] = rr[u];
         }
     }
     __syncthreads();
-    fft_stages<kQXpow>(a, pw, log2pw, lc, itw, M);  // only the 2M+1 wrapped columns are read
+    fft_stages<kQXpow, PadX>(a, pw, log2pw, lc, itw, M);  // only the 2M+1 wrapped columns are read
     const double inv = ddiv(1.0, (double)pw);
     const int nc = 2 * M + 1;
     for (int e = threadIdx.x; e < nc * R; e += NT) {
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(NT, 3) k_xpow_rows_inv(int pw, int ph, int log
         if (y >= ph) continue;
         const int dx = ci - M;
         const int x = dx < 0 ? dx + pw : dx;
-        const double2 v = a[(pd(x) << lc) | r];
+        const double2 v = a[(PadX::at(x) << lc) | r];
         cols[((size_t)p * nc + ci) * ph + y] = make_double2(dmul(v.x, inv), dmul(v.y, inv));
     }
 }
@@ -419,7 +430,7 @@ void launch_register_pairs(const Geom& g, const DevParams& p, const double2* d_s
     if (n_pairs <= 0) return;
     const int M = p.max_shift;
     const int lr = rows_lc(g.log2pw);
-    const size_t smem_r = sizeof(double2) * ((size_t)padded(g.pw) << lr);
+    const size_t smem_r = sizeof(double2) * ((size_t)padded_x(g.pw) << lr);
     set_smem(k_xpow_rows_inv, smem_r);
     k_xpow_rows_inv<<<dim3(cdiv(g.ph, 1 << lr), n_pairs), NT, smem_r, s>>>(g.pw, g.ph, g.log2pw, M, d_spec,
                                                                          d_prev, d_next, d_itw_row, d_cols);
