@@ -217,8 +217,11 @@ def run_reference(args) -> None:
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1000.0 * r["seconds"] / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "C3 wells (64 x 450 frames, 1024x1024 u8), bounded CPU sample",
-                   "frames_per_step": frames, "parallelism": f"host threads={cores}"},
+        "config": {"workload": "C3: 64 wells x 450 frames, 1024x1024 u8 (one full well per "
+                               "rank per step, well (i*N+r) mod 64)",
+                   "sample": f"bounded CPU sample: {frames} frames of a C3 well per step",
+                   "frames_per_step": frames, "parallelism": f"host threads={cores}",
+                   "params": "ExtractParams{} defaults (pyramid 3, window 15, threshold 0.2)"},
         "impl": "reference",
         "cpu_baseline": {"value": r["value"], "unit": UNIT, "cores": cores, "kind": r["kind"],
                          "sample": r["sample"]},
