@@ -685,16 +685,16 @@ __device__ __forceinline__ GTerms g_terms(const GLoad& o, float du, float dv) {
 constexpr int RG = 48;
 
 // Ring row stride SW and plane stride PL (floats).  SW is odd, so phase 3 (a warp walks 32 rows
-// of one column) is conflict-free.  With PAD, SW is also chosen so that 2 SW == HW (mod 32) and
-// PL == HW (mod 32): the phase-1 warps that wrap from one pixel-pair row to the next, and the
-// phase-2 warps that wrap from one plane to the next, then still address 32 consecutive banks.
-constexpr int ring_sw(int hw, bool pad) {
+// of one column) is conflict-free.  PAD 2: PL == HW (mod 32), so the phase-2 warps that wrap from
+// one plane to the next still address 32 consecutive banks.  PAD 1: also 2 SW == HW (mod 32), for
+// the phase-1 warps that wrap from one pixel-pair row to the next (no faster, 7.5 KB larger).
+constexpr int ring_sw(int hw, int pad) {
     int s = hw + 1;
-    if (pad && ((hw / 2) & 1))
+    if (pad == 1 && ((hw / 2) & 1))
         while (((2 * s - hw) & 31) != 0 || !(s & 1)) ++s;
     return s;
 }
-constexpr int ring_pl(int hw, bool pad) {
+constexpr int ring_pl(int hw, int pad) {
     int p = ring_sw(hw, pad) * RG;
     if (pad)
         while (((p - hw) & 31) != 0) ++p;
@@ -719,7 +719,7 @@ __device__ __forceinline__ void vsum_inplace(float* col) {
     col[((BOFF + FY - 1) % RG) * SW] = pv;
 }
 
-template <int R, bool PAD>
+template <int R, int PAD>
 __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                                       const float4* __restrict__ exA_f,
                                                       const float* __restrict__ exB_f,
@@ -989,7 +989,7 @@ int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
     return best;
 }
 
-template <int R, bool PAD>
+template <int R, int PAD>
 void launch_iter_t(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                    const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
     const size_t smem = sizeof(float) * 5 * (size_t)ring_pl(FX + 2 * R, PAD);
@@ -1004,8 +1004,10 @@ void launch_iter_t(const Geom& g, const IterArgs& a, const FlowBuffers& b, const
 template <int R>
 void launch_iter(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                  const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
-    // padded ring (A/B on the C3 bench: -2.1 % k_flow_iter time vs SW = HW + 1)
-    launch_iter_t<R, true>(g, a, b, d_prev, d_next, d_info, n_pairs, s);
+    // plane-padded ring (A/B on the C3 bench, k_flow_iter time: no padding 276.4 us, row and
+    // plane padding 270.1 us, plane padding only 270.0 us with 7.5 KB less shared memory per CTA,
+    // which keeps two CTAs inside the 164 KB carveout: L1 92 KB instead of 60 KB)
+    launch_iter_t<R, 2>(g, a, b, d_prev, d_next, d_info, n_pairs, s);
 }
 
 template <typename K>
