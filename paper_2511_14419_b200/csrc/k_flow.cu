@@ -374,67 +374,57 @@ __device__ __forceinline__ void pyr_tile(const Src& src, int w, int h, int tw, i
 // pyr_tile; loops and divisions are compile-time, the column blur walks 8 rows per thread.
 constexpr int Q2X = 32, Q2Y = 16, Q2W = 2 * Q2X + 6, Q2H = 2 * Q2Y + 6;
 
+// Even sizes: the 0.5 bilinear resample of the blurred image is the mean of each 2x2 block
+// (SURVEY.md §8 a6), so blur + resample is one separable 8-tap filter c = (k * [1, 1]) / 2
+// evaluated at stride 2: only the kept samples are computed (half the row-pass work, a quarter
+// of the column-pass work of blurring every pixel first).  fp32, like the rest of the pyramid.
 template <typename Src>
 __device__ __forceinline__ void pyr2_tile(const Src& src, int tw, int th, const float* kblur,
                                           float* out, float* smem) {
-    float* s_in = smem;                  // Q2H x Q2W input (edge-clamped by the source)
-    float* s_rb = s_in + Q2H * Q2W;      // Q2H x 64 row-blurred
-    float* s_bl = s_rb + Q2H * 2 * Q2X;  // 32 x 64 blurred
+    float* s_in = smem;              // Q2H x Q2W input (edge-clamped by the source)
+    float* s_r = s_in + Q2H * Q2W;   // Q2H x Q2X row-filtered, stride 2
     const int ox0 = blockIdx.x * Q2X, oy0 = blockIdx.y * Q2Y;
     const int ix0 = 2 * ox0 - 3, iy0 = 2 * oy0 - 3;
     const int tid = threadIdx.x;
     stage_src<QNT, 4>(src, s_in, ix0, iy0, Q2W, Q2H, 0.f);
+    float c[8];
+    c[0] = 0.5f * kblur[0];
+#pragma unroll
+    for (int u = 1; u < 7; ++u) c[u] = 0.5f * (kblur[u - 1] + kblur[u]);
+    c[7] = 0.5f * kblur[6];
     __syncthreads();
-    float k[7];
-#pragma unroll
-    for (int t = 0; t < 7; ++t) k[t] = kblur[t];
-    // row blur: two adjacent columns per thread from 8 loads
+    // rows: output column ox of input row yy from 8 consecutive inputs (four 8-byte loads)
     for (int i = tid; i < Q2H * Q2X; i += QNT) {
-        const int yy = i / Q2X, xx = 2 * (i - yy * Q2X);
-        const float* row = s_in + yy * Q2W + xx;
-        float v[8];
+        const int yy = i / Q2X, ox = i - yy * Q2X;
+        const float2* row = (const float2*)(s_in + yy * Q2W + 2 * ox);
+        float acc = 0.f;
 #pragma unroll
-        for (int t = 0; t < 8; ++t) v[t] = row[t];
-        float a0 = 0.f, a1 = 0.f;
-#pragma unroll
-        for (int t = 0; t < 7; ++t) {
-            a0 += k[t] * v[t];
-            a1 += k[t] * v[t + 1];
+        for (int m = 0; m < 4; ++m) {
+            const float2 v = row[m];
+            acc = fmaf(c[2 * m], v.x, acc);
+            acc = fmaf(c[2 * m + 1], v.y, acc);
         }
-        s_rb[yy * 2 * Q2X + xx] = a0;
-        s_rb[yy * 2 * Q2X + xx + 1] = a1;
+        s_r[i] = acc;
     }
     __syncthreads();
-    // column blur: 8 consecutive rows of one column per thread from 14 loads
+    // columns: two vertically adjacent outputs per thread share 6 of their 8 input rows
     {
-        const int xx = tid & (2 * Q2X - 1), yb = (tid >> 6) * 8;
-        float v[14];
+        const int xx = tid & (Q2X - 1), yy = 2 * (tid >> 5);
+        const int x = ox0 + xx;
+        float v[10];
 #pragma unroll
-        for (int t = 0; t < 14; ++t) v[t] = s_rb[(yb + t) * 2 * Q2X + xx];
+        for (int t = 0; t < 10; ++t) v[t] = s_r[(2 * yy + t) * Q2X + xx];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
+        for (int r = 0; r < 2; ++r) {
+            const int y = oy0 + yy + r;
             float acc = 0.f;
 #pragma unroll
-            for (int t = 0; t < 7; ++t) acc += k[t] * v[r + t];
-            s_bl[(yb + r) * 2 * Q2X + xx] = acc;
+            for (int t = 0; t < 8; ++t) acc = fmaf(c[t], v[2 * r + t], acc);
+            if (x < tw && y < th) out[(size_t)y * tw + x] = acc;
         }
     }
-    __syncthreads();
-    // resample: fraction 0.5 on both axes (pyr_tile's expression with ffx = ffy = 0.5)
-#pragma unroll
-    for (int k2 = 0; k2 < 2; ++k2) {
-        const int xx = tid & (Q2X - 1), yy = (tid >> 5) + 8 * k2;
-        const int x = ox0 + xx, y = oy0 + yy;
-        if (x >= tw || y >= th) continue;
-        const float* r0 = s_bl + (2 * yy) * 2 * Q2X + 2 * xx;
-        const float* r1 = r0 + 2 * Q2X;
-        const float f = 0.5f;
-        const float top = r0[0] * (1.f - f) + r0[1] * f;
-        const float bot = r1[0] * (1.f - f) + r1[1] * f;
-        out[(size_t)y * tw + x] = top * (1.f - f) + bot * f;
-    }
 }
-constexpr size_t pyr2_smem() { return sizeof(float) * (Q2H * Q2W + Q2H * 2 * Q2X + 2 * Q2Y * 2 * Q2X); }
+constexpr size_t pyr2_smem() { return sizeof(float) * (Q2H * Q2W + Q2H * Q2X); }
 
 template <typename T, bool HALF>
 __global__ void __launch_bounds__(QNT) k_pyr0_frame(Geom g, DevParams P, const T* den, float* pyr,
