@@ -173,18 +173,82 @@ def barrier(dist):
         dist.barrier()
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch_ranks(n: int, argv: list[str], need_gpus: bool = True) -> int:
+    """`bench.py --gpus N` without an external launcher: one process per GPU (RANK / LOCAL_RANK /
+    WORLD_SIZE / MASTER_* set as torchrun would, rendezvous on 127.0.0.1).  Refuses to run when
+    fewer than N GPUs are visible instead of measuring fewer.  Returns the worst exit code."""
+    if need_gpus:
+        import torch
+        vis = torch.cuda.device_count()
+        if vis < n:
+            print(f"bench.py: --gpus {n} but only {vis} CUDA device(s) are visible", file=sys.stderr)
+            return 3
+    port = free_port()
+    procs = []
+    for r in range(n):
+        env = dict(os.environ, RANK=str(r), WORLD_SIZE=str(n), LOCAL_RANK=str(r),
+                   LOCAL_WORLD_SIZE=str(n), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + argv, env=env))
+    rcs = [p.wait() for p in procs]
+    return max((abs(rc) for rc in rcs), default=0)
+
+
+def bind_numa(local: int) -> str:
+    """Pins this rank to the host cores of its GPU's NUMA node (before the pinned host buffers
+    are first touched, so they land in local memory).  Best effort: returns what was done."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        bus = pynvml.nvmlDeviceGetPciInfo(pynvml.nvmlDeviceGetHandleByIndex(local)).busId
+        bus = bus.decode() if isinstance(bus, bytes) else bus
+        dev = bus.lower()[-12:]  # dddd:bb:dd.f
+        with open(f"/sys/bus/pci/devices/{dev}/numa_node") as f:
+            node = int(f.read().strip())
+        if node < 0:
+            return "no NUMA affinity reported"
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            spec = f.read().strip()
+        cpus = set()
+        for part in spec.split(","):
+            a, _, b = part.partition("-")
+            cpus.update(range(int(a), int(b or a) + 1))
+        os.sched_setaffinity(0, cpus)
+        return f"node {node} ({len(cpus)} cores)"
+    except Exception as e:  # pragma: no cover - depends on the host
+        return f"not bound ({type(e).__name__})"
+
+
 def wells_for(rank: int, world: int, steps: int) -> list[int]:
     """C3 well of each step of this rank: well (i*N + r) mod 64."""
     return [(i * world + rank) % C3_WELLS for i in range(steps)]
 
 
 # ------------------------------------------------------------------ CPU reference leg
+def sample_frames(cores: int) -> int:
+    """Frames of a C3 well per CPU sample: 8 pairs per host thread (8c + 1), at most one well."""
+    return max(3, min(8 * cores + 1, 450))
+
+
 def cpu_reference(frames_per_sample: int, seconds_budget: float, steps: int, warmup: int,
                   threads: int | None = None) -> dict:
     """Times the reference CPU extract_roi (oracle/_ref when built, else the C restatement) on
     bounded samples of C3 wells with every host thread."""
     from oracle.oracle_py import Oracle, reference_available
     from paper_2511_14419_b200 import synth
+    if not reference_available() and not os.environ.get("FROI_BENCH_ALLOW_PORT"):
+        # the reference arm must time the reference itself (oracle/_ref, compiled in place from
+        # /root/reference by oracle/Makefile); timing the restatement instead would void it
+        raise SystemExit("bench.py: oracle/_ref/libfroi_ref.so is missing (build it here with "
+                         "`make -C oracle ref`); refusing to time the C restatement as the reference")
     kind = "reference" if reference_available() else "port"
     o = Oracle(kind)
     cfg = synth.config("C3")
@@ -209,8 +273,10 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     cores = os.cpu_count() or 1
-    # one pair per host thread per step (~2.5 core-s per 1024^2 pair)
-    frames = max(3, min(cores + 1, 129))
+    # 8 pairs per host thread per step (~2.5 core-s per 1024^2 pair): with n = 8c + 1 frames the
+    # reference's static partition (parallel.hpp:33-46) keeps every thread busy in the pair loop
+    # and 15 of 16 in the denoise loop; a (c + 1)-frame sample left 7 of 16 idle in denoise
+    frames = sample_frames(cores)
     r = cpu_reference(frames, 0, args.steps, args.warmup, cores)
     line = {
         "metric": METRIC, "value": r["value"], "unit": UNIT, "n_gpus": args.gpus,
@@ -230,6 +296,31 @@ def run_reference(args) -> None:
     print(json.dumps(line), flush=True)
 
 
+# ------------------------------------------------------------------ launcher self-test (CPU)
+def run_selftest(args) -> None:
+    """The multi-rank plumbing of the GPU leg without a GPU (gloo): each rank takes its wells,
+    reports a per-rank device time, and rank 0 prints the max-over-ranks time, the whole-job
+    frame count and every rank's wells.  tests/test_multirank_cpu.py drives it through
+    launch_ranks exactly as `bench.py --gpus N` does on a GPU box."""
+    import torch
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    dist = init_dist(world, "gloo")
+    dev = torch.device("cpu")
+    wells = wells_for(rank, world, args.warmup + args.steps)[args.warmup:]
+    ms = reduce_max(dist, 100.0 + 10.0 * rank, dev)
+    frames = reduce_sum(dist, float(len(wells) * args.frames), dev)
+    allw = [None] * world if dist is not None else [wells]
+    if dist is not None:
+        dist.all_gather_object(allw, wells)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "ms_max": ms, "frames": frames,
+                          "value": frames / (ms / 1000.0), "wells": allw}), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
 # ------------------------------------------------------------------ GPU leg
 def run_ours(args) -> None:
     import torch
@@ -237,6 +328,12 @@ def run_ours(args) -> None:
     from paper_2511_14419_b200.params import CFrameStats
 
     rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} device(s) visible")
+    numa = bind_numa(local)
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     dist = init_dist(world, "nccl")
@@ -341,8 +438,7 @@ def run_ours(args) -> None:
     if rank == 0 and not args.no_cpu_baseline:
         # ~10 s of the reference on every host thread: 8 pairs per thread of one C3 well
         cores = os.cpu_count() or 1
-        frames = max(3, min(8 * cores + 1, 450))
-        r = cpu_reference(frames, 0, 1, 0, cores)
+        r = cpu_reference(sample_frames(cores), 0, 1, 0, cores)
         cpu = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
 
     if rank == 0:
@@ -357,6 +453,7 @@ def run_ours(args) -> None:
                        "frames_per_well": F, "wells_per_step_per_gpu": 1,
                        "global_batch": world * F, "parallelism": f"wells sharded over {world} GPU(s)",
                        "lanes": "2 execution lanes per GPU (consecutive 32-pair batches overlap)",
+                       "host": f"one process per GPU; rank 0 pinned buffers on NUMA {numa}",
                        "l2": "each step reads a 472 MB well (> 126 MB L2); no flush",
                        "params": "ExtractParams{} defaults (pyramid 3, window 15, threshold 0.2)"},
             "roofline": roofline,
@@ -392,6 +489,8 @@ def main():
     ap.add_argument("--max-pairs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--selftest", action="store_true",
+                    help="CPU/gloo self-test of the multi-rank launcher (no GPU work)")
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram bytes per k_flow_iter launch from the committed ncu capture")
     args = ap.parse_args()
@@ -402,8 +501,16 @@ def main():
         if os.path.exists(p):
             with open(p) as f:
                 args.ncu_traffic = json.load(f).get("dram_bytes_per_launch")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
     if args.impl == "reference":
+        # the CPU arm runs on rank 0 only; under torchrun the other ranks exit 0 without work
         run_reference(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(launch_ranks(args.gpus, sys.argv[1:], need_gpus=not args.selftest))
+    if args.selftest:
+        run_selftest(args)
     else:
         run_ours(args)
 

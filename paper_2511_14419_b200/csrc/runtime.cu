@@ -89,6 +89,27 @@ std::string validate(const froi_params* p) {
     return "";
 }
 
+// Levels build_pyramid (flow.hpp:289-298) would make, without this implementation's cap.
+int pyramid_levels_uncapped(const froi_params& p, int W, int H) {
+    int L = 1;
+    for (int l = 1, w = W, h = H; l < p.pyramid_levels; ++l) {
+        const int tw = int(w * p.pyramid_scale), th = int(h * p.pyramid_scale);
+        if (tw < 32 || th < 32) break;
+        w = tw;
+        h = th;
+        L = l + 1;
+    }
+    return L;
+}
+
+// "" or the usage error for a geometry the GPU tables cannot hold (never a silent cap)
+std::string check_geometry(const froi_params& p, int W, int H) {
+    if (pyramid_levels_uncapped(p, W, H) > kMaxLevels)
+        return "flow: this pyramid_levels / pyramid_scale would build more than " +
+               std::to_string(kMaxLevels) + " levels, which the GPU kernels do not support";
+    return "";
+}
+
 Geom make_geom(const froi_params& p, int W, int H, int depth) {
     Geom g{};
     g.W = W;
@@ -892,6 +913,8 @@ int froi_pyramid_levels(const froi_params* p, int width, int height, int* levels
     const std::string m = validate(p);
     if (!m.empty()) return fail(1, m);
     if (width <= 0 || height <= 0) return fail(2, "frame dimensions must be positive");
+    const std::string gm = check_geometry(*p, width, height);
+    if (!gm.empty()) return fail(1, gm);
     const Geom g = make_geom(*p, width, height, 8);
     if (levels_out) *levels_out = g.L;
     for (int l = 0; l < g.L; ++l) {
@@ -921,6 +944,10 @@ int froi_ctx_create(int device, const froi_params* p, int width, int height, int
         return fail(1, "estimate_shift: max_shift must be in [1, min(w,h)/4)");
     if (next_pow2(width) > 8192 || next_pow2(height) > 8192)
         return fail(1, "frames wider or taller than 8192 px are not supported by the GPU FFT");
+    {
+        const std::string gm = check_geometry(*p, width, height);
+        if (!gm.empty()) return fail(1, gm);
+    }
     froi_ctx* c = new froi_ctx();
     ABI_TRY
     c->device = device;

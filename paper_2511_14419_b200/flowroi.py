@@ -26,6 +26,7 @@ reference throws usage_error / data_error.
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import threading
 from dataclasses import dataclass
@@ -91,12 +92,16 @@ class Context:
         _native.check(_native.lib.froi_ctx_create(device, ctypes.byref(self._cp), width, height,
                                                   depth, max_pairs, ctypes.byref(self._h)),
                       "froi_ctx_create")
-        self.lock = threading.Lock()
+        self.lock = threading.RLock()
+        self.users = 0  # holders of this context from the module cache (see _context)
 
     def close(self) -> None:
-        if self._h:
-            _native.lib.froi_ctx_destroy(self._h)
-            self._h = ctypes.c_void_p()
+        # never while another thread runs on this context: ctypes releases the GIL inside the
+        # native call, so froi_ctx_destroy must wait for the context's lock
+        with self.lock:
+            if self._h:
+                _native.lib.froi_ctx_destroy(self._h)
+                self._h = ctypes.c_void_p()
 
     def __del__(self):  # pragma: no cover - interpreter shutdown order
         try:
@@ -171,19 +176,31 @@ class Context:
 
 _ctx_cache: dict = {}
 _ctx_lock = threading.Lock()
+_CTX_CACHE_MAX = 8
 
 
-def _context(width: int, height: int, depth: int, params: ExtractParams, device: int = 0) -> Context:
+@contextlib.contextmanager
+def _context(width: int, height: int, depth: int, params: ExtractParams, device: int = 0):
+    """A cached context, held for the duration of the ``with`` block: pinned against eviction
+    (``users``) and locked, so concurrent callers of one context serialise and a context is only
+    ever closed while nobody holds it."""
     cp = params.to_c()
     key = (device, width, height, depth, bytes(cp))
     with _ctx_lock:
         ctx = _ctx_cache.get(key)
         if ctx is None:
-            if len(_ctx_cache) >= 8:
-                _ctx_cache.pop(next(iter(_ctx_cache))).close()
+            idle = [k for k, c in _ctx_cache.items() if c.users == 0]
+            while len(_ctx_cache) >= _CTX_CACHE_MAX and idle:
+                _ctx_cache.pop(idle.pop(0)).close()
             ctx = Context(width, height, depth, params, device)
             _ctx_cache[key] = ctx
-        return ctx
+        ctx.users += 1
+    try:
+        with ctx.lock:
+            yield ctx
+    finally:
+        with _ctx_lock:
+            ctx.users -= 1
 
 
 def _split_shifts(stats, n: int) -> list:
@@ -211,18 +228,18 @@ def extract_roi(seq, params: ExtractParams | None = None, workers: int = 1,
     if n < 2:
         raise DataError("extract_roi: sequence needs at least 2 frames")
     params.denoise.validate()
-    ctx = _context(w, h, depth, params)
-    masks, stats = ctx.extract_wells(frames[None])
+    with _context(w, h, depth, params) as ctx:
+        masks, stats = ctx.extract_wells(frames[None])
+        st = ctx.stage_times() if timers is not None else None
     if info is not None:
         info.shifts = _split_shifts(stats, n)
         info.raw_fractions = [stats[i].raw_fraction for i in range(n)]
         info.mask_counts = [stats[i].mask_count for i in range(n)]
         info.components = [stats[i].components for i in range(n)]
     if timers is not None:
-        t = ctx.stage_times()
-        timers.denoise_ns += t.denoise_ns
-        timers.flow_ns += t.flow_ns
-        timers.roi_ns += t.roi_ns
+        timers.denoise_ns += st.denoise_ns
+        timers.flow_ns += st.flow_ns
+        timers.roi_ns += st.roi_ns
     return masks[0]
 
 
@@ -246,8 +263,8 @@ def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth
 
     def work(dev: int, wells: list[int]):
         try:
-            ctx = _context(w, h, depth, params, dev)
-            m, st = ctx.extract_wells(frames[wells], layout)
+            with _context(w, h, depth, params, dev) as ctx:
+                m, st = ctx.extract_wells(frames[wells], layout)
             results[dev] = (wells, m, st)
         except Exception as e:  # first error re-raised like parallel_for (parallel.hpp:31-48)
             errors.append(e)
@@ -284,10 +301,9 @@ def denoise(frame: np.ndarray, params: ExtractParams | None = None, depth: int |
     f = np.asarray(frame)
     depth = depth or _default_depth(f)
     h, w = f.shape
-    ctx = _small_ctx(w, h, depth, params.copy())
     a = _u16(f)
     out = np.empty_like(a)
-    with ctx.lock:
+    with _small_ctx(w, h, depth, params.copy()) as ctx:
         _native.check(_native.lib.froi_denoise(ctx.handle, a.ctypes.data, out.ctypes.data), "denoise")
     return out.astype(f.dtype) if f.dtype == np.uint8 else out
 
@@ -304,10 +320,9 @@ def estimate_shift(reference: np.ndarray, moving: np.ndarray, max_shift: int = 1
     depth = depth or _default_depth(a)
     p = ExtractParams()
     p.max_shift = max_shift
-    ctx = _context(w, h, depth, p)
     s = CShift()
     a16, b16 = _u16(a), _u16(b)
-    with ctx.lock:
+    with _context(w, h, depth, p) as ctx:
         _native.check(_native.lib.froi_estimate_shift(ctx.handle, a16.ctypes.data, b16.ctypes.data,
                                                       max_shift, ctypes.byref(s)), "estimate_shift")
     return Shift(s.dx, s.dy, s.confidence)
@@ -328,11 +343,10 @@ def compute_flow(prev: np.ndarray, nxt: np.ndarray, params: FlowParams | Extract
     h, w = a.shape
     depth = depth or _default_depth(a)
     ep.max_shift = max(1, min(ep.max_shift, min(w, h) // 4 - 1))
-    ctx = _context(w, h, depth, ep)
     u = np.empty((h, w), np.float32)
     v = np.empty((h, w), np.float32)
     a16, b16 = _u16(a), _u16(b)
-    with ctx.lock:
+    with _context(w, h, depth, ep) as ctx:
         _native.check(_native.lib.froi_compute_flow(ctx.handle, a16.ctypes.data, b16.ctypes.data,
                                                     u.ctypes.data, v.ctypes.data), "compute_flow")
     return u, v
@@ -348,9 +362,8 @@ def polynomial_expansion(img: np.ndarray, poly_n: int = 5, poly_sigma: float = 1
     ep.flow.poly_sigma = poly_sigma
     ep.flow.validate()
     ep.max_shift = max(1, min(ep.max_shift, min(w, h) // 4 - 1))
-    ctx = _context(w, h, 8, ep)
     planes = np.empty((6, h, w), np.float32)
-    with ctx.lock:
+    with _context(w, h, 8, ep) as ctx:
         _native.check(_native.lib.froi_polynomial_expansion(ctx.handle, im.ctypes.data,
                                                             planes.ctypes.data), "polynomial_expansion")
     return planes
@@ -373,12 +386,11 @@ def saliency(u: np.ndarray, v: np.ndarray, frame: np.ndarray, flow_weight: float
     ep.roi.flow_weight = flow_weight
     ep.roi.gradient_source = gradient_source
     ep.roi.validate()
-    ctx = _small_ctx(w, h, depth, ep)
     out = np.empty((h, w), np.float64)
     uu = np.ascontiguousarray(u, dtype=np.float32)
     vv = np.ascontiguousarray(v, dtype=np.float32)
     f16 = _u16(f)
-    with ctx.lock:
+    with _small_ctx(w, h, depth, ep) as ctx:
         _native.check(_native.lib.froi_saliency(ctx.handle, uu.ctypes.data, vv.ctypes.data,
                                                 f16.ctypes.data, out.ctypes.data), "saliency")
     return out
@@ -390,9 +402,8 @@ def threshold_mask(sal: np.ndarray, roi_threshold: float) -> np.ndarray:
         raise UsageError("threshold_mask: roi_threshold must be in (0,1)")
     m = np.ascontiguousarray(sal, dtype=np.float64)
     h, w = m.shape
-    ctx = _small_ctx(w, h, 8, ExtractParams())
     out = np.empty((h, w), np.uint8)
-    with ctx.lock:
+    with _small_ctx(w, h, 8, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_threshold_mask(ctx.handle, m.ctypes.data, roi_threshold,
                                                       out.ctypes.data), "threshold_mask")
     return out
@@ -403,8 +414,7 @@ def morph_cleanup(mask: np.ndarray, open_radius: int = 1, close_radius: int = 1,
     """``flowroi::morph_cleanup`` (roi.hpp:237-246)."""
     m = np.array(mask, dtype=np.uint8, copy=True, order="C")
     h, w = m.shape
-    ctx = _small_ctx(w, h, 8, ExtractParams())
-    with ctx.lock:
+    with _small_ctx(w, h, 8, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_morph_cleanup(ctx.handle, m.ctypes.data, open_radius,
                                                      close_radius, min_area), "morph_cleanup")
     return m
@@ -424,10 +434,9 @@ def component_areas(mask: np.ndarray) -> np.ndarray:
     """Areas of the 8-connected components (``label_components``, roi.hpp:184-234), sorted."""
     m = np.ascontiguousarray(mask, dtype=np.uint8)
     h, w = m.shape
-    ctx = _small_ctx(w, h, 8, ExtractParams())
     n = ctypes.c_size_t(0)
     areas = np.zeros(w * h, np.uint32)
-    with ctx.lock:
+    with _small_ctx(w, h, 8, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_component_areas(ctx.handle, m.ctypes.data, areas.ctypes.data,
                                                        areas.size, ctypes.byref(n)), "component_areas")
     return np.sort(areas[:n.value].astype(np.int64))
@@ -439,9 +448,8 @@ def temporal_ensemble(masks: np.ndarray, t: int, k: int) -> np.ndarray:
     n, h, w = m.shape
     if t < 0 or t >= n:
         raise DataError("temporal_ensemble: index out of range")
-    ctx = _small_ctx(w, h, 8, ExtractParams())
     out = np.empty_like(m)
-    with ctx.lock:
+    with _small_ctx(w, h, 8, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_temporal_ensemble(ctx.handle, m.ctypes.data, n, k,
                                                          out.ctypes.data), "temporal_ensemble")
     return out[t]
@@ -455,13 +463,12 @@ def mask_from_flow(u: np.ndarray, v: np.ndarray, raw: np.ndarray, dx: int = 0, d
     h, w = f.shape
     depth = depth or _default_depth(f)
     ep = params.copy()
-    ctx = _small_ctx(w, h, depth, ep)
     mask = np.empty((h, w), np.uint8)
     st = CFrameStats()
     uu = np.ascontiguousarray(u, dtype=np.float32)
     vv = np.ascontiguousarray(v, dtype=np.float32)
     f16 = _u16(f)
-    with ctx.lock:
+    with _small_ctx(w, h, depth, ep) as ctx:
         _native.check(_native.lib.froi_mask_from_flow(ctx.handle, uu.ctypes.data, vv.ctypes.data,
                                                       f16.ctypes.data, dx, dy, mask.ctypes.data,
                                                       ctypes.byref(st)), "mask_from_flow")
@@ -548,9 +555,8 @@ def dwt_forward(frame: np.ndarray, levels: int = 5, depth: int | None = None) ->
     f = _u16(frame)
     d = depth or _default_depth(np.asarray(frame))
     h, w = f.shape
-    ctx = _small_ctx(w, h, d, ExtractParams())
     out = np.empty((h, w), np.int32)
-    with ctx.lock:
+    with _small_ctx(w, h, d, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_dwt_forward(ctx.handle, f.ctypes.data, int(levels), out.ctypes.data),
                       "dwt_forward")
     return out
@@ -560,9 +566,8 @@ def dwt_inverse(coeffs: np.ndarray, levels: int = 5, depth: int = 8) -> np.ndarr
     """Inverse of ``dwt_forward`` (``dwt_inverse``, dwt.hpp:143-171) -> uint16 frame."""
     c = np.ascontiguousarray(coeffs, dtype=np.int32)
     h, w = c.shape
-    ctx = _small_ctx(w, h, depth, ExtractParams())
     out = np.empty((h, w), np.uint16)
-    with ctx.lock:
+    with _small_ctx(w, h, depth, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_dwt_inverse(ctx.handle, c.ctypes.data, int(levels), out.ctypes.data),
                       "dwt_inverse")
     return out
@@ -579,8 +584,7 @@ def map_mask_to_subbands(mask: np.ndarray, levels: int = 5) -> list[np.ndarray]:
         dims.append((ch, cw))
     out = np.zeros(sum(a * b for a, b in dims), np.uint8)
     n = ctypes.c_size_t(0)
-    ctx = _small_ctx(w, h, 8, ExtractParams())
-    with ctx.lock:
+    with _small_ctx(w, h, 8, ExtractParams()) as ctx:
         _native.check(_native.lib.froi_map_mask_to_subbands(ctx.handle, m.ctypes.data, int(levels),
                                                             out.ctypes.data, out.size, ctypes.byref(n)),
                       "map_mask_to_subbands")

@@ -73,6 +73,15 @@ def test_pyramid_geometry():
     assert levels(2048, 2048, 5)[-1] == (128, 128)
     assert levels(96, 96, 3) == [(96, 96), (48, 48)]  # stops before a level < 32 px
     assert levels(100, 70, 4, 0.7) == [(100, 70), (70, 49), (49, 34)]
+    # 0.9 on 1024^2 would build 29 levels (build_pyramid, flow.hpp:289-298): the GPU tables hold
+    # 16, so the geometry is refused with a usage error instead of silently capped
+    p = ExtractParams()
+    p.flow.pyramid_levels = 40
+    p.flow.pyramid_scale = 0.9
+    c = p.to_c()
+    L = ctypes.c_int()
+    assert _native.lib.froi_pyramid_levels(ctypes.byref(c), 1024, 1024, ctypes.byref(L), None, None) == 1
+    assert b"16 levels" in _native.lib.froi_last_error()
 
 
 def test_context_without_gpu_fails_cleanly():

@@ -61,3 +61,36 @@ def test_shard_wells_assignment():
     assert sorted(w for ws in s.values() for w in ws) == list(range(64))
     assert all(len(ws) == 8 for ws in s.values())
     assert s[3] == [3, 11, 19, 27, 35, 43, 51, 59]
+
+
+def _bench(*args, timeout=180):
+    import subprocess
+    import sys
+    env = {k: v for k, v in os.environ.items()
+           if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR", "MASTER_PORT")}
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
+                          capture_output=True, text=True, timeout=timeout, env=env)
+
+
+def test_bench_launcher_spawns_n_ranks():
+    """`bench.py --gpus 2` with no external launcher spawns two ranks (gloo self-test mode):
+    rank 0 prints one line with n_gpus 2, the max over ranks and the whole-job frame count."""
+    import json
+    r = _bench("--gpus", "2", "--selftest", "--steps", "4", "--warmup", "3")
+    assert r.returncode == 0, r.stderr
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["ms_max"] == 110.0
+    assert d["frames"] == 2 * 4 * 450
+    w0, w1 = d["wells"]
+    assert w0 == [6, 8, 10, 12] and w1 == [7, 9, 11, 13]
+
+
+def test_bench_refuses_missing_gpus():
+    """Asking for more GPUs than are visible fails loudly instead of measuring fewer."""
+    import torch
+    n = torch.cuda.device_count() + 1
+    r = _bench("--gpus", str(n), "--steps", "1", "--warmup", "3", timeout=120)
+    assert r.returncode != 0
+    assert "visible" in r.stderr
