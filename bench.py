@@ -321,6 +321,36 @@ def run_selftest(args) -> None:
         dist.destroy_process_group()
 
 
+# ------------------------------------------------------------------ drop-in leg
+def run_dropin(frames: np.ndarray, steps: int, warmup: int, ref_pixels) -> dict | None:
+    """Times oracle/_ref/dropin_bench: flowroi_gpu::extract_roi (include/froi/flowroi_gpu.hpp)
+    over the reference's own types — a Sequence of uint16 Frames in, std::vector<RoiMask> bytes
+    out, the call compress_sequence makes (pipeline.hpp:142) — on one C3 well, host clock around
+    the synchronous call.  The binary is built against the reference headers here (make -C oracle
+    dropin) and travels with the snapshot; None when it is absent."""
+    exe = os.path.join(ROOT, "oracle", "_ref", "dropin_bench")
+    if not os.path.exists(exe):
+        return None
+    n, h, w = frames.shape
+    path = f"/dev/shm/froi_dropin_{os.getpid()}.raw"
+    try:
+        frames.tofile(path)
+        r = subprocess.run([exe, path, str(w), str(h), str(n), str(steps), str(warmup)],
+                           capture_output=True, text=True, timeout=600)
+    finally:
+        if os.path.exists(path):
+            os.unlink(path)
+    lines = [json.loads(x) for x in r.stdout.splitlines() if x.startswith("{")]
+    if r.returncode != 0 or not lines:
+        return {"error": (r.stderr or r.stdout)[-300:]}
+    d = lines[-1]
+    return {"value": d["dropin_frames_per_s"], "unit": UNIT, "ms_per_step": d["ms_per_step"],
+            "steps": d["steps"], "frames_per_step": d["frames"],
+            "path": "flowroi_gpu::extract_roi(Sequence of uint16 Frames) -> std::vector<RoiMask> "
+                    "(pageable host memory both ways; host clock around the call)",
+            "masks_match_e2e": (d["mask_pixels"] == ref_pixels) if ref_pixels is not None else None}
+
+
 # ------------------------------------------------------------------ GPU leg
 def run_ours(args) -> None:
     import torch
@@ -416,6 +446,13 @@ def run_ours(args) -> None:
                "h2d_bytes_per_step": F * px, "d2h_bytes_per_step": F * H * SB + F * 32,
                "ms_per_step": ems / args.steps}
 
+    # ---- the reference-type drop-in (flowroi_gpu::extract_roi over Sequence -> vector<RoiMask>)
+    dropin = None
+    if rank == 0 and not args.no_dropin:
+        last = hv[step_slot[nsteps - 1]]
+        ref_pixels = int(np.unpackbits(hmask.numpy()).sum()) if e2e else None
+        dropin = run_dropin(last, min(args.steps, 5), 2, ref_pixels)
+
     # ---- roofline of the fused flow kernel + pipeline figure
     pk = peaks()
     mb = model_bytes_per_pair(W, H, 1, cfg.params.flow.pyramid_levels)
@@ -469,6 +506,7 @@ def run_ours(args) -> None:
                 "flow_iter_ns", "mask_ns")) / 1e6 / max(1, ksteps),
             "cpu_baseline": cpu,
             "e2e": e2e,
+            "dropin_e2e": dropin,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -489,6 +527,7 @@ def main():
     ap.add_argument("--max-pairs", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-dropin", action="store_true")
     ap.add_argument("--selftest", action="store_true",
                     help="CPU/gloo self-test of the multi-rank launcher (no GPU work)")
     ap.add_argument("--ncu-traffic", type=float, default=None,

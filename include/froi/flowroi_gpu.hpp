@@ -17,6 +17,7 @@
 #include <memory>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "flowroi/roi.hpp"
@@ -80,26 +81,20 @@ inline froi_ctx* context(int device, const froi_params& p, int w, int h, int dep
     return c;
 }
 
-// Frame::pixels are uint16 whatever the depth; 8-bit frames travel as bytes (half the H2D).
-inline std::vector<uint8_t> pack(const flowroi::Sequence& seq, int& sample_bytes) {
-    const flowroi::Frame& f0 = seq[0];
-    const std::size_t px = f0.size();
-    sample_bytes = f0.depth == 8 ? 1 : 2;
-    std::vector<uint8_t> buf(px * seq.size() * sample_bytes);
-    for (std::size_t t = 0; t < seq.size(); ++t) {
-        const flowroi::Frame& f = seq[t];
-        if (!f.same_shape(f0)) throw data_error("sequence frames must share dimensions and depth");
-        if (sample_bytes == 1) {
-            uint8_t* d = buf.data() + px * t;
-            for (std::size_t i = 0; i < px; ++i) {
-                if (f.pixels[i] > 255) throw data_error("frame sample exceeds the 8-bit depth");
-                d[i] = static_cast<uint8_t>(f.pixels[i]);
-            }
-        } else {
-            std::memcpy(buf.data() + 2 * px * t, f.pixels.data(), 2 * px);
-        }
-    }
-    return buf;
+// n empty-initialised masks, constructed by several threads: a RoiMask zero-fills W*H fresh bytes
+// (core.hpp:84-85), which single-threaded costs about as much as the GPU work of a pair.
+inline std::vector<flowroi::RoiMask> make_masks(std::size_t n, int w, int h) {
+    std::vector<flowroi::RoiMask> m(n);
+    const unsigned hw = std::thread::hardware_concurrency();
+    const std::size_t T = std::max<std::size_t>(1, std::min<std::size_t>({8, hw ? hw : 1, n}));
+    std::vector<std::thread> th;
+    for (std::size_t k = 1; k < T; ++k)
+        th.emplace_back([&m, k, T, w, h] {
+            for (std::size_t t = k; t < m.size(); t += T) m[t] = flowroi::RoiMask(w, h);
+        });
+    for (std::size_t t = 0; t < m.size(); t += T) m[t] = flowroi::RoiMask(w, h);
+    for (auto& x : th) x.join();
+    return m;
 }
 
 }  // namespace detail
@@ -120,21 +115,20 @@ inline std::vector<flowroi::RoiMask> extract_roi(const flowroi::Sequence& seq,
     const froi_params cp = to_c(params);
     const flowroi::Frame& f0 = seq[0];
     froi_ctx* ctx = detail::context(0, cp, f0.width, f0.height, f0.depth);
-    int sb = 1;
-    const std::vector<uint8_t> frames = detail::pack(seq, sb);
-    const std::size_t px = f0.size();
-    std::vector<uint8_t> bytes(px * n);
-    std::vector<froi_frame_stats> stats(n);
-    check(froi_extract_roi(ctx, frames.data(), sb, px * sb, static_cast<int>(n), FROI_MASK_BYTES,
-                           bytes.data(), stats.data()),
-          "extract_roi");
-    std::vector<flowroi::RoiMask> masks;
-    masks.reserve(n);
+    // the Frames and RoiMasks go to the library as they are: one pointer each, uint16 samples
+    // (narrowed to bytes for 8-bit frames by the library's host threads on the way into its
+    // pinned staging ring), masks unpacked from the returned PBM rows straight into RoiMask::bits
+    std::vector<const void*> fp(n);
     for (std::size_t t = 0; t < n; ++t) {
-        flowroi::RoiMask m(f0.width, f0.height);
-        std::memcpy(m.bits.data(), bytes.data() + px * t, px);
-        masks.push_back(std::move(m));
+        if (!seq[t].same_shape(f0)) throw data_error("sequence frames must share dimensions and depth");
+        fp[t] = seq[t].pixels.data();
     }
+    std::vector<flowroi::RoiMask> masks = detail::make_masks(n, f0.width, f0.height);
+    std::vector<uint8_t*> mp(n);
+    for (std::size_t t = 0; t < n; ++t) mp[t] = masks[t].bits.data();
+    std::vector<froi_frame_stats> stats(n);
+    check(froi_extract_frames(ctx, fp.data(), 2, static_cast<int>(n), FROI_MASK_BYTES, mp.data(), stats.data()),
+          "extract_roi");
     if (info) {
         info->shifts.resize(n);
         info->raw_fractions.resize(n);

@@ -131,24 +131,26 @@ inline flowroi::CompressResult compress_sequence(const flowroi::Sequence& seq,
     } else {
         const flowroi::Frame& f0 = seq[0];
         froi_ctx* ctx = detail::context(0, to_c(params), f0.width, f0.height, f0.depth);
-        int sb = 1;
-        const std::vector<uint8_t> frames = detail::pack(seq, sb);
-        const std::size_t px = f0.size();
         chunk = std::max(2, chunk);
-        res.masks.assign(n, flowroi::RoiMask(f0.width, f0.height));
+        res.masks = detail::make_masks(n, f0.width, f0.height);
         res.info.shifts.resize(n);
         res.info.raw_fractions.resize(n);
-        std::vector<uint8_t> bytes(px * (std::size_t)chunk);
+        // Frames and RoiMasks are handed over by pointer (no packing or copying here)
+        std::vector<const void*> fp(n);
+        std::vector<uint8_t*> mp(n);
+        for (std::size_t t = 0; t < n; ++t) {
+            if (!seq[t].same_shape(f0)) throw data_error("sequence frames must share dimensions and depth");
+            fp[t] = seq[t].pixels.data();
+            mp[t] = res.masks[t].bits.data();
+        }
         std::vector<froi_frame_stats> stats((std::size_t)chunk);
         detail::EncodePool pool(detail::encode_workers(config.workers), seq, res, config.codec);
         check(froi_stream_reset(ctx, 1), "compress_sequence");
         for (std::size_t a = 0; a < n; a += (std::size_t)chunk) {
             const int k = (int)std::min<std::size_t>((std::size_t)chunk, n - a);
-            check(froi_stream_push(ctx, frames.data() + px * sb * a, 0, sb, px * sb, k, FROI_MASK_BYTES,
-                                   bytes.data(), 0, stats.data()),
+            check(froi_stream_push_frames(ctx, fp.data() + a, 2, k, FROI_MASK_BYTES, mp.data() + a, stats.data()),
                   "compress_sequence");
             for (int t = 0; t < k; ++t) {
-                std::memcpy(res.masks[a + t].bits.data(), bytes.data() + px * t, px);
                 res.info.shifts[a + t] = flowroi::Shift{stats[t].dx, stats[t].dy, stats[t].confidence};
                 res.info.raw_fractions[a + t] = stats[t].raw_fraction;
             }

@@ -170,6 +170,20 @@ int froi_extract_wells(froi_ctx* ctx, const void* frames, int sample_bytes,
                        size_t frame_stride_bytes, int n_wells, int n_frames, int mask_layout,
                        uint8_t* masks_out, froi_frame_stats* stats_out);
 
+/* Host entries (froi_extract_roi / _wells / _frames, froi_stream_push) stream the frames through
+ * bounded rings: frames of any host memory are converted into a pinned staging
+ * ring by host threads (pinned frames of the context's sample type are copied directly), copied
+ * into a device ring of a few batches' frames just ahead of the batch that needs them, and each
+ * batch's masks return while later batches compute.  Device and pinned memory do not grow with
+ * the call.  A sample above the depth's maxval (u16 frames of an 8-bit context) is a data error.
+ *
+ * Per-frame pointers: the reference's Sequence holds separately allocated Frames (core.hpp:61-75)
+ * and extract_roi returns separately allocated RoiMasks (roi.hpp:309-311).  frames[t] points at
+ * width*height samples of `sample_bytes` (Frame::pixels are uint16: sample_bytes 2), masks[t] at
+ * one mask in `mask_layout`; host memory of any kind. */
+int froi_extract_frames(froi_ctx* ctx, const void* const* frames, int sample_bytes, int n_frames,
+                        int mask_layout, uint8_t* const* masks, froi_frame_stats* stats_out);
+
 /* Device-resident variant used for the device-side throughput figure: d_frames is a device
  * pointer (well-major, as above), d_masks_pbm receives PBM-packed masks on the device.
  * stats_out is a HOST pointer (nullable). Asynchronous work is complete on return. */
@@ -188,6 +202,10 @@ int froi_stream_reset(froi_ctx* ctx, int n_wells);
 int froi_stream_push(froi_ctx* ctx, const void* frames, int frames_on_device, int sample_bytes,
                      size_t frame_stride_bytes, int chunk, int mask_layout, uint8_t* masks_out,
                      int masks_on_device, froi_frame_stats* stats_out);
+/* froi_stream_push with one host pointer per frame and per mask (frames[w*chunk + t],
+ * masks[w*chunk + t]), for separately allocated Frames / RoiMasks. */
+int froi_stream_push_frames(froi_ctx* ctx, const void* const* frames, int sample_bytes, int chunk,
+                            int mask_layout, uint8_t* const* masks, froi_frame_stats* stats_out);
 
 /* ---- sub-operators (parity taps; each computes on the GPU with the product kernels) ---- */
 /* denoise (denoise.hpp:84-90): median then bilateral, or copy if disabled. */

@@ -19,7 +19,11 @@
 #include <array>
 #include <vector>
 
+#include <memory>
+#include <thread>
+
 #include "../../include/froi/froi.h"
+#include "host_pool.hpp"
 #include "kernels.cuh"
 
 using namespace froi;
@@ -307,20 +311,28 @@ struct froi_ctx {
     // streaming state
     int stream_wells = 0;
     std::vector<long long> stream_next_t;  // next frame index per well
-    uint8_t* d_carry = nullptr;            // last raw frame per well
+    uint8_t* d_carry[2] = {nullptr, nullptr};  // last raw frame per well (current / next push)
+    int carry_cur = 0;
     size_t carry_cap = 0;
     // timing
     cudaEvent_t ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     froi_stage_times times{};
     froi_kernel_times ktimes{};
-    // ingest arena (grow-only) + copy stream for H2D / compute overlap
-    uint8_t* d_arena = nullptr;
-    size_t arena_cap = 0;
+    // host ingest / egress pipeline (run_host_call): bounded rings, whatever the call size
+    std::unique_ptr<HostPool> pool;      // frame conversion into staging, mask unpacking
+    std::unique_ptr<HostPool> courier;   // one thread: waits for each batch, then delivers it
+    uint8_t* d_ring = nullptr;           // ingest ring: ring_frames device frame slots
+    int ring_chunk = 0, ring_frames = 0; // upload chunk (frames) and ring size (frames)
+    uint8_t* h_stage = nullptr;          // pinned staging ring: kStageChunks chunks
+    std::vector<cudaEvent_t> stage_free; // staging chunk i may be refilled
+    uint8_t* d_outring = nullptr;        // egress ring: kOutBatches x Pcap PBM masks
+    uint8_t* h_outring = nullptr;        // pinned twin of d_outring (general destinations)
+    std::vector<cudaEvent_t> delivered;  // per batch of a call: its masks are in host memory
     cudaStream_t copy_stream = nullptr;
     cudaStream_t d2h_stream = nullptr;       // per-batch mask read-back (host PBM), off the lanes
     std::vector<cudaEvent_t> d2h_ev;         // batch b's masks are final
     cudaEvent_t d2h_done = nullptr;
-    std::vector<cudaEvent_t> well_ready;
+    std::vector<cudaEvent_t> chunk_ready;  // per upload chunk of a call
     uint64_t launches = 0;
 
     MaskBuffers mask_buffers(int tb_) const {
@@ -473,6 +485,9 @@ void ctx_alloc(froi_ctx* c) {
     FROI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
     FROI_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
+    // the constant tables above went through pageable cudaMemcpy on the legacy stream, which may
+    // return before the DMA lands and does not order the non-blocking streams: finish them here
+    FROI_CUDA(cudaDeviceSynchronize());
 }
 
 void ctx_free(froi_ctx* c) {
@@ -490,7 +505,8 @@ void ctx_free(froi_ctx* c) {
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_cand_idx, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
                     c->d_bits_clean, c->d_bits_keep, c->d_run_x0, c->d_run_x1, c->d_run_n, c->d_run_par, c->d_run_area,
-                    c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry, c->d_arena};
+                    c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry[0], c->d_carry[1],
+                    c->d_ring, c->d_outring};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -507,7 +523,13 @@ void ctx_free(froi_ctx* c) {
         if (e) cudaEventDestroy(e);
     for (auto& a : c->bev)
         for (auto e : a) cudaEventDestroy(e);
-    for (auto e : c->well_ready) cudaEventDestroy(e);
+    c->courier.reset();  // joins its thread (idle between calls)
+    c->pool.reset();
+    for (auto e : c->chunk_ready) cudaEventDestroy(e);
+    for (auto e : c->stage_free) cudaEventDestroy(e);
+    for (auto e : c->delivered) cudaEventDestroy(e);
+    if (c->h_stage) cudaFreeHost(c->h_stage);
+    if (c->h_outring) cudaFreeHost(c->h_outring);
     for (auto e : c->d2h_ev) cudaEventDestroy(e);
     if (c->d2h_done) cudaEventDestroy(c->d2h_done);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
@@ -660,17 +682,13 @@ froi_ctx* lane_of(froi_ctx* c) {
     return c->lane;
 }
 
-// Enqueue every batch of `jobs`, then synchronise once: stage times from each batch's events,
-// PairInfo rows in job order.
-// host_pbm (nullable, pinned): each batch's PBM masks are copied to the same offsets of host_pbm
-// on the batch's lane right after its mask stage, overlapping the later batches.
-// first (> 0): size of batch 0 when the frames are still arriving from the host, so the GPU
-// starts on a few pairs while the rest of the upload is in flight; later batches are Pcap pairs.
+void accumulate_batch_times(froi_ctx* c, size_t nb);
+
+// Device-resident frames and masks: enqueue every batch of `jobs`, then synchronise once; stage
+// times from each batch's events, PairInfo rows in job order.
 void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm,
-                 std::vector<PairInfo>& infos, uint8_t* host_pbm = nullptr, int first = 0) {
-    const size_t P = (size_t)c->Pcap, F = first > 0 && first < c->Pcap ? (size_t)first : P;
-    auto bstart = [&](size_t b) { return b == 0 ? 0 : std::min(jobs.size(), F + (b - 1) * P); };
-    const size_t nb = jobs.size() <= F ? 1 : 1 + (jobs.size() - F + P - 1) / P;
+                 std::vector<PairInfo>& infos) {
+    const size_t P = (size_t)c->Pcap, nb = (jobs.size() + P - 1) / P;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
         FROI_CUDA(cudaFreeHost(c->h_info));
@@ -690,32 +708,10 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         FROI_CUDA(cudaEventRecord(c->ev_fork, c->stream));
         FROI_CUDA(cudaStreamWaitEvent(lane->stream, c->ev_fork, 0));
     }
-    const size_t mb = (size_t)c->g.H * c->g.SB;
     for (size_t b = 0; b < nb; ++b) {
-        const size_t j0 = bstart(b), j1 = bstart(b + 1);
+        const size_t j0 = b * P, j1 = std::min(jobs.size(), j0 + P);
         froi_ctx* x = (lane && (b & 1)) ? lane : c;
         run_batch(x, c, jobs, j0, j1, out_pbm, b, j0);
-        if (host_pbm) {
-            long long lo = jobs[j0].out_index, hi = lo;
-            for (size_t j = j0; j < j1; ++j) {
-                lo = std::min(lo, jobs[j].out_index);
-                hi = std::max(hi, jobs[j].out_index);
-            }
-            // read back on its own stream, so neither lane waits for the copy
-            while (c->d2h_ev.size() <= b) {
-                cudaEvent_t e;
-                FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                c->d2h_ev.push_back(e);
-            }
-            FROI_CUDA(cudaEventRecord(c->d2h_ev[b], x->stream));
-            FROI_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->d2h_ev[b], 0));
-            FROI_CUDA(cudaMemcpyAsync(host_pbm + mb * lo, out_pbm + mb * lo, mb * (size_t)(hi - lo + 1),
-                                      cudaMemcpyDeviceToHost, c->d2h_stream));
-        }
-    }
-    if (host_pbm) {
-        FROI_CUDA(cudaEventRecord(c->d2h_done, c->d2h_stream));
-        FROI_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
     }
     if (lane) {
         // later work on the owner's stream (frame-0 copies, ensemble, delivery) follows both lanes
@@ -723,6 +719,12 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         FROI_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
     }
     FROI_CUDA(cudaStreamSynchronize(c->stream));
+    accumulate_batch_times(c, nb);
+    infos.insert(infos.end(), c->h_info, c->h_info + jobs.size());
+}
+
+// Stage times of the nb batches of the last call from their events (after the host sync).
+void accumulate_batch_times(froi_ctx* c, size_t nb) {
     auto ns = [](float m) { return (uint64_t)((double)m * 1e6); };
     froi_kernel_times& K = c->ktimes;
     for (size_t b = 0; b < nb; ++b) {
@@ -739,7 +741,28 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         K.flow_iter_ns += ns(ms[5]);
         K.mask_ns += ns(ms[6]);
     }
-    infos.insert(infos.end(), c->h_info, c->h_info + jobs.size());
+}
+
+// One frame of host samples into the context's sample type: Frame::pixels are uint16 whatever
+// the depth (core.hpp:30), so 8-bit frames are narrowed here, with the Frame invariant
+// (core.hpp:24-25, every sample < 2^depth) checked on the way.
+void convert_frame(const uint8_t* src, int src_bytes, uint8_t* dst, int dst_bytes, size_t px) {
+    if (src_bytes == dst_bytes) {
+        std::memcpy(dst, src, px * src_bytes);
+        return;
+    }
+    if (src_bytes == 2) {
+        const uint16_t* s16 = (const uint16_t*)src;
+        uint16_t hi = 0;
+        for (size_t i = 0; i < px; ++i) {
+            hi |= s16[i];
+            dst[i] = (uint8_t)s16[i];
+        }
+        if (hi > 255) throw Error(2, "frame sample exceeds the 8-bit depth");
+        return;
+    }
+    uint16_t* d16 = (uint16_t*)dst;
+    for (size_t i = 0; i < px; ++i) d16[i] = src[i];
 }
 
 void fill_stats(const Geom& g, const PairInfo& I, froi_frame_stats* st) {
@@ -751,7 +774,9 @@ void fill_stats(const Geom& g, const PairInfo& I, froi_frame_stats* st) {
     st->components = I.components;
 }
 
-// Ingest host frames (any sample width) into a device buffer of the context's sample type.
+// Ingest host frames (any sample width) into a device buffer of the context's sample type, on
+// the context stream (used by the single-frame parity taps; the throughput entries go through
+// run_host_call).  The conversion buffer is kept alive until its copy has completed.
 void upload_frames(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, long long n,
                    uint8_t* dst) {
     const Geom& g = c->g;
@@ -765,40 +790,18 @@ void upload_frames(froi_ctx* c, const void* frames, int sample_bytes, size_t str
                                     cudaMemcpyHostToDevice, c->stream));
         return;
     }
-    // sample-width conversion on the host (API convenience path, not the throughput path)
     std::vector<uint8_t> tmp(c->frame_bytes);
     for (long long f = 0; f < n; ++f) {
-        const uint8_t* src = (const uint8_t*)frames + stride * f;
-        if (sample_bytes == 2 && g.sample_bytes == 1) {
-            const uint16_t* s16 = (const uint16_t*)src;
-            for (size_t i = 0; i < px; ++i) {
-                if (s16[i] > 255) throw Error(2, "frame sample exceeds the 8-bit depth");
-                tmp[i] = (uint8_t)s16[i];
-            }
-        } else {
-            uint16_t* d16 = (uint16_t*)tmp.data();
-            for (size_t i = 0; i < px; ++i) d16[i] = src[i];
-        }
-        FROI_CUDA(cudaMemcpy(dst + c->frame_bytes * f, tmp.data(), c->frame_bytes, cudaMemcpyHostToDevice));
-    }
-}
-
-void check_frames_range(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, long long n) {
-    // Frame invariant (core.hpp:24-25): every sample < 2^depth.
-    if (sample_bytes != 2 || c->g.depth == 16) return;
-    const size_t px = (size_t)c->g.W * c->g.H;
-    for (long long f = 0; f < n; ++f) {
-        const uint16_t* s16 = (const uint16_t*)((const uint8_t*)frames + stride * f);
-        for (size_t i = 0; i < px; ++i)
-            if (s16[i] > 255) throw Error(2, "frame sample exceeds the 8-bit depth");
+        convert_frame((const uint8_t*)frames + stride * f, sample_bytes, tmp.data(), g.sample_bytes, px);
+        FROI_CUDA(cudaMemcpyAsync(dst + c->frame_bytes * f, tmp.data(), c->frame_bytes, cudaMemcpyHostToDevice,
+                                  c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));  // tmp is reused by the next frame
     }
 }
 
 // Whole wells: frames on device (well-major, contiguous in ctx sample type).
 void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int n_wells, int n_frames,
-                       uint8_t* d_out, std::vector<PairInfo>& infos, const cudaEvent_t* ready = nullptr,
-                       uint8_t* host_pbm = nullptr, int first = 0) {
-    // ready (nullable): per (well, frame) event after which the frame is resident
+                       uint8_t* d_out, std::vector<PairInfo>& infos) {
     const Geom& g = c->g;
     std::vector<PairJob> jobs;
     jobs.reserve((size_t)n_wells * (n_frames - 1));
@@ -809,13 +812,12 @@ void extract_wells_dev(froi_ctx* c, const uint8_t* d_frames, size_t stride, int 
             J.raw_next = d_frames + stride * ((size_t)w * n_frames + t);
             J.out_index = (long long)w * n_frames + t;
             J.stats_index = J.out_index;
-            J.ready = ready ? ready[(size_t)w * n_frames + t] : nullptr;  // chunk holding frame t
             jobs.push_back(J);
         }
     c->times = froi_stage_times{};
     c->ktimes = froi_kernel_times{};
     c->launches = 0;
-    run_batches(c, jobs, d_out, infos, host_pbm, first);
+    run_batches(c, jobs, d_out, infos);
     // frame 0 borrows frame 1's mask (roi.hpp:348)
     const size_t mb = (size_t)g.H * g.SB;
     for (int w = 0; w < n_wells; ++w)
@@ -847,27 +849,388 @@ void stats_for_wells(froi_ctx* c, const std::vector<PairInfo>& infos, int n_well
     }
 }
 
-void deliver_masks(froi_ctx* c, const uint8_t* d_pbm, long long n_masks, int layout, uint8_t* host_out) {
-    const Geom& g = c->g;
-    const size_t mb = (size_t)g.H * g.SB;
-    if (layout == FROI_MASK_PBM) {
-        FROI_CUDA(cudaMemcpyAsync(host_out, d_pbm, mb * n_masks, cudaMemcpyDeviceToHost, c->stream));
-        FROI_CUDA(cudaStreamSynchronize(c->stream));
-        return;
+int check_layout(int layout) {
+    return layout == FROI_MASK_BYTES || layout == FROI_MASK_PBM;
+}
+
+// ------------------------------------------------------------------ host ingest / egress pipeline
+//
+// One host call (froi_extract_wells / froi_extract_frames / froi_stream_push) streams its frames
+// through bounded rings, so device and pinned host memory do not grow with the call:
+//
+//   host frames --(pool: copy or u16<->u8 conversion)--> pinned staging ring (kStageChunks
+//   chunks) --copy stream--> device ingest ring (kRingChunks chunks of ring_chunk frames)
+//   --batches on the execution lanes--> device egress ring (kOutBatches batches of PBM masks)
+//   --d2h stream--> caller's pinned PBM buffers directly, or the pinned egress twin from which
+//   the courier thread unpacks each batch into the caller's RoiMask bytes (or copies PBM rows).
+//
+// Frames are uploaded in (well, frame) order just ahead of the batch that first needs them;
+// each upload chunk records an event the batch's denoise waits on.  Pinned sources of the
+// context's sample type skip the staging ring.  A ring slot is rewritten only after the last
+// batch reading it has finished (stream-ordered waits, no host sync), a staging chunk only after
+// its previous copy has completed, an egress slot only after its masks reached the host.
+// Temporal ensembling (k > 0) needs every mask of a well before any output: those calls keep
+// the masks on the device until the end (full egress buffer) and deliver them afterwards.
+constexpr int kRingChunks = 6;
+constexpr int kStageChunks = 3;
+constexpr int kOutBatches = 4;
+
+struct HostCall {
+    int n_wells = 0, n_frames = 0;        // frames per well in this call
+    int t_begin = 1;                      // next frame of each well's first pair (0: prev = carry)
+    int src_bytes = 1;                    // sample bytes of the host frames
+    std::vector<const uint8_t*> host;     // [w*n + t] host frame (nullptr: dev[] has it)
+    std::vector<const uint8_t*> dev;      // [w*n + t] device-resident frame (context sample type)
+    std::vector<const uint8_t*> carry;    // [w] device frame t = -1 when t_begin == 0
+    uint8_t* new_carry = nullptr;         // device [w] frames: receives each well's last frame
+    int layout = FROI_MASK_PBM;
+    std::vector<uint8_t*> mask;           // [w*n + t] host destination (layout)
+    uint8_t* dev_masks = nullptr;         // device PBM destination [w*n + t] instead of mask[]
+    bool frame0_rule = true;              // mask (w, 0) := mask (w, 1) (roi.hpp:348)
+};
+
+bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess;
+    cudaGetLastError();  // an unregistered pointer may leave an error behind on older drivers
+    return ok && (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged);
+}
+
+void ensure_pipeline(froi_ctx* c) {
+    if (!c->pool) {
+        const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+        const int dev = c->device;
+        c->pool.reset(new HostPool(std::max(1, std::min(8, hw - 1)), [dev] { cudaSetDevice(dev); }));
+        c->courier.reset(new HostPool(1, [dev] { cudaSetDevice(dev); }));
     }
-    const size_t px = (size_t)g.W * g.H;
-    const long long chunk = std::max<long long>(1, (long long)(256u << 20) / (long long)px);
-    ensure_seq_tmp(c, px * std::min<long long>(chunk, n_masks));
-    for (long long m0 = 0; m0 < n_masks; m0 += chunk) {
-        const long long nm = std::min(chunk, n_masks - m0);
-        launch_unpack_pbm(g, d_pbm + mb * m0, c->d_seq_tmp, (int)nm, c->stream);
-        FROI_CUDA(cudaMemcpyAsync(host_out + px * m0, c->d_seq_tmp, px * nm, cudaMemcpyDeviceToHost, c->stream));
-        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    if (!c->d_ring) {
+        c->ring_chunk = std::max(8, c->Pcap);
+        c->ring_frames = kRingChunks * c->ring_chunk;
+        FROI_CUDA(cudaMalloc(&c->d_ring, c->frame_bytes * c->ring_frames));
+        const size_t mb = (size_t)c->g.H * c->g.SB;
+        FROI_CUDA(cudaMalloc(&c->d_outring, mb * c->Pcap * kOutBatches));
     }
 }
 
-int check_layout(int layout) {
-    return layout == FROI_MASK_BYTES || layout == FROI_MASK_PBM;
+void ensure_staging(froi_ctx* c) {
+    if (c->h_stage) return;
+    FROI_CUDA(cudaMallocHost((void**)&c->h_stage, c->frame_bytes * c->ring_chunk * kStageChunks));
+    for (int i = 0; i < kStageChunks; ++i) {
+        cudaEvent_t e;
+        FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->stage_free.push_back(e);
+    }
+}
+
+void ensure_host_outring(froi_ctx* c) {
+    if (c->h_outring) return;
+    const size_t mb = (size_t)c->g.H * c->g.SB;
+    FROI_CUDA(cudaMallocHost((void**)&c->h_outring, mb * c->Pcap * kOutBatches));
+}
+
+cudaEvent_t event_at(std::vector<cudaEvent_t>& v, size_t i) {
+    while (v.size() <= i) {
+        cudaEvent_t e;
+        FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        v.push_back(e);
+    }
+    return v[i];
+}
+
+// One PBM mask (H rows of SB bytes, MSB first) into the caller's layout.
+void put_mask(const Geom& g, const uint8_t* pbm, int layout, uint8_t* dst) {
+    const size_t mb = (size_t)g.H * g.SB;
+    if (layout == FROI_MASK_PBM) {
+        std::memcpy(dst, pbm, mb);
+        return;
+    }
+    // RoiMask bytes (core.hpp:78-101): 8 pixels per PBM byte through a 256-entry table
+    static const auto table = [] {
+        std::array<uint64_t, 256> t{};
+        for (int v = 0; v < 256; ++v) {
+            uint64_t x = 0;
+            for (int b = 0; b < 8; ++b) x |= (uint64_t)((v >> (7 - b)) & 1) << (8 * b);  // little endian
+            t[v] = x;
+        }
+        return t;
+    }();
+    const int full = g.W / 8, rem = g.W % 8;
+    for (int y = 0; y < g.H; ++y) {
+        const uint8_t* r = pbm + (size_t)y * g.SB;
+        uint8_t* o = dst + (size_t)y * g.W;
+        for (int i = 0; i < full; ++i) std::memcpy(o + 8 * i, &table[r[i]], 8);
+        if (rem) std::memcpy(o + 8 * full, &table[r[full]], rem);
+    }
+}
+
+// Runs one host call end to end (see the comment block above).  Throws froi::Error; on any error
+// every queued copy, kernel and host task has finished before the exception leaves.
+void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos) {
+    const Geom& g = c->g;
+    const size_t fb = c->frame_bytes, mb = (size_t)g.H * g.SB;
+    const int n = io.n_frames, nw = io.n_wells;
+    const size_t nk = (size_t)nw * n;
+    const bool ring_out = !io.dev_masks && c->params.adjacent_factor == 0;
+    ensure_pipeline(c);
+    // pairs in (well, frame) order; frame (w, t) of the call has upload index k = w*n + t
+    std::vector<PairJob> jobs;
+    std::vector<std::pair<int, int>> wt;
+    jobs.reserve(nk);
+    for (int w = 0; w < nw; ++w)
+        for (int t = io.t_begin; t < n; ++t) {
+            jobs.push_back(PairJob{});
+            wt.emplace_back(w, t);
+        }
+    const size_t P = (size_t)c->Pcap, nb = (jobs.size() + P - 1) / P;
+    if (c->h_info_cap < jobs.size()) {
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+        FROI_CUDA(cudaFreeHost(c->h_info));
+        c->h_info = nullptr;
+        c->h_info_cap = 0;
+        FROI_CUDA(cudaMallocHost((void**)&c->h_info, sizeof(PairInfo) * jobs.size()));
+        c->h_info_cap = jobs.size();
+    }
+    while (c->bev.size() < nb) {
+        std::array<cudaEvent_t, 8> a;
+        for (auto& e : a) FROI_CUDA(cudaEventCreate(&e));
+        c->bev.push_back(a);
+    }
+    for (size_t b = 0; b < nb; ++b) event_at(c->delivered, b), event_at(c->d2h_ev, b);
+    uint8_t* d_full = nullptr;  // egress without the ring (ensemble / device destinations)
+    if (!ring_out) {
+        if (io.dev_masks) d_full = io.dev_masks;
+        else {
+            ensure_seq_out(c, mb * nk);
+            d_full = c->d_seq_out;
+        }
+    }
+    bool any_staged = false;
+    for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !is_pinned(io.host[k]));
+    if (any_staged) ensure_staging(c);
+    const bool general_out = ring_out && !(io.layout == FROI_MASK_PBM && [&] {
+        for (size_t k = 0; k < nk; ++k)
+            if (!is_pinned(io.mask[k])) return false;
+        return true;
+    }());
+    if (general_out) ensure_host_outring(c);
+
+    c->times = froi_stage_times{};
+    c->ktimes = froi_kernel_times{};
+    c->launches = 0;
+    const int CH = c->ring_chunk, RF = c->ring_frames;
+    std::vector<int> last_reader(RF, -1);     // batch that last reads each ring slot
+    std::vector<cudaEvent_t> ready(nk, nullptr);
+    size_t next_k = 0, n_chunks = 0, n_staged = 0;
+    std::vector<HostPool::TaskPtr> tasks(nb);
+    // the previous call's kernels may still read the rings: order this call's copies after them
+    FROI_CUDA(cudaEventRecord(c->ev[7], c->stream));
+    FROI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[7], 0));
+
+    // upload every host frame with index <= kmax that is not resident yet
+    auto upload_to = [&](size_t kmax) {
+        while (next_k <= kmax && next_k < nk) {
+            // first chunk in 8-frame sub-chunks: the first batch's denoise follows the copy
+            // exactly the frames this batch still needs, at most one staging chunk, never across
+            // the ring's wrap
+            const size_t k0 = next_k, cap = k0 < (size_t)CH ? 8 : (size_t)CH;
+            const size_t k1 = std::min({nk, kmax + 1, k0 + cap, (k0 / RF + 1) * (size_t)RF});
+            next_k = k1;
+            bool any = false, direct = true;
+            int wait_b = -1;
+            for (size_t k = k0; k < k1; ++k) {
+                if (!io.host[k]) continue;
+                any = true;
+                direct &= io.src_bytes == g.sample_bytes && is_pinned(io.host[k]);
+                wait_b = std::max(wait_b, last_reader[k % RF]);
+            }
+            if (!any) continue;
+            if (wait_b >= 0) FROI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->bev[wait_b][7], 0));
+            uint8_t* dst = c->d_ring + fb * (k0 % RF);
+            if (direct) {
+                for (size_t k = k0; k < k1;) {  // contiguous runs of pinned frames: one copy each
+                    if (!io.host[k]) {
+                        ++k;
+                        continue;
+                    }
+                    size_t e = k + 1;
+                    while (e < k1 && io.host[e] && io.host[e] == io.host[e - 1] + fb) ++e;
+                    FROI_CUDA(cudaMemcpyAsync(dst + fb * (k - k0), io.host[k], fb * (e - k), cudaMemcpyHostToDevice,
+                                              c->copy_stream));
+                    k = e;
+                }
+            } else {
+                const size_t slot = n_staged++ % kStageChunks;
+                FROI_CUDA(cudaEventSynchronize(c->stage_free[slot]));  // its previous copy is done
+                uint8_t* st = c->h_stage + fb * CH * slot;
+                const size_t px = (size_t)g.W * g.H;
+                c->pool->parallel_for(k1 - k0, [&](size_t i) {
+                    if (io.host[k0 + i]) convert_frame(io.host[k0 + i], io.src_bytes, st + fb * i, g.sample_bytes, px);
+                });
+                FROI_CUDA(cudaMemcpyAsync(dst, st, fb * (k1 - k0), cudaMemcpyHostToDevice, c->copy_stream));
+                FROI_CUDA(cudaEventRecord(c->stage_free[slot], c->copy_stream));
+            }
+            if (io.new_carry)  // a well's last frame becomes the next push's carry
+                for (size_t k = k0; k < k1; ++k)
+                    if ((int)(k % n) == n - 1 && io.host[k])
+                        FROI_CUDA(cudaMemcpyAsync(io.new_carry + fb * (k / n), dst + fb * (k - k0), fb,
+                                                  cudaMemcpyDeviceToDevice, c->copy_stream));
+            cudaEvent_t e = event_at(c->chunk_ready, n_chunks++);
+            FROI_CUDA(cudaEventRecord(e, c->copy_stream));
+            for (size_t k = k0; k < k1; ++k) ready[k] = e;
+        }
+    };
+    auto frame_ptr = [&](int w, int t) -> const uint8_t* {
+        if (t < 0) return io.carry[w];
+        const size_t k = (size_t)w * n + t;
+        return io.host[k] ? c->d_ring + fb * (k % RF) : io.dev[k];
+    };
+    froi_ctx* lane = nb >= 2 ? lane_of(c) : nullptr;
+    if (lane) {
+        FROI_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+        FROI_CUDA(cudaStreamWaitEvent(lane->stream, c->ev_fork, 0));
+    }
+    auto settle = [&] {  // on error: let everything queued finish before buffers are reused
+        for (auto& t : tasks)
+            if (t) try {
+                    t->wait();
+                } catch (...) {
+                }
+        cudaStreamSynchronize(c->copy_stream);
+        if (lane) cudaStreamSynchronize(lane->stream);
+        cudaStreamSynchronize(c->d2h_stream);
+        cudaStreamSynchronize(c->stream);
+    };
+    try {
+        for (size_t b = 0; b < nb; ++b) {
+            const size_t j0 = b * P, j1 = std::min(jobs.size(), j0 + P);
+            // frames of this batch: uploaded (in order) just before it is enqueued
+            size_t kmax = 0;
+            for (size_t j = j0; j < j1; ++j) kmax = std::max(kmax, (size_t)wt[j].first * n + wt[j].second);
+            upload_to(kmax);
+            for (size_t j = j0; j < j1; ++j) {
+                const int w = wt[j].first, t = wt[j].second;
+                PairJob& J = jobs[j];
+                J.raw_prev = frame_ptr(w, t - 1);
+                J.raw_next = frame_ptr(w, t);
+                const size_t kn = (size_t)w * n + t;
+                J.ready = io.host[kn] ? ready[kn] : nullptr;
+                if (t > 0 && io.host[kn - 1]) {
+                    // prev frame's chunk: the first batch waits on both (frame runs share events)
+                    if (!J.ready) J.ready = ready[kn - 1];
+                    last_reader[(kn - 1) % RF] = (int)b;
+                }
+                if (io.host[kn]) last_reader[kn % RF] = (int)b;
+                J.out_index = ring_out ? (long long)((b % kOutBatches) * P + (j - j0)) : (long long)kn;
+                J.stats_index = (long long)kn;
+            }
+            froi_ctx* x = (lane && (b & 1)) ? lane : c;
+            if (ring_out && b >= (size_t)kOutBatches)  // its egress slot has reached the host
+                FROI_CUDA(cudaStreamWaitEvent(x->stream, c->delivered[b - kOutBatches], 0));
+            // jobs whose two frames come from different chunks: make the prev chunk's event the
+            // one on the frame-slot run (run_batch dedups consecutive frames by pointer)
+            run_batch(x, c, jobs, j0, j1, ring_out ? c->d_outring : d_full, b, j0);
+            if (!ring_out) continue;
+            // ---- egress of batch b
+            FROI_CUDA(cudaEventRecord(c->d2h_ev[b], x->stream));
+            FROI_CUDA(cudaStreamWaitEvent(c->d2h_stream, c->d2h_ev[b], 0));
+            const uint8_t* dsrc = c->d_outring + mb * P * (b % kOutBatches);
+            if (!general_out) {
+                for (size_t j = j0; j < j1;) {  // runs of contiguous pinned destinations
+                    size_t e = j + 1;
+                    while (e < j1 && io.mask[(size_t)wt[e].first * n + wt[e].second] ==
+                                         io.mask[(size_t)wt[e - 1].first * n + wt[e - 1].second] + mb)
+                        ++e;
+                    FROI_CUDA(cudaMemcpyAsync(io.mask[(size_t)wt[j].first * n + wt[j].second], dsrc + mb * (j - j0),
+                                              mb * (e - j), cudaMemcpyDeviceToHost, c->d2h_stream));
+                    j = e;
+                }
+                if (io.frame0_rule)
+                    for (size_t j = j0; j < j1; ++j)
+                        if (wt[j].second == 1)
+                            FROI_CUDA(cudaMemcpyAsync(io.mask[(size_t)wt[j].first * n], dsrc + mb * (j - j0), mb,
+                                                      cudaMemcpyDeviceToHost, c->d2h_stream));
+                FROI_CUDA(cudaEventRecord(c->delivered[b], c->d2h_stream));
+            } else {
+                if (b >= (size_t)kOutBatches) tasks[b - kOutBatches]->wait();  // pinned slot is free
+                uint8_t* hslot = c->h_outring + mb * P * (b % kOutBatches);
+                FROI_CUDA(cudaMemcpyAsync(hslot, dsrc, mb * (j1 - j0), cudaMemcpyDeviceToHost, c->d2h_stream));
+                cudaEvent_t done = c->delivered[b];
+                FROI_CUDA(cudaEventRecord(done, c->d2h_stream));
+                HostPool* pool = c->pool.get();
+                tasks[b] = c->courier->submit([&, done, hslot, j0, j1, pool] {
+                    FROI_CUDA(cudaEventSynchronize(done));
+                    pool->parallel_for(j1 - j0, [&](size_t i) {
+                        const int w = wt[j0 + i].first, t = wt[j0 + i].second;
+                        put_mask(g, hslot + mb * i, io.layout, io.mask[(size_t)w * n + t]);
+                        if (io.frame0_rule && t == 1) put_mask(g, hslot + mb * i, io.layout, io.mask[(size_t)w * n]);
+                    });
+                });
+            }
+        }
+        upload_to(nk ? nk - 1 : 0);  // frames no pair reads (e.g. a push's carry-only tail)
+        for (auto& t : tasks)
+            if (t) t->wait();
+        FROI_CUDA(cudaEventRecord(c->d2h_done, c->d2h_stream));
+        FROI_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
+        FROI_CUDA(cudaEventRecord(c->ev[6], c->copy_stream));  // carry copies
+        FROI_CUDA(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
+        if (lane) {
+            FROI_CUDA(cudaEventRecord(c->ev_join, lane->stream));
+            FROI_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+        }
+        if (!ring_out) {
+            if (io.frame0_rule)
+                for (int w = 0; w < nw; ++w)
+                    FROI_CUDA(cudaMemcpyAsync(d_full + mb * ((size_t)w * n), d_full + mb * ((size_t)w * n + 1), mb,
+                                              cudaMemcpyDeviceToDevice, c->stream));
+            if (c->params.adjacent_factor > 0) {  // temporal ensemble (roi.hpp:356-362)
+                ensure_seq_tmp(c, mb * n);
+                for (int w = 0; w < nw; ++w) {
+                    uint8_t* base = d_full + mb * ((size_t)w * n);
+                    launch_ensemble(g, base, c->d_seq_tmp, n, c->params.adjacent_factor, c->stream);
+                    FROI_CUDA(cudaMemcpyAsync(base, c->d_seq_tmp, mb * n, cudaMemcpyDeviceToDevice, c->stream));
+                    ++c->launches;
+                }
+            }
+            if (!io.dev_masks) {  // deliver through the pinned egress twin, kOutBatches*Pcap at a time
+                ensure_host_outring(c);
+                const size_t step = P * kOutBatches;
+                for (size_t m0 = 0; m0 < nk; m0 += step) {
+                    const size_t m1 = std::min(nk, m0 + step);
+                    FROI_CUDA(cudaMemcpyAsync(c->h_outring, d_full + mb * m0, mb * (m1 - m0), cudaMemcpyDeviceToHost,
+                                              c->stream));
+                    FROI_CUDA(cudaStreamSynchronize(c->stream));
+                    c->pool->parallel_for(m1 - m0, [&](size_t i) {
+                        put_mask(g, c->h_outring + mb * i, io.layout, io.mask[m0 + i]);
+                    });
+                }
+            }
+        }
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    } catch (...) {
+        settle();
+        throw;
+    }
+    accumulate_batch_times(c, nb);
+    infos.assign(c->h_info, c->h_info + jobs.size());
+}
+
+// Per-frame stats of a host call: pair rows in (well, frame) order, frame 0 of a well borrows
+// frame 1's row with the identity shift (roi.hpp:348-349).
+void stats_for_call(froi_ctx* c, const HostCall& io, const std::vector<PairInfo>& infos,
+                    froi_frame_stats* stats) {
+    if (!stats) return;
+    size_t k = 0;
+    for (int w = 0; w < io.n_wells; ++w) {
+        froi_frame_stats* s = stats + (size_t)w * io.n_frames;
+        for (int t = io.t_begin; t < io.n_frames; ++t) fill_stats(c->g, infos[k++], &s[t]);
+        if (io.t_begin == 1) {
+            s[0] = s[1];
+            s[0].dx = 0;
+            s[0].dy = 0;
+            s[0].confidence = 1.0;
+        }
+    }
 }
 
 }  // namespace
@@ -1048,84 +1411,53 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
     if (stride < (size_t)c->g.W * c->g.H * sample_bytes) return fail(1, "frame stride too small");
     ABI_TRY
     FROI_CUDA(cudaSetDevice(c->device));
-    check_frames_range(c, frames, sample_bytes, stride, (long long)n_wells * n_frames);
-    const long long nm = (long long)n_wells * n_frames;
-    const size_t mb = (size_t)c->g.H * c->g.SB;
-    // ingest: frames resident on the device (BASELINE config 3 is 30 GB, well inside HBM); wells are
-    // copied on a separate stream and each well's pairs wait only for its own frames
-    const size_t need = c->frame_bytes * nm;
-    if (c->arena_cap < need) {
-        if (c->d_arena) FROI_CUDA(cudaFree(c->d_arena));
-        c->d_arena = nullptr;
-        c->arena_cap = 0;
-        FROI_CUDA(cudaMalloc(&c->d_arena, need));
-        c->arena_cap = need;
+    const size_t nk = (size_t)n_wells * n_frames;
+    const size_t ms = layout == FROI_MASK_PBM ? (size_t)c->g.H * c->g.SB : (size_t)c->g.W * c->g.H;
+    HostCall io;
+    io.n_wells = n_wells;
+    io.n_frames = n_frames;
+    io.src_bytes = sample_bytes;
+    io.layout = layout;
+    io.host.resize(nk);
+    io.dev.assign(nk, nullptr);
+    io.mask.resize(nk);
+    for (size_t k = 0; k < nk; ++k) {
+        io.host[k] = (const uint8_t*)frames + stride * k;
+        io.mask[k] = masks_out + ms * k;
     }
-    uint8_t* d_frames = c->d_arena;
-    // copy granularity: a first chunk of Pcap + 1 frames (exactly what the first batch needs)
-    // then chunks of Pcap frames, each with an event the consuming frame slots wait on.  (A shorter
-    // first batch starts sooner but leaves the two lanes in step for the rest of the call: 3 %
-    // slower on a 450-frame well.)
-    const int fchunk = std::max(1, c->Pcap);
-    const int first = c->Pcap;
-    // the first chunk itself goes in sub-chunks of 8 frames: the first batch's denoise runs
-    // sub-chunk by sub-chunk behind the copy (end to end +0.6 % on the C3 bench)
-    constexpr int first_sub = 8;
-    const bool direct = sample_bytes == c->g.sample_bytes && stride == c->frame_bytes;
-    std::vector<cudaEvent_t> ready;
-    if (direct) {
-        // the previous call's kernels may still read the arena: order the copies after them
-        FROI_CUDA(cudaEventRecord(c->ev[7], c->stream));
-        FROI_CUDA(cudaStreamWaitEvent(c->copy_stream, c->ev[7], 0));
-        ready.resize((size_t)n_wells * n_frames);
-        size_t ne = 0;
-        for (int w = 0; w < n_wells; ++w)
-            for (int f0 = 0; f0 < n_frames;) {
-                int len = fchunk;
-                if (w == 0 && first && f0 < first + 1)
-                    len = first_sub > 0 ? std::min(first_sub, first + 1 - f0) : first + 1 - f0;
-                const int f1 = std::min(n_frames, f0 + len);
-                const size_t off = c->frame_bytes * ((size_t)n_frames * w + f0);
-                FROI_CUDA(cudaMemcpyAsync(d_frames + off, (const uint8_t*)frames + off,
-                                          c->frame_bytes * (f1 - f0), cudaMemcpyHostToDevice, c->copy_stream));
-                if (c->well_ready.size() <= ne) {
-                    cudaEvent_t e;
-                    FROI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-                    c->well_ready.push_back(e);
-                }
-                cudaEvent_t e = c->well_ready[ne++];
-                FROI_CUDA(cudaEventRecord(e, c->copy_stream));
-                for (int f = f0; f < f1; ++f) ready[(size_t)w * n_frames + f] = e;
-                f0 = f1;
-            }
-    } else {
-        upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
-    }
-    ensure_seq_out(c, mb * nm);
     std::vector<PairInfo> infos;
-    // PBM into pinned memory without the ensemble: masks stream back batch by batch
-    cudaPointerAttributes pa{};
-    const bool pinned = cudaPointerGetAttributes(&pa, masks_out) == cudaSuccess && pa.type == cudaMemoryTypeHost;
-    cudaGetLastError();  // a pageable pointer may leave an error behind
-    const bool stream_back = layout == FROI_MASK_PBM && c->params.adjacent_factor == 0 && pinned;
-    extract_wells_dev(c, d_frames, c->frame_bytes, n_wells, n_frames, c->d_seq_out, infos,
-                      direct ? ready.data() : nullptr, stream_back ? masks_out : nullptr);
-    if (stream_back) {
-        // only frame 0 of each well (a copy of frame 1's mask, made after the batches) is left
-        for (int w = 0; w < n_wells; ++w)
-            FROI_CUDA(cudaMemcpyAsync(masks_out + mb * ((size_t)w * n_frames), c->d_seq_out + mb * ((size_t)w * n_frames),
-                                      mb, cudaMemcpyDeviceToHost, c->stream));
-        FROI_CUDA(cudaStreamSynchronize(c->stream));
-    } else {
-        deliver_masks(c, c->d_seq_out, nm, layout, masks_out);
-    }
-    stats_for_wells(c, infos, n_wells, n_frames, stats_out);
+    run_host_call(c, io, infos);
+    stats_for_call(c, io, infos, stats_out);
     ABI_CATCH
 }
 
 int froi_extract_roi(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, int n_frames,
                      int layout, uint8_t* masks_out, froi_frame_stats* stats_out) {
     return froi_extract_wells(c, frames, sample_bytes, stride, 1, n_frames, layout, masks_out, stats_out);
+}
+
+int froi_extract_frames(froi_ctx* c, const void* const* frames, int sample_bytes, int n_frames, int layout,
+                        uint8_t* const* masks, froi_frame_stats* stats_out) {
+    if (!c || !frames || !masks) return fail(1, "null argument");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(1, "sample_bytes must be 1 or 2");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (n_frames < 2) return fail(2, "extract_roi: sequence needs at least 2 frames");
+    for (int t = 0; t < n_frames; ++t)
+        if (!frames[t] || !masks[t]) return fail(1, "null frame or mask pointer");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    HostCall io;
+    io.n_wells = 1;
+    io.n_frames = n_frames;
+    io.src_bytes = sample_bytes;
+    io.layout = layout;
+    io.host.assign((const uint8_t* const*)frames, (const uint8_t* const*)frames + n_frames);
+    io.dev.assign(n_frames, nullptr);
+    io.mask.assign(masks, masks + n_frames);
+    std::vector<PairInfo> infos;
+    run_host_call(c, io, infos);
+    stats_for_call(c, io, infos, stats_out);
+    ABI_CATCH
 }
 
 int froi_extract_wells_device(froi_ctx* c, const void* d_frames, int sample_bytes, size_t stride,
@@ -1154,93 +1486,104 @@ int froi_stream_reset(froi_ctx* c, int n_wells) {
     c->stream_next_t.assign(n_wells, 0);
     const size_t need = c->frame_bytes * n_wells;
     if (c->carry_cap < need) {
-        if (c->d_carry) FROI_CUDA(cudaFree(c->d_carry));
-        c->d_carry = nullptr;
-        FROI_CUDA(cudaMalloc(&c->d_carry, need));
+        for (auto& d : c->d_carry) {
+            if (d) FROI_CUDA(cudaFree(d));
+            d = nullptr;
+        }
+        c->carry_cap = 0;
+        for (auto& d : c->d_carry) FROI_CUDA(cudaMalloc(&d, need));
         c->carry_cap = need;
     }
     ABI_CATCH
+}
+
+}  // extern "C"
+
+namespace {
+// Shared body of froi_stream_push / froi_stream_push_frames: frame k = w*chunk + t at
+// frame_at(k), mask k at mask_at(k) (host) or masks_out + k*mb (device PBM).
+template <typename FrameAt, typename MaskAt>
+int stream_push_impl(froi_ctx* c, FrameAt frame_at, int frames_on_device, int sample_bytes, int chunk,
+                     int layout, MaskAt mask_at, uint8_t* dev_masks, froi_frame_stats* stats_out) {
+    const bool first = c->stream_next_t[0] == 0;
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    const int nw = c->stream_wells;
+    const size_t nk = (size_t)nw * chunk, fb = c->frame_bytes;
+    // the pushed frames stream through the same rings as froi_extract_wells; the previous push's
+    // last frame of each well (the carry) is the first pair's prev, and this push's last frames
+    // become the next carry (double-buffered, so reading one never races writing the other)
+    HostCall io;
+    io.n_wells = nw;
+    io.n_frames = chunk;
+    io.t_begin = first ? 1 : 0;
+    io.frame0_rule = first;
+    io.src_bytes = sample_bytes;
+    io.layout = layout;
+    io.host.assign(nk, nullptr);
+    io.dev.assign(nk, nullptr);
+    for (size_t k = 0; k < nk; ++k) (frames_on_device ? io.dev[k] : io.host[k]) = frame_at(k);
+    for (int w = 0; w < nw; ++w) io.carry.push_back(c->d_carry[c->carry_cur] + fb * w);
+    uint8_t* next_carry = c->d_carry[1 - c->carry_cur];
+    if (!frames_on_device) io.new_carry = next_carry;
+    if (dev_masks) io.dev_masks = dev_masks;
+    else {
+        io.mask.resize(nk);
+        for (size_t k = 0; k < nk; ++k) io.mask[k] = mask_at(k);
+    }
+    std::vector<PairInfo> infos;
+    run_host_call(c, io, infos);
+    if (frames_on_device) {
+        for (int w = 0; w < nw; ++w)
+            FROI_CUDA(cudaMemcpyAsync(next_carry + fb * w, io.dev[(size_t)w * chunk + chunk - 1], fb,
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        FROI_CUDA(cudaStreamSynchronize(c->stream));
+    }
+    c->carry_cur = 1 - c->carry_cur;
+    stats_for_call(c, io, infos, stats_out);
+    for (int w = 0; w < nw; ++w) c->stream_next_t[w] += chunk;
+    ABI_CATCH
+}
+
+int stream_push_checks(froi_ctx* c, int frames_on_device, int sample_bytes, int chunk, int layout,
+                       int masks_on_device) {
+    if (c->stream_wells < 1) return fail(1, "froi_stream_reset first");
+    if (c->params.adjacent_factor != 0) return fail(1, "streaming requires adjacent_factor == 0");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (masks_on_device && layout != FROI_MASK_PBM) return fail(1, "device masks are PBM only");
+    if (chunk < 1) return fail(2, "chunk must be >= 1");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(1, "sample_bytes must be 1 or 2");
+    if (c->stream_next_t[0] == 0 && chunk < 2) return fail(2, "the first push of a sequence needs at least 2 frames");
+    if (frames_on_device && sample_bytes != c->g.sample_bytes)
+        return fail(1, "device frames must use the context sample width");
+    return 0;
+}
+}  // namespace
+
+extern "C" {
+
+int froi_stream_push_frames(froi_ctx* c, const void* const* frames, int sample_bytes, int chunk, int layout,
+                            uint8_t* const* masks, froi_frame_stats* stats_out) {
+    if (!c || !frames || !masks) return fail(1, "null argument");
+    if (int rc = stream_push_checks(c, 0, sample_bytes, chunk, layout, 0)) return rc;
+    const size_t nk = (size_t)c->stream_wells * chunk;
+    for (size_t k = 0; k < nk; ++k)
+        if (!frames[k] || !masks[k]) return fail(1, "null frame or mask pointer");
+    return stream_push_impl(
+        c, [&](size_t k) { return (const uint8_t*)frames[k]; }, 0, sample_bytes, chunk, layout,
+        [&](size_t k) { return masks[k]; }, nullptr, stats_out);
 }
 
 int froi_stream_push(froi_ctx* c, const void* frames, int frames_on_device, int sample_bytes,
                      size_t stride, int chunk, int layout, uint8_t* masks_out, int masks_on_device,
                      froi_frame_stats* stats_out) {
     if (!c || !frames || !masks_out) return fail(1, "null argument");
-    if (c->stream_wells < 1) return fail(1, "froi_stream_reset first");
-    if (c->params.adjacent_factor != 0) return fail(1, "streaming requires adjacent_factor == 0");
-    if (!check_layout(layout)) return fail(1, "unknown mask layout");
-    if (masks_on_device && layout != FROI_MASK_PBM) return fail(1, "device masks are PBM only");
-    if (chunk < 1) return fail(2, "chunk must be >= 1");
-    const bool first = c->stream_next_t[0] == 0;
-    if (first && chunk < 2) return fail(2, "the first push of a sequence needs at least 2 frames");
-    if (frames_on_device && sample_bytes != c->g.sample_bytes)
-        return fail(1, "device frames must use the context sample width");
-    ABI_TRY
-    FROI_CUDA(cudaSetDevice(c->device));
-    const Geom& g = c->g;
-    const int nw = c->stream_wells;
-    const long long nm = (long long)nw * chunk;
-    const size_t mb = (size_t)g.H * g.SB;
-    // device view of the pushed frames
-    uint8_t* d_frames;
-    size_t dstride;
-    if (frames_on_device) {
-        d_frames = (uint8_t*)frames;
-        dstride = stride;
-    } else {
-        ensure_seq_tmp(c, c->frame_bytes * nm);
-        d_frames = c->d_seq_tmp;
-        dstride = c->frame_bytes;
-        upload_frames(c, frames, sample_bytes, stride, nm, d_frames);
-    }
-    uint8_t* d_out = masks_on_device ? masks_out : nullptr;
-    if (!d_out) {
-        ensure_seq_out(c, mb * nm);
-        d_out = c->d_seq_out;
-    }
-    std::vector<PairJob> jobs;
-    for (int w = 0; w < nw; ++w) {
-        for (int k = 0; k < chunk; ++k) {
-            if (first && k == 0) continue;
-            PairJob J;
-            J.raw_prev = k == 0 ? (const void*)(c->d_carry + c->frame_bytes * w)
-                                : (const void*)(d_frames + dstride * ((size_t)w * chunk + k - 1));
-            J.raw_next = d_frames + dstride * ((size_t)w * chunk + k);
-            J.out_index = (long long)w * chunk + k;
-            J.stats_index = J.out_index;
-            jobs.push_back(J);
-        }
-    }
-    c->times = froi_stage_times{};
-    c->ktimes = froi_kernel_times{};
-    c->launches = 0;
-    std::vector<PairInfo> infos;
-    run_batches(c, jobs, d_out, infos);
-    if (first)
-        for (int w = 0; w < nw; ++w)
-            FROI_CUDA(cudaMemcpyAsync(d_out + mb * ((size_t)w * chunk), d_out + mb * ((size_t)w * chunk + 1), mb,
-                                      cudaMemcpyDeviceToDevice, c->stream));
-    // carry the last frame of every well
-    for (int w = 0; w < nw; ++w)
-        FROI_CUDA(cudaMemcpyAsync(c->d_carry + c->frame_bytes * w, d_frames + dstride * ((size_t)w * chunk + chunk - 1),
-                                  c->frame_bytes, cudaMemcpyDeviceToDevice, c->stream));
-    if (!masks_on_device) deliver_masks(c, d_out, nm, layout, masks_out);
-    FROI_CUDA(cudaStreamSynchronize(c->stream));
-    if (stats_out) {
-        size_t k = 0;
-        for (int w = 0; w < nw; ++w)
-            for (int t = first ? 1 : 0; t < chunk; ++t) fill_stats(g, infos[k++], &stats_out[(size_t)w * chunk + t]);
-        if (first)
-            for (int w = 0; w < nw; ++w) {
-                froi_frame_stats& s0 = stats_out[(size_t)w * chunk];
-                s0 = stats_out[(size_t)w * chunk + 1];
-                s0.dx = 0;
-                s0.dy = 0;
-                s0.confidence = 1.0;
-            }
-    }
-    for (int w = 0; w < nw; ++w) c->stream_next_t[w] += chunk;
-    ABI_CATCH
+    if (int rc = stream_push_checks(c, frames_on_device, sample_bytes, chunk, layout, masks_on_device)) return rc;
+    if (stride < (size_t)c->g.W * c->g.H * sample_bytes) return fail(1, "frame stride too small");
+    const size_t ms = layout == FROI_MASK_PBM ? (size_t)c->g.H * c->g.SB : (size_t)c->g.W * c->g.H;
+    return stream_push_impl(
+        c, [&](size_t k) { return (const uint8_t*)frames + stride * k; }, frames_on_device, sample_bytes, chunk,
+        layout, [&](size_t k) { return masks_out + ms * k; }, masks_on_device ? masks_out : nullptr, stats_out);
 }
 
 // ------------------------------------------------------------------ sub-operator taps
@@ -1296,7 +1639,10 @@ void upload_flow(froi_ctx* c, const float* u, const float* v) {
     const size_t px = (size_t)c->g.W * c->g.H;
     std::vector<float2> f(px);
     for (size_t i = 0; i < px; ++i) f[i] = make_float2(u[i], v[i]);
-    FROI_CUDA(cudaMemcpy(c->d_flow0, f.data(), sizeof(float2) * px, cudaMemcpyHostToDevice));
+    // on the context stream (non-blocking: the legacy stream would not order it), and complete
+    // before the staging vector goes away
+    FROI_CUDA(cudaMemcpyAsync(c->d_flow0, f.data(), sizeof(float2) * px, cudaMemcpyHostToDevice, c->stream));
+    FROI_CUDA(cudaStreamSynchronize(c->stream));
 }
 
 }  // namespace

@@ -1,0 +1,156 @@
+"""Full-length BASELINE configurations through the entry points the bench times, against the
+pinned CPU oracle (VERDICT r1 "Next round" #1).
+
+* C3: one whole 450-frame 1024^2 well (449 pairs = 15 batches of Pcap 32 on two execution lanes,
+  nr = 8 flow strips at level 0 — the bench's configuration) through
+    - ``froi_extract_wells_device`` (the bench's device-resident ``value`` leg),
+    - ``froi_extract_wells`` from pinned frames into pinned PBM rows (the bench's ``e2e`` leg),
+    - ``froi_extract_wells`` from pageable frames into RoiMask bytes (staging + courier path),
+    - ``froi_extract_frames`` with one pointer per uint16 frame (the C++ drop-in's call);
+  all four byte-identical, then compared with ``Oracle("port").extract_roi`` on every host core.
+* C2: the full 64-frame sequence.  C4: one 2048^2 12-bit well of 8 frames (L = 5).
+* Shifts and confidences bit-identical on every pair; the mask stage bit-exact given the GPU's
+  own flow on sampled pairs (batch boundaries included); flow within max |d| <= 2e-2 px and mean
+  EPE <= 1e-3 px on those pairs; end-to-end mask mismatch <= 1e-4 per frame.  The per-config
+  mismatch rates are printed (pytest -s) and recorded in DESIGN.md §5.
+"""
+import ctypes
+import multiprocessing
+import os
+from concurrent.futures import ProcessPoolExecutor
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+FLOW_MAX_ABS = 2e-2
+FLOW_MEAN_EPE = 1e-3
+MASK_MISMATCH_MAX = 1e-4
+
+
+def _apply_shift(f, dx, dy):
+    h, w = f.shape
+    return f[np.clip(np.arange(h) + dy, 0, h - 1)][:, np.clip(np.arange(w) + dx, 0, w - 1)]
+
+
+def _oracle_flow_job(args):
+    from oracle.oracle_py import Oracle
+    a, b, depth, params = args
+    return Oracle("port").compute_flow(a, b, depth, params)
+
+
+def _unpack(pbm, w):
+    return np.unpackbits(pbm, axis=-1)[..., :w]
+
+
+def _gpu_paths(gpu, frames, depth, params, max_pairs=0):
+    """Masks (bytes) from the four host/device entries of one context; asserts they agree."""
+    import torch
+
+    from paper_2511_14419_b200.params import CFrameStats
+    n, h, w = frames.shape
+    ctx = gpu.Context(w, h, depth, params, device=0, max_pairs=max_pairs)
+    try:
+        sb = (w + 7) // 8
+        # device-resident (bench value leg)
+        dfr = torch.from_numpy(frames if depth == 8 else frames.view(np.int16)).cuda()
+        dm = torch.empty((n, h, sb), dtype=torch.uint8, device="cuda")
+        st_dev = (CFrameStats * n)()
+        ctx.extract_wells_device(dfr.data_ptr(), 1, n, dm.data_ptr(), st_dev)
+        torch.cuda.synchronize()
+        dev_pbm = dm.cpu().numpy()
+        # pinned frames -> pinned PBM (bench e2e leg)
+        hin = torch.empty(frames.shape, dtype=torch.uint8 if depth == 8 else torch.int16, pin_memory=True)
+        hin.numpy()[:] = frames.view(np.uint8 if depth == 8 else np.int16)
+        hout = torch.empty((n, h, sb), dtype=torch.uint8, pin_memory=True)
+        st_pin = (CFrameStats * n)()
+        ctx.extract_wells_into(hin.numpy().view(frames.dtype)[None], hout.numpy()[None], st_pin)
+        pin_pbm = hout.numpy().copy()
+        # pageable frames -> RoiMask bytes (staging ring + courier unpack)
+        bytes_masks, st_pg = ctx.extract_wells(frames[None], layout="bytes")
+        # one pointer per uint16 frame and per mask (the C++ drop-in's froi_extract_frames)
+        f16 = [np.ascontiguousarray(frames[t], dtype=np.uint16) for t in range(n)]
+        outs = [np.empty((h, w), np.uint8) for _ in range(n)]
+        fp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in f16])
+        mp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in outs])
+        st_fr = (CFrameStats * n)()
+        from paper_2511_14419_b200 import _native
+        with ctx.lock:
+            _native.check(_native.lib.froi_extract_frames(ctx.handle, fp, 2, n, 0, mp, st_fr), "extract_frames")
+    finally:
+        ctx.close()
+    dev = _unpack(dev_pbm, w)
+    assert np.array_equal(dev, _unpack(pin_pbm, w)), "pinned host entry differs from the device entry"
+    assert np.array_equal(dev, bytes_masks[0]), "pageable/bytes entry differs from the device entry"
+    assert np.array_equal(dev, np.stack(outs)), "per-frame-pointer entry differs from the device entry"
+    rows = lambda st: [(s.dx, s.dy, s.confidence, s.mask_count) for s in st]  # noqa: E731
+    assert rows(st_dev) == rows(st_pin) == rows(st_pg[:n]) == rows(st_fr)
+    return dev, st_dev
+
+
+def check_full(gpu, oracle, frames, depth, params, label, sample_pairs, max_pairs=0):
+    from paper_2511_14419_b200.params import ExtractInfo  # noqa: F401
+    n, h, w = frames.shape
+    got, st = _gpu_paths(gpu, frames, depth, params, max_pairs)
+    want, shifts, fracs = oracle.extract_roi(frames, depth, params, workers=os.cpu_count() or 1)
+    assert [(s.dx, s.dy, s.confidence) for s in st] == [(s.dx, s.dy, s.confidence) for s in shifts], label
+    mism = np.array([float((got[t] != want[t]).mean()) for t in range(n)])
+    # flow tolerance and mask-stage exactness on the sampled pairs
+    den = {}
+    for t in sorted(set(sample_pairs) | {t - 1 for t in sample_pairs}):
+        den[t] = gpu.denoise(frames[t], params, depth=depth)
+    jobs, gflows = [], {}
+    for t in sample_pairs:
+        s = shifts[t]
+        nxt = _apply_shift(den[t], s.dx, s.dy)
+        gflows[t] = gpu.compute_flow(den[t - 1], nxt, params, depth=depth)
+        jobs.append((den[t - 1], nxt, depth, params))
+    with ProcessPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1),
+                             mp_context=multiprocessing.get_context("spawn")) as ex:
+        oflows = list(ex.map(_oracle_flow_job, jobs))
+    flow_err = {}
+    for t, (ou, ov) in zip(sample_pairs, oflows):
+        gu, gv = gflows[t]
+        du, dv = gu.astype(np.float64) - ou, gv.astype(np.float64) - ov
+        flow_err[t] = (float(max(np.abs(du).max(), np.abs(dv).max())), float(np.hypot(du, dv).mean()))
+        m, _ = oracle.mask_from_flow(gu, gv, frames[t], depth, shifts[t].dx, shifts[t].dy, params)
+        assert np.array_equal(m, got[t]), f"{label}: mask stage differs at frame {t}"
+    print(f"\n{label}: {n} frames, mask mismatch per frame max {mism.max():.2e} mean {mism.mean():.2e}, "
+          f"frames with any mismatch {int((mism > 0).sum())}/{n}; sampled flow (max|d|, mean EPE) "
+          f"{ {t: (round(a, 5), round(b, 7)) for t, (a, b) in flow_err.items()} }")
+    for t, (mx, mean) in flow_err.items():
+        assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (label, t, mx, mean)
+    assert mism.max() <= MASK_MISMATCH_MAX, (label, mism.max(), int(mism.argmax()))
+    return mism
+
+
+@pytest.fixture(scope="module")
+def synth():
+    from paper_2511_14419_b200 import synth as S
+    return S
+
+
+def test_c3_full_well_bench_entries(gpu, oracle, synth):
+    """One whole C3 well through the bench's entries at the bench's batch geometry."""
+    cfg = synth.config("C3")
+    frames = synth.well_frames(cfg, 0, 450)
+    # first and last pair, both sides of several 32-pair batch boundaries, the tail batch
+    check_full(gpu, oracle, frames, 8, cfg.params, "C3 well 0 x 450",
+               sample_pairs=[1, 32, 33, 64, 65, 224, 225, 416, 417, 449])
+
+
+def test_c2_full_sequence(gpu, oracle, synth):
+    cfg = synth.config("C2")
+    frames = synth.well_frames(cfg, 0, 64)
+    check_full(gpu, oracle, frames, 8, cfg.params, "C2 x 64", sample_pairs=[1, 2, 31, 32, 33, 62, 63])
+
+
+def test_c4_16bit_well(gpu, oracle, synth):
+    cfg = synth.config("C4")
+    frames = synth.well_frames(cfg, 0, 8)
+    # 2048^2: Pcap 8, so 7 pairs are one batch; max_pairs 3 also runs it as three batches on two lanes
+    check_full(gpu, oracle, frames, 16, cfg.params, "C4 well 0 x 8", sample_pairs=[1, 4, 7])
+    got3, _ = _gpu_paths(gpu, frames, 16, cfg.params, max_pairs=3)
+    got8, _ = _gpu_paths(gpu, frames, 16, cfg.params)
+    assert np.array_equal(got3, got8), "batch size changed the C4 masks"
