@@ -123,11 +123,22 @@ inline std::vector<flowroi::RoiMask> extract_roi(const flowroi::Sequence& seq,
         if (!seq[t].same_shape(f0)) throw data_error("sequence frames must share dimensions and depth");
         fp[t] = seq[t].pixels.data();
     }
-    std::vector<flowroi::RoiMask> masks = detail::make_masks(n, f0.width, f0.height);
-    std::vector<uint8_t*> mp(n);
-    for (std::size_t t = 0; t < n; ++t) mp[t] = masks[t].bits.data();
+    // each RoiMask is constructed (zero-filled W*H bytes, core.hpp:84-85) by the library's host
+    // threads right before its mask is unpacked into it, while the GPU works on later pairs
+    std::vector<flowroi::RoiMask> masks(n);
+    struct Sink {
+        std::vector<flowroi::RoiMask>* m;
+        int w, h;
+        static uint8_t* at(void* u, int, int t) {
+            Sink* s = static_cast<Sink*>(u);
+            flowroi::RoiMask& r = (*s->m)[static_cast<std::size_t>(t)];
+            r = flowroi::RoiMask(s->w, s->h);
+            return r.bits.data();
+        }
+    } sink{&masks, f0.width, f0.height};
     std::vector<froi_frame_stats> stats(n);
-    check(froi_extract_frames(ctx, fp.data(), 2, static_cast<int>(n), FROI_MASK_BYTES, mp.data(), stats.data()),
+    check(froi_extract_frames_sink(ctx, fp.data(), 2, static_cast<int>(n), FROI_MASK_BYTES, &Sink::at, &sink,
+                                   stats.data()),
           "extract_roi");
     if (info) {
         info->shifts.resize(n);

@@ -184,6 +184,15 @@ int froi_extract_wells(froi_ctx* ctx, const void* frames, int sample_bytes,
 int froi_extract_frames(froi_ctx* ctx, const void* const* frames, int sample_bytes, int n_frames,
                         int mask_layout, uint8_t* const* masks, froi_frame_stats* stats_out);
 
+/* A mask destination supplied on demand: called (from the library's host threads, concurrently,
+ * each (well, frame) once; frame 0 after frame 1) just before mask `frame` of `well` is written;
+ * returns where its W*H bytes (or PBM rows) go.  Lets a caller allocate its RoiMasks while the GPU
+ * works instead of before the call. */
+typedef uint8_t* (*froi_mask_sink)(void* user, int well, int frame);
+int froi_extract_frames_sink(froi_ctx* ctx, const void* const* frames, int sample_bytes, int n_frames,
+                             int mask_layout, froi_mask_sink sink, void* user,
+                             froi_frame_stats* stats_out);
+
 /* Device-resident variant used for the device-side throughput figure: d_frames is a device
  * pointer (well-major, as above), d_masks_pbm receives PBM-packed masks on the device.
  * stats_out is a HOST pointer (nullable). Asynchronous work is complete on return. */

@@ -885,6 +885,8 @@ struct HostCall {
     uint8_t* new_carry = nullptr;         // device [w] frames: receives each well's last frame
     int layout = FROI_MASK_PBM;
     std::vector<uint8_t*> mask;           // [w*n + t] host destination (layout)
+    froi_mask_sink sink = nullptr;        // or: destination asked for just before it is written
+    void* sink_user = nullptr;
     uint8_t* dev_masks = nullptr;         // device PBM destination [w*n + t] instead of mask[]
     bool frame0_rule = true;              // mask (w, 0) := mask (w, 1) (roi.hpp:348)
 };
@@ -894,6 +896,24 @@ bool is_pinned(const void* p) {
     const bool ok = cudaPointerGetAttributes(&a, p) == cudaSuccess;
     cudaGetLastError();  // an unregistered pointer may leave an error behind on older drivers
     return ok && (a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged);
+}
+
+// Pinned-ness of n buffers of `bytes` each: a run of back-to-back buffers is one allocation when
+// its first and last byte are both pinned (two queries per run instead of one per buffer).
+std::vector<char> pinned_flags(const std::vector<const uint8_t*>& p, size_t bytes) {
+    std::vector<char> f(p.size(), 0);
+    for (size_t i = 0; i < p.size();) {
+        if (!p[i]) {
+            ++i;
+            continue;
+        }
+        size_t e = i + 1;
+        while (e < p.size() && p[e] && p[e] == p[e - 1] + bytes) ++e;
+        const bool pin = is_pinned(p[i]) && is_pinned(p[e - 1] + bytes - 1);
+        for (size_t k = i; k < e; ++k) f[k] = pin;
+        i = e;
+    }
+    return f;
 }
 
 void ensure_pipeline(froi_ctx* c) {
@@ -1004,15 +1024,23 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             d_full = c->d_seq_out;
         }
     }
+    const std::vector<char> src_pinned = pinned_flags(io.host, (size_t)g.W * g.H * io.src_bytes);
     bool any_staged = false;
-    for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !is_pinned(io.host[k]));
+    for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !src_pinned[k]);
     if (any_staged) ensure_staging(c);
-    const bool general_out = ring_out && !(io.layout == FROI_MASK_PBM && [&] {
-        for (size_t k = 0; k < nk; ++k)
-            if (!is_pinned(io.mask[k])) return false;
-        return true;
+    const bool general_out = ring_out && (io.sink || io.layout != FROI_MASK_PBM || [&] {
+        const std::vector<char> f = pinned_flags(std::vector<const uint8_t*>(io.mask.begin(), io.mask.end()), mb);
+        for (char x : f)
+            if (!x) return true;
+        return false;
     }());
     if (general_out) ensure_host_outring(c);
+    auto dest = [&](int w, int t) -> uint8_t* {
+        if (!io.sink) return io.mask[(size_t)w * n + t];
+        uint8_t* d = io.sink(io.sink_user, w, t);
+        if (!d) throw Error(1, "mask sink returned a null destination");
+        return d;
+    };
 
     c->times = froi_stage_times{};
     c->ktimes = froi_kernel_times{};
@@ -1040,7 +1068,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             for (size_t k = k0; k < k1; ++k) {
                 if (!io.host[k]) continue;
                 any = true;
-                direct &= io.src_bytes == g.sample_bytes && is_pinned(io.host[k]);
+                direct &= io.src_bytes == g.sample_bytes && src_pinned[k];
                 wait_b = std::max(wait_b, last_reader[k % RF]);
             }
             if (!any) continue;
@@ -1161,8 +1189,8 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                     FROI_CUDA(cudaEventSynchronize(done));
                     pool->parallel_for(j1 - j0, [&](size_t i) {
                         const int w = wt[j0 + i].first, t = wt[j0 + i].second;
-                        put_mask(g, hslot + mb * i, io.layout, io.mask[(size_t)w * n + t]);
-                        if (io.frame0_rule && t == 1) put_mask(g, hslot + mb * i, io.layout, io.mask[(size_t)w * n]);
+                        put_mask(g, hslot + mb * i, io.layout, dest(w, t));
+                        if (io.frame0_rule && t == 1) put_mask(g, hslot + mb * i, io.layout, dest(w, 0));
                     });
                 });
             }
@@ -1201,7 +1229,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                                               c->stream));
                     FROI_CUDA(cudaStreamSynchronize(c->stream));
                     c->pool->parallel_for(m1 - m0, [&](size_t i) {
-                        put_mask(g, c->h_outring + mb * i, io.layout, io.mask[m0 + i]);
+                        put_mask(g, c->h_outring + mb * i, io.layout, dest((int)((m0 + i) / n), (int)((m0 + i) % n)));
                     });
                 }
             }
@@ -1434,6 +1462,31 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
 int froi_extract_roi(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, int n_frames,
                      int layout, uint8_t* masks_out, froi_frame_stats* stats_out) {
     return froi_extract_wells(c, frames, sample_bytes, stride, 1, n_frames, layout, masks_out, stats_out);
+}
+
+int froi_extract_frames_sink(froi_ctx* c, const void* const* frames, int sample_bytes, int n_frames,
+                             int layout, froi_mask_sink sink, void* user, froi_frame_stats* stats_out) {
+    if (!c || !frames || !sink) return fail(1, "null argument");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(1, "sample_bytes must be 1 or 2");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (n_frames < 2) return fail(2, "extract_roi: sequence needs at least 2 frames");
+    for (int t = 0; t < n_frames; ++t)
+        if (!frames[t]) return fail(1, "null frame pointer");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    HostCall io;
+    io.n_wells = 1;
+    io.n_frames = n_frames;
+    io.src_bytes = sample_bytes;
+    io.layout = layout;
+    io.host.assign((const uint8_t* const*)frames, (const uint8_t* const*)frames + n_frames);
+    io.dev.assign(n_frames, nullptr);
+    io.sink = sink;
+    io.sink_user = user;
+    std::vector<PairInfo> infos;
+    run_host_call(c, io, infos);
+    stats_for_call(c, io, infos, stats_out);
+    ABI_CATCH
 }
 
 int froi_extract_frames(froi_ctx* c, const void* const* frames, int sample_bytes, int n_frames, int layout,
