@@ -14,6 +14,8 @@ from .params import (CFrameStats, CKernelTimes, CParams, CShift, CStageTimes, Da
                      InternalError, UsageError)
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib", "libfroi.so")
+# profiling A/B only (profiles/tools/stage_ab.py): another in-tree build of the same library
+LIB_PATH = os.environ.get("FROI_LIB", LIB_PATH)
 
 _P = ctypes.c_void_p
 _I = ctypes.c_int
@@ -70,6 +72,8 @@ def _load() -> ctypes.CDLL:
             "(python -c 'import __graft_entry__ as g; g.build()'); there is no CPU fallback")
     lib = ctypes.CDLL(LIB_PATH)
     for name, (res, args) in SIGNATURES.items():
+        if "FROI_LIB" in os.environ and not hasattr(lib, name):
+            continue  # an older build under A/B comparison
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args

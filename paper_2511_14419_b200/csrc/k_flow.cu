@@ -545,12 +545,6 @@ __global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* _
     }
 }
 
-__device__ __forceinline__ float2 prior_at(const Geom& g, const IterArgs& a, size_t pair_off,
-                                           int x, int y) {
-    if (a.mode == 0) return make_float2(0.f, 0.f);
-    return a.flow_in[pair_off + g.loff[a.l] + (size_t)y * g.lw[a.l] + x];
-}
-
 // Packed fp32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2): two independent lanes per instruction.
 __device__ __forceinline__ void fma2(float& dx, float& dy, float ax, float ay, float bx, float by,
                                      float cx, float cy) {
@@ -929,27 +923,31 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         // scale, so it is never applied.  fp32 with a compensated determinant (Kahan: the g12^2
         // rounding error is carried exactly).
         const int tx = threadIdx.x % FX, x = x0 + tx;
-#pragma unroll 1
+        const int ty0 = threadIdx.x / FX;
+        const float* Gs = G + tx;
+#pragma unroll
         for (int j = 0; j < FY / (FNT / FX); ++j) {
-            const int ty = threadIdx.x / FX + j * (FNT / FX), y = y0 + ty;
-            if (x >= w || y >= h) continue;
+            const int ty = ty0 + j * (FNT / FX), y = y0 + ty;
             const int rr = b0 + ty;
-            const int sidx = (rr >= RG ? rr - RG : rr) * SW + tx;
-            const float g11 = G[sidx], g12 = G[PL + sidx], g22 = G[2 * PL + sidx];
-            const float h1 = G[3 * PL + sidx], h2 = G[4 * PL + sidx];
+            const int sidx = (rr >= RG ? rr - RG : rr) * SW;
+            const float g11 = Gs[sidx], g12 = Gs[PL + sidx], g22 = Gs[2 * PL + sidx];
+            const float h1 = Gs[3 * PL + sidx], h2 = Gs[4 * PL + sidx];
+            if (x >= w || y >= h) continue;
             const float q = g12 * g12;
             const float qe = fmaf(g12, g12, -q);
             const float det = fmaf(g11, g22, -q) - qe;
             const float frob2 = fmaf(g11, g11, fmaf(2.f * g12, g12, g22 * g22));
+            const unsigned o = (unsigned)(y * w + x);
             float2 r;
-            if (!(det > 1e-9f * frob2)) {
-                r = prior_at(g, a, pair_off, x, y);
-            } else {
+            if (det > 1e-9f * frob2) {
                 const float rd = __fdividef(1.f, det);
                 r.x = (g22 * h1 - g12 * h2) * rd;
                 r.y = (g11 * h2 - g12 * h1) * rd;
+            } else {
+                // singular: keep the prior (flow.hpp:245-246), zero on the coarsest first pass
+                r = a.mode ? fin[o] : make_float2(0.f, 0.f);
             }
-            out[y * w + x] = r;
+            out[o] = r;
         }
         __syncthreads();  // ring rows are rewritten by the next tile
     }
