@@ -471,6 +471,23 @@ def run_ours(args) -> None:
         "denoise_ns", "fft_forward_ns", "expand_ns", "register_ns", "expand_shifted_ns",
         "flow_iter_ns", "mask_ns"))) for k, v in kt_sum.items() if k.endswith("_ns")}
 
+    # fp64 roofline of the exact-fp64 stages: ncu-counted fp64 instructions per frame / pair
+    # (profiles/fp64_work.json) over their event-timed stage time, against the measured fp64 peak
+    fp64 = None
+    fw = os.path.join(ROOT, "profiles", "fp64_work.json")
+    if os.path.exists(fw) and kt_sum.get("pairs"):
+        with open(fw) as f:
+            w64 = json.load(f)
+        pk64 = w64["peak"]["fp64_inst_per_s"]
+        fp64 = {"bound": "fp64", "unit": "fp64 inst/s", "peak": pk64, "peak_source": "measured (fp64_peak.cu)"}
+        for stage, units, per in (("denoise", kt_sum["frames"], w64["inst_per_frame"]["denoise"]),
+                                  ("fft_forward", kt_sum["frames"], w64["inst_per_frame"]["fft_forward"]),
+                                  ("register", kt_sum["pairs"], w64["inst_per_pair"]["register"])):
+            t = kt_sum.get(stage + "_ns", 0) * 1e-9
+            if t > 0:
+                ach = per * units / t
+                fp64[stage] = {"achieved": ach, "frac": ach / pk64}
+
     cpu = None
     if rank == 0 and not args.no_cpu_baseline:
         # ~10 s of the reference on every host thread: 8 pairs per thread of one C3 well
@@ -499,6 +516,7 @@ def run_ours(args) -> None:
                                   "frac": mb["total"] * pairs_per_s / 1e9 / pk["hbm_gbs"],
                                   "pairs_per_s_per_gpu": pairs_per_s},
             "stage_share": stage_frac,
+            "fp64_roofline": fp64,
             # per-step device time inside the per-stage events of the one-lane leg (vs ms_per_step
             # of the two-lane timed leg)
             "stage_ms_per_step_1lane": sum(kt_sum.get(x, 0) for x in (

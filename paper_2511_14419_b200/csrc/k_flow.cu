@@ -791,6 +791,8 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                 bl_split(gyB, prB.y, h, yaB, lB.fy);
                 const unsigned iA0 = (unsigned)(yaA * w + xaA), iA1 = iA0 + (unsigned)w;
                 const unsigned iB0 = (unsigned)(yaB * w + xaB), iB1 = iB0 + (unsigned)w;
+                FROI_DCHECK(iA1 + 1 < (unsigned)(w * h) && iB1 + 1 < (unsigned)(w * h));
+                FROI_DCHECK(siA >= 0 && siA < RG * SW && siB >= 0 && siB < RG * SW);
                 lA.q00 = __ldg(nA + iA0);
                 lA.q01 = __ldg(nA + iA0 + 1);
                 lA.q10 = __ldg(nA + iA1);
@@ -930,6 +932,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
             const int ty = ty0 + j * (FNT / FX), y = y0 + ty;
             const int rr = b0 + ty;
             const int sidx = (rr >= RG ? rr - RG : rr) * SW;
+            FROI_DCHECK(sidx >= 0 && sidx + tx < RG * SW);
             const float g11 = Gs[sidx], g12 = Gs[PL + sidx], g22 = Gs[2 * PL + sidx];
             const float h1 = Gs[3 * PL + sidx], h2 = Gs[4 * PL + sidx];
             if (x >= w || y >= h) continue;

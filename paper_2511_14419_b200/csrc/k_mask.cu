@@ -1211,6 +1211,7 @@ __global__ void __launch_bounds__(RNT) k_ccl_runs(Geom g, MaskBuffers b) {
         unsigned int ts, te;
         unsigned int ks = off_s + warp_excl_scan(__popc(starts), ts);
         unsigned int ke = off_e + warp_excl_scan(__popc(ends), te);
+        FROI_DCHECK(ks + __popc(starts) <= (unsigned)g.RMAX && ke + __popc(ends) <= (unsigned)g.RMAX);
         for (uint32_t bits = starts; bits; bits &= bits - 1) x0[ks++] = (uint16_t)(j * 32 + __ffs(bits) - 1);
         for (uint32_t bits = ends; bits; bits &= bits - 1) x1[ke++] = (uint16_t)(j * 32 + __ffs(bits) - 1);
         off_s += ts;
@@ -1245,6 +1246,7 @@ __global__ void __launch_bounds__(RNT) k_ccl_union(Geom g, MaskBuffers b) {
             const int mid = (lo + hi) >> 1;
             if ((int)px1[mid] < a - 1) lo = mid + 1; else hi = mid;
         }
+        FROI_DCHECK(n <= g.RMAX && np <= g.RMAX && a <= e && e < g.W);
         for (int j = lo; j < np && (int)px0[j] <= e + 1; ++j)
             runite(par, y * g.RMAX + k, (y - 1) * g.RMAX + j);
     }

@@ -19,8 +19,10 @@
 #include <array>
 #include <vector>
 
+#include <map>
 #include <memory>
 #include <thread>
+#include <tuple>
 
 #include "../../include/froi/froi.h"
 #include "host_pool.hpp"
@@ -236,6 +238,11 @@ T* dalloc(size_t count, size_t* total) {
 
 }  // namespace
 
+static bool default_graphs() {
+    const char* e = getenv("FROI_GRAPHS");
+    return !(e && atoi(e) == 0);
+}
+
 static int default_lanes() {
     const char* e = getenv("FROI_LANES");
     return (e && atoi(e) == 1) ? 1 : 2;
@@ -334,6 +341,16 @@ struct froi_ctx {
     cudaEvent_t d2h_done = nullptr;
     std::vector<cudaEvent_t> chunk_ready;  // per upload chunk of a call
     uint64_t launches = 0;
+    // CUDA graphs of a batch's kernel sequence, one per (table buffer, pairs, frame slots, output):
+    // captured on first use, replayed with this batch's stage events swapped into its 8 event nodes
+    struct BatchGraph {
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        cudaGraphNode_t ev_node[8] = {};
+        uint64_t launches = 0;
+    };
+    std::map<std::tuple<int, int, int, const void*>, BatchGraph> graphs;
+    bool use_graphs = default_graphs();
 
     MaskBuffers mask_buffers(int tb_) const {
         MaskBuffers b;
@@ -490,8 +507,17 @@ void ctx_alloc(froi_ctx* c) {
     FROI_CUDA(cudaDeviceSynchronize());
 }
 
+void drop_graphs(froi_ctx* c) {
+    for (auto& kv : c->graphs) {
+        if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+        if (kv.second.graph) cudaGraphDestroy(kv.second.graph);
+    }
+    c->graphs.clear();
+}
+
 void ctx_free(froi_ctx* c) {
     cudaSetDevice(c->device);
+    drop_graphs(c);
     if (c->lane) {
         ctx_free(c->lane);
         delete c->lane;
@@ -610,37 +636,98 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
     FROI_CUDA(cudaEventRecord(c->tables_free[tb], s));
 
     cudaEvent_t* ev = owner->bev[bi].data();
-    FROI_CUDA(cudaEventRecord(ev[0], s));
-    FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
-    // denoise each run of frame slots as soon as the ingest chunk holding it has landed (the
-    // first batch of a host call starts after its first sub-chunk instead of the whole batch)
-    int n_denoise = 0;
-    for (int s0 = 0; s0 < nf; ++n_denoise) {
+    // runs of frame slots that share an ingest event
+    std::vector<std::pair<int, int>> runs;
+    for (int s0 = 0; s0 < nf;) {
         int s1 = s0 + 1;
         while (s1 < nf && slot_ready[s1] == slot_ready[s0]) ++s1;
-        if (slot_ready[s0]) FROI_CUDA(cudaStreamWaitEvent(s, slot_ready[s0], 0));
-        launch_denoise(g, c->dp, c->d_frame_raw[tb] + s0, c->d_den + c->frame_bytes * s0, c->d_sums + s0,
-                       c->h_spatial.data(), c->d_lut, s1 - s0, s);
+        runs.emplace_back(s0, s1);
         s0 = s1;
     }
-    FROI_CUDA(cudaEventRecord(ev[1], s));
-    launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
-    FROI_CUDA(cudaEventRecord(ev[2], s));
-    FlowBuffers fb = c->flow_buffers();
-    launch_expand_frames(g, c->dp, fb, nf, s);
-    FROI_CUDA(cudaEventRecord(ev[3], s));
-    launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
-                          c->d_cols, c->d_surf, c->d_info, n_pairs, s);
-    FROI_CUDA(cudaEventRecord(ev[4], s));
-    launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
-    FROI_CUDA(cudaEventRecord(ev[5], s));
-    const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
-    FROI_CUDA(cudaEventRecord(ev[6], s));
-    MaskBuffers mb = c->mask_buffers(tb);
-    mb.flow = cur ? c->d_flow1 : c->d_flow0;
-    mb.out_pbm = out_pbm;
-    launch_mask_stage(g, c->dp, mb, n_pairs, s, &owner->launches);
-    FROI_CUDA(cudaEventRecord(ev[7], s));
+    // the stage sequence; `rec` records stage event i (a plain record, or an external event node
+    // inside a capture), `first_wait` orders each denoise run after its ingest event
+    auto enqueue = [&](auto rec, bool per_run) {
+        rec(0);
+        FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
+        // denoise each run of frame slots as soon as the ingest chunk holding it has landed (the
+        // first batch of a host call starts after its first sub-chunk instead of the whole batch)
+        if (per_run) {
+            for (auto& r : runs) {
+                if (slot_ready[r.first]) FROI_CUDA(cudaStreamWaitEvent(s, slot_ready[r.first], 0));
+                launch_denoise(g, c->dp, c->d_frame_raw[tb] + r.first, c->d_den + c->frame_bytes * r.first,
+                               c->d_sums + r.first, c->h_spatial.data(), c->d_lut, r.second - r.first, s);
+            }
+        } else {
+            launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, nf, s);
+        }
+        rec(1);
+        launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
+        rec(2);
+        FlowBuffers fb = c->flow_buffers();
+        launch_expand_frames(g, c->dp, fb, nf, s);
+        rec(3);
+        launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
+                              c->d_cols, c->d_surf, c->d_info, n_pairs, s);
+        rec(4);
+        launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+        rec(5);
+        const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
+        rec(6);
+        MaskBuffers mb = c->mask_buffers(tb);
+        mb.flow = cur ? c->d_flow1 : c->d_flow0;
+        mb.out_pbm = out_pbm;
+        uint64_t ml = 0;
+        launch_mask_stage(g, c->dp, mb, n_pairs, s, &ml);
+        rec(7);
+        return ml;
+    };
+    // a CUDA graph per batch shape; the first batch of a host call, whose frames arrive in
+    // sub-chunks, keeps one denoise launch per sub-chunk (it starts before its frames are all in)
+    const bool graph = c->use_graphs && runs.size() <= 2;
+    int n_denoise = graph ? 1 : (int)runs.size();
+    if (graph) {
+        for (auto& r : runs)
+            if (slot_ready[r.first]) FROI_CUDA(cudaStreamWaitEvent(s, slot_ready[r.first], 0));
+        const auto key = std::make_tuple(tb, n_pairs, nf, (const void*)out_pbm);
+        auto it = c->graphs.find(key);
+        if (it == c->graphs.end()) {
+            froi_ctx::BatchGraph bg;
+            FROI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            try {
+                bg.launches = enqueue([&](int i) { FROI_CUDA(cudaEventRecordWithFlags(ev[i], s, cudaEventRecordExternal)); },
+                                      false);
+            } catch (...) {
+                cudaGraph_t junk = nullptr;
+                cudaStreamEndCapture(s, &junk);
+                if (junk) cudaGraphDestroy(junk);
+                throw;
+            }
+            FROI_CUDA(cudaStreamEndCapture(s, &bg.graph));
+            size_t nn = 0;
+            FROI_CUDA(cudaGraphGetNodes(bg.graph, nullptr, &nn));
+            std::vector<cudaGraphNode_t> nodes(nn);
+            FROI_CUDA(cudaGraphGetNodes(bg.graph, nodes.data(), &nn));
+            for (cudaGraphNode_t nd : nodes) {
+                cudaGraphNodeType ty;
+                FROI_CUDA(cudaGraphNodeGetType(nd, &ty));
+                if (ty != cudaGraphNodeTypeEventRecord) continue;
+                cudaEvent_t e;
+                FROI_CUDA(cudaGraphEventRecordNodeGetEvent(nd, &e));
+                for (int i = 0; i < 8; ++i)
+                    if (e == ev[i]) bg.ev_node[i] = nd;
+            }
+            for (int i = 0; i < 8; ++i)
+                if (!bg.ev_node[i]) throw Error(3, "batch graph: stage event node missing");
+            FROI_CUDA(cudaGraphInstantiate(&bg.exec, bg.graph, 0));
+            it = c->graphs.emplace(key, bg).first;
+        }
+        froi_ctx::BatchGraph& bg = it->second;
+        for (int i = 0; i < 8; ++i) FROI_CUDA(cudaGraphExecEventRecordNodeSetEvent(bg.exec, bg.ev_node[i], ev[i]));
+        FROI_CUDA(cudaGraphLaunch(bg.exec, s));
+        owner->launches += bg.launches;
+    } else {
+        owner->launches += enqueue([&](int i) { FROI_CUDA(cudaEventRecord(ev[i], s)); }, true);
+    }
     FROI_CUDA(cudaMemcpyAsync(owner->h_info + info_off, c->d_info, sizeof(PairInfo) * n_pairs,
                               cudaMemcpyDeviceToHost, s));
     froi_kernel_times& K = owner->ktimes;
@@ -1395,7 +1482,16 @@ int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p) {
     ctx->params = *p;
     ctx->dp = make_dev_params(*p);
     ctx->dp.norm_lut = ctx->d_norm_lut;
-    return 0;
+    // captured batch graphs hold the old parameters as kernel arguments
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(ctx->device));
+    FROI_CUDA(cudaStreamSynchronize(ctx->stream));
+    drop_graphs(ctx);
+    if (ctx->lane) {
+        FROI_CUDA(cudaStreamSynchronize(ctx->lane->stream));
+        drop_graphs(ctx->lane);
+    }
+    ABI_CATCH
 }
 
 int froi_ctx_stage_times(const froi_ctx* ctx, froi_stage_times* out) {
