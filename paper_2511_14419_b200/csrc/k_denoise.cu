@@ -1,14 +1,19 @@
 // k_denoise.cu — fused median + bilateral denoise (denoise.hpp:28-90), bit-exact.
 //
-// One CTA produces a 32x16 output tile of one frame slot.  The raw tile (halo = median radius +
-// bilateral radius, edge-replicated) and the median tile (halo = bilateral radius) live in
-// shared memory; the bilateral sums run in fp64 in the reference's dy-major / dx-minor order
-// with explicit round-to-nearest operations (no FMA), the range LUT and spatial weights are the
-// host-computed libm values, and rounding is std::lround (half away from zero).  The CTA also
-// reduces the integer sum of its denoised pixels for the registration mean
-// (registration.hpp:27-29), which is exact in integers.
+// k_denoise_u8_m1b2 (the default radii on 8-bit frames): persistent CTAs over 32x32 tiles, the
+// next tile's raw pixels in flight; medians from sorted row triples; the 5x5 bilateral window in
+// registers.  k_denoise (other radii, 16-bit): one CTA per 32x16 output tile, raw tile (halo =
+// median radius + bilateral radius, edge-replicated) and median tile (halo = bilateral radius)
+// in shared memory.  Both: bilateral sums in fp64 in the reference's dy-major / dx-minor order
+// with explicit round-to-nearest operations (no FMA), the host-computed libm range LUT and
+// spatial weights, rounding as std::lround (half away from zero); the CTA also reduces the
+// integer sum of its denoised pixels for the registration mean (registration.hpp:27-29), exact
+// in integers.
 //
-// Roofline: HBM-bound at 2 B/px for u8 (read raw, write den) — SURVEY.md App. C row "D".
+// Bound: the fp64 pipe, not HBM.  The byte model (SURVEY.md App. C row "D") is 2 B/px, which
+// the kernel moves at ~70 GB/s; its ~118 fp64 instructions per pixel (4 per bilateral tap: the
+// weight product, two sums and the weighted sample) run at ~44 % of the measured fp64 peak
+// (profiles/fp64_work.json, profiles/r02_fp64.md).
 #include "kernels.cuh"
 
 namespace froi {

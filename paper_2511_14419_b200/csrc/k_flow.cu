@@ -7,12 +7,14 @@
 //   k_polyexp    5-tap separable Gaussian-weighted quadratic fit per pixel; writes the four
 //                planes the warp gathers together as one float4 {a11,a12,a22,bx} plus {by};
 //                the constant term c is only produced by the debug tap        (flow.hpp:118-153)
-//   k_flow_iter  one launch per (level, iteration), one CTA per 32x32 output tile of one pair:
-//                phase 1 builds the five normal-equation products G over the tile + 7 px halo
-//                (prior from the same level, or upsampled from the coarser level on the first
-//                iteration, then bilinear warp of the next frame's planes), phase 2/3 take the
-//                15x15 clipped box sums in shared memory, phase 4 solves the 2x2 system in fp64
-//                with the reference's singularity test                       (flow.hpp:204-255)
+//   k_flow_iter  one launch per (level, iteration); one CTA (512 threads, 2 per SM) per strip of
+//                nr vertically stacked 64x32 output tiles of one pair: phase 1 builds the five
+//                normal-equation products G over the rows each tile adds (tile + 7 px halo; the
+//                14 overlap rows stay in a 48-row shared ring), with the prior from the same level
+//                (or upsampled by k_upsample) and the bilinear warp of the next frame's planes;
+//                phases 2/3 take the 15x15 clipped box sums in place (vertical then horizontal
+//                running sums); phase 4 solves the 2x2 system on the window sums in fp32 with a
+//                compensated determinant and the reference's singularity test (flow.hpp:204-255)
 //
 // Level-0 images are read straight from the denoised u8/u16 frames (normalised on the fly, with
 // the registration shift applied as a clamped gather, registration.hpp:100-107), so the fp32

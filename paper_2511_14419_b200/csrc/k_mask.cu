@@ -4,9 +4,12 @@
 //   saliency   S = w*N(|flow|) + (1.0-w)*N(|grad I|) recomputed on the fly wherever needed:
 //              |flow| is glibc hypotf (float), |grad I| the restated glibc hypot of central
 //              differences of apply_shift(raw, s)/maxval, N the 1st/99th-percentile clamp.
-//   selection  exact order statistics by MSD radix select on the IEEE bit patterns (11-bit
-//              digits, integer histograms, no float atomics): the four percentiles in one set of
-//              passes, then the round(t*n)-th largest saliency; a pass also records min/max of the
+//   selection  exact order statistics on the IEEE bit patterns (integer histograms, no float
+//              atomics): the first pass bins keys by an exponent window (sign | exponent | 7
+//              mantissa bits over 31 octaves), which normally isolates few enough keys (<= 16384)
+//              to collect and finish by an 8-bit-digit radix select in shared memory; 11-bit
+//              radix digits remain the fallback.  The four percentiles run as one set of passes,
+//              then the round(t*n)-th largest saliency; a pass also records min/max of the
 //              still-matching keys so tied groups finish early.
 //   threshold  S > boundary plus ties admitted in row-major order (per-chunk tie counts, an
 //              exclusive scan, then warp-ballot ranks), written as 32-bit packed words.
@@ -440,8 +443,17 @@ constexpr int PNT_MG = 256;
 // Row-blocked: each CTA owns whole rows of one pair (32-bit indexing).  Queries 0/1 (|flow|
 // percentiles) and 2/3 (|grad I|) share their first-pass histograms, so two are built (the
 // exponent-window digit) and added to both queries of each pair.
+#ifndef FROI_MG_FAST
+#define FROI_MG_FAST 0
+#endif
+#ifndef FROI_MG_NPX
+#define FROI_MG_NPX 4
+#endif
+#ifndef FROI_MG_MINB
+#define FROI_MG_MINB 4
+#endif
 template <typename T>
-__global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
+__global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
     __shared__ double lut[256];
     __shared__ unsigned int hist[2][kFpwBins];
     __shared__ unsigned long long smn[2], smx[2];
@@ -469,7 +481,7 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
     double mng = __longlong_as_double(0x7ff0000000000000ll), mxg = 0.0;
     // NPX pixels per thread per step: all their loads (flow, the four gradient neighbours) are
     // issued before any of their arithmetic, so each thread keeps ~NPX*5 loads in flight
-    constexpr int NPX = 4;
+    constexpr int NPX = FROI_MG_NPX;
     const float2* __restrict__ flw = px.flow;
     const T* __restrict__ raw = px.raw;
     for (int y = y0; y < y1; ++y) {
@@ -509,12 +521,28 @@ __global__ void __launch_bounds__(PNT_MG, 4) k_mag_grad(Geom g, DevParams P, Mas
                 const bool v = FULL || x < W;
                 unsigned long long kf = 0, kg = 0;
                 if (v) {
+#if FROI_MG_FAST
+                    // branch-free fast paths of the sqrt / division sequences (common.cuh): the
+                    // same bits whenever their range test passes, the rare rest redone exactly
+                    const double fx = fl[k].x, fy = fl[k].y;
+                    const double f2 = dadd(dmul(fx, fx), dmul(fy, fy));
+                    bool okf;
+                    const double fs = dsqrt_fast(f2, okf);
+                    const float f = (float)(okf ? fs : dsqrt(f2));
+#else
                     const float f = hypotf_glibc(fl[k].x, fl[k].y);
+#endif
                     double gg;
                     if (sizeof(T) == 1 && P.gradient_source == 0) {
                         const double gx = dmul(0.5, dsub(lut[vr[k]], lut[vl[k]]));
                         const double gy = dmul(0.5, dsub(lut[vd[k]], lut[vu[k]]));
+#if FROI_MG_FAST
+                        bool okg;
+                        gg = hypot_glibc_fast(gx, gy, okg);
+                        if (!okg) gg = hypot_glibc(gx, gy);
+#else
                         gg = hypot_glibc(gx, gy);
+#endif
                     } else {
                         gg = px.grad(x, y);
                     }
