@@ -471,6 +471,17 @@ __global__ void __launch_bounds__(QNT) k_pyr_level(Geom g, DevParams P, int l, f
 
 // ------------------------------------------------------------------ flow iteration
 constexpr int FX = 64, FY = 32, FNT = 512;
+// timing diagnostics only (the last two give wrong results): no L1 prefetch of the
+// prior / no box sums / gathers at the pixel itself
+#ifndef FROI_FLOW_NOPF
+#define FROI_FLOW_NOPF 0
+#endif
+#ifndef FROI_DIAG_NOBOX
+#define FROI_DIAG_NOBOX 0
+#endif
+#ifndef FROI_DIAG_ZEROFLOW
+#define FROI_DIAG_ZEROFLOW 0
+#endif
 
 struct IterArgs {
     int l;        // level
@@ -734,7 +745,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     const float* nB = opaque((sh ? exB_p + pair_off : exB_f + (size_t)next[p] * g.lsum) + lo);
     const float2* fin = opaque(a.flow_in + pair_off + lo);
     float2* out = opaque(a.flow_out + pair_off + lo);
-    if (a.mode) {
+    if (!FROI_FLOW_NOPF && a.mode) {
         // the first tile's prior rows (its later tiles' rows are prefetched during phase 2):
         // later pair rounds of the first tile then find them in L1
         const int xs = max(0, x0 - R), xe = min(w, x0 + FX + R);
@@ -787,6 +798,12 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
                                  : "l"(fin + (unsigned)(gyA * w + gx)), "l"(fin + (unsigned)(gyB * w + gx)));
                 GLoad lA, lB;
                 int xaA, yaA, xaB, yaB;
+                if (FROI_DIAG_ZEROFLOW) {  // diagnostic: gather at the pixel itself (coalesced)
+                    prA.x = prA.x * 1e-30f;
+                    prA.y = prA.y * 1e-30f;
+                    prB.x = prB.x * 1e-30f;
+                    prB.y = prB.y * 1e-30f;
+                }
                 bl_split(gx, prA.x, w, xaA, lA.fx);
                 bl_split(gyA, prA.y, h, yaA, lA.fy);
                 bl_split(gx, prB.x, w, xaB, lB.fx);
@@ -871,7 +888,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         __syncthreads();
         // the threads phase 2 leaves idle pull the next tile's prior rows into L1, so its
         // gathers do not start behind an L2/DRAM round trip
-        if (a.mode && k + 1 < nr && threadIdx.x >= 5 * HW) {
+        if (!FROI_FLOW_NOPF && a.mode && k + 1 < nr && threadIdx.x >= 5 * HW) {
             const int ny0 = ys + FY * (k + 1) + R;
             const int xs = max(0, x0 - R), xe = min(w, x0 + FX + R);
             constexpr int NL = (HW * 8 + 127) / 128 + 1;
@@ -884,7 +901,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         // phase 2: vertical running sums down each of the 5*HW ring columns (FY outputs each),
         // in place over this tile's first FY ring rows
         const int b0 = (FY * k) % RG;  // 0, 32 or 16
-        if (threadIdx.x < 5 * HW) {
+        if (!FROI_DIAG_NOBOX && threadIdx.x < 5 * HW) {
             const int vc = threadIdx.x / HW, vx = threadIdx.x - vc * HW;
             float* col = G + vc * PL + vx;
             if (b0 == 0) vsum_inplace<R, 0, SW>(col);
@@ -896,7 +913,7 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
         // place one step behind; a segment first takes the 2R inputs it shares with the next
         // segment into registers, so after one barrier every thread owns what it overwrites
         constexpr int NSEG = FX / 32;
-        const bool hact = threadIdx.x < 5 * FY * NSEG;
+        const bool hact = !FROI_DIAG_NOBOX && threadIdx.x < 5 * FY * NSEG;
         const int hc = threadIdx.x / (FY * NSEG);
         const int hrem = threadIdx.x - hc * FY * NSEG;
         const int hsg = hrem / FY, hty = hrem - hsg * FY;  // a warp walks 32 rows of one segment
