@@ -540,6 +540,8 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
                         bool okg;
                         gg = hypot_glibc_fast(gx, gy, okg);
                         if (!okg) gg = hypot_glibc(gx, gy);
+#elif defined(FROI_DIAG_MG_NOHYPOT)
+                        gg = dadd(fabs(gx), fabs(gy));
 #else
                         gg = hypot_glibc(gx, gy);
 #endif
@@ -555,10 +557,12 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
                     mng = gg < mng ? gg : mng;
                     mxg = gg > mxg ? gg : mxg;
                 }
+#ifndef FROI_DIAG_MG_NOHIST
                 if (v) {  // exponent-window bins are spread out: plain shared atomics
                     atomicAdd(&hist[0][fpw_bin(kf, 2)], 1u);
                     atomicAdd(&hist[1][fpw_bin(kg, 1)], 1u);
                 }
+#endif
             }
             };
             if (xb + NPX * PNT_MG <= W) consume(std::true_type{});

@@ -238,6 +238,11 @@ T* dalloc(size_t count, size_t* total) {
 
 }  // namespace
 
+static bool default_fork() {
+    const char* e = getenv("FROI_FORK");
+    return !(e && atoi(e) == 0);
+}
+
 static bool default_graphs() {
     const char* e = getenv("FROI_GRAPHS");
     return !(e && atoi(e) == 0);
@@ -336,6 +341,11 @@ struct froi_ctx {
     uint8_t* h_outring = nullptr;        // pinned twin of d_outring (general destinations)
     std::vector<cudaEvent_t> delivered;  // per batch of a call: its masks are in host memory
     cudaStream_t copy_stream = nullptr;
+    // intra-batch fork: the frame expansions (HBM-bound) run on `side` while the forward FFT and
+    // registration (fp64-bound) run on the batch's stream; both branches live in the batch graph
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_den = nullptr, ev_exp = nullptr;
+    bool fork = default_fork();
     cudaStream_t d2h_stream = nullptr;       // per-batch mask read-back (host PBM), off the lanes
     std::vector<cudaEvent_t> d2h_ev;         // batch b's masks are final
     cudaEvent_t d2h_done = nullptr;
@@ -500,6 +510,9 @@ void ctx_alloc(froi_ctx* c) {
     c->h_info_cap = P;
     for (int i = 0; i < 8; ++i) FROI_CUDA(cudaEventCreate(&c->ev[i]));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    FROI_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    FROI_CUDA(cudaEventCreateWithFlags(&c->ev_den, cudaEventDisableTiming));
+    FROI_CUDA(cudaEventCreateWithFlags(&c->ev_exp, cudaEventDisableTiming));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->d2h_stream, cudaStreamNonBlocking));
     FROI_CUDA(cudaEventCreateWithFlags(&c->d2h_done, cudaEventDisableTiming));
     // the constant tables above went through pageable cudaMemcpy on the legacy stream, which may
@@ -559,6 +572,9 @@ void ctx_free(froi_ctx* c) {
     for (auto e : c->d2h_ev) cudaEventDestroy(e);
     if (c->d2h_done) cudaEventDestroy(c->d2h_done);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_den) cudaEventDestroy(c->ev_den);
+    if (c->ev_exp) cudaEventDestroy(c->ev_exp);
     if (c->d2h_stream) cudaStreamDestroy(c->d2h_stream);
     if (c->stream) cudaStreamDestroy(c->stream);
 }
@@ -646,6 +662,7 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
     }
     // the stage sequence; `rec` records stage event i (a plain record, or an external event node
     // inside a capture), `first_wait` orders each denoise run after its ingest event
+    bool fork_now = false;  // set for graph captures when the context forks (below)
     auto enqueue = [&](auto rec, bool per_run) {
         rec(0);
         FROI_CUDA(cudaMemsetAsync(c->d_sums, 0, sizeof(unsigned long long) * nf, s));
@@ -661,16 +678,33 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
             launch_denoise(g, c->dp, c->d_frame_raw[tb], c->d_den, c->d_sums, c->h_spatial.data(), c->d_lut, nf, s);
         }
         rec(1);
-        launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
-        rec(2);
         FlowBuffers fb = c->flow_buffers();
-        launch_expand_frames(g, c->dp, fb, nf, s);
-        rec(3);
-        launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
-                              c->d_cols, c->d_surf, c->d_info, n_pairs, s);
-        rec(4);
-        launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
-        rec(5);
+        if (fork_now) {
+            // expansions of the frame slots on the side branch, FFT + registration on this one
+            FROI_CUDA(cudaEventRecord(c->ev_den, s));
+            FROI_CUDA(cudaStreamWaitEvent(c->side, c->ev_den, 0));
+            launch_expand_frames(g, c->dp, fb, nf, c->side);
+            FROI_CUDA(cudaEventRecord(c->ev_exp, c->side));
+            launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
+            rec(2);
+            rec(3);
+            launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
+                                  c->d_cols, c->d_surf, c->d_info, n_pairs, s);
+            rec(4);
+            launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+            FROI_CUDA(cudaStreamWaitEvent(s, c->ev_exp, 0));
+            rec(5);
+        } else {
+            launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
+            rec(2);
+            launch_expand_frames(g, c->dp, fb, nf, s);
+            rec(3);
+            launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
+                                  c->d_cols, c->d_surf, c->d_info, n_pairs, s);
+            rec(4);
+            launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+            rec(5);
+        }
         const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
         rec(6);
         MaskBuffers mb = c->mask_buffers(tb);
@@ -693,6 +727,7 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
         if (it == c->graphs.end()) {
             froi_ctx::BatchGraph bg;
             FROI_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            fork_now = c->fork;
             try {
                 bg.launches = enqueue([&](int i) { FROI_CUDA(cudaEventRecordWithFlags(ev[i], s, cudaEventRecordExternal)); },
                                       false);
