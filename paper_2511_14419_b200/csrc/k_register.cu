@@ -185,6 +185,70 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
     }
 }
 
+// Warp-per-row forward transform for 1024-point rows (the 1024^2 geometries): one warp holds its
+// row in registers, 32 elements per lane.  Layout B (lane l holds positions 32l..32l+31 of the
+// bit-reversed array) makes the stages of half-length 1..16 lane-local with warp-uniform twiddles;
+// one padded shared-memory transpose gives layout A (lane l holds positions l + 32m), where the
+// stages of half-length 32..512 are lane-local.  Every butterfly is the reference's, with the same
+// operands and twiddle as fft_pass; only two shared-memory round trips remain (vs eight).
+constexpr int RW_WARPS = 4;
+
+__device__ __forceinline__ int brev5(int x) { return (int)(__brev((unsigned)x) >> 27); }
+
+template <typename T>
+__global__ void __launch_bounds__(32 * RW_WARPS, 3) k_fft_rows_w1024(int W, int H, int ph,
+                                                                     const T* __restrict__ den,
+                                                                     const unsigned long long* __restrict__ sums,
+                                                                     const double* __restrict__ wx,
+                                                                     const double* __restrict__ wy,
+                                                                     const double2* __restrict__ tw,
+                                                                     double2* __restrict__ spec) {
+    extern __shared__ double2 xs_dyn[];  // RW_WARPS x (33 * 32)
+    const int warp = threadIdx.x >> 5, l = threadIdx.x & 31;
+    const int y = blockIdx.x * RW_WARPS + warp, slot = blockIdx.y;
+    if (y >= ph) return;  // warp-uniform
+    const T* f = den + (size_t)slot * W * H;
+    const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
+    const double wyv = __ldg(wy + y);
+    const T* row = f + (size_t)min(y, H - 1) * W;
+    const int bl = brev5(l);
+    double2 e[32];
+    // position 32l + m holds input x = brev10(32l + m) = 32 brev5(m) + brev5(l)
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+        const int x = 32 * ((int)(__brev((unsigned)m) >> 27)) + bl;
+        const double sv = (double)row[min(x, W - 1)];
+        e[m] = make_double2(dmul(dmul(dsub(sv, mean), __ldg(wx + x)), wyv), 0.0);
+    }
+#pragma unroll
+    for (int s = 0; s < 5; ++s) {
+        const int h = 1 << s;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            if (m & h) continue;
+            bfly(e[m], e[m + h], __ldg(tw + h - 1 + (m & (h - 1))));
+        }
+    }
+    double2* xw = xs_dyn + warp * (33 * 32);
+#pragma unroll
+    for (int m = 0; m < 32; ++m) xw[33 * l + m] = e[m];  // position p at p + p / 32
+    __syncwarp();
+#pragma unroll
+    for (int m = 0; m < 32; ++m) e[m] = xw[l + 33 * m];
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+        const int hm = 1 << j, h = 32 << j;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) {
+            if (m & hm) continue;
+            bfly(e[m], e[m + hm], __ldg(tw + h - 1 + l + 32 * (m & (hm - 1))));
+        }
+    }
+    double2* out = spec + ((size_t)slot * ph + y) * 1024;
+#pragma unroll
+    for (int m = 0; m < 32; ++m) out[l + 32 * m] = e[m];
+}
+
 __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int lcb,
                                                  const double2* __restrict__ tw,
                                                  double2* __restrict__ spec) {
@@ -406,7 +470,23 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
     const int lr = rows_lc(g.log2pw);
     const size_t smem_r = sizeof(double2) * (((size_t)padded(g.pw) << lr) + g.pw);
     const int row_blocks = cdiv(g.ph, 1 << lr);
-    if (g.sample_bytes == 1) {
+    static const bool rows_w = [] {
+        const char* e = getenv("FROI_FFT_ROWS_W");
+        return !(e && atoi(e) == 0);
+    }();
+    if (rows_w && g.pw == 1024) {
+        const dim3 grid(cdiv(g.ph, RW_WARPS), n_slots);
+        const size_t sm = sizeof(double2) * RW_WARPS * 33 * 32;
+        if (g.sample_bytes == 1) {
+            set_smem(k_fft_rows_w1024<uint8_t>, sm);
+            k_fft_rows_w1024<uint8_t><<<grid, 32 * RW_WARPS, sm, s>>>(g.W, g.H, g.ph, (const uint8_t*)d_den, d_sums,
+                                                                     d_wx, d_wy, d_tw_row, d_spec);
+        } else {
+            set_smem(k_fft_rows_w1024<uint16_t>, sm);
+            k_fft_rows_w1024<uint16_t><<<grid, 32 * RW_WARPS, sm, s>>>(g.W, g.H, g.ph, (const uint16_t*)d_den, d_sums,
+                                                                      d_wx, d_wy, d_tw_row, d_spec);
+        }
+    } else if (g.sample_bytes == 1) {
         set_smem(k_fft_rows_fwd<uint8_t>, smem_r);
         k_fft_rows_fwd<uint8_t><<<dim3(row_blocks, n_slots), NT, smem_r, s>>>(
             g.W, g.H, g.pw, g.ph, g.log2pw, (const uint8_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
