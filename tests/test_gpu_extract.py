@@ -257,3 +257,61 @@ def test_extract_odd_shapes(gpu, oracle, w, h):
     f = textured_frame(w, h, 8, w + h)
     frames = np.stack([cyclic_shift(f, t % 2, t // 2) for t in range(4)])
     _check_sequence(gpu, oracle, frames, params=p)
+
+
+def test_per_frame_pointer_entries(gpu):
+    """froi_extract_frames (one uint16 pointer per frame and per mask), froi_extract_frames_sink
+    (each destination requested once, frame 0 after frame 1) and froi_stream_push_frames give the
+    bytes of the contiguous entry; a u16 sample above 255 in an 8-bit context is a data error."""
+    import ctypes
+
+    from paper_2511_14419_b200 import _native
+    from paper_2511_14419_b200.flowroi import Context
+    from paper_2511_14419_b200.params import DataError
+    n, size = 11, 96
+    f = textured_frame(size, size, 8, 123)
+    frames = np.stack([cyclic_shift(f, t, (2 * t) % 5) for t in range(n)]).astype(np.uint8)
+    ctx = Context(size, size, 8, max_pairs=3)
+    want, _ = ctx.extract_wells(frames[None])
+    f16 = [np.ascontiguousarray(frames[t], dtype=np.uint16) for t in range(n)]
+    fp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in f16])
+    # per-frame pointers
+    outs = [np.empty((size, size), np.uint8) for _ in range(n)]
+    mp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in outs])
+    _native.check(_native.lib.froi_extract_frames(ctx.handle, fp, 2, n, 0, mp, None))
+    assert np.array_equal(np.stack(outs), want[0])
+    # sink: destinations handed out on demand
+    sunk = {}
+    order = []
+    SINK = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int, ctypes.c_int)
+
+    def sink(user, well, frame):
+        order.append(frame)
+        a = np.empty((size, size), np.uint8)
+        sunk[frame] = a
+        return a.ctypes.data
+
+    cb = SINK(sink)
+    _native.check(_native.lib.froi_extract_frames_sink(ctx.handle, fp, 2, n, 0, ctypes.cast(cb, ctypes.c_void_p),
+                                                      None, None))
+    assert sorted(order) == list(range(n))
+    assert order.index(0) > order.index(1)
+    assert np.array_equal(np.stack([sunk[t] for t in range(n)]), want[0])
+    # streaming with per-frame pointers, uneven pushes
+    _native.check(_native.lib.froi_stream_reset(ctx.handle, 1))
+    got = []
+    for a, b in ((0, 4), (4, 5), (5, 11)):
+        k = b - a
+        so = [np.empty((size, size), np.uint8) for _ in range(k)]
+        sp = (ctypes.c_void_p * k)(*[x.ctypes.data for x in so])
+        _native.check(_native.lib.froi_stream_push_frames(ctx.handle, ctypes.cast(fp, ctypes.c_void_p).value + 8 * a,
+                                                          2, k, 0, sp, None))
+        got += so
+    assert np.array_equal(np.stack(got), want[0])
+    # the Frame invariant: samples < 2^depth
+    bad = [np.ascontiguousarray(x, dtype=np.uint16) for x in f16]
+    bad[3][5, 7] = 300
+    bp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in bad])
+    with pytest.raises(DataError):
+        _native.check(_native.lib.froi_extract_frames(ctx.handle, bp, 2, n, 0, mp, None))
+    ctx.close()
