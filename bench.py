@@ -414,12 +414,14 @@ def run_ours(args) -> None:
     # above overlaps consecutive batches on two lanes)
     ksteps = min(2, args.steps)
     ctx.set_lanes(1)
+    ctx.set_fork(False)  # each stage's events bracket only its own kernels
     ctx.extract_wells_device(dev[step_slot[0]].data_ptr(), 1, F, dmask.data_ptr())
     for i in range(args.warmup, args.warmup + ksteps):
         ctx.extract_wells_device(dev[step_slot[i]].data_ptr(), 1, F, dmask.data_ptr())
         for k, v in ctx.kernel_times().items():
             kt_sum[k] = kt_sum.get(k, 0) + v
     ctx.set_lanes(2)
+    ctx.set_fork(True)
     torch.cuda.synchronize()
     ms_max = reduce_max(dist, ms, device)
     masks_local = args.steps * F
@@ -465,7 +467,7 @@ def run_ours(args) -> None:
                 "peak_source": pk["source"], "traffic": args.ncu_traffic,
                 "bytes_per_launch": mb["flow"] * pairs / flow_launches,
                 "avg_launch_us": flow_ns / flow_launches / 1e3,
-                "timed_on": f"{ksteps} step(s) with one execution lane (kernel durations)"}
+                "timed_on": f"{ksteps} step(s) with one execution lane and no intra-batch fork (kernel durations)"}
     pairs_per_s = (F - 1) * args.steps / (ms / 1000.0) if ms > 0 else 0.0
     stage_frac = {k.replace("_ns", ""): v / max(1, sum(kt_sum.get(x, 0) for x in (
         "denoise_ns", "fft_forward_ns", "expand_ns", "register_ns", "expand_shifted_ns",

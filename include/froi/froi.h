@@ -153,6 +153,10 @@ int froi_ctx_stream(const froi_ctx* ctx, void** stream_out);
  * between two buffer sets on two streams so their kernels overlap; outputs are identical.
  * Per-stage times (froi_ctx_kernel_times) are exact kernel durations only with 1 lane. */
 int froi_ctx_set_lanes(froi_ctx* ctx, int lanes);
+/* Intra-batch overlap (1, default, or $FROI_FORK=0 at creation): each batch's frame expansions run
+ * on a side branch concurrently with its forward FFT and registration.  0 serialises them, so the
+ * per-stage times of froi_ctx_kernel_times bracket each stage's own kernels; outputs are identical. */
+int froi_ctx_set_fork(froi_ctx* ctx, int fork);
 
 /* ---- stage entry: extract_roi (roi.hpp:309-364) ----
  * Host frames: n_frames frames of width*height samples; frame f starts at

@@ -38,6 +38,7 @@ SIGNATURES = {
     "froi_ctx_kernel_times": (_I, [_P, ctypes.POINTER(CKernelTimes)]),
     "froi_ctx_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "froi_ctx_set_lanes": (_I, [_P, ctypes.c_int]),
+    "froi_ctx_set_fork": (_I, [_P, ctypes.c_int]),
     "froi_dwt_forward": (_I, [_P, _P, ctypes.c_int, _P]),
     "froi_dwt_inverse": (_I, [_P, _P, ctypes.c_int, _P]),
     "froi_dwt_forward_device": (_I, [_P, _P, ctypes.c_int, ctypes.c_int, _P]),

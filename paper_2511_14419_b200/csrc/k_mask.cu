@@ -920,25 +920,30 @@ __device__ __forceinline__ SrcMap make_thr_src<SrcMap>(const Geom&, const DevPar
 }
 
 // Per-chunk tie counts, only for pairs that admit part of a tie group (thr_mode 3).
+// (grid-stride over the nch row chunks: a few CTAs per pair, so the common case -- no partial tie
+// group -- costs a handful of early exits instead of one per chunk)
 template <class Src>
 __global__ void __launch_bounds__(TNT) k_thr_count(Geom g, DevParams P, MaskBuffers b,
-                                                   const double* map) {
-    const int p = blockIdx.y, chunk = blockIdx.x;
+                                                   const double* map, int nch) {
+    const int p = blockIdx.y;
     const PairInfo& I = b.info[p];
     if (I.thr_mode != 3 || I.bits_ready) return;
     __shared__ unsigned long long se;
-    if (threadIdx.x == 0) se = 0;
-    __syncthreads();
     const Src src = make_thr_src<Src>(g, P, b, p, map);
     const double bd = I.boundary;
-    const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
-    unsigned int ce = 0;
-    for (long long i = (long long)y0 * g.W + threadIdx.x; i < (long long)y1 * g.W; i += TNT)
-        ce += src.value(i) == bd;
-    for (int o = 16; o > 0; o >>= 1) ce += __shfl_xor_sync(0xffffffffu, ce, o);
-    if ((threadIdx.x & 31) == 0 && ce) atomicAdd(&se, (unsigned long long)ce);
-    __syncthreads();
-    if (threadIdx.x == 0) b.tie_cnt[(size_t)p * gridDim.x + chunk] = se;
+    for (int chunk = blockIdx.x; chunk < nch; chunk += gridDim.x) {
+        if (threadIdx.x == 0) se = 0;
+        __syncthreads();
+        const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
+        unsigned int ce = 0;
+        for (long long i = (long long)y0 * g.W + threadIdx.x; i < (long long)y1 * g.W; i += TNT)
+            ce += src.value(i) == bd;
+        for (int o = 16; o > 0; o >>= 1) ce += __shfl_xor_sync(0xffffffffu, ce, o);
+        if ((threadIdx.x & 31) == 0 && ce) atomicAdd(&se, (unsigned long long)ce);
+        __syncthreads();
+        if (threadIdx.x == 0) b.tie_cnt[(size_t)p * nch + chunk] = se;
+        __syncthreads();
+    }
 }
 
 // Exclusive scan of the per-chunk tie counts (thr_mode 3 only).
@@ -974,17 +979,13 @@ __global__ void __launch_bounds__(1024) k_thr_scan(MaskBuffers b, int nch) {
 
 // Packed thresholded mask, bit x%32 of word (y, x/32); ties admitted in row-major order.
 template <class Src>
-__global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuffers b,
-                                                   const double* map) {
-    const int p = blockIdx.y, chunk = blockIdx.x;
-    const PairInfo I = b.info[p];
-    if (I.bits_ready) return;  // written by the collect pass, settled by k_thr_fixup
+__device__ __forceinline__ void thr_write_chunk(const Geom& g, const DevParams& P, const MaskBuffers& b,
+                                                const double* map, const PairInfo& I, int p, int chunk,
+                                                int nch, unsigned int* wcnt, unsigned long long& base) {
     const int y0 = chunk * TROWS, y1 = min(g.H, y0 + TROWS);
     uint32_t* out = b.bits_thr + (size_t)p * g.H * g.WW;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     constexpr int NW = TNT / 32;
-    __shared__ unsigned int wcnt[NW];
-    __shared__ unsigned long long base;
     const int nwords = (y1 - y0) * g.WW;
     if (I.thr_mode == 1) {
         for (int i = threadIdx.x; i < nwords; i += TNT) out[(size_t)y0 * g.WW + i] = 0u;
@@ -1005,7 +1006,8 @@ __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuff
         }
         return;
     }
-    if (threadIdx.x == 0) base = b.tie_cnt[(size_t)p * gridDim.x + chunk];
+    __syncthreads();  // the previous chunk is done with base / wcnt
+    if (threadIdx.x == 0) base = b.tie_cnt[(size_t)p * nch + chunk];
     __syncthreads();
     for (int r0 = 0; r0 < nwords; r0 += NW) {
         const int wi = r0 + warp;
@@ -1036,6 +1038,20 @@ __global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuff
         }
         __syncthreads();
     }
+}
+
+// Packed thresholded mask, bit x%32 of word (y, x/32); ties admitted in row-major order.
+// Grid-stride over the row chunks (see k_thr_count).
+template <class Src>
+__global__ void __launch_bounds__(TNT) k_thr_write(Geom g, DevParams P, MaskBuffers b,
+                                                   const double* map, int nch) {
+    const int p = blockIdx.y;
+    const PairInfo I = b.info[p];
+    if (I.bits_ready) return;  // written by the collect pass, settled by k_thr_fixup
+    __shared__ unsigned int wcnt[TNT / 32];
+    __shared__ unsigned long long base;
+    for (int chunk = blockIdx.x; chunk < nch; chunk += gridDim.x)
+        thr_write_chunk<Src>(g, P, b, map, I, p, chunk, nch, wcnt, base);
 }
 
 // Settles the boundary bin's candidates after phase B's collect pass wrote every other pixel's
@@ -1531,9 +1547,10 @@ template <class Src>
 void run_threshold(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
                    const double* map, cudaStream_t s, uint64_t* launches) {
     const int nch = cdiv(g.H, TROWS);
-    k_thr_count<Src><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    const int gx = std::min(nch, 16);
+    k_thr_count<Src><<<dim3(gx, n_pairs), TNT, 0, s>>>(g, P, b, map, nch);
     k_thr_scan<<<n_pairs, 1024, 0, s>>>(b, nch);
-    k_thr_write<Src><<<dim3(nch, n_pairs), TNT, 0, s>>>(g, P, b, map);
+    k_thr_write<Src><<<dim3(gx, n_pairs), TNT, 0, s>>>(g, P, b, map, nch);
     FROI_LAUNCH_CHECK();
     *launches += 3;
 }

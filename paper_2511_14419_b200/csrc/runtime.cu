@@ -799,6 +799,7 @@ froi_ctx* lane_of(froi_ctx* c) {
         FROI_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
         FROI_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     }
+    c->lane->fork = c->fork;
     c->lane->dp = c->dp;  // set_params may have changed the run-time parameters
     c->lane->params = c->params;
     return c->lane;
@@ -1552,6 +1553,22 @@ int froi_ctx_set_lanes(froi_ctx* ctx, int lanes) {
     if (lanes != 1 && lanes != 2) return fail(1, "lanes must be 1 or 2");
     ctx->lanes = lanes;
     return 0;
+}
+
+int froi_ctx_set_fork(froi_ctx* ctx, int fork) {
+    if (!ctx) return fail(1, "null context");
+    if (fork != 0 && fork != 1) return fail(1, "fork must be 0 or 1");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(ctx->device));
+    FROI_CUDA(cudaStreamSynchronize(ctx->stream));
+    ctx->fork = fork != 0;
+    drop_graphs(ctx);  // the captured graphs hold the old branch structure
+    if (ctx->lane) {
+        FROI_CUDA(cudaStreamSynchronize(ctx->lane->stream));
+        ctx->lane->fork = ctx->fork;
+        drop_graphs(ctx->lane);
+    }
+    ABI_CATCH
 }
 
 int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out) {

@@ -128,6 +128,10 @@ class Context:
         """1 or 2 execution lanes (two overlap consecutive batches; outputs are identical)."""
         _native.check(_native.lib.froi_ctx_set_lanes(self._h, int(lanes)))
 
+    def set_fork(self, fork: bool) -> None:
+        """Intra-batch overlap of the expansions with the FFT / registration (default on)."""
+        _native.check(_native.lib.froi_ctx_set_fork(self._h, 1 if fork else 0))
+
     def stream(self) -> int:
         s = ctypes.c_void_p()
         _native.check(_native.lib.froi_ctx_stream(self._h, ctypes.byref(s)))

@@ -28,6 +28,8 @@ dev = frames.cuda()
 masks = torch.empty((F, 1024, 128), dtype=torch.uint8, device="cuda")
 ctx = flowroi.Context(1024, 1024, 8, cfg.params)
 ctx.set_lanes(1)
+if os.environ.get("STAGE_AB_NOFORK"):
+    ctx.set_fork(False)
 ctx.extract_wells_device(dev[0].data_ptr(), 1, F, masks.data_ptr())  # warm-up
 acc = {}
 for w in range(nw):
@@ -42,6 +44,7 @@ for k, v in acc.items():
 out["flow_iter_avg_launch_us"] = round(acc["flow_iter_ns"] / 1e3 / acc["flow_iter_launches"], 2)
 out["stage_us_per_pair"] = round(sum(v for k, v in acc.items() if k.endswith("_ns")) / 1e3 / pairs, 2)
 ctx.set_lanes(2)
+ctx.set_fork(True)
 ctx.extract_wells_device(dev[0].data_ptr(), 1, F, masks.data_ptr())
 s = torch.cuda.ExternalStream(ctx.stream())
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -29,8 +29,12 @@ def main(out):
             ctx = F.Context(256, 256, 8, c2.params, device=0, max_pairs=mp)
             ctx.set_lanes(lanes)
             m, _ = ctx.extract_wells(frames, layout="pbm")
-            ctx.close()
             res[f"wells_mp{mp}_l{lanes}"] = m
+            if mp == 4:  # the intra-batch fork off: same bytes
+                ctx.set_fork(False)
+                m, _ = ctx.extract_wells(frames, layout="pbm")
+                res[f"wells_mp{mp}_l{lanes}_nofork"] = m
+            ctx.close()
     c4 = synth.scaled(synth.config("C4"), width=256, height=256, n_cells=30)
     res["u16"] = F.extract_roi(synth.well_frames(c4, 0, 3), c4.params, depth=16)
     p = c2.params.copy()
