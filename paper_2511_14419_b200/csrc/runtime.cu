@@ -1043,7 +1043,11 @@ void ensure_pipeline(froi_ctx* c) {
     if (!c->pool) {
         const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
         const int dev = c->device;
-        c->pool.reset(new HostPool(std::max(1, std::min(8, hw - 1)), [dev] { cudaSetDevice(dev); }));
+        // host threads for frame conversion and mask delivery: all but two hardware threads (the
+        // caller's and the courier), at most 16; $FROI_HOST_THREADS overrides
+        int nt = std::max(1, std::min(16, hw - 2));
+        if (const char* e = getenv("FROI_HOST_THREADS")) nt = std::max(1, atoi(e));
+        c->pool.reset(new HostPool(nt, [dev] { cudaSetDevice(dev); }));
         c->courier.reset(new HostPool(1, [dev] { cudaSetDevice(dev); }));
     }
     if (!c->d_ring) {
