@@ -19,6 +19,7 @@ from paper_2511_14419_b200 import flowroi, synth  # noqa: E402
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "run"
 nw = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+max_pairs = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 cfg = synth.config("C3")
 F = 450
 frames = torch.empty((nw, F, 1024, 1024), dtype=torch.uint8)
@@ -26,7 +27,7 @@ for w in range(nw):
     synth.well_frames(cfg, w, F, out=frames[w].numpy())
 dev = frames.cuda()
 masks = torch.empty((F, 1024, 128), dtype=torch.uint8, device="cuda")
-ctx = flowroi.Context(1024, 1024, 8, cfg.params)
+ctx = flowroi.Context(1024, 1024, 8, cfg.params, max_pairs=max_pairs)
 ctx.set_lanes(1)
 if os.environ.get("STAGE_AB_NOFORK"):
     ctx.set_fork(False)
