@@ -508,7 +508,7 @@ def run_ours(args) -> None:
                                    "rank per step, well (i*N+r) mod 64)",
                        "frames_per_well": F, "wells_per_step_per_gpu": 1,
                        "global_batch": world * F, "parallelism": f"wells sharded over {world} GPU(s)",
-                       "lanes": "2 execution lanes per GPU (consecutive 32-pair batches overlap)",
+                       "lanes": "2 execution lanes per GPU (consecutive 64-pair batches overlap)",
                        "graphs": "each batch's kernel sequence replayed as a CUDA graph (FROI_GRAPHS=0 disables)",
                        "host": f"one process per GPU; rank 0 pinned buffers on NUMA {numa}",
                        "l2": "each step reads a 472 MB well (> 126 MB L2); no flush",

@@ -129,11 +129,17 @@ inline std::vector<flowroi::RoiMask> extract_roi(const flowroi::Sequence& seq,
     struct Sink {
         std::vector<flowroi::RoiMask>* m;
         int w, h;
-        static uint8_t* at(void* u, int, int t) {
+        // called from the library's host threads: must not throw across the C ABI (a null return
+        // makes the call fail with an internal error instead)
+        static uint8_t* at(void* u, int, int t) noexcept {
             Sink* s = static_cast<Sink*>(u);
-            flowroi::RoiMask& r = (*s->m)[static_cast<std::size_t>(t)];
-            r = flowroi::RoiMask(s->w, s->h);
-            return r.bits.data();
+            try {
+                flowroi::RoiMask& r = (*s->m)[static_cast<std::size_t>(t)];
+                r = flowroi::RoiMask(s->w, s->h);
+                return r.bits.data();
+            } catch (...) {
+                return nullptr;
+            }
         }
     } sink{&masks, f0.width, f0.height};
     std::vector<froi_frame_stats> stats(n);

@@ -191,7 +191,8 @@ int froi_extract_frames(froi_ctx* ctx, const void* const* frames, int sample_byt
 /* A mask destination supplied on demand: called (from the library's host threads, concurrently,
  * each (well, frame) once; frame 0 after frame 1) just before mask `frame` of `well` is written;
  * returns where its W*H bytes (or PBM rows) go.  Lets a caller allocate its RoiMasks while the GPU
- * works instead of before the call. */
+ * works instead of before the call.  The sink must not unwind (C++ exceptions must not cross
+ * it); returning NULL fails the call with FROI_ERR_USAGE. */
 typedef uint8_t* (*froi_mask_sink)(void* user, int well, int frame);
 int froi_extract_frames_sink(froi_ctx* ctx, const void* const* frames, int sample_bytes, int n_frames,
                              int mask_layout, froi_mask_sink sink, void* user,

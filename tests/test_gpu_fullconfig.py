@@ -1,7 +1,7 @@
 """Full-length BASELINE configurations through the entry points the bench times, against the
 pinned CPU oracle (VERDICT r1 "Next round" #1).
 
-* C3: one whole 450-frame 1024^2 well (449 pairs = 15 batches of Pcap 32 on two execution lanes,
+* C3: one whole 450-frame 1024^2 well (449 pairs = 8 batches of Pcap 64 on two execution lanes,
   nr = 8 flow strips at level 0 — the bench's configuration) through
     - ``froi_extract_wells_device`` (the bench's device-resident ``value`` leg),
     - ``froi_extract_wells`` from pinned frames into pinned PBM rows (the bench's ``e2e`` leg),
@@ -144,9 +144,9 @@ def test_c3_full_well_bench_entries(gpu, oracle, synth):
     """One whole C3 well through the bench's entries at the bench's batch geometry."""
     cfg = synth.config("C3")
     frames = synth.well_frames(cfg, 0, 450)
-    # first and last pair, both sides of several 32-pair batch boundaries, the tail batch
+    # first and last pair, both sides of several 64-pair batch boundaries, the 1-pair tail batch
     check_full(gpu, oracle, frames, 8, cfg.params, "C3 well 0 x 450",
-               sample_pairs=[1, 32, 33, 64, 65, 224, 225, 416, 417, 449])
+               sample_pairs=[1, 64, 65, 128, 129, 320, 321, 448, 449])
 
 
 def test_c2_full_sequence(gpu, oracle, synth):
@@ -158,7 +158,7 @@ def test_c2_full_sequence(gpu, oracle, synth):
 def test_c4_16bit_well(gpu, oracle, synth):
     cfg = synth.config("C4")
     frames = synth.well_frames(cfg, 0, 8)
-    # 2048^2: Pcap 8, so 7 pairs are one batch; max_pairs 3 also runs it as three batches on two lanes
+    # 2048^2: Pcap 16, so 7 pairs are one batch; max_pairs 3 also runs it as three batches on two lanes
     check_full(gpu, oracle, frames, 16, cfg.params, "C4 well 0 x 8", sample_pairs=[1, 4, 7],
                flow_max=FLOW_MAX_ABS_WELL)
     got3, _ = _gpu_paths(gpu, frames, 16, cfg.params, max_pairs=3)
