@@ -975,8 +975,11 @@ __global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
     }
 }
 
+#ifndef FROI_NR_MAX
+#define FROI_NR_MAX 32
+#endif
 // tiles per strip: the least (rounds of resident CTAs) x (rows each CTA computes, halo included)
-// among strips of 1..8 tiles that still fill every CTA slot (2 per SM) once
+// among strips of 1..32 tiles (powers of two) that still fill every CTA slot (2 per SM) once
 int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
     static const int sms = [] {
         int dev = 0, n = 148;
@@ -987,7 +990,7 @@ int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
     const int tx = cdiv(g.lw[l], FX), ty = cdiv(g.lh[l], FY);
     int best = 1;
     long long best_cost = -1;
-    for (int nr = 1; nr <= 8; nr *= 2) {
+    for (int nr = 1; nr <= FROI_NR_MAX; nr *= 2) {
         const long long ctas = (long long)tx * cdiv(ty, nr) * n_pairs;
         if (nr > 1 && ctas < slots) break;
         const long long cost = cdiv(ctas, slots) * (long long)(FY * std::min(nr, ty) + 2 * R);

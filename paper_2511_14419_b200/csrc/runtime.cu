@@ -238,6 +238,10 @@ T* dalloc(size_t count, size_t* total) {
 
 }  // namespace
 
+#ifndef FROI_PCAP_MAX
+#define FROI_PCAP_MAX 64
+#endif
+
 static bool default_fork() {
     const char* e = getenv("FROI_FORK");
     return !(e && atoi(e) == 0);
@@ -1128,7 +1132,16 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             jobs.push_back(PairJob{});
             wt.emplace_back(w, t);
         }
-    const size_t P = (size_t)c->Pcap, nb = (jobs.size() + P - 1) / P;
+    // which frames go through the pinned staging ring (pageable, or another sample width)
+    const std::vector<char> src_pinned = pinned_flags(io.host, (size_t)g.W * g.H * io.src_bytes);
+    bool any_staged = false;
+    for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !src_pinned[k]);
+    // batches: Pcap pairs, except a first batch of Pcap / 4 when the frames need host conversion,
+    // so the GPU starts after a quarter of the first batch's frames are converted, not all of them
+    const size_t P = (size_t)c->Pcap;
+    const size_t F0 = any_staged ? std::max<size_t>(1, P / 4) : P;
+    auto bstart = [&](size_t b) { return b == 0 ? (size_t)0 : std::min(jobs.size(), F0 + (b - 1) * P); };
+    const size_t nb = jobs.size() <= F0 ? 1 : 1 + (jobs.size() - F0 + P - 1) / P;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
         FROI_CUDA(cudaFreeHost(c->h_info));
@@ -1151,9 +1164,6 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             d_full = c->d_seq_out;
         }
     }
-    const std::vector<char> src_pinned = pinned_flags(io.host, (size_t)g.W * g.H * io.src_bytes);
-    bool any_staged = false;
-    for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !src_pinned[k]);
     if (any_staged) ensure_staging(c);
     const bool general_out = ring_out && (io.sink || io.layout != FROI_MASK_PBM || [&] {
         const std::vector<char> f = pinned_flags(std::vector<const uint8_t*>(io.mask.begin(), io.mask.end()), mb);
@@ -1257,7 +1267,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
     };
     try {
         for (size_t b = 0; b < nb; ++b) {
-            const size_t j0 = b * P, j1 = std::min(jobs.size(), j0 + P);
+            const size_t j0 = bstart(b), j1 = bstart(b + 1);
             // frames of this batch: uploaded (in order) just before it is enqueued
             size_t kmax = 0;
             for (size_t j = j0; j < j1; ++j) kmax = std::max(kmax, (size_t)wt[j].first * n + wt[j].second);
@@ -1479,7 +1489,7 @@ int froi_ctx_create(int device, const froi_params* p, int width, int height, int
         // 64 pairs per batch at 1024^2 (~10.6 GB per execution lane): the level-0 flow grid then
         // fills 13.8 waves instead of 6.9 (one-lane stage time -3.7 %, two-lane frames/s +1.1 %
         // over 32, profiles/tools/pcap_ab.sh); proportionally fewer for larger frames
-        max_pairs = std::max(2, std::min(64, int(64.0 / std::max(mpx, 0.25))));
+        max_pairs = std::max(2, std::min(FROI_PCAP_MAX, int(64.0 / std::max(mpx, 0.25))));
     }
     c->Pcap = max_pairs;
     c->Fcap = 2 * max_pairs;
