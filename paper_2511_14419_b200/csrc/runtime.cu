@@ -811,11 +811,31 @@ froi_ctx* lane_of(froi_ctx* c) {
 
 void accumulate_batch_times(froi_ctx* c, size_t nb);
 
+// Batch boundaries over n pairs: a first batch of `first` (<= cap) pairs, then batches of cap.  A
+// short tail (< cap / 2) is evened out with the batch before it: the two run on different
+// execution lanes, so both lanes finish together instead of one lane trailing a full batch while
+// the other has (nearly) nothing left.  $FROI_TAIL=0 keeps the plain split.
+std::vector<size_t> batch_bounds(size_t n, size_t cap, size_t first) {
+    static const bool tail = [] {
+        const char* e = getenv("FROI_TAIL");
+        return !(e && atoi(e) == 0);
+    }();
+    std::vector<size_t> b{0};
+    for (size_t pos = 0; pos < n;) {
+        pos = std::min(n, pos + (b.size() == 1 ? std::min(first, cap) : cap));
+        b.push_back(pos);
+    }
+    const size_t nbat = b.size() - 1;
+    if (tail && nbat >= 2 && n - b[nbat - 1] < cap / 2) b[nbat - 1] = b[nbat - 2] + (n - b[nbat - 2] + 1) / 2;
+    return b;
+}
+
 // Device-resident frames and masks: enqueue every batch of `jobs`, then synchronise once; stage
 // times from each batch's events, PairInfo rows in job order.
 void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm,
                  std::vector<PairInfo>& infos) {
-    const size_t P = (size_t)c->Pcap, nb = (jobs.size() + P - 1) / P;
+    const std::vector<size_t> bb = batch_bounds(jobs.size(), (size_t)c->Pcap, (size_t)c->Pcap);
+    const size_t nb = bb.size() - 1;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
         FROI_CUDA(cudaFreeHost(c->h_info));
@@ -836,7 +856,7 @@ void run_batches(froi_ctx* c, const std::vector<PairJob>& jobs, uint8_t* out_pbm
         FROI_CUDA(cudaStreamWaitEvent(lane->stream, c->ev_fork, 0));
     }
     for (size_t b = 0; b < nb; ++b) {
-        const size_t j0 = b * P, j1 = std::min(jobs.size(), j0 + P);
+        const size_t j0 = bb[b], j1 = bb[b + 1];
         froi_ctx* x = (lane && (b & 1)) ? lane : c;
         run_batch(x, c, jobs, j0, j1, out_pbm, b, j0);
     }
@@ -1139,9 +1159,9 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
     // batches: Pcap pairs, except a first batch of Pcap / 4 when the frames need host conversion,
     // so the GPU starts after a quarter of the first batch's frames are converted, not all of them
     const size_t P = (size_t)c->Pcap;
-    const size_t F0 = any_staged ? std::max<size_t>(1, P / 4) : P;
-    auto bstart = [&](size_t b) { return b == 0 ? (size_t)0 : std::min(jobs.size(), F0 + (b - 1) * P); };
-    const size_t nb = jobs.size() <= F0 ? 1 : 1 + (jobs.size() - F0 + P - 1) / P;
+    const std::vector<size_t> bb = batch_bounds(jobs.size(), P, any_staged ? std::max<size_t>(1, P / 4) : P);
+    auto bstart = [&](size_t b) { return bb[b]; };
+    const size_t nb = bb.size() - 1;
     if (c->h_info_cap < jobs.size()) {
         FROI_CUDA(cudaStreamSynchronize(c->stream));
         FROI_CUDA(cudaFreeHost(c->h_info));
