@@ -123,28 +123,29 @@ inline std::vector<flowroi::RoiMask> extract_roi(const flowroi::Sequence& seq,
         if (!seq[t].same_shape(f0)) throw data_error("sequence frames must share dimensions and depth");
         fp[t] = seq[t].pixels.data();
     }
-    // each RoiMask is constructed (zero-filled W*H bytes, core.hpp:84-85) by the library's host
-    // threads right before its mask is unpacked into it, while the GPU works on later pairs
+    // each RoiMask is built by the library's host threads from its finished bytes in one pass
+    // (std::vector::assign: no zero-fill, core.hpp:84-85), while the GPU works on later pairs
     std::vector<flowroi::RoiMask> masks(n);
-    struct Sink {
+    struct Put {
         std::vector<flowroi::RoiMask>* m;
         int w, h;
-        // called from the library's host threads: must not throw across the C ABI (a null return
-        // makes the call fail with an internal error instead)
-        static uint8_t* at(void* u, int, int t) noexcept {
-            Sink* s = static_cast<Sink*>(u);
+        // called from the library's host threads: must not throw across the C ABI
+        static int at(void* u, int, int t, const uint8_t* bytes) noexcept {
+            Put* p = static_cast<Put*>(u);
             try {
-                flowroi::RoiMask& r = (*s->m)[static_cast<std::size_t>(t)];
-                r = flowroi::RoiMask(s->w, s->h);
-                return r.bits.data();
+                flowroi::RoiMask& r = (*p->m)[static_cast<std::size_t>(t)];
+                r.width = p->w;
+                r.height = p->h;
+                r.bits.assign(bytes, bytes + static_cast<std::size_t>(p->w) * p->h);
+                return 0;
             } catch (...) {
-                return nullptr;
+                return 1;
             }
         }
-    } sink{&masks, f0.width, f0.height};
+    } put{&masks, f0.width, f0.height};
     std::vector<froi_frame_stats> stats(n);
-    check(froi_extract_frames_sink(ctx, fp.data(), 2, static_cast<int>(n), FROI_MASK_BYTES, &Sink::at, &sink,
-                                   stats.data()),
+    check(froi_extract_frames_put(ctx, fp.data(), 2, static_cast<int>(n), FROI_MASK_BYTES, &Put::at, &put,
+                                  stats.data()),
           "extract_roi");
     if (info) {
         info->shifts.resize(n);

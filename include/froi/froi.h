@@ -198,6 +198,16 @@ int froi_extract_frames_sink(froi_ctx* ctx, const void* const* frames, int sampl
                              int mask_layout, froi_mask_sink sink, void* user,
                              froi_frame_stats* stats_out);
 
+/* Finished masks handed over instead of written: the library unpacks each mask into a buffer of
+ * its own and calls put(user, well, frame, mask) from its host threads (concurrently; each
+ * (well, frame) once, frame 0 after frame 1); the caller copies the W*H bytes (or PBM rows) out
+ * before returning 0.  This is the drop-in's path: a RoiMask built from the bytes in one pass
+ * (std::vector::assign) costs one memory write instead of a zero-fill plus the unpack.  A
+ * non-zero return fails the call with FROI_ERR_USAGE; the callback must not unwind. */
+typedef int (*froi_mask_put)(void* user, int well, int frame, const uint8_t* mask);
+int froi_extract_frames_put(froi_ctx* ctx, const void* const* frames, int sample_bytes, int n_frames,
+                            int mask_layout, froi_mask_put put, void* user, froi_frame_stats* stats_out);
+
 /* Device-resident variant used for the device-side throughput figure: d_frames is a device
  * pointer (well-major, as above), d_masks_pbm receives PBM-packed masks on the device.
  * stats_out is a HOST pointer (nullable). Asynchronous work is complete on return. */

@@ -49,6 +49,7 @@ SIGNATURES = {
     "froi_extract_wells_device": (_I, [_P, _P, _I, _SZ, _I, _I, _P, _P]),
     "froi_extract_frames": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "froi_extract_frames_sink": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
+    "froi_extract_frames_put": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
     "froi_stream_reset": (_I, [_P, _I]),
     "froi_stream_push": (_I, [_P, _P, _I, _I, _SZ, _I, _I, _P, _I, _P]),
     "froi_stream_push_frames": (_I, [_P, _P, _I, _I, _I, _P, _P]),

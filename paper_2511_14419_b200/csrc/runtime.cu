@@ -1033,6 +1033,7 @@ struct HostCall {
     int layout = FROI_MASK_PBM;
     std::vector<uint8_t*> mask;           // [w*n + t] host destination (layout)
     froi_mask_sink sink = nullptr;        // or: destination asked for just before it is written
+    froi_mask_put put = nullptr;          // or: finished mask handed over (caller copies it)
     void* sink_user = nullptr;
     uint8_t* dev_masks = nullptr;         // device PBM destination [w*n + t] instead of mask[]
     bool frame0_rule = true;              // mask (w, 0) := mask (w, 1) (roi.hpp:348)
@@ -1185,7 +1186,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
         }
     }
     if (any_staged) ensure_staging(c);
-    const bool general_out = ring_out && (io.sink || io.layout != FROI_MASK_PBM || [&] {
+    const bool general_out = ring_out && (io.sink || io.put || io.layout != FROI_MASK_PBM || [&] {
         const std::vector<char> f = pinned_flags(std::vector<const uint8_t*>(io.mask.begin(), io.mask.end()), mb);
         for (char x : f)
             if (!x) return true;
@@ -1197,6 +1198,18 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
         uint8_t* d = io.sink(io.sink_user, w, t);
         if (!d) throw Error(1, "mask sink returned a null destination");
         return d;
+    };
+    // one finished mask into the caller's hands: written to its destination, or -- for a put
+    // callback -- unpacked into this thread's scratch and handed over
+    auto deliver = [&](const uint8_t* pbm, int w, int t) {
+        if (io.put) {
+            thread_local std::vector<uint8_t> scratch;
+            scratch.resize(io.layout == FROI_MASK_PBM ? mb : (size_t)g.W * g.H);
+            put_mask(g, pbm, io.layout, scratch.data());
+            if (io.put(io.sink_user, w, t, scratch.data()) != 0) throw Error(1, "mask put callback failed");
+            return;
+        }
+        put_mask(g, pbm, io.layout, dest(w, t));
     };
 
     c->times = froi_stage_times{};
@@ -1346,8 +1359,8 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                     FROI_CUDA(cudaEventSynchronize(done));
                     pool->parallel_for(j1 - j0, [&](size_t i) {
                         const int w = wt[j0 + i].first, t = wt[j0 + i].second;
-                        put_mask(g, hslot + mb * i, io.layout, dest(w, t));
-                        if (io.frame0_rule && t == 1) put_mask(g, hslot + mb * i, io.layout, dest(w, 0));
+                        deliver(hslot + mb * i, w, t);
+                        if (io.frame0_rule && t == 1) deliver(hslot + mb * i, w, 0);
                     });
                 });
             }
@@ -1386,7 +1399,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                                               c->stream));
                     FROI_CUDA(cudaStreamSynchronize(c->stream));
                     c->pool->parallel_for(m1 - m0, [&](size_t i) {
-                        put_mask(g, c->h_outring + mb * i, io.layout, dest((int)((m0 + i) / n), (int)((m0 + i) % n)));
+                        deliver(c->h_outring + mb * i, (int)((m0 + i) / n), (int)((m0 + i) % n));
                     });
                 }
             }
@@ -1647,6 +1660,31 @@ int froi_extract_wells(froi_ctx* c, const void* frames, int sample_bytes, size_t
 int froi_extract_roi(froi_ctx* c, const void* frames, int sample_bytes, size_t stride, int n_frames,
                      int layout, uint8_t* masks_out, froi_frame_stats* stats_out) {
     return froi_extract_wells(c, frames, sample_bytes, stride, 1, n_frames, layout, masks_out, stats_out);
+}
+
+int froi_extract_frames_put(froi_ctx* c, const void* const* frames, int sample_bytes, int n_frames,
+                            int layout, froi_mask_put put, void* user, froi_frame_stats* stats_out) {
+    if (!c || !frames || !put) return fail(1, "null argument");
+    if (sample_bytes != 1 && sample_bytes != 2) return fail(1, "sample_bytes must be 1 or 2");
+    if (!check_layout(layout)) return fail(1, "unknown mask layout");
+    if (n_frames < 2) return fail(2, "extract_roi: sequence needs at least 2 frames");
+    for (int t = 0; t < n_frames; ++t)
+        if (!frames[t]) return fail(1, "null frame pointer");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(c->device));
+    HostCall io;
+    io.n_wells = 1;
+    io.n_frames = n_frames;
+    io.src_bytes = sample_bytes;
+    io.layout = layout;
+    io.host.assign((const uint8_t* const*)frames, (const uint8_t* const*)frames + n_frames);
+    io.dev.assign(n_frames, nullptr);
+    io.put = put;
+    io.sink_user = user;
+    std::vector<PairInfo> infos;
+    run_host_call(c, io, infos);
+    stats_for_call(c, io, infos, stats_out);
+    ABI_CATCH
 }
 
 int froi_extract_frames_sink(froi_ctx* c, const void* const* frames, int sample_bytes, int n_frames,

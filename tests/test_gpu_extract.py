@@ -297,6 +297,18 @@ def test_per_frame_pointer_entries(gpu):
     assert sorted(order) == list(range(n))
     assert order.index(0) > order.index(1)
     assert np.array_equal(np.stack([sunk[t] for t in range(n)]), want[0])
+    # put: finished masks handed over (the drop-in's path)
+    got_put = {}
+    PUT = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.c_int, ctypes.c_int, ctypes.c_void_p)
+
+    def put(user, well, frame, ptr):
+        got_put[frame] = np.ctypeslib.as_array((ctypes.c_uint8 * (size * size)).from_address(ptr)).reshape(size, size).copy()
+        return 0
+
+    pcb = PUT(put)
+    _native.check(_native.lib.froi_extract_frames_put(ctx.handle, fp, 2, n, 0, ctypes.cast(pcb, ctypes.c_void_p),
+                                                     None, None))
+    assert np.array_equal(np.stack([got_put[t] for t in range(n)]), want[0])
     # streaming with per-frame pointers, uneven pushes
     _native.check(_native.lib.froi_stream_reset(ctx.handle, 1))
     got = []
