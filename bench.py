@@ -250,6 +250,11 @@ def cpu_reference(frames_per_sample: int, seconds_budget: float, steps: int, war
         raise SystemExit("bench.py: oracle/_ref/libfroi_ref.so is missing (build it here with "
                          "`make -C oracle ref`); refusing to time the C restatement as the reference")
     kind = "reference" if reference_available() else "port"
+    # every host core: undo the rank's NUMA pinning (bind_numa) for the reference's own threads
+    try:
+        os.sched_setaffinity(0, range(os.cpu_count() or 1))
+    except OSError:
+        pass
     o = Oracle(kind)
     cfg = synth.config("C3")
     cores = threads or os.cpu_count() or 1

@@ -19,6 +19,7 @@
 #include <array>
 #include <vector>
 
+#include <chrono>
 #include <map>
 #include <memory>
 #include <thread>
@@ -337,6 +338,7 @@ struct froi_ctx {
     // host ingest / egress pipeline (run_host_call): bounded rings, whatever the call size
     std::unique_ptr<HostPool> pool;      // frame conversion into staging, mask unpacking
     std::unique_ptr<HostPool> courier;   // one thread: waits for each batch, then delivers it
+    std::unique_ptr<HostPool> dpool;     // mask delivery threads (unpacking), apart from conversion
     uint8_t* d_ring = nullptr;           // ingest ring: ring_frames device frame slots
     int ring_chunk = 0, ring_frames = 0; // upload chunk (frames) and ring size (frames)
     uint8_t* h_stage = nullptr;          // pinned staging ring: kStageChunks chunks
@@ -567,6 +569,7 @@ void ctx_free(froi_ctx* c) {
     for (auto& a : c->bev)
         for (auto e : a) cudaEventDestroy(e);
     c->courier.reset();  // joins its thread (idle between calls)
+    c->dpool.reset();
     c->pool.reset();
     for (auto e : c->chunk_ready) cudaEventDestroy(e);
     for (auto e : c->stage_free) cudaEventDestroy(e);
@@ -1068,12 +1071,16 @@ void ensure_pipeline(froi_ctx* c) {
     if (!c->pool) {
         const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
         const int dev = c->device;
-        // host threads for frame conversion and mask delivery: all but two hardware threads (the
-        // caller's and the courier), at most 16; $FROI_HOST_THREADS overrides
-        int nt = std::max(1, std::min(16, hw - 2));
-        if (const char* e = getenv("FROI_HOST_THREADS")) nt = std::max(1, atoi(e));
-        c->pool.reset(new HostPool(nt, [dev] { cudaSetDevice(dev); }));
-        c->courier.reset(new HostPool(1, [dev] { cudaSetDevice(dev); }));
+        // host threads: all but two hardware threads (the caller's and the courier), at most 16
+        // ($FROI_HOST_THREADS overrides), split between frame conversion (the caller's pool) and
+        // mask delivery (the courier's), so a batch's delivery never queues behind the next
+        // batches' conversions
+        int nt = std::max(2, std::min(16, hw - 2));
+        if (const char* e = getenv("FROI_HOST_THREADS")) nt = std::max(2, atoi(e));
+        auto init = [dev] { cudaSetDevice(dev); };
+        c->pool.reset(new HostPool(nt - nt / 2, init));
+        c->dpool.reset(new HostPool(nt / 2, init));
+        c->courier.reset(new HostPool(1, init));
     }
     if (!c->d_ring) {
         c->ring_chunk = std::max(8, c->Pcap);
@@ -1109,6 +1116,18 @@ cudaEvent_t event_at(std::vector<cudaEvent_t>& v, size_t i) {
     return v[i];
 }
 
+// $FROI_TRACE=1: host-side phase times of each host call on stderr (diagnostics)
+static bool trace_on() {
+    static const bool on = [] {
+        const char* e = getenv("FROI_TRACE");
+        return e && atoi(e) == 1;
+    }();
+    return on;
+}
+static double now_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 // One PBM mask (H rows of SB bytes, MSB first) into the caller's layout.
 void put_mask(const Geom& g, const uint8_t* pbm, int layout, uint8_t* dst) {
     const size_t mb = (size_t)g.H * g.SB;
@@ -1138,6 +1157,8 @@ void put_mask(const Geom& g, const uint8_t* pbm, int layout, uint8_t* dst) {
 // Runs one host call end to end (see the comment block above).  Throws froi::Error; on any error
 // every queued copy, kernel and host task has finished before the exception leaves.
 void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos) {
+    double t_convert = 0.0, t_stage_wait = 0.0, t_tail_tasks = 0.0;
+    const double t_call0 = trace_on() ? now_ms() : 0.0;
     const Geom& g = c->g;
     const size_t fb = c->frame_bytes, mb = (size_t)g.H * g.SB;
     const int n = io.n_frames, nw = io.n_wells;
@@ -1154,7 +1175,10 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             wt.emplace_back(w, t);
         }
     // which frames go through the pinned staging ring (pageable, or another sample width)
-    const std::vector<char> src_pinned = pinned_flags(io.host, (size_t)g.W * g.H * io.src_bytes);
+    // (frames of another sample width are staged whatever their memory: no pinned-ness queries)
+    const std::vector<char> src_pinned = io.src_bytes == g.sample_bytes
+                                             ? pinned_flags(io.host, (size_t)g.W * g.H * io.src_bytes)
+                                             : std::vector<char>(nk, 0);
     bool any_staged = false;
     for (size_t k = 0; k < nk; ++k) any_staged |= io.host[k] && (io.src_bytes != g.sample_bytes || !src_pinned[k]);
     // batches: Pcap pairs, except a first batch of Pcap / 4 when the frames need host conversion,
@@ -1258,12 +1282,16 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                 }
             } else {
                 const size_t slot = n_staged++ % kStageChunks;
+                const double tw0 = trace_on() ? now_ms() : 0.0;
                 FROI_CUDA(cudaEventSynchronize(c->stage_free[slot]));  // its previous copy is done
+                if (trace_on()) t_stage_wait += now_ms() - tw0;
                 uint8_t* st = c->h_stage + fb * CH * slot;
                 const size_t px = (size_t)g.W * g.H;
+                const double tc0 = trace_on() ? now_ms() : 0.0;
                 c->pool->parallel_for(k1 - k0, [&](size_t i) {
                     if (io.host[k0 + i]) convert_frame(io.host[k0 + i], io.src_bytes, st + fb * i, g.sample_bytes, px);
                 });
+                if (trace_on()) t_convert += now_ms() - tc0;
                 FROI_CUDA(cudaMemcpyAsync(dst, st, fb * (k1 - k0), cudaMemcpyHostToDevice, c->copy_stream));
                 FROI_CUDA(cudaEventRecord(c->stage_free[slot], c->copy_stream));
             }
@@ -1354,7 +1382,7 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
                 FROI_CUDA(cudaMemcpyAsync(hslot, dsrc, mb * (j1 - j0), cudaMemcpyDeviceToHost, c->d2h_stream));
                 cudaEvent_t done = c->delivered[b];
                 FROI_CUDA(cudaEventRecord(done, c->d2h_stream));
-                HostPool* pool = c->pool.get();
+                HostPool* pool = c->dpool.get();
                 tasks[b] = c->courier->submit([&, done, hslot, j0, j1, pool] {
                     FROI_CUDA(cudaEventSynchronize(done));
                     pool->parallel_for(j1 - j0, [&](size_t i) {
@@ -1366,8 +1394,10 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
             }
         }
         upload_to(nk ? nk - 1 : 0);  // frames no pair reads (e.g. a push's carry-only tail)
+        const double te0 = trace_on() ? now_ms() : 0.0;
         for (auto& t : tasks)
             if (t) t->wait();
+        if (trace_on()) t_tail_tasks = now_ms() - te0;
         FROI_CUDA(cudaEventRecord(c->d2h_done, c->d2h_stream));
         FROI_CUDA(cudaStreamWaitEvent(c->stream, c->d2h_done, 0));
         FROI_CUDA(cudaEventRecord(c->ev[6], c->copy_stream));  // carry copies
@@ -1411,6 +1441,9 @@ void run_host_call(froi_ctx* c, const HostCall& io, std::vector<PairInfo>& infos
     }
     accumulate_batch_times(c, nb);
     infos.assign(c->h_info, c->h_info + jobs.size());
+    if (trace_on())
+        fprintf(stderr, "froi trace: host call %.2f ms: conversion %.2f, staging waits %.2f, delivery tail %.2f (%zu batches)\n",
+                now_ms() - t_call0, t_convert, t_stage_wait, t_tail_tasks, nb);
 }
 
 // Per-frame stats of a host call: pair rows in (well, frame) order, frame 0 of a well borrows
