@@ -515,7 +515,7 @@ def run_ours(args) -> None:
                        "global_batch": world * F, "parallelism": f"wells sharded over {world} GPU(s)",
                        "lanes": "2 execution lanes per GPU (consecutive 64-pair batches overlap)",
                        "graphs": "each batch's kernel sequence replayed as a CUDA graph (FROI_GRAPHS=0 disables)",
-                       "host": f"one process per GPU; rank 0 pinned buffers on NUMA {numa}",
+                       "host": f"one process per GPU; rank 0 NUMA binding: {numa}",
                        "l2": "each step reads a 472 MB well (> 126 MB L2); no flush",
                        "params": "ExtractParams{} defaults (pyramid 3, window 15, threshold 0.2)"},
             "roofline": roofline,

@@ -21,6 +21,8 @@
 // level-0 image is never materialised.
 #include "kernels.cuh"
 
+#include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 namespace froi {
@@ -716,8 +718,11 @@ __device__ __forceinline__ void vsum_inplace(float* col) {
     col[((BOFF + FY - 1) % RG) * SW] = pv;
 }
 
+#ifndef FROI_FLOW_MINB
+#define FROI_FLOW_MINB 2
+#endif
 template <int R, int PAD>
-__global__ void __launch_bounds__(FNT, 2) k_flow_iter(Geom g, IterArgs a,
+__global__ void __launch_bounds__(FNT, FROI_FLOW_MINB) k_flow_iter(Geom g, IterArgs a,
                                                       const float4* __restrict__ exA_f,
                                                       const float* __restrict__ exB_f,
                                                       const float4* __restrict__ exA_p,
@@ -1005,7 +1010,14 @@ int strip_tiles(const Geom& g, int l, int n_pairs, int R) {
 template <int R, int PAD>
 void launch_iter_t(const Geom& g, const IterArgs& a, const FlowBuffers& b, const int* d_prev,
                    const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s) {
-    const size_t smem = sizeof(float) * 5 * (size_t)ring_pl(FX + 2 * R, PAD);
+    size_t smem = sizeof(float) * 5 * (size_t)ring_pl(FX + 2 * R, PAD);
+    // experiment knob: request at least this much shared memory (forces fewer CTAs per SM,
+    // leaving room for the other lane's kernels)
+    static const size_t smem_min = [] {
+        const char* e = getenv("FROI_FLOW_SMEM_MIN");
+        return e ? (size_t)atol(e) : (size_t)0;
+    }();
+    smem = std::max(smem, smem_min);
     // kernel attributes are per device: set on every call (one host thread may drive several)
     FROI_CUDA(cudaFuncSetAttribute(k_flow_iter<R, PAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int nr = strip_tiles(g, a.l, n_pairs, R);
