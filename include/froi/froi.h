@@ -157,6 +157,13 @@ int froi_ctx_set_lanes(froi_ctx* ctx, int lanes);
  * on a side branch concurrently with its forward FFT and registration.  0 serialises them, so the
  * per-stage times of froi_ctx_kernel_times bracket each stage's own kernels; outputs are identical. */
 int froi_ctx_set_fork(froi_ctx* ctx, int fork);
+/* Flow precision (0, default: fp32 flow within the stated tolerance; 1: bit-exact).
+ * With 1 the pyramid, polynomial expansion, flow_step with the reference's running-sum box_mean,
+ * and the coarse-to-fine prior run in fp64 in the reference's operation order (k_flow64.cu), so
+ * flows and masks are byte-identical to the reference's; slower, and allocates its double buffers
+ * (about 14 GB per lane at 1024^2 with 64-pair batches) on first use.  Status 3 if they do not fit. */
+int froi_ctx_set_flow_exact(froi_ctx* ctx, int exact);
+int froi_ctx_get_flow_exact(const froi_ctx* ctx, int* exact_out);
 
 /* ---- stage entry: extract_roi (roi.hpp:309-364) ----
  * Host frames: n_frames frames of width*height samples; frame f starts at

@@ -39,6 +39,8 @@ SIGNATURES = {
     "froi_ctx_stream": (_I, [_P, ctypes.POINTER(_P)]),
     "froi_ctx_set_lanes": (_I, [_P, ctypes.c_int]),
     "froi_ctx_set_fork": (_I, [_P, ctypes.c_int]),
+    "froi_ctx_set_flow_exact": (_I, [_P, ctypes.c_int]),
+    "froi_ctx_get_flow_exact": (_I, [_P, ctypes.POINTER(ctypes.c_int)]),
     "froi_dwt_forward": (_I, [_P, _P, ctypes.c_int, _P]),
     "froi_dwt_inverse": (_I, [_P, _P, ctypes.c_int, _P]),
     "froi_dwt_forward_device": (_I, [_P, _P, ctypes.c_int, ctypes.c_int, _P]),

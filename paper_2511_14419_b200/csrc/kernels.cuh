@@ -148,6 +148,33 @@ int launch_flow(const Geom& g, const DevParams& p, const FlowBuffers& b, const i
 void launch_expand_image(const Geom& g, const DevParams& p, const float* d_img, float* d_planes,
                          cudaStream_t s);
 
+// k_flow64.cu: the bit-exact fp64 flow (froi_ctx_set_flow_exact)
+struct Flow64Const {
+    double g0[16], g1[16], g2[16];  // polynomial-expansion kernels w, w t, w t^2 (index t + r)
+    double blur[16];                // gaussian_blur3's normalised taps (sigma 1)
+    int blur_r, poly_r;
+    double inv_m20, inv_m22, i01, i11, i12;  // expansion_moments' inverse (flow.hpp:92-112)
+};
+struct Flow64Buffers {
+    double* img_f;   // frame-slot pyramid images, all levels [slot][lsum]
+    double* ex_f;    // frame-slot expansions [slot][5 planes bx, by, a11, a12, a22][lsum]
+    double* tmp_f;   // row-blur scratch of the frame slots [slot][W*H]
+    double* img_p;   // pair-slot shifted pyramids
+    double* ex_p;    // pair-slot shifted expansions
+    double* tmp_p;   // row-blur scratch of the pair slots
+    double* prod;    // [pair][5][W*H] products, then window means
+    double* rowm;    // [pair][5][W*H] row means
+    float2* flow0;   // the float2 flow ping-pong shared with the fp32 path
+    float2* flow1;
+};
+int launch_expand_frames64(const Geom& g, const Flow64Const& C, const Flow64Buffers& b, const void* den,
+                           int n_slots, cudaStream_t s);
+int launch_expand_shifted64(const Geom& g, const Flow64Const& C, const Flow64Buffers& b, const void* den,
+                            const int* d_next, const PairInfo* d_info, int n_pairs, cudaStream_t s);
+// all levels and iterations; *cur_out = the buffer holding the level-0 flow; returns launches
+int launch_flow64(const Geom& g, const DevParams& p, const Flow64Buffers& b, const int* d_prev, const int* d_next,
+                  const PairInfo* d_info, int n_pairs, cudaStream_t s, int* cur_out);
+
 // k_mask.cu
 struct MaskBuffers {
     const float2* flow;           // [pair][lsum] level-0 flow at offset 0

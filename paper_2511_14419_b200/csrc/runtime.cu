@@ -210,6 +210,46 @@ DevParams make_dev_params(const froi_params& p) {
     return d;
 }
 
+// The bit-exact flow's constants (k_flow64.cu): the same host expressions as make_dev_params,
+// kept in double (polynomial_expansion flow.hpp:118-127, expansion_moments :92-112,
+// gaussian_blur3 :259-266).
+Flow64Const make_flow64_const(const froi_params& p) {
+    Flow64Const c{};
+    const int r = (p.poly_n - 1) / 2;
+    c.poly_r = r;
+    for (int t = -r; t <= r; ++t) {
+        const double w = std::exp(-double(t) * t / (2.0 * p.poly_sigma * p.poly_sigma));
+        c.g0[t + r] = w;
+        c.g1[t + r] = w * t;
+        c.g2[t + r] = w * t * t;
+    }
+    double s0 = 0, s2 = 0, s4 = 0;
+    for (int t = -r; t <= r; ++t) {
+        const double w = c.g0[t + r];
+        s0 += w;
+        s2 += w * t * t;
+        s4 += w * t * t * t * t;
+    }
+    const double m00 = s0 * s0, m20 = s2 * s0, m40 = s4 * s0, m22 = s2 * s2;
+    const double det = m00 * (m40 * m40 - m22 * m22) - m20 * (m20 * m40 - m22 * m20) +
+                       m20 * (m20 * m22 - m40 * m20);
+    c.inv_m20 = 1.0 / m20;
+    c.inv_m22 = 1.0 / m22;
+    c.i01 = (m20 * m22 - m20 * m40) / det;
+    c.i11 = (m00 * m40 - m20 * m20) / det;
+    c.i12 = (m20 * m20 - m00 * m22) / det;
+    const double sigma = 1.0;
+    const int br = std::max(1, int(std::ceil(2.5 * sigma)));
+    c.blur_r = br;
+    double sum = 0.0;
+    for (int t = -br; t <= br; ++t) {
+        c.blur[t + br] = std::exp(-double(t) * t / (2.0 * sigma * sigma));
+        sum += c.blur[t + br];
+    }
+    for (int i = 0; i < 2 * br + 1; ++i) c.blur[i] /= sum;
+    return c;
+}
+
 // fft_inplace twiddle sequence (fft.hpp:27-37): stage len = 2h stores w_0..w_{h-1} at [h-1, 2h-2]
 std::vector<double2> twiddles(int n, bool inverse) {
     std::vector<double2> tw(n > 1 ? n - 1 : 1);
@@ -368,6 +408,26 @@ struct froi_ctx {
     std::map<std::tuple<int, int, int, const void*>, BatchGraph> graphs;
     bool use_graphs = default_graphs();
 
+    // bit-exact fp64 flow (froi_ctx_set_flow_exact): its constants and buffers, allocated on first use
+    bool flow_exact = false;
+    Flow64Const f64c{};
+    double *d64_img_f = nullptr, *d64_ex_f = nullptr, *d64_img_p = nullptr, *d64_ex_p = nullptr;
+    double *d64_prod = nullptr, *d64_rowm = nullptr;
+
+    Flow64Buffers flow64_buffers() const {
+        Flow64Buffers b;
+        b.img_f = d64_img_f;
+        b.ex_f = d64_ex_f;
+        b.tmp_f = d64_prod;  // the frame expansions' row blur runs before the flow needs prod
+        b.img_p = d64_img_p;
+        b.ex_p = d64_ex_p;
+        b.tmp_p = d64_rowm;  // (the shifted expansions may overlap them on the other branch)
+        b.prod = d64_prod;
+        b.rowm = d64_rowm;
+        b.flow0 = d_flow0;
+        b.flow1 = d_flow1;
+        return b;
+    }
     MaskBuffers mask_buffers(int tb_) const {
         MaskBuffers b;
         b.flow = nullptr;
@@ -526,6 +586,22 @@ void ctx_alloc(froi_ctx* c) {
     FROI_CUDA(cudaDeviceSynchronize());
 }
 
+// Buffers of the bit-exact flow (double images and expansions per slot, two [pair][5][W*H]
+// scratch planes sets), allocated when the mode is first switched on.
+void ensure_flow64(froi_ctx* c) {
+    if (c->d64_ex_f) return;
+    const Geom& g = c->g;
+    const size_t px = (size_t)g.W * g.H, ls = (size_t)g.lsum;
+    size_t& t = c->device_bytes;
+    c->d64_img_f = dalloc<double>(ls * c->Fcap, &t);
+    c->d64_ex_f = dalloc<double>(5 * ls * c->Fcap, &t);
+    c->d64_img_p = dalloc<double>(ls * c->Pcap, &t);
+    c->d64_ex_p = dalloc<double>(5 * ls * c->Pcap, &t);
+    // prod doubles as the frame slots' blur scratch (Fcap <= 5 Pcap), rowm as the pair slots'
+    c->d64_prod = dalloc<double>(5 * px * std::max<size_t>(c->Pcap, (c->Fcap + 4) / 5), &t);
+    c->d64_rowm = dalloc<double>(5 * px * c->Pcap, &t);
+}
+
 void drop_graphs(froi_ctx* c) {
     for (auto& kv : c->graphs) {
         if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
@@ -551,7 +627,8 @@ void ctx_free(froi_ctx* c) {
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_cand_idx, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
                     c->d_bits_clean, c->d_bits_keep, c->d_run_x0, c->d_run_x1, c->d_run_n, c->d_run_par, c->d_run_area,
                     c->d_out_batch, c->d_seq_out, c->d_seq_tmp, c->d_carry[0], c->d_carry[1],
-                    c->d_ring, c->d_outring};
+                    c->d_ring, c->d_outring, c->d64_img_f, c->d64_ex_f, c->d64_img_p, c->d64_ex_p,
+                    c->d64_prod, c->d64_rowm};
     for (void* p : ptrs)
         if (p) cudaFree(p);
     for (int i = 0; i < 2; ++i) {
@@ -686,11 +763,21 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
         }
         rec(1);
         FlowBuffers fb = c->flow_buffers();
+        Flow64Buffers fb64 = c->flow64_buffers();
+        // the flow's expansions: fp32 (k_flow.cu) or the bit-exact fp64 mode (k_flow64.cu)
+        auto expand_frames = [&](cudaStream_t st) {
+            if (c->flow_exact) launch_expand_frames64(g, c->f64c, fb64, c->d_den, nf, st);
+            else launch_expand_frames(g, c->dp, fb, nf, st);
+        };
+        auto expand_shifted = [&](cudaStream_t st) {
+            if (c->flow_exact) launch_expand_shifted64(g, c->f64c, fb64, c->d_den, c->d_next[tb], c->d_info, n_pairs, st);
+            else launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, st);
+        };
         if (fork_now) {
             // expansions of the frame slots on the side branch, FFT + registration on this one
             FROI_CUDA(cudaEventRecord(c->ev_den, s));
             FROI_CUDA(cudaStreamWaitEvent(c->side, c->ev_den, 0));
-            launch_expand_frames(g, c->dp, fb, nf, c->side);
+            expand_frames(c->side);
             FROI_CUDA(cudaEventRecord(c->ev_exp, c->side));
             launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
             rec(2);
@@ -698,21 +785,23 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
             launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
                                   c->d_cols, c->d_surf, c->d_info, n_pairs, s);
             rec(4);
-            launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+            expand_shifted(s);
             FROI_CUDA(cudaStreamWaitEvent(s, c->ev_exp, 0));
             rec(5);
         } else {
             launch_fft_forward(g, c->d_den, c->d_sums, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_spec, nf, s);
             rec(2);
-            launch_expand_frames(g, c->dp, fb, nf, s);
+            expand_frames(s);
             rec(3);
             launch_register_pairs(g, c->dp, c->d_spec, c->d_prev[tb], c->d_next[tb], c->d_itw_row, c->d_itw_col,
                                   c->d_cols, c->d_surf, c->d_info, n_pairs, s);
             rec(4);
-            launch_expand_shifted(g, c->dp, fb, c->d_next[tb], c->d_info, n_pairs, s);
+            expand_shifted(s);
             rec(5);
         }
-        const int cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
+        int cur = 0;
+        if (c->flow_exact) launch_flow64(g, c->dp, fb64, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s, &cur);
+        else cur = launch_flow(g, c->dp, fb, c->d_prev[tb], c->d_next[tb], c->d_info, n_pairs, s);
         rec(6);
         MaskBuffers mb = c->mask_buffers(tb);
         mb.flow = cur ? c->d_flow1 : c->d_flow0;
@@ -779,7 +868,12 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
     K.batches += 1;
     // launches: denoise (one per ingest run), fft 2, expand (1 + 2(L-1)) x2, register 3,
     // flow L*iters + (L-1) upsamplings (+ the mask stage's own count)
-    owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations + (g.L - 1);
+    // (bit-exact flow: expand (1 + 2(L-1) + L) x2, flow 4 L iters + (L-1))
+    if (c->flow_exact)
+        owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1) + g.L) + 3 + 4 * (uint64_t)g.L * c->dp.iterations +
+                           (g.L - 1);
+    else
+        owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations + (g.L - 1);
 }
 
 // The second lane, created on first use with the owner's device, parameters and capacity.
@@ -809,6 +903,10 @@ froi_ctx* lane_of(froi_ctx* c) {
     c->lane->fork = c->fork;
     c->lane->dp = c->dp;  // set_params may have changed the run-time parameters
     c->lane->params = c->params;
+    c->lane->f64c = c->f64c;
+    if (c->flow_exact) ensure_flow64(c->lane);
+    if (c->lane->flow_exact != c->flow_exact) drop_graphs(c->lane);
+    c->lane->flow_exact = c->flow_exact;
     return c->lane;
 }
 
@@ -1548,6 +1646,7 @@ int froi_ctx_create(int device, const froi_params* p, int width, int height, int
     c->params = *p;
     c->g = make_geom(*p, width, height, depth);
     c->dp = make_dev_params(*p);
+    c->f64c = make_flow64_const(*p);
     FROI_CUDA(cudaSetDevice(device));
     FROI_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     if (max_pairs <= 0) {
@@ -1601,6 +1700,7 @@ int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p) {
     ctx->params = *p;
     ctx->dp = make_dev_params(*p);
     ctx->dp.norm_lut = ctx->d_norm_lut;
+    ctx->f64c = make_flow64_const(*p);
     // captured batch graphs hold the old parameters as kernel arguments
     ABI_TRY
     FROI_CUDA(cudaSetDevice(ctx->device));
@@ -1652,6 +1752,24 @@ int froi_ctx_set_fork(froi_ctx* ctx, int fork) {
         drop_graphs(ctx->lane);
     }
     ABI_CATCH
+}
+
+int froi_ctx_set_flow_exact(froi_ctx* ctx, int exact) {
+    if (!ctx) return fail(1, "null context");
+    if (exact != 0 && exact != 1) return fail(1, "exact must be 0 or 1");
+    ABI_TRY
+    FROI_CUDA(cudaSetDevice(ctx->device));
+    FROI_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (exact) ensure_flow64(ctx);  // the lane's on its next use (lane_of)
+    if (ctx->flow_exact != (exact != 0)) drop_graphs(ctx);  // captured graphs hold the other flow
+    ctx->flow_exact = exact != 0;
+    ABI_CATCH
+}
+
+int froi_ctx_get_flow_exact(const froi_ctx* ctx, int* out) {
+    if (!ctx || !out) return fail(1, "null argument");
+    *out = ctx->flow_exact ? 1 : 0;
+    return 0;
 }
 
 int froi_ctx_launch_count(const froi_ctx* ctx, uint64_t* out) {
@@ -2005,9 +2123,16 @@ int froi_compute_flow(froi_ctx* c, const uint16_t* prev, const uint16_t* next, f
     taps_upload(c, fr, 2);
     taps_copy_den(c, 2);
     FlowBuffers fb = c->flow_buffers();
-    launch_expand_frames(c->g, c->dp, fb, 2, c->stream);
     taps_set_info(c, 0, 0);
-    const int cur = launch_flow(c->g, c->dp, fb, c->d_prev[0], c->d_next[0], c->d_info, 1, c->stream);
+    int cur = 0;
+    if (c->flow_exact) {
+        const Flow64Buffers fb64 = c->flow64_buffers();
+        launch_expand_frames64(c->g, c->f64c, fb64, c->d_den, 2, c->stream);
+        launch_flow64(c->g, c->dp, fb64, c->d_prev[0], c->d_next[0], c->d_info, 1, c->stream, &cur);
+    } else {
+        launch_expand_frames(c->g, c->dp, fb, 2, c->stream);
+        cur = launch_flow(c->g, c->dp, fb, c->d_prev[0], c->d_next[0], c->d_info, 1, c->stream);
+    }
     const size_t px = (size_t)c->g.W * c->g.H;
     std::vector<float2> f(px);
     FROI_CUDA(cudaMemcpyAsync(f.data(), cur ? c->d_flow1 : c->d_flow0, sizeof(float2) * px, cudaMemcpyDeviceToHost,

@@ -132,6 +132,17 @@ class Context:
         """Intra-batch overlap of the expansions with the FFT / registration (default on)."""
         _native.check(_native.lib.froi_ctx_set_fork(self._h, 1 if fork else 0))
 
+    def set_flow_exact(self, exact: bool) -> None:
+        """Bit-exact fp64 flow (k_flow64.cu; flows and masks byte-identical to the reference's)
+        instead of the default fp32 flow within the stated tolerance.  Allocates its double
+        buffers on first use."""
+        _native.check(_native.lib.froi_ctx_set_flow_exact(self._h, 1 if exact else 0), "set_flow_exact")
+
+    def flow_exact(self) -> bool:
+        v = ctypes.c_int(0)
+        _native.check(_native.lib.froi_ctx_get_flow_exact(self._h, ctypes.byref(v)))
+        return bool(v.value)
+
     def stream(self) -> int:
         s = ctypes.c_void_p()
         _native.check(_native.lib.froi_ctx_stream(self._h, ctypes.byref(s)))
@@ -184,12 +195,13 @@ _CTX_CACHE_MAX = 8
 
 
 @contextlib.contextmanager
-def _context(width: int, height: int, depth: int, params: ExtractParams, device: int = 0):
+def _context(width: int, height: int, depth: int, params: ExtractParams, device: int = 0,
+             exact_flow: bool = False):
     """A cached context, held for the duration of the ``with`` block: pinned against eviction
     (``users``) and locked, so concurrent callers of one context serialise and a context is only
-    ever closed while nobody holds it."""
+    ever closed while nobody holds it.  ``exact_flow`` selects the bit-exact fp64 flow."""
     cp = params.to_c()
-    key = (device, width, height, depth, bytes(cp))
+    key = (device, width, height, depth, bytes(cp), bool(exact_flow))
     with _ctx_lock:
         ctx = _ctx_cache.get(key)
         if ctx is None:
@@ -197,6 +209,8 @@ def _context(width: int, height: int, depth: int, params: ExtractParams, device:
             while len(_ctx_cache) >= _CTX_CACHE_MAX and idle:
                 _ctx_cache.pop(idle.pop(0)).close()
             ctx = Context(width, height, depth, params, device)
+            if exact_flow:
+                ctx.set_flow_exact(True)
             _ctx_cache[key] = ctx
         ctx.users += 1
     try:
@@ -213,11 +227,12 @@ def _split_shifts(stats, n: int) -> list:
 
 def extract_roi(seq, params: ExtractParams | None = None, workers: int = 1,
                 info: ExtractInfo | None = None, timers: StageTimes | None = None,
-                depth: int | None = None) -> np.ndarray:
+                depth: int | None = None, exact_flow: bool = False) -> np.ndarray:
     """``flowroi::extract_roi`` (roi.hpp:309-364) on the GPU.  Returns masks [n, h, w] (uint8 0/1).
 
     ``workers`` keeps the reference signature; the output never depends on it
-    (parallel.hpp:17-19).  A single sequence runs on one GPU."""
+    (parallel.hpp:17-19).  A single sequence runs on one GPU.  ``exact_flow``: the bit-exact
+    fp64 flow, so the masks are byte-identical to the reference's (slower)."""
     params = params or ExtractParams()
     params.roi.validate()
     params.flow.validate()
@@ -232,7 +247,7 @@ def extract_roi(seq, params: ExtractParams | None = None, workers: int = 1,
     if n < 2:
         raise DataError("extract_roi: sequence needs at least 2 frames")
     params.denoise.validate()
-    with _context(w, h, depth, params) as ctx:
+    with _context(w, h, depth, params, exact_flow=exact_flow) as ctx:
         masks, stats = ctx.extract_wells(frames[None])
         st = ctx.stage_times() if timers is not None else None
     if info is not None:
@@ -253,7 +268,7 @@ def shard_wells(n_wells: int, devices: list[int]) -> dict:
 
 
 def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth: int | None = None,
-                  devices: list[int] | None = None, layout: str = "bytes"):
+                  devices: list[int] | None = None, layout: str = "bytes", exact_flow: bool = False):
     """Independent wells [wells, n, h, w], sharded well-wise over ``devices`` (one host thread
     per GPU, no collective).  Returns (masks, list of per-well ExtractInfo)."""
     params = params or ExtractParams()
@@ -267,7 +282,7 @@ def extract_wells(frames: np.ndarray, params: ExtractParams | None = None, depth
 
     def work(dev: int, wells: list[int]):
         try:
-            with _context(w, h, depth, params, dev) as ctx:
+            with _context(w, h, depth, params, dev, exact_flow) as ctx:
                 m, st = ctx.extract_wells(frames[wells], layout)
             results[dev] = (wells, m, st)
         except Exception as e:  # first error re-raised like parallel_for (parallel.hpp:31-48)
@@ -333,8 +348,9 @@ def estimate_shift(reference: np.ndarray, moving: np.ndarray, max_shift: int = 1
 
 
 def compute_flow(prev: np.ndarray, nxt: np.ndarray, params: FlowParams | ExtractParams | None = None,
-                 depth: int | None = None):
-    """``flowroi::compute_flow`` (flow.hpp:304-345): returns (u, v) float32 [h, w]."""
+                 depth: int | None = None, exact: bool = False):
+    """``flowroi::compute_flow`` (flow.hpp:304-345): returns (u, v) float32 [h, w].  ``exact``:
+    the bit-exact fp64 flow (identical to the reference's) instead of the fp32 one."""
     ep = ExtractParams()
     if isinstance(params, ExtractParams):
         ep = params.copy()
@@ -350,7 +366,7 @@ def compute_flow(prev: np.ndarray, nxt: np.ndarray, params: FlowParams | Extract
     u = np.empty((h, w), np.float32)
     v = np.empty((h, w), np.float32)
     a16, b16 = _u16(a), _u16(b)
-    with _context(w, h, depth, ep) as ctx:
+    with _context(w, h, depth, ep, exact_flow=exact) as ctx:
         _native.check(_native.lib.froi_compute_flow(ctx.handle, a16.ctypes.data, b16.ctypes.data,
                                                     u.ctypes.data, v.ctypes.data), "compute_flow")
     return u, v

@@ -2,7 +2,7 @@
 
   FROI_LIB=paper_2511_14419_b200/_lib/libfroi_base.so python profiles/tools/stage_ab.py TAG [wells]
 
-Runs `wells` full C3 wells (450 frames, device-resident) with ONE execution lane, so each stage's
+STAGE_AB_EXACT=1 times the bit-exact fp64 flow mode.  Runs `wells` full C3 wells (450 frames, device-resident) with ONE execution lane, so each stage's
 events bracket only its own kernels, and prints one JSON line: us per pair per stage, the flow
 kernel's launch count/average, and the two-lane frames/s of the same wells.
 """
@@ -31,6 +31,8 @@ ctx = flowroi.Context(1024, 1024, 8, cfg.params, max_pairs=max_pairs)
 ctx.set_lanes(1)
 if os.environ.get("STAGE_AB_NOFORK"):
     ctx.set_fork(False)
+if os.environ.get("STAGE_AB_EXACT"):  # the bit-exact fp64 flow
+    ctx.set_flow_exact(True)
 ctx.extract_wells_device(dev[0].data_ptr(), 1, F, masks.data_ptr())  # warm-up
 acc = {}
 for w in range(nw):
