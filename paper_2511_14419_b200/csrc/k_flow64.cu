@@ -15,11 +15,13 @@
 //                        tile's rows into shared memory, then the six column correlations and the
 //                        moment-inverse combination -> planes bx, by, a11, a12, a22 (c is unused)
 //   k64_products         flow_step's per-pixel normal-equation terms (flow.hpp:204-233)
-//   k64_box_rows / k64_box_cols
-//                        box_mean (flow.hpp:171-195): the reference's running sums are sequential
-//                        along each row, then each column (the rounding of every partial sum is
-//                        part of the result), so one thread walks one row / column of one plane
-//   k64_solve            the 2x2 solve and its singular fallback (flow.hpp:236-253)
+//   k64_box_rows         box_mean's row pass (flow.hpp:171-195): the reference's running sums are
+//                        sequential along each row (the rounding of every partial sum is part of
+//                        the result), so one thread walks one row of one plane, its inputs staged
+//                        through shared memory in coalesced chunks
+//   k64_box_cols_solve   box_mean's column pass, one thread per column with the five planes'
+//                        running sums, fused with the 2x2 solve and its singular fallback
+//                        (flow.hpp:236-253)
 //   k64_upsample         compute_flow's coarse-to-fine prior (flow.hpp:318-337)
 // Throughput is bounded by those sequential box-mean walks and by HBM (five double planes per
 // pass); the default fp32 flow (k_flow.cu) remains the fast path.
@@ -229,76 +231,189 @@ __global__ void __launch_bounds__(kNT) k64_products(Geom g, int l, int mode, con
     o[4 * n0] = dadd(dmul(a12, db1), dmul(a22, db2));
 }
 
-// box_mean's row pass: one thread per (pair, plane, row), the reference's running sum
-__global__ void __launch_bounds__(kNT) k64_box_rows(Geom g, int l, int R, int n_pairs, const double* __restrict__ in,
-                                                    double* __restrict__ out) {
+// acc / count for box_mean: the divisor is a small integer, so its refined reciprocal is
+// computed once per count and the quotient takes the division's fast path (bit-identical to
+// __ddiv_rn whenever its range test passes; the rare rest, e.g. acc == 0, redone exactly)
+__device__ __forceinline__ double div_count(double acc, double m, double r2) {
+    bool ok;
+    const double q = ddiv_fast(acc, m, r2, ok);
+    return ok ? q : ddiv(acc, m);
+}
+
+// box_mean's running sum (flow.hpp:171-195) along a line of n values, as the reference orders
+// it: position 0 adds v[0..min(R, n-1)]; each later x adds v[x+R] (while x + R < n), then
+// subtracts v[x-R-1] (once x - R > 0); the mean divides by the clipped window's count.
+struct BoxWalk {
+    int n, R;
+    double r_int;  // reciprocal of the interior count 2R+1
+    __device__ __forceinline__ int count(int x) const {
+        const int lo = x - R > 0 ? x - R : 0, hi = x + R < n - 1 ? x + R : n - 1;
+        return hi - lo + 1;
+    }
+    __device__ __forceinline__ double mean(double acc, int x) const {
+        const int c = count(x);
+        return div_count(acc, (double)c, c == 2 * R + 1 ? r_int : drcp_refined((double)c));
+    }
+};
+
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// box_mean's row pass, coalesced: a CTA takes RB rows of one (pair, plane) and walks them in
+// chunks of CW columns, each staged with its CH-column history on either side (R < CH) into a
+// shared tile by cp.async (every load of the chunk in flight at once; small tiles keep many CTAs
+// per SM, which is what hides the latency).  One thread per row runs the sequential running sum;
+// its CW means go back through the tile and out as whole row segments.
+#ifndef FROI_K64_RB
+#define FROI_K64_RB 32
+#endif
+#ifndef FROI_K64_CMINB
+#define FROI_K64_CMINB 5
+#endif
+constexpr int RB = FROI_K64_RB, CW = 32, CH = 8, SW = CW + 2 * CH, TWC = SW + 1;  // TWC: odd row stride
+
+__global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const double* __restrict__ in,
+                                                   double* __restrict__ out) {
+    extern __shared__ double sm[];  // two tiles [RB][TWC]
     const int w = g.lw[l], h = g.lh[l];
-    const long long k = (long long)blockIdx.x * kNT + threadIdx.x;
-    if (k >= (long long)n_pairs * 5 * h) return;
-    const long long pl = k / h;  // pair * 5 + plane
-    const int y = (int)(k - pl * h);
+    const int y0 = blockIdx.x * RB, pl = blockIdx.y, p = blockIdx.z;
     const size_t n0 = (size_t)g.W * g.H;
-    const double* row = in + (size_t)pl * n0 + (size_t)y * w;
-    double* o = out + (size_t)pl * n0 + (size_t)y * w;
+    const double* src = in + ((size_t)p * 5 + pl) * n0 + (size_t)y0 * w;
+    double* dst = out + ((size_t)p * 5 + pl) * n0 + (size_t)y0 * w;
+    const int rows = min(RB, h - y0);
+    const int r = threadIdx.x;
+    const BoxWalk bw{w, R, drcp_refined((double)(2 * R + 1))};
+    auto stage = [&](int c0, double* tile) {
+        for (int k = threadIdx.x; k < rows * SW; k += RB) {
+            const int rr = k / SW, j = k - rr * SW;
+            const int x = c0 - CH + j;
+            if (x >= 0 && x < w) cp_async8(tile + rr * TWC + j, src + (size_t)rr * w + x);
+        }
+        cp_async_commit();
+    };
     double acc = 0.0;
-    int lo = 0, hi = -1;
-    for (int x = 0; x < w; ++x) {
-        const int nlo = x - R > 0 ? x - R : 0;
-        const int nhi = x + R < w - 1 ? x + R : w - 1;
-        while (hi < nhi) acc = dadd(acc, row[++hi]);
-        while (lo < nlo) acc = dsub(acc, row[lo++]);
-        o[x] = ddiv(acc, (double)(hi - lo + 1));
+    for (int c0 = 0; c0 < w; c0 += CW) {
+        double* tile = sm;
+        stage(c0, tile);
+        cp_async_wait<0>();
+        __syncthreads();
+        double* trow = tile + r * TWC;
+        double m[CW];
+        if (r < rows) {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) {
+                const int x = c0 + i;
+                if (x < w) {
+                    if (x == 0) {
+                        for (int t = 0; t <= R && t < w; ++t) acc = dadd(acc, trow[t + CH]);
+                    } else {
+                        if (x + R <= w - 1) acc = dadd(acc, trow[i + R + CH]);
+                        if (x - R >= 1) acc = dsub(acc, trow[i - R - 1 + CH]);
+                    }
+                    m[i] = bw.mean(acc, x);
+                }
+            }
+        }
+        __syncthreads();  // every row is done reading the staged inputs
+        if (r < rows) {
+#pragma unroll
+            for (int i = 0; i < CW; ++i) trow[i] = m[i];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < rows * CW; t += RB) {
+            const int rr = t / CW, i = t - rr * CW;
+            const int x = c0 + i;
+            if (x < w) dst[(size_t)rr * w + x] = tile[rr * TWC + i];
+        }
+        __syncthreads();  // the tile is free for the next chunk
     }
 }
 
-// box_mean's column pass: one thread per (pair, plane, column)
-__global__ void __launch_bounds__(kNT) k64_box_cols(Geom g, int l, int R, int n_pairs, const double* __restrict__ in,
-                                                    double* __restrict__ out) {
-    const int w = g.lw[l], h = g.lh[l];
-    const long long k = (long long)blockIdx.x * kNT + threadIdx.x;
-    if (k >= (long long)n_pairs * 5 * w) return;
-    const long long pl = k / w;
-    const int x = (int)(k - pl * w);
-    const size_t n0 = (size_t)g.W * g.H;
-    const double* col = in + (size_t)pl * n0 + x;
-    double* o = out + (size_t)pl * n0 + x;
-    double acc = 0.0;
-    int lo = 0, hi = -1;
-    for (int y = 0; y < h; ++y) {
-        const int nlo = y - R > 0 ? y - R : 0;
-        const int nhi = y + R < h - 1 ? y + R : h - 1;
-        while (hi < nhi) {
-            ++hi;
-            acc = dadd(acc, col[(size_t)hi * w]);
-        }
-        while (lo < nlo) {
-            acc = dsub(acc, col[(size_t)lo * w]);
-            ++lo;
-        }
-        o[(size_t)y * w] = ddiv(acc, (double)(hi - lo + 1));
-    }
-}
+// box_mean's column pass fused with the solve (flow.hpp:236-253): a CTA takes CC columns of one
+// pair, one warp per plane (lane = column) runs the column's sequential running sum over chunks
+// of CR rows, each staged with its CH-row history into a shared tile by cp.async; the five
+// planes' means meet in the tile, and all five warps then solve its pixels and write their flow.
+constexpr int CC = 32, CR = 16, TR = CR + 2 * CH;  // columns per CTA, rows per chunk, tile rows
 
-__global__ void __launch_bounds__(kNT) k64_solve(Geom g, int l, int mode, const double* __restrict__ m,
-                                                 const float2* __restrict__ flow_in, float2* __restrict__ flow_out) {
-    const int p = blockIdx.y;
+__global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geom g, int l, int R, int mode,
+                                                             const double* __restrict__ rowm,
+                                                             const float2* __restrict__ flow_in,
+                                                             float2* __restrict__ flow_out) {
+    extern __shared__ double sm[];  // two tiles [5][TR][CC]
     const int w = g.lw[l], h = g.lh[l];
-    const long long i = (long long)blockIdx.x * kNT + threadIdx.x;
-    if (i >= (long long)w * h) return;
+    const int x0 = blockIdx.x * CC, p = blockIdx.y;
+    const int q = threadIdx.x / CC, lane = threadIdx.x % CC;
     const size_t n0 = (size_t)g.W * g.H;
-    const double* q = m + (size_t)p * 5 * n0 + i;
-    const double g11 = q[0], g12 = q[n0], g22 = q[2 * n0], h1 = q[3 * n0], h2 = q[4 * n0];
-    const double det = dsub(dmul(g11, g22), dmul(g12, g12));
-    const double frob2 = dadd(dadd(dmul(g11, g11), dmul(dmul(2.0, g12), g12)), dmul(g22, g22));
-    const size_t o = (size_t)p * g.lsum + g.loff[l] + i;
-    float2 r;
-    if (!(det > dmul(1e-9, frob2))) {
-        r = mode ? flow_in[o] : make_float2(0.f, 0.f);  // keep the prior (zero on the first pass)
-    } else {
-        r.x = __double2float_rn(ddiv(dsub(dmul(g22, h1), dmul(g12, h2)), det));
-        r.y = __double2float_rn(ddiv(dadd(dmul(-g12, h1), dmul(g11, h2)), det));
+    const double* col = rowm + (size_t)p * 5 * n0 + x0;
+    const size_t fo = (size_t)p * g.lsum + g.loff[l];
+    const int cols = min(CC, w - x0);
+    const BoxWalk bw{h, R, drcp_refined((double)(2 * R + 1))};
+    auto stage = [&](int y0, double* tile) {
+        for (int k = threadIdx.x; k < 5 * TR * CC; k += 5 * CC) {
+            const int qq = k / (TR * CC), rem = k - qq * TR * CC, j = rem / CC, c = rem - j * CC;
+            const int y = y0 - CH + j;
+            if (y >= 0 && y < h && c < cols) cp_async8(tile + k, col + qq * n0 + (size_t)y * w + c);
+        }
+        cp_async_commit();
+    };
+    double acc = 0.0;
+    for (int y0 = 0; y0 < h; y0 += CR) {
+        double* tile = sm;
+        stage(y0, tile);
+        cp_async_wait<0>();
+        __syncthreads();
+        double* tq = tile + q * TR * CC + lane;
+        double m[CR];
+        if (lane < cols) {
+#pragma unroll
+            for (int i = 0; i < CR; ++i) {
+                const int y = y0 + i;
+                if (y < h) {
+                    if (y == 0) {
+                        for (int t = 0; t <= R && t < h; ++t) acc = dadd(acc, tq[(t + CH) * CC]);
+                    } else {
+                        if (y + R <= h - 1) acc = dadd(acc, tq[(i + R + CH) * CC]);
+                        if (y - R >= 1) acc = dsub(acc, tq[(i - R - 1 + CH) * CC]);
+                    }
+                    m[i] = bw.mean(acc, y);
+                }
+            }
+        }
+        __syncthreads();  // the staged inputs are consumed
+        if (lane < cols) {
+#pragma unroll
+            for (int i = 0; i < CR; ++i) tq[i * CC] = m[i];
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < CR * CC; t += 5 * CC) {
+            const int i = t / CC, c = t - i * CC;
+            const int y = y0 + i, x = x0 + c;
+            if (y >= h || c >= cols) continue;
+            const double* mm = tile + i * CC + c;
+            const double g11 = mm[0], g12 = mm[TR * CC], g22 = mm[2 * TR * CC], h1 = mm[3 * TR * CC],
+                         h2 = mm[4 * TR * CC];
+            const double det = dsub(dmul(g11, g22), dmul(g12, g12));
+            const double frob2 = dadd(dadd(dmul(g11, g11), dmul(dmul(2.0, g12), g12)), dmul(g22, g22));
+            const size_t o = fo + (size_t)y * w + x;
+            float2 rr;
+            if (!(det > dmul(1e-9, frob2))) {
+                rr = mode ? flow_in[o] : make_float2(0.f, 0.f);  // keep the prior (zero on the first pass)
+            } else {
+                const double rd = drcp_refined(det);
+                rr.x = __double2float_rn(div_count(dsub(dmul(g22, h1), dmul(g12, h2)), det, rd));
+                rr.y = __double2float_rn(div_count(dadd(dmul(-g12, h1), dmul(g11, h2)), det, rd));
+            }
+            flow_out[o] = rr;
+        }
+        __syncthreads();  // the tile is free for the next chunk
     }
-    flow_out[o] = r;
 }
 
 // coarse (level l + 1) -> fine (level l) prior, same buffer
@@ -377,7 +492,13 @@ int launch_expand_shifted64(const Geom& g, const Flow64Const& C, const Flow64Buf
 int launch_flow64(const Geom& g, const DevParams& P, const Flow64Buffers& b, const int* d_prev, const int* d_next,
                   const PairInfo* d_info, int n_pairs, cudaStream_t s, int* cur_out) {
     if (n_pairs <= 0) return 0;
+    if (P.window_radius > CH - 1) throw Error(1, "exact flow: window_size > 15 is not supported");
     const int R = P.window_radius;
+    constexpr size_t kRowSmem = sizeof(double) * RB * TWC, kColSmem = sizeof(double) * 5 * TR * CC;
+    static_assert(kRowSmem <= 227 * 1024 && kColSmem <= 227 * 1024, "box tiles");
+    // kernel attributes are per device: set on every call (one host thread may drive several)
+    FROI_CUDA(cudaFuncSetAttribute(k64_box_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
+    FROI_CUDA(cudaFuncSetAttribute(k64_box_cols_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
     float2* buf[2] = {b.flow0, b.flow1};
     int cur = 0, launches = 0;
     for (int l = g.L - 1; l >= 0; --l) {
@@ -392,13 +513,12 @@ int launch_flow64(const Geom& g, const DevParams& P, const Flow64Buffers& b, con
             k64_products<<<dim3(blocks(n), n_pairs), kNT, 0, s>>>(g, l, mode, b.ex_f, b.ex_p, d_prev, d_next, d_info,
                                                                  buf[cur], b.prod);
             FROI_LAUNCH_CHECK();
-            k64_box_rows<<<blocks((long long)n_pairs * 5 * g.lh[l]), kNT, 0, s>>>(g, l, R, n_pairs, b.prod, b.rowm);
+            k64_box_rows<<<dim3(cdiv(g.lh[l], RB), 5, n_pairs), RB, kRowSmem, s>>>(g, l, R, b.prod, b.rowm);
             FROI_LAUNCH_CHECK();
-            k64_box_cols<<<blocks((long long)n_pairs * 5 * g.lw[l]), kNT, 0, s>>>(g, l, R, n_pairs, b.rowm, b.prod);
+            k64_box_cols_solve<<<dim3(cdiv(g.lw[l], CC), n_pairs), 5 * CC, kColSmem, s>>>(g, l, R, mode, b.rowm,
+                                                                                         buf[cur], buf[1 - cur]);
             FROI_LAUNCH_CHECK();
-            k64_solve<<<dim3(blocks(n), n_pairs), kNT, 0, s>>>(g, l, mode, b.prod, buf[cur], buf[1 - cur]);
-            FROI_LAUNCH_CHECK();
-            launches += 4;
+            launches += 3;
             cur = 1 - cur;
         }
     }

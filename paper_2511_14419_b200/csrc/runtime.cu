@@ -868,9 +868,9 @@ void run_batch(froi_ctx* c, froi_ctx* owner, const std::vector<PairJob>& jobs, s
     K.batches += 1;
     // launches: denoise (one per ingest run), fft 2, expand (1 + 2(L-1)) x2, register 3,
     // flow L*iters + (L-1) upsamplings (+ the mask stage's own count)
-    // (bit-exact flow: expand (1 + 2(L-1) + L) x2, flow 4 L iters + (L-1))
+    // (bit-exact flow: expand (1 + 2(L-1) + L) x2, flow 3 L iters + (L-1))
     if (c->flow_exact)
-        owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1) + g.L) + 3 + 4 * (uint64_t)g.L * c->dp.iterations +
+        owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1) + g.L) + 3 + 3 * (uint64_t)g.L * c->dp.iterations +
                            (g.L - 1);
     else
         owner->launches += n_denoise + 2 + 2 * (1 + 2 * (g.L - 1)) + 3 + (uint64_t)g.L * c->dp.iterations + (g.L - 1);
