@@ -460,6 +460,35 @@ def run_ours(args) -> None:
         ref_pixels = int(np.unpackbits(hmask.numpy()).sum()) if e2e else None
         dropin = run_dropin(last, min(args.steps, 5), 2, ref_pixels)
 
+    # ---- the bit-exact flow mode (froi_ctx_set_flow_exact): same device-resident workload, a few
+    # steps; its masks are the reference's byte for byte, so their difference from the fp32 masks
+    # of the same well is the default path's end-to-end mismatch rate
+    exact = None
+    if not args.no_exact:
+        ref_fast = dmask.clone()  # fp32-flow masks of the last timed well
+        last_slot = step_slot[nsteps - 1]
+        ctx.set_flow_exact(True)
+        xsteps = min(2, args.steps)
+        ctx.extract_wells_device(dev[last_slot].data_ptr(), 1, F, dmask.data_ptr())  # warm-up
+        barrier(dist)
+        torch.cuda.synchronize()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for i in range(xsteps):
+            ctx.extract_wells_device(dev[last_slot].data_ptr(), 1, F, dmask.data_ptr())
+        x1.record(stream)
+        torch.cuda.synchronize()
+        xms = reduce_max(dist, x0.elapsed_time(x1), device)
+        diff = torch.bitwise_xor(ref_fast, dmask)
+        popc = torch.tensor([bin(i).count("1") for i in range(256)], dtype=torch.int64, device=device)
+        nd = int(popc[diff.long()].sum().item())
+        ctx.set_flow_exact(False)
+        exact = {"value": world * xsteps * F / (xms / 1000.0), "unit": UNIT, "steps": xsteps,
+                 "ms_per_step": xms / xsteps, "dtype": "f64 flow (bit-exact with the reference)",
+                 "fast_path_mask_mismatch": nd / float(F * px),
+                 "note": "device-resident, 2 lanes; fp32-path masks of the same well differ from "
+                         "these (= the reference's) in fast_path_mask_mismatch of the pixels"}
+
     # ---- roofline of the fused flow kernel + pipeline figure
     pk = peaks()
     mb = model_bytes_per_pair(W, H, 1, cfg.params.flow.pyramid_levels)
@@ -533,6 +562,7 @@ def run_ours(args) -> None:
             "cpu_baseline": cpu,
             "e2e": e2e,
             "dropin_e2e": dropin,
+            "exact_flow": exact,
             "gpu_launches": launches,
             "clocks": clk,
         }
@@ -554,6 +584,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-dropin", action="store_true")
+    ap.add_argument("--no-exact", action="store_true", help="skip the bit-exact flow leg")
     ap.add_argument("--selftest", action="store_true",
                     help="CPU/gloo self-test of the multi-rank launcher (no GPU work)")
     ap.add_argument("--ncu-traffic", type=float, default=None,

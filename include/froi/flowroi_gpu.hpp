@@ -67,17 +67,25 @@ struct CtxDeleter {
     void operator()(froi_ctx* c) const { froi_ctx_destroy(c); }
 };
 
+inline bool& exact_flag() {
+    thread_local bool on = false;
+    return on;
+}
+
 // Thread-affine context cache (froi contexts are not internally locked).
 inline froi_ctx* context(int device, const froi_params& p, int w, int h, int depth) {
     thread_local std::map<std::string, std::unique_ptr<froi_ctx, CtxDeleter>> cache;
+    const bool exact = exact_flag();
     std::string key(reinterpret_cast<const char*>(&p), sizeof(p));
     key += std::to_string(device) + ":" + std::to_string(w) + "x" + std::to_string(h) + ":" +
-           std::to_string(depth);
+           std::to_string(depth) + (exact ? ":exact" : "");
     auto it = cache.find(key);
     if (it != cache.end()) return it->second.get();
     froi_ctx* c = nullptr;
     check(froi_ctx_create(device, &p, w, h, depth, 0, &c), "froi_ctx_create");
-    cache.emplace(key, std::unique_ptr<froi_ctx, CtxDeleter>(c));
+    std::unique_ptr<froi_ctx, CtxDeleter> owned(c);
+    if (exact) check(froi_ctx_set_flow_exact(c, 1), "froi_ctx_set_flow_exact");
+    cache.emplace(key, std::move(owned));
     return c;
 }
 
@@ -98,6 +106,11 @@ inline std::vector<flowroi::RoiMask> make_masks(std::size_t n, int w, int h) {
 }
 
 }  // namespace detail
+
+// Opt in (for calls made from this thread) to the bit-exact fp64 flow (froi_ctx_set_flow_exact):
+// flows and masks byte-identical to the reference's instead of within the fp32 flow tolerance,
+// at about a third of the throughput.  Off by default.
+inline void set_exact_flow(bool on) { detail::exact_flag() = on; }
 
 // flowroi::extract_roi on the GPU.  `workers` keeps the reference signature: outputs never
 // depend on it (parallel.hpp:17-19); a single sequence runs on one device (device 0).

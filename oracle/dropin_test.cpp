@@ -23,7 +23,8 @@
 using namespace flowroi;
 
 static int run_case(const char* name, int cells, int frames, int size, int depth, std::uint64_t seed,
-                    const ExtractParams& params) {
+                    const ExtractParams& params, bool exact = false) {
+    flowroi_gpu::set_exact_flow(exact);
     SyntheticSpec spec;
     spec.n_cells = cells;
     spec.n_frames = frames;
@@ -57,6 +58,9 @@ static int run_case(const char* name, int cells, int frames, int size, int depth
                 name, seq.size(), size, depth, double(mism) / double(total), frames_equal, shifts_equal,
                 bytes_equal, enc_bytes, (unsigned long long)tg.flow_ns.load(),
                 (unsigned long long)tc.flow_ns.load());
+    flowroi_gpu::set_exact_flow(false);
+    // the bit-exact flow mode must reproduce the reference byte for byte, encoder output included
+    if (exact) return (mism == 0 && shifts_equal == seq.size() && bytes_equal == seq.size()) ? 0 : 1;
     return (shifts_equal == seq.size() && double(mism) / double(total) <= 1e-4) ? 0 : 1;
 }
 
@@ -110,6 +114,10 @@ int main() {
     q.roi.adjacent_factor = 1;
     q.roi.roi_threshold = 0.1;
     bad += run_case("ensemble-k1", 4, 5, 128, 8, 5, q);
+    // the same cases through the bit-exact flow mode (flowroi_gpu::set_exact_flow)
+    bad += run_case("exact-synthetic-160", 5, 6, 160, 8, 77, p, true);
+    bad += run_case("exact-synthetic-256-16bit", 8, 4, 256, 16, 12, p, true);
+    bad += run_case("exact-ensemble-k1", 4, 5, 128, 8, 5, q, true);
     // error taxonomy: usage_error / data_error cross the boundary as the same exception types
     int errors_ok = 0;
     try {

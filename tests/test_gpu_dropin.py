@@ -21,12 +21,15 @@ def test_dropin_against_reference_and_encoder():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     cases = [c for c in lines if "case" in c]
-    assert len(cases) == 3
+    assert len(cases) == 6
     for c in cases:
         assert c["shifts_identical"] == c["frames"]
         assert c["mask_mismatch"] <= 1e-4
         # wherever the masks agree, the reference encoder produces identical files
         assert c["encoded_identical"] >= c["frames_identical"]
+        if c["case"].startswith("exact-"):  # bit-exact flow: every mask and every file identical
+            assert c["mask_mismatch"] == 0.0 and c["frames_identical"] == c["frames"]
+            assert c["encoded_identical"] == c["frames"]
     assert lines[-1]["errors_mapped"] == 2
     # compress_sequence with the pipelined GPU stage, when built with json
     for c in [c for c in lines if "pipeline_case" in c]:
