@@ -56,6 +56,7 @@ struct Bl {
         i01 = y0 * w + x1;
         i10 = y1 * w + x0;
         i11 = y1 * w + x1;
+        FROI_DCHECK(x0 >= 0 && y0 >= 0 && i11 < w * h && i00 <= i11);
     }
     __device__ __forceinline__ double at(const double* p) const {
         const double top = dadd(dmul(p[i00], ofx), dmul(p[i01], fx));
@@ -289,6 +290,7 @@ __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const d
     double* dst = out + ((size_t)p * 5 + pl) * n0 + (size_t)y0 * w;
     const int rows = min(RB, h - y0);
     const int r = threadIdx.x;
+    FROI_DCHECK(R < CH && rows > 0);
     const BoxWalk bw{w, R, drcp_refined((double)(2 * R + 1))};
     auto stage = [&](int c0, double* tile) {
         for (int k = threadIdx.x; k < rows * SW; k += RB) {
@@ -354,6 +356,7 @@ __global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geo
     const double* col = rowm + (size_t)p * 5 * n0 + x0;
     const size_t fo = (size_t)p * g.lsum + g.loff[l];
     const int cols = min(CC, w - x0);
+    FROI_DCHECK(R < CH && cols > 0);
     const BoxWalk bw{h, R, drcp_refined((double)(2 * R + 1))};
     auto stage = [&](int y0, double* tile) {
         for (int k = threadIdx.x; k < 5 * TR * CC; k += 5 * CC) {

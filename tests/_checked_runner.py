@@ -5,7 +5,7 @@
 Cases: C1 (512^2, one pair); a two-well 256^2 sequence of 13 frames on two lanes with 4-pair
 batches (multi-batch, lane alternation, egress ring); the same through the host entry with pinned
 PBM output; a 12-bit 256^2 sequence; and a low-threshold case that exercises partial tie
-admission and the CCL area filter.
+admission and the CCL area filter; C1 and the two wells through the bit-exact flow mode.
 """
 import os
 import sys
@@ -41,6 +41,13 @@ def main(out):
     p.roi.roi_threshold = 0.05
     p.roi.min_area = 40
     res["lowthr"] = F.extract_roi(frames[0, :4], p)
+    # the bit-exact flow mode: C1, and the two wells multi-batch on two lanes
+    res["c1_exact"] = F.extract_roi(synth.well_frames(cfg, 0, 2), cfg.params, exact_flow=True)
+    ctx = F.Context(256, 256, 8, c2.params, device=0, max_pairs=3)
+    ctx.set_flow_exact(True)
+    m, _ = ctx.extract_wells(frames, layout="pbm")
+    res["exact_wells_mp3"] = m
+    ctx.close()
     np.savez_compressed(out, **res)
 
 
