@@ -11,7 +11,8 @@ pinned CPU oracle (VERDICT r1 "Next round" #1).
 * C2: the full 64-frame sequence.  C4: one 2048^2 12-bit well of 8 frames (L = 5).
 * Shifts and confidences bit-identical on every pair; the mask stage bit-exact given the GPU's
   own flow on sampled pairs (batch boundaries included); flow within max |d| <= 2e-2 px and mean
-  EPE <= 1e-3 px on those pairs; end-to-end mask mismatch <= 1e-4 per frame.  The per-config
+  EPE <= 1e-3 px on those pairs; end-to-end mask mismatch <= 1e-4 per frame; and through the
+  bit-exact flow mode every mask of the sequence identical to the oracle's.  The per-config
   mismatch rates are printed (pytest -s) and recorded in DESIGN.md §5.
 """
 import ctypes
@@ -131,7 +132,23 @@ def check_full(gpu, oracle, frames, depth, params, label, sample_pairs, max_pair
     for t, (mx, mean) in flow_err.items():
         assert mx <= flow_max and mean <= FLOW_MEAN_EPE, (label, t, mx, mean)
     assert mism.max() <= MASK_MISMATCH_MAX, (label, mism.max(), int(mism.argmax()))
+    # the bit-exact flow mode on the same sequence and batch geometry: every mask identical
+    exact = _exact_masks(gpu, frames, depth, params, max_pairs)
+    bad = [t for t in range(n) if not np.array_equal(exact[t], want[t])]
+    print(f"{label}: bit-exact flow mode, frames differing from the oracle: {len(bad)}/{n}")
+    assert not bad, (label, bad[:10])
     return mism
+
+
+def _exact_masks(gpu, frames, depth, params, max_pairs=0):
+    n, h, w = frames.shape
+    ctx = gpu.Context(w, h, depth, params, device=0, max_pairs=max_pairs)
+    try:
+        ctx.set_flow_exact(True)
+        m, _ = ctx.extract_wells(frames[None], layout="bytes")
+    finally:
+        ctx.close()
+    return m[0]
 
 
 @pytest.fixture(scope="module")
