@@ -463,32 +463,9 @@ int column_lcb(const Geom& g) {
 
 }  // namespace
 
-void launch_fft_forward_group(const Geom& g, const void* d_den, const unsigned long long* d_sums,
-                              const double* d_wx, const double* d_wy, const double2* d_tw_row,
-                              const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s);
-
-// Frames in groups whose spectra stay L2-resident between the row and the column pass (the
-// column pass then reads them from L2 and overwrites them in place before they are written back):
-// FROI_FFT_GROUP frames per group, 0 = one group (experiment switch).
 void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long long* d_sums,
                         const double* d_wx, const double* d_wy, const double2* d_tw_row,
                         const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s) {
-    static const int group = [] {
-        const char* e = getenv("FROI_FFT_GROUP");
-        return e ? atoi(e) : 0;
-    }();
-    const int G = group > 0 ? group : n_slots;
-    const size_t fb = (size_t)g.W * g.H * g.sample_bytes;
-    for (int f0 = 0; f0 < n_slots; f0 += G) {
-        const int nf = std::min(G, n_slots - f0);
-        launch_fft_forward_group(g, (const uint8_t*)d_den + fb * f0, d_sums + f0, d_wx, d_wy, d_tw_row, d_tw_col,
-                                 d_spec + (size_t)g.pw * g.ph * f0, nf, s);
-    }
-}
-
-void launch_fft_forward_group(const Geom& g, const void* d_den, const unsigned long long* d_sums,
-                              const double* d_wx, const double* d_wy, const double2* d_tw_row,
-                              const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s) {
     if (n_slots <= 0) return;
     const int lr = rows_lc(g.log2pw);
     const size_t smem_r = sizeof(double2) * (((size_t)padded(g.pw) << lr) + g.pw);
