@@ -253,7 +253,7 @@ struct BoxWalk {
     }
     __device__ __forceinline__ double mean(double acc, int x) const {
         const int c = count(x);
-        return div_count(acc, (double)c, c == 2 * R + 1 ? r_int : drcp_refined((double)c));
+        return c == 2 * R + 1 ? div_count(acc, (double)c, r_int) : ddiv(acc, (double)c);
     }
 };
 
@@ -270,8 +270,9 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // box_mean's row pass, coalesced: a CTA takes RB rows of one (pair, plane) and walks them in
 // chunks of CW columns, each staged with its CH-column history on either side (R < CH) into a
 // shared tile by cp.async (every load of the chunk in flight at once; small tiles keep many CTAs
-// per SM, which is what hides the latency).  One thread per row runs the sequential running sum;
-// its CW means go back through the tile and out as whole row segments.
+// per SM, which is what hides the latency).  One thread per row runs the sequential running sum,
+// writing each mean in place over the input it no longer needs; the CW means then leave as whole
+// row segments.
 #ifndef FROI_K64_RB
 #define FROI_K64_RB 32
 #endif
@@ -292,11 +293,17 @@ __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const d
     const int r = threadIdx.x;
     FROI_DCHECK(R < CH && rows > 0);
     const BoxWalk bw{w, R, drcp_refined((double)(2 * R + 1))};
+    static_assert(RB % 32 == 0 && SW <= 64 && CW == 32, "staging: a warp covers a tile row in two steps");
+    const int lane = threadIdx.x & 31, wrp = threadIdx.x >> 5;
+    // a warp stages whole tile rows (lane = column, then lane + 32): no index division per element
     auto stage = [&](int c0, double* tile) {
-        for (int k = threadIdx.x; k < rows * SW; k += RB) {
-            const int rr = k / SW, j = k - rr * SW;
-            const int x = c0 - CH + j;
-            if (x >= 0 && x < w) cp_async8(tile + rr * TWC + j, src + (size_t)rr * w + x);
+        const int xa = c0 - CH + lane, xb = xa + 32;
+        const bool oka = xa >= 0 && xa < w, okb = lane + 32 < SW && xb < w;
+        const double* s = src + (size_t)wrp * w;
+        double* d = tile + wrp * TWC + lane;
+        for (int rr = wrp; rr < rows; rr += RB / 32, s += (size_t)(RB / 32) * w, d += (RB / 32) * TWC) {
+            if (oka) cp_async8(d, s + xa);
+            if (okb) cp_async8(d + 32, s + xb);
         }
         cp_async_commit();
     };
@@ -307,9 +314,10 @@ __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const d
         cp_async_wait<0>();
         __syncthreads();
         double* trow = tile + r * TWC;
-        double m[CW];
+        // in place: after step i, tile column i (x - CH) is never read again (its subtraction,
+        // if any, was at step i - CH + R + 1 <= i), so the mean of x goes there
         if (r < rows) {
-#pragma unroll
+#pragma unroll 4
             for (int i = 0; i < CW; ++i) {
                 const int x = c0 + i;
                 if (x < w) {
@@ -319,21 +327,13 @@ __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const d
                         if (x + R <= w - 1) acc = dadd(acc, trow[i + R + CH]);
                         if (x - R >= 1) acc = dsub(acc, trow[i - R - 1 + CH]);
                     }
-                    m[i] = bw.mean(acc, x);
+                    trow[i] = bw.mean(acc, x);
                 }
             }
         }
-        __syncthreads();  // every row is done reading the staged inputs
-        if (r < rows) {
-#pragma unroll
-            for (int i = 0; i < CW; ++i) trow[i] = m[i];
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < rows * CW; t += RB) {
-            const int rr = t / CW, i = t - rr * CW;
-            const int x = c0 + i;
-            if (x < w) dst[(size_t)rr * w + x] = tile[rr * TWC + i];
-        }
+        __syncthreads();  // every row's means are in place
+        if (c0 + lane < w)
+            for (int rr = wrp; rr < rows; rr += RB / 32) dst[(size_t)rr * w + c0 + lane] = tile[rr * TWC + lane];
         __syncthreads();  // the tile is free for the next chunk
     }
 }
@@ -358,11 +358,13 @@ __global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geo
     const int cols = min(CC, w - x0);
     FROI_DCHECK(R < CH && cols > 0);
     const BoxWalk bw{h, R, drcp_refined((double)(2 * R + 1))};
+    // warp q stages plane q's tile rows (lane = column): no index division per element
     auto stage = [&](int y0, double* tile) {
-        for (int k = threadIdx.x; k < 5 * TR * CC; k += 5 * CC) {
-            const int qq = k / (TR * CC), rem = k - qq * TR * CC, j = rem / CC, c = rem - j * CC;
-            const int y = y0 - CH + j;
-            if (y >= 0 && y < h && c < cols) cp_async8(tile + k, col + qq * n0 + (size_t)y * w + c);
+        if (lane < cols) {
+            const double* s = col + q * n0 + lane;
+            double* d = tile + q * TR * CC + lane;
+            const int jb = max(0, CH - y0), je = min(TR, h - y0 + CH);
+            for (int j = jb; j < je; ++j) cp_async8(d + j * CC, s + (size_t)(y0 - CH + j) * w);
         }
         cp_async_commit();
     };
@@ -373,9 +375,9 @@ __global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geo
         cp_async_wait<0>();
         __syncthreads();
         double* tq = tile + q * TR * CC + lane;
-        double m[CR];
+        // in place, as in k64_box_rows: the mean of row y0 + i goes to tile row i after step i
         if (lane < cols) {
-#pragma unroll
+#pragma unroll 4
             for (int i = 0; i < CR; ++i) {
                 const int y = y0 + i;
                 if (y < h) {
@@ -385,19 +387,13 @@ __global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geo
                         if (y + R <= h - 1) acc = dadd(acc, tq[(i + R + CH) * CC]);
                         if (y - R >= 1) acc = dsub(acc, tq[(i - R - 1 + CH) * CC]);
                     }
-                    m[i] = bw.mean(acc, y);
+                    tq[i * CC] = bw.mean(acc, y);
                 }
             }
         }
-        __syncthreads();  // the staged inputs are consumed
-        if (lane < cols) {
-#pragma unroll
-            for (int i = 0; i < CR; ++i) tq[i * CC] = m[i];
-        }
-        __syncthreads();
-        for (int t = threadIdx.x; t < CR * CC; t += 5 * CC) {
-            const int i = t / CC, c = t - i * CC;
-            const int y = y0 + i, x = x0 + c;
+        __syncthreads();  // the chunk's five planes of means are in place
+        for (int i = q; i < CR; i += 5) {  // warp = row of the chunk, lane = column
+            const int c = lane, y = y0 + i, x = x0 + c;
             if (y >= h || c >= cols) continue;
             const double* mm = tile + i * CC + c;
             const double g11 = mm[0], g12 = mm[TR * CC], g22 = mm[2 * TR * CC], h1 = mm[3 * TR * CC],
@@ -443,6 +439,18 @@ __global__ void __launch_bounds__(kNT) k64_upsample(Geom g, int l, float2* __res
 }
 
 inline unsigned blocks(long long n) { return (unsigned)cdiv<long long>(n, kNT); }
+
+constexpr size_t kRowSmem = sizeof(double) * RB * TWC, kColSmem = sizeof(double) * 5 * TR * CC;
+static_assert(kRowSmem <= 48 * 1024 && kColSmem <= 48 * 1024, "box tiles fit the default shared memory");
+
+// box_mean's two passes, the column pass fused with the solve
+void box_pass(int R, const Geom& g, int l, int mode, int n_pairs, const Flow64Buffers& b, const float2* fin,
+              float2* fout, cudaStream_t s) {
+    k64_box_rows<<<dim3(cdiv(g.lh[l], RB), 5, n_pairs), RB, kRowSmem, s>>>(g, l, R, b.prod, b.rowm);
+    FROI_LAUNCH_CHECK();
+    k64_box_cols_solve<<<dim3(cdiv(g.lw[l], CC), n_pairs), 5 * CC, kColSmem, s>>>(g, l, R, mode, b.rowm, fin, fout);
+    FROI_LAUNCH_CHECK();
+}
 
 // pyramid levels >= 1 and the expansions of every level, for frame slots (info == nullptr) or
 // the shifted pair slots
@@ -497,11 +505,6 @@ int launch_flow64(const Geom& g, const DevParams& P, const Flow64Buffers& b, con
     if (n_pairs <= 0) return 0;
     if (P.window_radius > CH - 1) throw Error(1, "exact flow: window_size > 15 is not supported");
     const int R = P.window_radius;
-    constexpr size_t kRowSmem = sizeof(double) * RB * TWC, kColSmem = sizeof(double) * 5 * TR * CC;
-    static_assert(kRowSmem <= 227 * 1024 && kColSmem <= 227 * 1024, "box tiles");
-    // kernel attributes are per device: set on every call (one host thread may drive several)
-    FROI_CUDA(cudaFuncSetAttribute(k64_box_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kRowSmem));
-    FROI_CUDA(cudaFuncSetAttribute(k64_box_cols_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kColSmem));
     float2* buf[2] = {b.flow0, b.flow1};
     int cur = 0, launches = 0;
     for (int l = g.L - 1; l >= 0; --l) {
@@ -516,11 +519,7 @@ int launch_flow64(const Geom& g, const DevParams& P, const Flow64Buffers& b, con
             k64_products<<<dim3(blocks(n), n_pairs), kNT, 0, s>>>(g, l, mode, b.ex_f, b.ex_p, d_prev, d_next, d_info,
                                                                  buf[cur], b.prod);
             FROI_LAUNCH_CHECK();
-            k64_box_rows<<<dim3(cdiv(g.lh[l], RB), 5, n_pairs), RB, kRowSmem, s>>>(g, l, R, b.prod, b.rowm);
-            FROI_LAUNCH_CHECK();
-            k64_box_cols_solve<<<dim3(cdiv(g.lw[l], CC), n_pairs), 5 * CC, kColSmem, s>>>(g, l, R, mode, b.rowm,
-                                                                                         buf[cur], buf[1 - cur]);
-            FROI_LAUNCH_CHECK();
+            box_pass(R, g, l, mode, n_pairs, b, buf[cur], buf[1 - cur], s);
             launches += 3;
             cur = 1 - cur;
         }
