@@ -133,3 +133,27 @@ def test_exact_batches_and_lanes(gpu, oracle):
         finally:
             ctx.close()
     assert np.array_equal(outs[0], want) and np.array_equal(outs[1], want)
+
+
+def test_exact_streaming_push(gpu, oracle):
+    """Live acquisition (froi_stream_push) in the exact mode: pushes of 3, 1 and 2 frames give the
+    oracle's masks for the whole sequence, frame-0 rule included."""
+    from paper_2511_14419_b200 import _native
+    from paper_2511_14419_b200.params import ExtractParams
+    f = textured_frame(96, 96, 8, 8)
+    frames = np.stack([cyclic_shift(f, t, -t) for t in range(6)]).astype(np.uint8)
+    want, _, _ = oracle.extract_roi(frames, 8, ExtractParams())
+    ctx = gpu.Context(96, 96, 8)
+    try:
+        ctx.set_flow_exact(True)
+        _native.check(_native.lib.froi_stream_reset(ctx.handle, 1))
+        got = []
+        for chunk in (frames[0:3], frames[3:4], frames[4:6]):
+            c = np.ascontiguousarray(chunk)
+            out = np.empty((len(c), 96, 96), np.uint8)
+            _native.check(_native.lib.froi_stream_push(ctx.handle, c.ctypes.data, 0, 1, 96 * 96, len(c),
+                                                       0, out.ctypes.data, 0, None))
+            got.append(out)
+    finally:
+        ctx.close()
+    assert np.array_equal(np.concatenate(got), want)
