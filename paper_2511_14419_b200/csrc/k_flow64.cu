@@ -279,7 +279,12 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 #ifndef FROI_K64_CMINB
 #define FROI_K64_CMINB 5
 #endif
+#ifndef FROI_K64_SB
+#define FROI_K64_SB 8
+#endif
 constexpr int RB = FROI_K64_RB, CW = 32, CH = 8, SW = CW + 2 * CH, TWC = SW + 1;  // TWC: odd row stride
+constexpr int SB = FROI_K64_SB;  // walk steps whose inputs are loaded together
+static_assert(CW % SB == 0 && 16 % SB == 0, "walk blocks");
 
 __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const double* __restrict__ in,
                                                    double* __restrict__ out) {
@@ -316,18 +321,45 @@ __global__ void __launch_bounds__(RB) k64_box_rows(Geom g, int l, int R, const d
         double* trow = tile + r * TWC;
         // in place: after step i, tile column i (x - CH) is never read again (its subtraction,
         // if any, was at step i - CH + R + 1 <= i), so the mean of x goes there
-        if (r < rows) {
-#pragma unroll 4
-            for (int i = 0; i < CW; ++i) {
-                const int x = c0 + i;
-                if (x < w) {
-                    if (x == 0) {
-                        for (int t = 0; t <= R && t < w; ++t) acc = dadd(acc, trow[t + CH]);
-                    } else {
-                        if (x + R <= w - 1) acc = dadd(acc, trow[i + R + CH]);
-                        if (x - R >= 1) acc = dsub(acc, trow[i - R - 1 + CH]);
+        // SB steps at a time: their 2 SB inputs are read before any of their means is written
+        // (the compiler cannot prove the in-place writes never alias the reads), so one shared-
+        // memory latency is paid per SB steps instead of per step
+        if (r < rows && c0 >= R + 1 && c0 + CW + R <= w) {
+            // interior chunk: every step adds and subtracts, and the window holds 2R+1 values
+            const double m = (double)(2 * R + 1);
+            for (int i0 = 0; i0 < CW; i0 += SB) {
+                double va[SB], vs[SB];
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    va[k] = trow[i0 + k + R + CH];
+                    vs[k] = trow[i0 + k - R - 1 + CH];
+                }
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    acc = dsub(dadd(acc, va[k]), vs[k]);
+                    trow[i0 + k] = div_count(acc, m, bw.r_int);
+                }
+            }
+        } else if (r < rows) {
+            for (int i0 = 0; i0 < CW; i0 += SB) {
+                double va[SB], vs[SB];
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    va[k] = trow[i0 + k + R + CH];
+                    vs[k] = trow[i0 + k - R - 1 + CH];
+                }
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    const int i = i0 + k, x = c0 + i;
+                    if (x < w) {
+                        if (x == 0) {
+                            for (int t = 0; t <= R && t < w; ++t) acc = dadd(acc, trow[t + CH]);
+                        } else {
+                            if (x + R <= w - 1) acc = dadd(acc, va[k]);
+                            if (x - R >= 1) acc = dsub(acc, vs[k]);
+                        }
+                        trow[i] = bw.mean(acc, x);
                     }
-                    trow[i] = bw.mean(acc, x);
                 }
             }
         }
@@ -376,18 +408,41 @@ __global__ void __launch_bounds__(5 * CC, FROI_K64_CMINB) k64_box_cols_solve(Geo
         __syncthreads();
         double* tq = tile + q * TR * CC + lane;
         // in place, as in k64_box_rows: the mean of row y0 + i goes to tile row i after step i
-        if (lane < cols) {
-#pragma unroll 4
-            for (int i = 0; i < CR; ++i) {
-                const int y = y0 + i;
-                if (y < h) {
-                    if (y == 0) {
-                        for (int t = 0; t <= R && t < h; ++t) acc = dadd(acc, tq[(t + CH) * CC]);
-                    } else {
-                        if (y + R <= h - 1) acc = dadd(acc, tq[(i + R + CH) * CC]);
-                        if (y - R >= 1) acc = dsub(acc, tq[(i - R - 1 + CH) * CC]);
+        if (lane < cols && y0 >= R + 1 && y0 + CR + R <= h) {  // interior chunk, as in k64_box_rows
+            const double m = (double)(2 * R + 1);
+            for (int i0 = 0; i0 < CR; i0 += SB) {
+                double va[SB], vs[SB];
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    va[k] = tq[(i0 + k + R + CH) * CC];
+                    vs[k] = tq[(i0 + k - R - 1 + CH) * CC];
+                }
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    acc = dsub(dadd(acc, va[k]), vs[k]);
+                    tq[(i0 + k) * CC] = div_count(acc, m, bw.r_int);
+                }
+            }
+        } else if (lane < cols) {
+            for (int i0 = 0; i0 < CR; i0 += SB) {  // SB steps' inputs first, as in k64_box_rows
+                double va[SB], vs[SB];
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    va[k] = tq[(i0 + k + R + CH) * CC];
+                    vs[k] = tq[(i0 + k - R - 1 + CH) * CC];
+                }
+#pragma unroll
+                for (int k = 0; k < SB; ++k) {
+                    const int i = i0 + k, y = y0 + i;
+                    if (y < h) {
+                        if (y == 0) {
+                            for (int t = 0; t <= R && t < h; ++t) acc = dadd(acc, tq[(t + CH) * CC]);
+                        } else {
+                            if (y + R <= h - 1) acc = dadd(acc, va[k]);
+                            if (y - R >= 1) acc = dsub(acc, vs[k]);
+                        }
+                        tq[i * CC] = bw.mean(acc, y);
                     }
-                    tq[i * CC] = bw.mean(acc, y);
                 }
             }
         }
