@@ -2,7 +2,7 @@
 pinned CPU oracle (VERDICT r1 "Next round" #1).
 
 * C3: one whole 450-frame 1024^2 well (449 pairs = 8 batches of Pcap 64 on two execution lanes,
-  nr = 8 flow strips at level 0 — the bench's configuration) through
+  16-tile flow strips at level 0 — the bench's configuration) through
     - ``froi_extract_wells_device`` (the bench's device-resident ``value`` leg),
     - ``froi_extract_wells`` from pinned frames into pinned PBM rows (the bench's ``e2e`` leg),
     - ``froi_extract_wells`` from pageable frames into RoiMask bytes (staging + courier path),
