@@ -197,6 +197,30 @@ __global__ void __launch_bounds__(kNT) k64_polyexp(Geom g, Flow64Const C, int l,
 }
 
 // ------------------------------------------------------------------ flow step
+// flow_step's five normal-equation terms g11, g12, g22, gh1, gh2 at pixel (x, y) of level l:
+// pe / ne are the previous / next frame's expansion planes at the level, (du, dv) the prior
+struct Prod5 {
+    double v[5];
+};
+__device__ __forceinline__ Prod5 products_at(int w, int h, size_t ls, const double* pe, const double* ne, int x,
+                                             int y, double du, double dv) {
+    const size_t i = (size_t)y * w + x;
+    Bl b;
+    b.setup(w, h, dadd((double)x, du), dadd((double)y, dv));
+    const double a11 = dmul(0.5, dadd(pe[2 * ls + i], b.at(ne + 2 * ls)));
+    const double a12 = dmul(0.5, dadd(pe[3 * ls + i], b.at(ne + 3 * ls)));
+    const double a22 = dmul(0.5, dadd(pe[4 * ls + i], b.at(ne + 4 * ls)));
+    const double db1 = dadd(dadd(dmul(-0.5, dsub(b.at(ne), pe[i])), dmul(a11, du)), dmul(a12, dv));
+    const double db2 = dadd(dadd(dmul(-0.5, dsub(b.at(ne + ls), pe[ls + i])), dmul(a12, du)), dmul(a22, dv));
+    Prod5 o;
+    o.v[0] = dadd(dmul(a11, a11), dmul(a12, a12));
+    o.v[1] = dmul(dadd(a11, a22), a12);
+    o.v[2] = dadd(dmul(a12, a12), dmul(a22, a22));
+    o.v[3] = dadd(dmul(a11, db1), dmul(a12, db2));
+    o.v[4] = dadd(dmul(a12, db1), dmul(a22, db2));
+    return o;
+}
+
 // products of flow_step: planes g11, g12, g22, gh1, gh2 into prod[pair][5][W*H]
 __global__ void __launch_bounds__(kNT) k64_products(Geom g, int l, int mode, const double* __restrict__ ex_f,
                                                     const double* __restrict__ ex_p, const int* __restrict__ prev,
@@ -216,20 +240,11 @@ __global__ void __launch_bounds__(kNT) k64_products(Geom g, int l, int mode, con
         du = (double)f.x;
         dv = (double)f.y;
     }
-    Bl b;
-    b.setup(w, h, dadd((double)x, du), dadd((double)y, dv));
-    const double a11 = dmul(0.5, dadd(pe[2 * ls + i], b.at(ne + 2 * ls)));
-    const double a12 = dmul(0.5, dadd(pe[3 * ls + i], b.at(ne + 3 * ls)));
-    const double a22 = dmul(0.5, dadd(pe[4 * ls + i], b.at(ne + 4 * ls)));
-    const double db1 = dadd(dadd(dmul(-0.5, dsub(b.at(ne), pe[i])), dmul(a11, du)), dmul(a12, dv));
-    const double db2 = dadd(dadd(dmul(-0.5, dsub(b.at(ne + ls), pe[ls + i])), dmul(a12, du)), dmul(a22, dv));
+    const Prod5 o = products_at(w, h, ls, pe, ne, x, y, du, dv);
     const size_t n0 = (size_t)g.W * g.H;
-    double* o = prod + (size_t)p * 5 * n0 + i;
-    o[0] = dadd(dmul(a11, a11), dmul(a12, a12));
-    o[n0] = dmul(dadd(a11, a22), a12);
-    o[2 * n0] = dadd(dmul(a12, a12), dmul(a22, a22));
-    o[3 * n0] = dadd(dmul(a11, db1), dmul(a12, db2));
-    o[4 * n0] = dadd(dmul(a12, db1), dmul(a22, db2));
+    double* d = prod + (size_t)p * 5 * n0 + i;
+#pragma unroll
+    for (int q = 0; q < 5; ++q) d[q * n0] = o.v[q];
 }
 
 // acc / count for box_mean: the divisor is a small integer, so its refined reciprocal is
