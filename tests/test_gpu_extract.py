@@ -259,6 +259,20 @@ def test_extract_odd_shapes(gpu, oracle, w, h):
     _check_sequence(gpu, oracle, frames, params=p)
 
 
+@pytest.mark.parametrize("w,h", [(8192, 40), (40, 8192)])
+def test_extract_maximum_extent(gpu, oracle, w, h):
+    """The largest FFT side the GPU supports (8192) on either axis, against the oracle; one more
+    pixel is refused with a usage error (never silently truncated)."""
+    from paper_2511_14419_b200.params import ExtractParams, UsageError
+    p = ExtractParams()
+    p.max_shift = 8
+    f = textured_frame(w, h, 8, 3)
+    frames = np.stack([cyclic_shift(f, t, -t) for t in range(3)])
+    _check_sequence(gpu, oracle, frames, params=p)
+    with pytest.raises(UsageError):
+        gpu.extract_roi(np.zeros((2, h + (h > w), w + (w > h)), np.uint8), p)
+
+
 def test_per_frame_pointer_entries(gpu):
     """froi_extract_frames (one uint16 pointer per frame and per mask), froi_extract_frames_sink
     (each destination requested once, frame 0 after frame 1) and froi_stream_push_frames give the
