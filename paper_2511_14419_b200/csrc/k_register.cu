@@ -95,11 +95,16 @@ __device__ __forceinline__ void fft_pass(double2* a, int n, int s, int lc,
 }
 
 // The n - 1 twiddles of a length-n transform into shared memory (dst, behind the data), so the
-// butterflies read them without L1 tag lookups; the caller's barrier publishes them.
-__device__ __forceinline__ const double2* stage_tw(double2* dst, const double2* __restrict__ tw, int n) {
+// butterflies read them without L1 tag lookups; the caller's barrier publishes them.  When data
+// and twiddles together would exceed a CTA's shared memory (8192-point transforms), the
+// butterflies read the twiddles from global memory instead (in_smem == 0).
+__device__ __forceinline__ const double2* stage_tw(double2* dst, const double2* __restrict__ tw, int n,
+                                                   int in_smem) {
+    if (!in_smem) return tw;
     for (int i = threadIdx.x; i < n - 1; i += blockDim.x) dst[i] = __ldg(tw + i);
     return dst;
 }
+constexpr size_t kMaxCtaSmem = 227 * 1024;
 
 // All log2n stages, QM per pass; input already bit-reversed.
 template <int QM, typename Pad = PadStd>
@@ -131,7 +136,7 @@ constexpr int kQRows = FFT_Q_ROWS, kQCols = FFT_Q_COLS, kQXpow = FFT_Q_XPOW;
 __host__ __device__ constexpr int rows_lc(int log2n) { return log2n >= 12 ? 0 : (log2n >= 8 ? 12 - log2n : 4); }
 
 template <typename T>
-__global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int ph, int log2pw,
+__global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int ph, int log2pw, int tw_smem,
                                                      const T* __restrict__ den,
                                                      const unsigned long long* __restrict__ sums,
                                                      const double* __restrict__ wx,
@@ -145,7 +150,7 @@ __global__ void __launch_bounds__(NT) k_fft_rows_fwd(int W, int H, int pw, int p
     const T* f = den + (size_t)slot * W * H;
     // windowed_spectrum_input (registration.hpp:26-42): exact integer sum, then one division
     const double mean = ddiv((double)sums[slot], (double)((long long)W * H));
-    const double2* stw = stage_tw(a + ((size_t)padded(pw) << lc), tw, pw);
+    const double2* stw = stage_tw(a + ((size_t)padded(pw) << lc), tw, pw, tw_smem);
     if (sizeof(T) == 1 && W == pw && H == ph && (W & 15) == 0 && (R << log2pw) == 16 * NT) {
         // 8-bit frames without padding: each thread reads 16 consecutive samples of one row with
         // one 128-bit load, then converts and scatters them to their bit-reversed slots.  The
@@ -249,7 +254,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS, 3) k_fft_rows_w1024(int W, int 
     for (int m = 0; m < 32; ++m) out[l + 32 * m] = e[m];
 }
 
-__global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int lcb,
+__global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int lcb, int tw_smem,
                                                  const double2* __restrict__ tw,
                                                  double2* __restrict__ spec) {
     extern __shared__ double2 sm[];
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(NT) k_fft_cols(int pw, int ph, int log2ph, int
         const unsigned dst = (unsigned)__cvta_generic_to_shared(a + ((pd(brev(row_of(i), log2ph)) << lcb) | (i & (cb - 1))));
         asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
-    const double2* stw = stage_tw(a + ((size_t)padded(ph) << lcb), tw, ph);
+    const double2* stw = stage_tw(a + ((size_t)padded(ph) << lcb), tw, ph, tw_smem);
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncthreads();
     fft_stages<kQCols>(a, ph, log2ph, lcb, stw);
@@ -468,7 +473,9 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
                         const double2* d_tw_col, double2* d_spec, int n_slots, cudaStream_t s) {
     if (n_slots <= 0) return;
     const int lr = rows_lc(g.log2pw);
-    const size_t smem_r = sizeof(double2) * (((size_t)padded(g.pw) << lr) + g.pw);
+    size_t smem_r = sizeof(double2) * (((size_t)padded(g.pw) << lr) + g.pw);
+    const int tw_r = smem_r <= kMaxCtaSmem;
+    if (!tw_r) smem_r -= sizeof(double2) * g.pw;
     const int row_blocks = cdiv(g.ph, 1 << lr);
     static const bool rows_w = [] {
         const char* e = getenv("FROI_FFT_ROWS_W");
@@ -489,17 +496,19 @@ void launch_fft_forward(const Geom& g, const void* d_den, const unsigned long lo
     } else if (g.sample_bytes == 1) {
         set_smem(k_fft_rows_fwd<uint8_t>, smem_r);
         k_fft_rows_fwd<uint8_t><<<dim3(row_blocks, n_slots), NT, smem_r, s>>>(
-            g.W, g.H, g.pw, g.ph, g.log2pw, (const uint8_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
+            g.W, g.H, g.pw, g.ph, g.log2pw, tw_r, (const uint8_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
     } else {
         set_smem(k_fft_rows_fwd<uint16_t>, smem_r);
         k_fft_rows_fwd<uint16_t><<<dim3(row_blocks, n_slots), NT, smem_r, s>>>(
-            g.W, g.H, g.pw, g.ph, g.log2pw, (const uint16_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
+            g.W, g.H, g.pw, g.ph, g.log2pw, tw_r, (const uint16_t*)d_den, d_sums, d_wx, d_wy, d_tw_row, d_spec);
     }
     FROI_LAUNCH_CHECK();
     const int lcb = column_lcb(g);
-    const size_t smem_c = sizeof(double2) * (((size_t)padded(g.ph) << lcb) + g.ph);
+    size_t smem_c = sizeof(double2) * (((size_t)padded(g.ph) << lcb) + g.ph);
+    const int tw_c = smem_c <= kMaxCtaSmem;
+    if (!tw_c) smem_c -= sizeof(double2) * g.ph;
     set_smem(k_fft_cols, smem_c);
-    k_fft_cols<<<dim3(g.pw >> lcb, n_slots), NT, smem_c, s>>>(g.pw, g.ph, g.log2ph, lcb, d_tw_col, d_spec);
+    k_fft_cols<<<dim3(g.pw >> lcb, n_slots), NT, smem_c, s>>>(g.pw, g.ph, g.log2ph, lcb, tw_c, d_tw_col, d_spec);
     FROI_LAUNCH_CHECK();
 }
 

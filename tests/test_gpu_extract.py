@@ -269,6 +269,8 @@ def test_extract_maximum_extent(gpu, oracle, w, h):
     f = textured_frame(w, h, 8, 3)
     frames = np.stack([cyclic_shift(f, t, -t) for t in range(3)])
     _check_sequence(gpu, oracle, frames, params=p)
+    want, _, _ = oracle.extract_roi(frames, 8, p)
+    assert np.array_equal(gpu.extract_roi(frames, p, exact_flow=True), want)  # bit-exact mode too
     with pytest.raises(UsageError):
         gpu.extract_roi(np.zeros((2, h + (h > w), w + (w > h)), np.uint8), p)
 
