@@ -560,30 +560,6 @@ __global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* _
     }
 }
 
-// Packed fp32x2 arithmetic (sm_100a FFMA2/FMUL2/FADD2): two independent lanes per instruction.
-__device__ __forceinline__ void fma2(float& dx, float& dy, float ax, float ay, float bx, float by,
-                                     float cx, float cy) {
-    asm("{.reg .b64 a, b, c, d;\n\t"
-        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\tmov.b64 c, {%6, %7};\n\t"
-        "fma.rn.f32x2 d, a, b, c;\n\tmov.b64 {%0, %1}, d;\n\t}"
-        : "=f"(dx), "=f"(dy)
-        : "f"(ax), "f"(ay), "f"(bx), "f"(by), "f"(cx), "f"(cy));
-}
-__device__ __forceinline__ void mul2(float& dx, float& dy, float ax, float ay, float bx, float by) {
-    asm("{.reg .b64 a, b, d;\n\t"
-        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
-        "mul.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
-        : "=f"(dx), "=f"(dy)
-        : "f"(ax), "f"(ay), "f"(bx), "f"(by));
-}
-__device__ __forceinline__ void add2(float& dx, float& dy, float ax, float ay, float bx, float by) {
-    asm("{.reg .b64 a, b, d;\n\t"
-        "mov.b64 a, {%2, %3};\n\tmov.b64 b, {%4, %5};\n\t"
-        "add.rn.f32x2 d, a, b;\n\tmov.b64 {%0, %1}, d;\n\t}"
-        : "=f"(dx), "=f"(dy)
-        : "f"(ax), "f"(ay), "f"(bx), "f"(by));
-}
-
 // Normal-equation products G of one pixel (flow.hpp:212-232).
 struct GTerms {
     float g11, g12, g22, h1, h2;

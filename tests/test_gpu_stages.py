@@ -39,6 +39,22 @@ def test_denoise_bit_exact(gpu, oracle, w, h, depth, seed):
         assert np.array_equal(got, want)
 
 
+def _c3_frames(n):
+    from paper_2511_14419_b200 import synth
+    return synth.well_frames(synth.config("C3"), 0, n)
+
+
+def test_denoise_full_frame(gpu, oracle):
+    """1024^2 u8 frames of the bench's workload and a uniform-noise frame: every pixel equal."""
+    frames = _c3_frames(2)
+    r = Rng(77)
+    noisy = np.array([[r.next_below(256) for _ in range(256)] for _ in range(256)], np.uint8)
+    for frame in (frames[0], frames[1], noisy):
+        got = gpu.denoise(frame.astype(np.uint16), depth=8)
+        want = oracle.denoise(frame, 8)
+        assert np.array_equal(got, want)
+
+
 def test_denoise_constant_identity(gpu):
     f = np.full((18, 24), 77, np.uint16)
     assert np.array_equal(gpu.denoise(f, depth=8), f)
