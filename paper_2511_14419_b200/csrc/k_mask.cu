@@ -452,7 +452,8 @@ constexpr int PNT_MG = 256;
 #ifndef FROI_MG_MINB
 #define FROI_MG_MINB 4
 #endif
-template <typename T>
+// TAB: 8-bit frames with the context's |grad I| table (DevParams::grad_tab)
+template <typename T, bool TAB>
 __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevParams P, MaskBuffers b) {
     __shared__ double lut[256];
     __shared__ unsigned int hist[2][kFpwBins];
@@ -497,6 +498,7 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
         for (int xb = 0; xb < W; xb += NPX * PNT_MG) {
             float2 fl[NPX];
             int vl[NPX], vr[NPX], vu[NPX], vd[NPX];
+            constexpr bool tab = TAB && sizeof(T) == 1;  // launched only with gradient_source 0
 #pragma unroll
             for (int k = 0; k < NPX; ++k) {
                 const int x = min(xb + (int)threadIdx.x + k * PNT_MG, W - 1);
@@ -510,6 +512,19 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
                     vu[k] = __ldg(rm + sx);
                     vd[k] = __ldg(rp + sx);
                 }
+            }
+            // 8-bit frames: |grad I| = grad_tab[index(|gx|)][index(|gy|)], the exact value
+            // hypot_glibc(gx, gy) gives (hypot only sees |gx|, |gy|); all table reads in flight
+            double gt[NPX];
+            if constexpr (tab) {
+                unsigned ix[NPX], iy[NPX];
+#pragma unroll
+                for (int k = 0; k < NPX; ++k) {
+                    ix[k] = __ldg(P.grad_map + ((unsigned)vr[k] << 8) + (unsigned)vl[k]);
+                    iy[k] = __ldg(P.grad_map + ((unsigned)vd[k] << 8) + (unsigned)vu[k]);
+                }
+#pragma unroll
+                for (int k = 0; k < NPX; ++k) gt[k] = __ldg(P.grad_tab + ix[k] * (unsigned)P.grad_nv + iy[k]);
             }
             // a whole chunk inside the row (every chunk when W is a multiple of NPX*PNT_MG) runs
             // without per-pixel validity branches
@@ -533,7 +548,9 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
                     const float f = hypotf_glibc(fl[k].x, fl[k].y);
 #endif
                     double gg;
-                    if (sizeof(T) == 1 && P.gradient_source == 0) {
+                    if constexpr (tab) {
+                        gg = gt[k];
+                    } else if (sizeof(T) == 1 && P.gradient_source == 0) {
                         const double gx = dmul(0.5, dsub(lut[vr[k]], lut[vl[k]]));
                         const double gy = dmul(0.5, dsub(lut[vd[k]], lut[vu[k]]));
 #if FROI_MG_FAST
@@ -1497,7 +1514,10 @@ void run_stats(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pa
     set_scan_smem();
     k_sel_init_a<<<n_pairs, 32, 0, s>>>(b, (unsigned long long)n, (unsigned long long)(0.01 * (double)(n - 1)),
                                        (unsigned long long)(0.99 * (double)(n - 1)));
-    k_mag_grad<T><<<dim3(mgb, n_pairs), PNT_MG, 0, s>>>(g, P, b);
+    if (sizeof(T) == 1 && P.gradient_source == 0 && P.grad_tab)
+        k_mag_grad<T, true><<<dim3(mgb, n_pairs), PNT_MG, 0, s>>>(g, P, b);
+    else
+        k_mag_grad<T, false><<<dim3(mgb, n_pairs), PNT_MG, 0, s>>>(g, P, b);
     k_sel_scan<<<n_pairs * 4, SCT, scan_smem(), s>>>(b, 4);
     FROI_LAUNCH_CHECK();
     *launches += 3;
@@ -1583,6 +1603,16 @@ void run_cleanup_output(const Geom& g, const DevParams& P, const MaskBuffers& b,
 }
 
 }  // namespace
+
+__global__ void k_grad_table(const double* __restrict__ mag, int nv, double* __restrict__ tab) {
+    const int i = blockIdx.y, j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < nv) tab[(size_t)i * nv + j] = hypot_glibc(mag[i], mag[j]);
+}
+
+void launch_grad_table(const double* d_mag, int nv, double* d_tab, cudaStream_t s) {
+    k_grad_table<<<dim3(cdiv(nv, 256), nv), 256, 0, s>>>(d_mag, nv, d_tab);
+    FROI_LAUNCH_CHECK();
+}
 
 void launch_mask_stage(const Geom& g, const DevParams& P, const MaskBuffers& b, int n_pairs,
                        cudaStream_t s, uint64_t* launches) {

@@ -100,6 +100,13 @@ struct DevParams {
     int min_area, open_radius, close_radius, gradient_source, max_shift;
     // 8-bit frames: normalize_frame's (float)(v * (1.0/maxval)) for v = 0..255 (device, context)
     const float* norm_lut;
+    // 8-bit frames: exact |grad I| by table (context constants, nullptr otherwise).  A central
+    // difference 0.5*(v[a] - v[b]) of normalised samples takes grad_nv distinct magnitudes
+    // (809 for maxval 255); grad_map[a*256 + b] is the index of |0.5*(v[a]-v[b])| among them and
+    // grad_tab[i*grad_nv + j] the restated glibc hypot of magnitudes i and j.
+    const unsigned short* grad_map;
+    const double* grad_tab;
+    int grad_nv;
 };
 
 // ---------------------------------------------------------------- launchers
@@ -202,6 +209,8 @@ struct MaskBuffers {
 };
 void launch_mask_stage(const Geom& g, const DevParams& p, const MaskBuffers& b, int n_pairs,
                        cudaStream_t s, uint64_t* launches);
+// grad_tab[i*nv + j] = hypot_glibc(mag[i], mag[j]) (context creation)
+void launch_grad_table(const double* d_mag, int nv, double* d_tab, cudaStream_t s);
 // Debug taps on the same kernels.
 void launch_saliency_map(const Geom& g, const DevParams& p, const MaskBuffers& b, double* d_out,
                          cudaStream_t s);

@@ -310,6 +310,9 @@ struct froi_ctx {
     // constants
     double *d_spatial = nullptr, *d_lut = nullptr, *d_wx = nullptr, *d_wy = nullptr;
     float* d_norm_lut = nullptr;
+    unsigned short* d_grad_map = nullptr;  // 8-bit frames: |grad I| table (DevParams::grad_*)
+    double* d_grad_tab = nullptr;
+    int grad_nv = 0;
     std::vector<double> h_spatial;
     double2 *d_tw_row = nullptr, *d_tw_col = nullptr, *d_itw_row = nullptr, *d_itw_col = nullptr;
     // frame slots
@@ -471,6 +474,18 @@ struct froi_ctx {
 
 namespace {
 
+// the |grad I| table only serves the image-gradient saliency (gradient_source 0)
+void set_grad_params(froi_ctx* c) {
+    static const bool off = [] {  // FROI_NO_GRAD_TABLE=1: compute every hypot (A/B runs)
+        const char* e = getenv("FROI_NO_GRAD_TABLE");
+        return e && atoi(e) != 0;
+    }();
+    const bool on = c->d_grad_tab && c->params.gradient_source == 0 && !off;
+    c->dp.grad_map = on ? c->d_grad_map : nullptr;
+    c->dp.grad_tab = on ? c->d_grad_tab : nullptr;
+    c->dp.grad_nv = on ? c->grad_nv : 0;
+}
+
 void ctx_alloc(froi_ctx* c) {
     const Geom& g = c->g;
     const size_t px = (size_t)g.W * g.H;
@@ -503,6 +518,34 @@ void ctx_alloc(froi_ctx* c) {
             FROI_CUDA(cudaMemcpy(c->d_norm_lut, nl.data(), 256 * sizeof(float), cudaMemcpyHostToDevice));
             c->dp.norm_lut = c->d_norm_lut;
         }
+        if (g.sample_bytes == 1) {
+            // gradient_magnitude (roi.hpp:65-74) of 8-bit frames: every central difference
+            // 0.5*(v[a]*inv - v[b]*inv) is one of a few hundred magnitudes, so hypot of a pixel's
+            // two differences is a table entry (the same restated glibc hypot, evaluated once)
+            const double inv = 1.0 / g.maxval;
+            std::vector<double> lv(256), mags;
+            for (int v = 0; v < 256; ++v) lv[v] = (double)v * inv;
+            mags.reserve(65536);
+            for (int a = 0; a < 256; ++a)
+                for (int b = 0; b < 256; ++b) mags.push_back(std::fabs(0.5 * (lv[a] - lv[b])));
+            std::vector<double> u(mags);
+            std::sort(u.begin(), u.end());
+            u.erase(std::unique(u.begin(), u.end()), u.end());
+            std::vector<unsigned short> map(65536);
+            for (int i = 0; i < 65536; ++i)
+                map[i] = (unsigned short)(std::lower_bound(u.begin(), u.end(), mags[i]) - u.begin());
+            c->grad_nv = (int)u.size();
+            c->d_grad_map = dalloc<unsigned short>(65536, &t);
+            FROI_CUDA(cudaMemcpy(c->d_grad_map, map.data(), 65536 * sizeof(unsigned short), cudaMemcpyHostToDevice));
+            double* d_mag = nullptr;
+            FROI_CUDA(cudaMalloc(&d_mag, u.size() * sizeof(double)));
+            FROI_CUDA(cudaMemcpy(d_mag, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice));
+            c->d_grad_tab = dalloc<double>(u.size() * u.size(), &t);
+            launch_grad_table(d_mag, c->grad_nv, c->d_grad_tab, 0);
+            FROI_CUDA(cudaDeviceSynchronize());
+            FROI_CUDA(cudaFree(d_mag));
+        }
+        set_grad_params(c);
         c->d_spatial = dalloc<double>(spatial.size(), &t);
         c->d_lut = dalloc<double>(lut.size(), &t);
         c->d_wx = dalloc<double>(wx.size(), &t);
@@ -621,7 +664,7 @@ void ctx_free(froi_ctx* c) {
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->stream) cudaStreamSynchronize(c->stream);
-    void* ptrs[] = {c->d_norm_lut, c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
+    void* ptrs[] = {c->d_norm_lut, c->d_grad_map, c->d_grad_tab, c->d_spatial, c->d_lut, c->d_wx, c->d_wy, c->d_tw_row, c->d_tw_col, c->d_itw_row,
                     c->d_itw_col, c->d_raw, c->d_den, c->d_sums, c->d_spec, c->d_pyr_f, c->d_exA_f,
                     c->d_exB_f, c->d_info, c->d_cols, c->d_surf, c->d_pyr_p, c->d_exA_p, c->d_exB_p,
                     c->d_flow0, c->d_flow1, c->d_sel, c->d_hist, c->d_cand, c->d_cand_count, c->d_cand_idx, c->d_fm, c->d_gr, c->d_tie, c->d_bits_thr,
@@ -1700,6 +1743,7 @@ int froi_ctx_set_params(froi_ctx* ctx, const froi_params* p) {
     ctx->params = *p;
     ctx->dp = make_dev_params(*p);
     ctx->dp.norm_lut = ctx->d_norm_lut;
+    set_grad_params(ctx);
     ctx->f64c = make_flow64_const(*p);
     // captured batch graphs hold the old parameters as kernel arguments
     ABI_TRY

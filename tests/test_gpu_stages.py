@@ -204,6 +204,22 @@ def test_saliency_bit_exact(gpu, oracle, source):
     assert not np.any(gpu.saliency(z, z, const))
 
 
+def test_saliency_gradient_table_full_range(gpu, oracle):
+    """8-bit frames take |grad I| from the context's table (every central-difference magnitude x
+    every other, evaluated once with the restated glibc hypot): uniform-noise frames hit tens of
+    thousands of distinct (|gx|, |gy|) entries, all below the 99th percentile compared exactly."""
+    rng = np.random.default_rng(5)
+    for shape, seed in (((256, 256), 1), ((200, 312), 2)):
+        h, w = shape
+        frame = rng.integers(0, 256, size=(h, w)).astype(np.uint8)
+        u = rng.normal(0, 2, size=(h, w)).astype(np.float32)
+        v = rng.normal(0, 2, size=(h, w)).astype(np.float32)
+        for fw in (0.0, 0.7):
+            got = gpu.saliency(u, v, frame, fw, 0, depth=8)
+            want = oracle.saliency(u, v, frame, 8, fw, 0)
+            assert np.array_equal(got, want)
+
+
 def test_threshold_bit_exact(gpu, oracle):
     rng = Rng(23)
     perm = list(range(100))
