@@ -152,9 +152,18 @@ struct SrcBufA {
         k[0] = k[1] = fkey(fm[i]);
         k[2] = k[3] = dkey(gr[i]);
     }
-    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
-        const float4 f = __ldg((const float4*)(fm + i));
-        const double2 g0 = __ldg((const double2*)(gr + i)), g1 = __ldg((const double2*)(gr + i + 2));
+    // raw loads of four pixels, issued one step ahead of their use (sel_pass_body)
+    struct Raw {
+        float4 f;
+        double2 g0, g1;
+    };
+    __device__ __forceinline__ Raw load4(long long i) const {
+        return Raw{__ldg((const float4*)(fm + i)), __ldg((const double2*)(gr + i)), __ldg((const double2*)(gr + i + 2))};
+    }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const { keys_of(load4(i), k); }
+    __device__ __forceinline__ void keys_of(const Raw& r, unsigned long long (*k)[4]) const {
+        const float4 f = r.f;
+        const double2 g0 = r.g0, g1 = r.g1;
         k[0][0] = k[1][0] = fkey(f.x);
         k[0][1] = k[1][1] = fkey(f.y);
         k[0][2] = k[1][2] = fkey(f.z);
@@ -180,9 +189,17 @@ struct SrcSal {
     static constexpr int NQ = 1;
     __device__ __forceinline__ double value(long long i) const { return sal_from(I, w, w1, fm[i], gr[i]); }
     __device__ __forceinline__ void keys(long long i, unsigned long long* k) const { k[0] = dkey(value(i)); }
-    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
-        const float4 f = __ldg((const float4*)(fm + i));
-        const double2 g0 = __ldg((const double2*)(gr + i)), g1 = __ldg((const double2*)(gr + i + 2));
+    struct Raw {
+        float4 f;
+        double2 g0, g1;
+    };
+    __device__ __forceinline__ Raw load4(long long i) const {
+        return Raw{__ldg((const float4*)(fm + i)), __ldg((const double2*)(gr + i)), __ldg((const double2*)(gr + i + 2))};
+    }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const { keys_of(load4(i), k); }
+    __device__ __forceinline__ void keys_of(const Raw& r, unsigned long long (*k)[4]) const {
+        const float4 f = r.f;
+        const double2 g0 = r.g0, g1 = r.g1;
         k[0][0] = dkey(sal_from(I, w, w1, f.x, g0.x));
         k[0][1] = dkey(sal_from(I, w, w1, f.y, g0.y));
         k[0][2] = dkey(sal_from(I, w, w1, f.z, g1.x));
@@ -195,8 +212,15 @@ struct SrcMap {
     static constexpr int NQ = 1;
     __device__ __forceinline__ double value(long long i) const { return map[i]; }
     __device__ __forceinline__ void keys(long long i, unsigned long long* k) const { k[0] = dkey(map[i]); }
-    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const {
-        const double2 g0 = __ldg((const double2*)(map + i)), g1 = __ldg((const double2*)(map + i + 2));
+    struct Raw {
+        double2 g0, g1;
+    };
+    __device__ __forceinline__ Raw load4(long long i) const {
+        return Raw{__ldg((const double2*)(map + i)), __ldg((const double2*)(map + i + 2))};
+    }
+    __device__ __forceinline__ void keys4(long long i, unsigned long long (*k)[4]) const { keys_of(load4(i), k); }
+    __device__ __forceinline__ void keys_of(const Raw& r, unsigned long long (*k)[4]) const {
+        const double2 g0 = r.g0, g1 = r.g1;
         k[0][0] = dkey(g0.x);
         k[0][1] = dkey(g0.y);
         k[0][2] = dkey(g1.x);
@@ -304,12 +328,19 @@ __device__ void sel_pass_body(const Geom& g, const MaskBuffers& b, int p, const 
         if ((((hqm >> q) & 1u) || ((cqm >> q) & 1u)) && ms[q] < 32) hi = false;
     auto main_loop = [&](auto hi_tag) {
     constexpr bool HI = decltype(hi_tag)::value;
+    // the next step's raw loads are issued before this step's keys are processed (two steps of
+    // loads in flight per thread)
+    typename Src::Raw nxt{};
+    if (vec && i0 + 4ll * threadIdx.x + 3 < i1) nxt = src.load4(i0 + 4ll * threadIdx.x);
     for (long long base0 = i0; base0 < i1; base0 += 4ll * blockDim.x) {
         const long long base = base0 + 4ll * threadIdx.x;
         unsigned long long k[NQ][4];
         bool v[4];
+        const typename Src::Raw cur = nxt;
+        const long long nb = base + 4ll * blockDim.x;
+        if (vec && nb + 3 < i1) nxt = src.load4(nb);
         if (vec && base + 3 < i1) {
-            src.keys4(base, k);
+            src.keys_of(cur, k);
             v[0] = v[1] = v[2] = v[3] = true;
         } else {
 #pragma unroll
@@ -621,13 +652,13 @@ __global__ void __launch_bounds__(PNT_MG, FROI_MG_MINB) k_mag_grad(Geom g, DevPa
     }
 }
 
-__global__ void __launch_bounds__(SNT) k_sel_pass_a(Geom g, MaskBuffers b) {
+__global__ void __launch_bounds__(SNT, 2) k_sel_pass_a(Geom g, MaskBuffers b) {
     const int p = blockIdx.y;
     SrcBufA src{opaque(b.fm + (size_t)p * g.W * g.H), opaque(b.gr + (size_t)p * g.W * g.H)};
     sel_pass_body(g, b, p, src);
 }
 
-__global__ void __launch_bounds__(SNT) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map,
+__global__ void __launch_bounds__(SNT, 2) k_sel_pass_b(Geom g, DevParams P, MaskBuffers b, const double* map,
                                                    int write_bits) {
     const int p = blockIdx.y;
     if (map) {
