@@ -539,10 +539,10 @@ void ctx_alloc(froi_ctx* c) {
             FROI_CUDA(cudaMemcpy(c->d_grad_map, map.data(), 65536 * sizeof(unsigned short), cudaMemcpyHostToDevice));
             double* d_mag = nullptr;
             FROI_CUDA(cudaMalloc(&d_mag, u.size() * sizeof(double)));
-            FROI_CUDA(cudaMemcpy(d_mag, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice));
+            FROI_CUDA(cudaMemcpyAsync(d_mag, u.data(), u.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
             c->d_grad_tab = dalloc<double>(u.size() * u.size(), &t);
-            launch_grad_table(d_mag, c->grad_nv, c->d_grad_tab, 0);
-            FROI_CUDA(cudaDeviceSynchronize());
+            launch_grad_table(d_mag, c->grad_nv, c->d_grad_tab, c->stream);
+            FROI_CUDA(cudaStreamSynchronize(c->stream));
             FROI_CUDA(cudaFree(d_mag));
         }
         set_grad_params(c);
