@@ -261,6 +261,33 @@ __global__ void __launch_bounds__(QNT, 3) k_denoise_u8_m1b2(int W, int H, int ma
                 h = max(max(a, b), c);
                 md = a + b + c - l - h;
             };
+            if (y0 - 2 >= 0 && y0 + QY + 2 <= H) {
+                // interior band: median row my is centred on raw row my + 1, so the window slides
+                // by exactly one raw row per output -- straight-line, constant row offsets
+                const uint8_t* q = raw_s + rb * QRW + cx;
+                int l0, m0, h0, l1, m1, h1;
+                auto tq = [&](const uint8_t* r, int& l, int& md, int& h) {
+                    const int a = r[-1], b = r[0], c = r[1];
+                    l = min(min(a, b), c);
+                    h = max(max(a, b), c);
+                    md = a + b + c - l - h;
+                };
+                tq(q, l0, m0, h0);
+                tq(q + QRW, l1, m1, h1);
+                int* out = med_s + rb * QMW + mx;
+                const int nrow = re - rb;  // 5 or 6
+#pragma unroll
+                for (int k = 0; k < 6; ++k) {
+                    if (k < nrow) {
+                        int l2, m2, h2;
+                        tq(q + (k + 2) * QRW, l2, m2, h2);
+                        const int m = med3i(max(max(l0, l1), l2), med3i(m0, m1, m2), min(min(h0, h1), h2));
+                        out[k * QMW] = m * (QREP * 8);
+                        l0 = l1; m0 = m1; h0 = h1;
+                        l1 = l2; m1 = m2; h1 = h2;
+                    }
+                }
+            } else {
             // the clamped centre row advances by 0 or 1 per median row
             int prev = clampi(y0 - 2 + rb, 0, H - 1) - (y0 - R1);
             int l0, m0, h0, l1, m1, h1, l2, m2, h2;
@@ -278,6 +305,7 @@ __global__ void __launch_bounds__(QNT, 3) k_denoise_u8_m1b2(int W, int H, int ma
                     prev = cy;
                 }
                 med_s[my * QMW + mx] = m * (QREP * 8);
+            }
             }
         }
         __syncthreads();
