@@ -336,7 +336,10 @@ __global__ void __launch_bounds__(QNT, 3) k_denoise_u8_m1b2(int W, int H, int ma
             for (int j = 0; j < NR + 4; ++j)
 #pragma unroll
                 for (int dx = 0; dx < 5; ++dx) {
-                    const double v = dsub(__hiloint2double(0x43300000, (int)((unsigned)mw[j][dx] / (QREP * 8))), B52);
+                    // 128 * median (the stored table offset) as a double: every product and sum
+                    // below is then exactly 128x the reference's (power-of-two scaling commutes
+                    // with round-to-nearest while nothing is subnormal), undone after the division
+                    const double v = dsub(__hiloint2double(0x43300000, mw[j][dx]), B52);
 #pragma unroll
                     for (int k = 0; k < NR; ++k) {
                         if (j < k || j > k + 4) continue;
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(QNT, 3) k_denoise_u8_m1b2(int W, int H, int ma
                 }
 #pragma unroll
             for (int k = 0; k < NR; ++k) {
-                double q = ddiv(num[k], dn[k]);
+                double q = dmul(ddiv(num[k], dn[k]), 1.0 / (QREP * 8));
                 q = (q < 0.0) ? 0.0 : q;
                 q = (dmax < q) ? dmax : q;
                 const int outv = (int)round(q);
