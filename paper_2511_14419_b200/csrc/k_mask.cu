@@ -1575,7 +1575,11 @@ void run_boundary(const Geom& g, const DevParams& P, const MaskBuffers& b, int n
     ++*launches;
     // threshold words fused into the collect pass when rows are whole 32-bit words
     const int bits = g.W % 32 == 0 ? 1 : 0;
-    for (int it = 0; it < sel_passes(kSelPassesB); ++it) {
+    // frames above 2 Mpx (C4's 2048^2): the boundary's exponent-window bin usually exceeds the
+    // kSelCap keys a collect can take, so an 11-bit radix pass comes before the collect -- run that
+    // third pass on the whole grid too instead of in k_sel_rest_b's one CTA per pair
+    const int passes_b = sel_passes(n > (1ll << 21) ? kSelPassesB + 1 : kSelPassesB);
+    for (int it = 0; it < passes_b; ++it) {
         k_sel_pass_b<<<dim3(bpp, n_pairs), SNT, pass_smem(1), s>>>(g, P, b, map, bits);
         k_sel_scan<<<n_pairs, SCT, scan_smem(), s>>>(b, 1, bits);
         FROI_LAUNCH_CHECK();

@@ -20,14 +20,16 @@ from paper_2511_14419_b200 import flowroi, synth  # noqa: E402
 tag = sys.argv[1] if len(sys.argv) > 1 else "run"
 nw = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 max_pairs = int(sys.argv[3]) if len(sys.argv) > 3 else 0
-cfg = synth.config("C3")
-F = 450
-frames = torch.empty((nw, F, 1024, 1024), dtype=torch.uint8)
+# STAGE_AB_CONFIG=C4 (or C2): the same measurement on another BASELINE configuration
+cfg = synth.config(os.environ.get("STAGE_AB_CONFIG", "C3"))
+F, W, H = cfg.n_frames, cfg.width, cfg.height
+u16 = cfg.sample_bytes == 2
+frames = torch.empty((nw, F, H, W), dtype=torch.int16 if u16 else torch.uint8)
 for w in range(nw):
-    synth.well_frames(cfg, w, F, out=frames[w].numpy())
+    synth.well_frames(cfg, w, F, out=frames[w].numpy().view("uint16" if u16 else "uint8"))
 dev = frames.cuda()
-masks = torch.empty((F, 1024, 128), dtype=torch.uint8, device="cuda")
-ctx = flowroi.Context(1024, 1024, 8, cfg.params, max_pairs=max_pairs)
+masks = torch.empty((F, H, (W + 7) // 8), dtype=torch.uint8, device="cuda")
+ctx = flowroi.Context(W, H, cfg.depth, cfg.params, max_pairs=max_pairs)
 ctx.set_lanes(1)
 if os.environ.get("STAGE_AB_NOFORK"):
     ctx.set_fork(False)
