@@ -519,6 +519,20 @@ __device__ __forceinline__ void bl_split(int i, float d, int n, int& i0, float& 
     }
 }
 
+// One fine-pixel value of the coarse-to-fine prior (flow.hpp:318-337) in fp32, with explicit
+// round-to-nearest operations in the reference's bilinear order (top row, bottom row, blend,
+// scale): the same bits whichever kernel (k_upsample / k_upsample2) computes it.
+__device__ __forceinline__ float up_ch(float a, float b, float d, float e, float ax, float ay, float s) {
+    const float oax = __fsub_rn(1.f, ax), oay = __fsub_rn(1.f, ay);
+    const float top = __fadd_rn(__fmul_rn(a, oax), __fmul_rn(b, ax));
+    const float bot = __fadd_rn(__fmul_rn(d, oax), __fmul_rn(e, ax));
+    return __fmul_rn(__fadd_rn(__fmul_rn(top, oay), __fmul_rn(bot, ay)), s);
+}
+__device__ __forceinline__ float2 up_px(float2 a, float2 b, float2 d, float2 e, float ax, float ay, float fx,
+                                        float fy) {
+    return make_float2(up_ch(a.x, b.x, d.x, e.x, ax, ay, fx), up_ch(a.y, b.y, d.y, e.y, ax, ay, fy));
+}
+
 // Coarse-to-fine upsampling of the prior (flow.hpp:318-337), fp32: one thread per fine pixel,
 // run once per level before its first iteration.  rfx = 1/fx (exact for the default 0.5 scale).
 __global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* __restrict__ coarse,
@@ -553,11 +567,58 @@ __global__ void __launch_bounds__(256) k_upsample(Geom g, int l, const float2* _
     for (int k = 0; k < NY; ++k) {
         const int y = blockIdx.y * 32 + (threadIdx.x >> 5) + 8 * k;
         if (x >= w || y >= h) continue;
-        const float2 a = q[k][0], b = q[k][1], d = q[k][2], e = q[k][3];
-        const float u = ((a.x * (1.f - ax) + b.x * ax) * (1.f - ay[k]) + (d.x * (1.f - ax) + e.x * ax) * ay[k]) * fx;
-        const float v = ((a.y * (1.f - ax) + b.y * ax) * (1.f - ay[k]) + (d.y * (1.f - ax) + e.y * ax) * ay[k]) * fy;
-        f[y * w + x] = make_float2(u, v);
+        f[y * w + x] = up_px(q[k][0], q[k][1], q[k][2], q[k][3], ax, ay[k], fx, fy);
     }
+}
+
+// The exact 2:1 case of k_upsample (fine size = 2 x coarse, the default pyramid): one thread per
+// coarse pixel (i, j) writes the fine 2x2 block (2i..2i+1, 2j..2j+1) as two 16-byte stores.  Away
+// from the border the bilinear corners are always coarse (i-1..i+1, j-1..j+1) with weights 0.75 /
+// 0.25, so nine loads serve four outputs; border blocks take k_upsample's per-pixel index rule.
+// Every output is up_px on the same operands as in k_upsample, so the two kernels agree bit for bit
+// (FROI_UPSAMPLE2=0 in the environment selects k_upsample everywhere; tests compare the two).
+__global__ void __launch_bounds__(256) k_upsample2(Geom g, int l, const float2* __restrict__ coarse,
+                                                   float2* __restrict__ fine, float fx, float fy) {
+    const int p = blockIdx.z;
+    const int w = g.lw[l], cw = g.lw[l + 1], ch = g.lh[l + 1];
+    const int i = blockIdx.x * 32 + (threadIdx.x & 31), j = blockIdx.y * 8 + (threadIdx.x >> 5);
+    if (i >= cw || j >= ch) return;
+    const float2* c = coarse + (size_t)p * g.lsum + g.loff[l + 1];
+    float2* f = fine + (size_t)p * g.lsum + g.loff[l];
+    float2 o[2][2];
+    if (i >= 1 && i <= cw - 2 && j >= 1 && j <= ch - 2) {
+        float2 v[3][3];
+#pragma unroll
+        for (int r = 0; r < 3; ++r)
+#pragma unroll
+            for (int q = 0; q < 3; ++q) v[r][q] = __ldg(c + (j - 1 + r) * cw + (i - 1 + q));
+#pragma unroll
+        for (int yy = 0; yy < 2; ++yy)
+#pragma unroll
+            for (int xx = 0; xx < 2; ++xx)
+                o[yy][xx] = up_px(v[yy][xx], v[yy][xx + 1], v[yy + 1][xx], v[yy + 1][xx + 1], xx ? 0.25f : 0.75f,
+                                  yy ? 0.25f : 0.75f, fx, fy);
+    } else {
+#pragma unroll
+        for (int yy = 0; yy < 2; ++yy) {
+            const int y = 2 * j + yy;
+            int y0;
+            float ay;
+            bl_split(0, (y + 0.5f) * 0.5f - 0.5f, ch, y0, ay);
+#pragma unroll
+            for (int xx = 0; xx < 2; ++xx) {
+                const int x = 2 * i + xx;
+                int x0;
+                float ax;
+                bl_split(0, (x + 0.5f) * 0.5f - 0.5f, cw, x0, ax);
+                const float2* r0 = c + y0 * cw + x0;
+                o[yy][xx] = up_px(__ldg(r0), __ldg(r0 + 1), __ldg(r0 + cw), __ldg(r0 + cw + 1), ax, ay, fx, fy);
+            }
+        }
+    }
+#pragma unroll
+    for (int yy = 0; yy < 2; ++yy)
+        *(float4*)(f + (size_t)(2 * j + yy) * w + 2 * i) = make_float4(o[yy][0].x, o[yy][0].y, o[yy][1].x, o[yy][1].y);
 }
 
 // Normal-equation products G of one pixel (flow.hpp:212-232).
@@ -1157,10 +1218,21 @@ int launch_flow(const Geom& g, const DevParams& P, const FlowBuffers& b, const i
                 // upscale the coarser estimate into this level of the same buffer (flow.hpp:318-337)
                 const float fx = (float)((double)g.lw[l] / g.lw[l + 1]);
                 const float fy = (float)((double)g.lh[l] / g.lh[l + 1]);
-                dim3 ug(cdiv(g.lw[l], 32), cdiv(g.lh[l], 32), n_pairs);
-                k_upsample<<<ug, 256, 0, s>>>(g, l, buf[cur], buf[cur], fx, fy,
-                                              (float)(1.0 / ((double)g.lw[l] / g.lw[l + 1])),
-                                              (float)(1.0 / ((double)g.lh[l] / g.lh[l + 1])));
+                // (16-byte stores: the level's base and the per-pair stride must keep float2 pairs aligned)
+                static const bool up2 = [] {
+                    const char* e = getenv("FROI_UPSAMPLE2");
+                    return !(e && atoi(e) == 0);
+                }();
+                if (up2 && g.lw[l] == 2 * g.lw[l + 1] && g.lh[l] == 2 * g.lh[l + 1] && g.lw[l + 1] >= 3 &&
+                    g.lh[l + 1] >= 3 && g.lsum % 2 == 0 && g.loff[l] % 2 == 0) {
+                    dim3 ug(cdiv(g.lw[l + 1], 32), cdiv(g.lh[l + 1], 8), n_pairs);
+                    k_upsample2<<<ug, 256, 0, s>>>(g, l, buf[cur], buf[cur], fx, fy);
+                } else {
+                    dim3 ug(cdiv(g.lw[l], 32), cdiv(g.lh[l], 32), n_pairs);
+                    k_upsample<<<ug, 256, 0, s>>>(g, l, buf[cur], buf[cur], fx, fy,
+                                                  (float)(1.0 / ((double)g.lw[l] / g.lw[l + 1])),
+                                                  (float)(1.0 / ((double)g.lh[l] / g.lh[l + 1])));
+                }
                 FROI_LAUNCH_CHECK();
             }
             a.flow_in = buf[cur];

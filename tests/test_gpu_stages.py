@@ -133,6 +133,33 @@ def test_flow_tolerance(gpu, oracle, w, h, dx, dy, seed):
     assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (mx, mean)
 
 
+def test_flow_upsample_kernels_agree(tmp_path):
+    """Exact 2:1 levels take k_upsample2 (nine loads per four outputs, 16-byte stores); the
+    generic k_upsample (FROI_UPSAMPLE2=0) must give the same flow bit for bit -- both evaluate the
+    same explicitly rounded expression.  256^2 (every level 2:1) and 200x152 (2:1 with a border)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, %r); sys.path.insert(0, %r)\n"
+        "from paper_2511_14419_b200 import flowroi as F\n"
+        "from fixtures import textured_frame, cyclic_shift\n"
+        "out = []\n"
+        "for w, h in ((256, 256), (200, 152)):\n"
+        "    f = textured_frame(w, h, 8, 5); g = cyclic_shift(f, 3, -2)\n"
+        "    u, v = F.compute_flow(f, g); out += [u.ravel(), v.ravel()]\n"
+        "np.save(sys.argv[1], np.concatenate(out))\n"
+    ) % (root, os.path.join(root, "tests"))
+    outs = []
+    for sel in ("1", "0"):
+        p = str(tmp_path / f"u{sel}.npy")
+        env = dict(os.environ, FROI_UPSAMPLE2=sel)
+        subprocess.run([sys.executable, "-c", code, p], check=True, env=env, timeout=300)
+        outs.append(np.load(p))
+    assert np.array_equal(outs[0].view(np.uint32), outs[1].view(np.uint32))
+
+
 def test_flow_identical_frames_exactly_zero(gpu):
     f = textured_frame(96, 80, 8, 21)
     u, v = gpu.compute_flow(f, f)
