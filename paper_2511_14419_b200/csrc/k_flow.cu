@@ -137,12 +137,12 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
             for (int t = 0; t < 6; ++t) v[t] = row[t];
 #pragma unroll
             for (int k = 0; k < 2; ++k) {
+                // (a0, a1) as one packed FFMA2 per tap: the same two roundings as two FFMAs
                 float a0 = 0.f, a1 = 0.f, a2 = 0.f;
 #pragma unroll
                 for (int t = 0; t < 5; ++t) {
-                    a0 += g0[t] * v[t + k];
-                    a1 += g1[t] * v[t + k];
-                    a2 += g2[t] * v[t + k];
+                    fma2(a0, a1, g0[t], g1[t], v[t + k], v[t + k], a0, a1);
+                    a2 = fmaf(g2[t], v[t + k], a2);
                 }
                 s_r[yy * PX + xx + k] = a0;
                 s_r[SH * PX + yy * PX + xx + k] = a1;
@@ -168,13 +168,11 @@ __device__ __forceinline__ void polyexp_tile(const Src& src, int w, int h, int r
             if (x >= w || y >= h) continue;
             float s1 = 0.f, sx = 0.f, sy = 0.f, sxx = 0.f, syy = 0.f, sxy = 0.f;
 #pragma unroll
-            for (int t = 0; t < 5; ++t) {
-                s1 += g0[t] * q0[t + k];
-                sx += g0[t] * q1[t + k];
-                sy += g1[t] * q0[t + k];
-                sxx += g0[t] * q2[t + k];
-                syy += g2[t] * q0[t + k];
-                sxy += g1[t] * q1[t + k];
+            for (int t = 0; t < 5; ++t) {  // packed pairs (FFMA2): same roundings as six FFMAs
+                fma2(s1, sx, g0[t], g0[t], q0[t + k], q1[t + k], s1, sx);
+                fma2(sy, sxy, g1[t], g1[t], q0[t + k], q1[t + k], sy, sxy);
+                sxx = fmaf(g0[t], q2[t + k], sxx);
+                syy = fmaf(g2[t], q0[t + k], syy);
             }
             const float bx = sx * inv_m20, by = sy * inv_m20;
             const float a12 = 0.5f * sxy * inv_m22;
