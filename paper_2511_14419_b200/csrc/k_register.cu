@@ -231,7 +231,16 @@ __global__ void __launch_bounds__(32 * RW_WARPS, 3) k_fft_rows_w1024(int W, int 
 #pragma unroll
         for (int m = 0; m < 32; ++m) {
             if (m & h) continue;
-            bfly(e[m], e[m + h], __ldg(tw + h - 1 + (m & (h - 1))));
+            if (s == 0 || (s == 1 && (m & 1) == 0)) {
+                // real inputs (imaginary parts +0: the windowed samples, then stage 0's sums) and
+                // the twiddle (1, 0) (every length's first w, fft.hpp:30): the reference's
+                // butterfly reduces exactly to u + v, u - v on the real parts, imaginary parts +0
+                const double a = e[m].x, b = e[m + h].x;
+                e[m] = make_double2(dadd(a, b), 0.0);
+                e[m + h] = make_double2(dsub(a, b), 0.0);
+            } else {
+                bfly(e[m], e[m + h], __ldg(tw + h - 1 + (m & (h - 1))));
+            }
         }
     }
     double2* xw = xs_dyn + warp * (33 * 32);
