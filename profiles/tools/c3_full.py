@@ -1,7 +1,7 @@
 """The whole C3 configuration (64 wells x 450 frames, 28,800 masks, 30.2 GB of 1024^2 u8 frames)
 through the public host API on one GPU (run on the GPU box):
 
-  python profiles/tools/c3_full.py [wells]
+  python profiles/tools/c3_full.py [wells] [config]      (config C3 by default; C4: 16 x 128 2048^2 u16)
 
 Each well is rendered into pinned memory (gen/synth.c, the bench's generator) while the previous
 well runs on the GPU; each call is froi_extract_wells (pinned frames in, PBM masks out, H2D and D2H
@@ -23,21 +23,23 @@ import torch  # noqa: E402
 from paper_2511_14419_b200 import flowroi, synth  # noqa: E402
 from paper_2511_14419_b200.params import CFrameStats  # noqa: E402
 
-nw = int(sys.argv[1]) if len(sys.argv) > 1 else 64
-cfg = synth.config("C3")
+cfg = synth.config(sys.argv[2] if len(sys.argv) > 2 else "C3")
+nw = int(sys.argv[1]) if len(sys.argv) > 1 else cfg.n_wells
 F, W, H = cfg.n_frames, cfg.width, cfg.height
-bufs = [torch.empty((F, H, W), dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+u16 = cfg.sample_bytes == 2
+bufs = [torch.empty((F, H, W), dtype=torch.int16 if u16 else torch.uint8, pin_memory=True) for _ in range(2)]
 masks = torch.empty((F, H, (W + 7) // 8), dtype=torch.uint8, pin_memory=True)
-ctx = flowroi.Context(W, H, 8, cfg.params)
+ctx = flowroi.Context(W, H, cfg.depth, cfg.params)
+view = (lambda t: t.numpy().view(np.uint16)) if u16 else (lambda t: t.numpy())
 stats = (CFrameStats * F)()
-synth.well_frames(cfg, 0, F, out=bufs[0].numpy())
+synth.well_frames(cfg, 0, F, out=view(bufs[0]))
 call_s, fracs, shifted, set_px = 0.0, [], 0, 0
 for w in range(nw):
-    cur = bufs[w % 2].numpy()
+    cur = view(bufs[w % 2])
     th = None
     if w + 1 < nw:  # render the next well while this one runs
         th = threading.Thread(target=synth.well_frames, args=(cfg, w + 1, F),
-                              kwargs={"out": bufs[(w + 1) % 2].numpy()})
+                              kwargs={"out": view(bufs[(w + 1) % 2])})
         th.start()
     t0 = time.perf_counter()
     ctx.extract_wells_into(cur[None], masks.numpy(), stats)
@@ -49,7 +51,8 @@ for w in range(nw):
     if th:
         th.join()
 ctx.close()
-out = {"wells": nw, "frames": nw * F, "masks": nw * F, "input_gb": nw * F * W * H / 1e9,
+out = {"config": cfg.name, "wells": nw, "frames": nw * F, "masks": nw * F,
+       "input_gb": nw * F * W * H * cfg.sample_bytes / 1e9,
        "gpu_call_s": round(call_s, 3), "masks_per_s": round(nw * F / call_s, 1),
        "raw_fraction_mean": round(float(np.mean([f[0] for f in fracs])), 5),
        "raw_fraction_min": round(float(min(f[1] for f in fracs)), 5),
