@@ -191,6 +191,23 @@ def test_flow_levels_and_16bit(gpu, oracle):
         assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (levels, mx, mean)
 
 
+@pytest.mark.parametrize("scale,levels", [(0.6, 3), (0.75, 4), (0.5, 3)])
+def test_flow_pyramid_scale(gpu, oracle, scale, levels):
+    """Pyramids that are not 2:1 (resize_bilinear at a general factor, flow.hpp:277-298; the
+    coarse-to-fine prior rescaled per axis, flow.hpp:318-337): the fp32 flow within the stated
+    tolerance and the bit-exact mode identical to the reference, on an odd-sized frame pair."""
+    from paper_2511_14419_b200.params import ExtractParams, FlowParams
+    f = textured_frame(150, 118, 8, 17)
+    g = cyclic_shift(f, 2, -3)
+    p = FlowParams(pyramid_levels=levels, pyramid_scale=scale)
+    ou, ov = oracle.compute_flow(f, g, 8, ExtractParams(flow=p))
+    gu, gv = gpu.compute_flow(f, g, p)
+    mx, mean = _flow_err(gu, gv, ou, ov)
+    assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (scale, mx, mean)
+    xu, xv = gpu.compute_flow(f, g, p, exact=True)
+    assert np.array_equal(xu, ou) and np.array_equal(xv, ov)
+
+
 def test_polynomial_expansion_kats(gpu, oracle):
     # constant -> A = b = 0, c = const (test_flow.cpp:66-79; fp32 tolerance)
     e = gpu.polynomial_expansion(np.full((32, 32), 0.42, np.float32))
