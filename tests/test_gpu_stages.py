@@ -208,6 +208,29 @@ def test_flow_pyramid_scale(gpu, oracle, scale, levels):
     assert np.array_equal(xu, ou) and np.array_equal(xv, ov)
 
 
+@pytest.mark.parametrize("levels,poly_n,poly_sigma,window,iters",
+                         [(1, 5, 1.1, 15, 3), (2, 7, 1.5, 9, 2), (4, 5, 1.1, 5, 1), (3, 3, 0.8, 3, 4),
+                          (3, 5, 1.1, 11, 3), (3, 7, 1.5, 13, 2)])
+def test_flow_params_fp32(gpu, oracle, levels, poly_n, poly_sigma, window, iters):
+    """The fp32 flow off the defaults: every box-window template (window 3..15 -> R 1..7), the
+    runtime-radius polynomial expansion (poly_n 3 / 7), 1..4 levels and 1..4 iterations, on u8 and
+    12-bit data -- within the stated tolerance of the fp64 reference."""
+    from paper_2511_14419_b200.params import ExtractParams, FlowParams
+    p = FlowParams(pyramid_levels=levels, poly_n=poly_n, poly_sigma=poly_sigma, window_size=window,
+                   iterations=iters)
+    ep = ExtractParams()
+    ep.flow = p
+    for depth in (8, 16):
+        f = textured_frame(120, 104, depth, 9)
+        if depth == 16:
+            f = (f >> 4).astype(np.uint16)
+        g = cyclic_shift(f, 2, -1)
+        gu, gv = gpu.compute_flow(f, g, p, depth=depth)
+        ou, ov = oracle.compute_flow(f, g, depth, ep)
+        mx, mean = _flow_err(gu, gv, ou, ov)
+        assert mx <= FLOW_MAX_ABS and mean <= FLOW_MEAN_EPE, (depth, levels, poly_n, window, iters, mx, mean)
+
+
 def test_polynomial_expansion_kats(gpu, oracle):
     # constant -> A = b = 0, c = const (test_flow.cpp:66-79; fp32 tolerance)
     e = gpu.polynomial_expansion(np.full((32, 32), 0.42, np.float32))
