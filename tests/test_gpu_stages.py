@@ -55,6 +55,28 @@ def test_denoise_full_frame(gpu, oracle):
         assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("mr,br,ss,sr", [(2, 2, 2.0, 0.04), (1, 3, 1.5, 0.1), (3, 1, 3.0, 0.02),
+                                          (1, 7, 4.0, 0.3), (2, 4, 0.7, 0.01), (1, 2, 2.0, 0.5)])
+def test_denoise_params_bit_exact(gpu, oracle, mr, br, ss, sr):
+    """Denoise off the defaults (the generic runtime-radius kernel, and the default-radius fast
+    kernel under other sigmas): median radius 1-3, bilateral radius 1-7, spatial / range sigmas
+    from 0.7 to 4 and 0.01 to 0.5 -- bit-exact on 8-bit, 12-bit-in-16 and impulse frames."""
+    from paper_2511_14419_b200.params import ExtractParams
+    p = ExtractParams()
+    p.denoise.median_radius = mr
+    p.denoise.bilateral_radius = br
+    p.denoise.bilateral_sigma_spatial = ss
+    p.denoise.bilateral_sigma_range = sr
+    for depth, seed in ((8, 3), (16, 4)):
+        f = textured_frame(77, 61, depth, seed)
+        if depth == 16:
+            f = (f >> 4).astype(np.uint16)
+        for frame in (f, _impulses(f, seed, value=(1 << depth) - 1)):
+            got = gpu.denoise(frame.astype(np.uint16), p, depth=depth)
+            want = oracle.denoise(frame, depth, p)
+            assert np.array_equal(got, want), (mr, br, ss, sr, depth)
+
+
 def test_denoise_constant_identity(gpu):
     f = np.full((18, 24), 77, np.uint16)
     assert np.array_equal(gpu.denoise(f, depth=8), f)
