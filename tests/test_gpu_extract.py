@@ -98,7 +98,8 @@ def test_extract_16bit(gpu, oracle, ref_or_none):
     _check_sequence(gpu, oracle, frames16, depth=16)
 
 
-@pytest.mark.parametrize("knob", ["threshold", "close", "levels", "ensemble", "gradflow"])
+@pytest.mark.parametrize("knob", ["threshold", "close", "levels", "ensemble", "gradflow", "denoise_off",
+                                  "open", "min_area", "flow_weight", "max_shift", "window", "scale"])
 def test_extract_param_grid(gpu, oracle, ref_or_none, knob):
     from paper_2511_14419_b200.params import ExtractParams
     p = ExtractParams()
@@ -112,6 +113,20 @@ def test_extract_param_grid(gpu, oracle, ref_or_none, knob):
         p.roi.adjacent_factor = 1
     elif knob == "gradflow":
         p.roi.gradient_source = 1
+    elif knob == "denoise_off":
+        p.denoise.enabled = False
+    elif knob == "open":
+        p.roi.open_radius = 2
+    elif knob == "min_area":
+        p.roi.min_area = 60
+    elif knob == "flow_weight":
+        p.roi.flow_weight = 0.3
+    elif knob == "max_shift":
+        p.max_shift = 8
+    elif knob == "window":
+        p.flow.window_size = 9
+    elif knob == "scale":
+        p.flow.pyramid_scale = 0.6
     frames = _sequence(ref_or_none, seed=4, n=4, size=96, cells=2)
     _check_sequence(gpu, oracle, frames, params=p)
 
