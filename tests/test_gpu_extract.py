@@ -358,3 +358,42 @@ def test_per_frame_pointer_entries(gpu):
     with pytest.raises(DataError):
         _native.check(_native.lib.froi_extract_frames(ctx.handle, bp, 2, n, 0, mp, None))
     ctx.close()
+
+
+@pytest.mark.parametrize("knob", ["default", "threshold", "close", "levels", "ensemble", "gradflow",
+                                  "denoise_off", "open", "min_area", "window", "scale", "poly7"])
+def test_extract_exact_flow_param_grid(gpu, oracle, ref_or_none, knob):
+    """The bit-exact flow mode end to end over the same parameter grid: every mask, shift,
+    confidence and raw fraction identical to the reference's."""
+    from paper_2511_14419_b200.params import ExtractInfo, ExtractParams
+    p = ExtractParams()
+    if knob == "threshold":
+        p.roi.roi_threshold = 0.1
+    elif knob == "close":
+        p.roi.close_radius = 3
+    elif knob == "levels":
+        p.flow.pyramid_levels = 2
+    elif knob == "ensemble":
+        p.roi.adjacent_factor = 1
+    elif knob == "gradflow":
+        p.roi.gradient_source = 1
+    elif knob == "denoise_off":
+        p.denoise.enabled = False
+    elif knob == "open":
+        p.roi.open_radius = 2
+    elif knob == "min_area":
+        p.roi.min_area = 60
+    elif knob == "window":
+        p.flow.window_size = 9
+    elif knob == "scale":
+        p.flow.pyramid_scale = 0.6
+    elif knob == "poly7":
+        p.flow.poly_n = 7
+        p.flow.poly_sigma = 1.5
+    frames = _sequence(ref_or_none, seed=4, n=4, size=96, cells=2)
+    info = ExtractInfo()
+    got = gpu.extract_roi(frames.astype(np.uint8), p, info=info, exact_flow=True)
+    want, shifts, fracs = oracle.extract_roi(frames, 8, p)
+    assert np.array_equal(got, want)
+    assert [(s.dx, s.dy, s.confidence) for s in info.shifts] == [(s.dx, s.dy, s.confidence) for s in shifts]
+    assert np.array_equal(np.array(info.raw_fractions), np.array(fracs))
